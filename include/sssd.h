@@ -1,0 +1,234 @@
+/*
+ * sssd.h — C ABI of libsssd.so, the B200 (sm_100a) implementation of the SSSD
+ * speculation-and-verification hot path.
+ *
+ * The reference (`specdraft`, /root/reference/pkg/src/specdraft) is a pure
+ * Python package: its "plugin boundary" is its public Python API
+ * (`__init__.py:10-111`).  Each entry point below is the batched device
+ * equivalent of one reference function; the comment names the reference
+ * interface it replaces.  The Python package `paper_2411_05894_b200` binds this
+ * header with ctypes and mirrors the reference API on top.
+ *
+ * Conventions
+ *   - Every pointer argument is a DEVICE pointer owned by the caller (the
+ *     library never allocates persistent memory); `stream` is a cudaStream_t.
+ *   - All launches are asynchronous on `stream`; return value is 0 or a
+ *     negative SSSD_E_* code (argument validation happens before any launch).
+ *     `sssd_error_string(code)` gives the message.
+ *   - Token ids are uint32 (the reference's on-disk `<u4`, datastore.py:17).
+ *   - No torch types cross this boundary.
+ */
+#ifndef SSSD_H
+#define SSSD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSSD_OK 0
+#define SSSD_E_ARG (-1)        /* invalid argument (message has details)          */
+#define SSSD_E_LIMIT (-2)      /* a configured size exceeds a compiled limit      */
+#define SSSD_E_CUDA (-3)       /* a CUDA runtime call failed                      */
+#define SSSD_E_WORKSPACE (-4)  /* workspace too small; sssd_*_workspace() sizes it */
+
+/* Compiled limits (checked on every call). */
+#define SSSD_MAX_P 8           /* max prefix length P (FusionConfig.P)           */
+#define SSSD_MAX_DEPTH 32      /* max branch_len / input_branch_len              */
+#define SSSD_MAX_DRAFT 256     /* max dec_len (draft nodes incl. root)           */
+#define SSSD_ROW_TOKENS 15     /* tokens inlined per suffix row                  */
+
+const char* sssd_error_string(int code);
+/* Last detailed message of a failed call on this thread. */
+const char* sssd_last_error(void);
+int sssd_version(void);
+
+/* ------------------------------------------------------------------------ */
+/* Datastore index (replaces datastore.py:81-109 build_suffix_array,       */
+/* datastore.py:229-242 build)                                              */
+/* ------------------------------------------------------------------------ */
+
+/* Bytes of scratch for sssd_sa_build on n tokens. */
+size_t sssd_sa_build_workspace(uint64_t n);
+
+/* Suffix array of tokens[0..n) by radix-sort prefix doubling.
+ * sa_out: uint32[n] (n < 2^32).  Bit-identical to the reference SA (unique). */
+int sssd_sa_build(const uint32_t* tokens, uint64_t n, uint32_t* sa_out, void* workspace,
+                  size_t workspace_bytes, void* stream);
+
+/* Suffix rows: row r = {sa[r], tokens[sa[r] .. sa[r]+15)} as 16 x uint32 (64 B,
+ * tokens past the corpus end are 0; validity is n - pos).  `rows` must be
+ * 64-byte aligned, n*64 bytes.  The lookup kernels read only rows (and
+ * `tokens` when P + branch_len > 15). */
+int sssd_rows_build(const uint32_t* tokens, uint64_t n, const uint32_t* sa, uint32_t* rows,
+                    void* stream);
+
+/* Copy the SA column of rows out as uint64 (the SSSD v1 file's `<u8` array). */
+int sssd_rows_sa64(const uint32_t* rows, uint64_t n, uint64_t* sa64_out, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Draft configuration (FusionConfig fusion.py:29-88 + query cfg             */
+/* datastore.py:46-78)                                                       */
+/* ------------------------------------------------------------------------ */
+typedef struct sssd_cfg {
+  int32_t P;                /* max prefix length                                 */
+  int32_t dec_len;          /* draft node budget incl. root                      */
+  int32_t branch_len;       /* datastore continuation length                     */
+  int32_t input_branch_len; /* input-cache continuation length                   */
+  int32_t M;                /* sample cap per prefix length                      */
+  int32_t T;                /* min continuations before shortening stops         */
+  int32_t use_datastore;    /* GenerationSession flags (draft.py:150-151)        */
+  int32_t use_input;
+  int32_t n_input_trees;    /* input trees passed to merge (<= P); P in propose  */
+  int32_t has_separator;
+  uint32_t separator;
+  int32_t disc_stride;      /* = max depth + 1                                   */
+  const double* disc;       /* device [(P+1)][disc_stride]: rank 0 = datastore,
+                               rank r = input p=P-r+1 (fusion.py:141-155)        */
+} sssd_cfg;
+
+/* Per-element record of a source's sorted element array:
+ * a continuation path = tok[off .. off+len) of the source's token buffer,
+ * `orig` = position in the reference's insertion order, `m` = backward match
+ * length (input source; 255 for datastore / user paths). */
+typedef struct sssd_elem {
+  uint32_t off;
+  uint32_t orig;
+  uint32_t len_m; /* len | (m << 8) */
+  uint32_t pad;
+} sssd_elem;
+
+/* Datastore view: rows over global SA ranks [rank_base, rank_base + n_rows),
+ * n_tokens = corpus length.  A single GPU holds all ranks (rank_base = 0). */
+typedef struct sssd_ds {
+  const uint32_t* rows;
+  const uint32_t* tokens; /* needed only when P + branch_len > 15 */
+  uint64_t n_tokens;
+  uint64_t rank_base;
+  uint64_t n_rows;
+} sssd_ds;
+
+/* Sequences: request b's live sequence is seq[seq_off[b] .. seq_off[b]+seq_len[b]). */
+typedef struct sssd_seqs {
+  const uint32_t* seq;
+  const int64_t* seq_off;
+  const int32_t* seq_len;
+  int32_t B;
+  int32_t max_len; /* upper bound of seq_len[] (workspace sizing) */
+} sssd_seqs;
+
+/* Outputs of one propose batch (FlattenedDraft draft.py:48-64, one per request). */
+typedef struct sssd_draft_out {
+  int32_t* size;     /* [B]                                     */
+  uint32_t* tokens;  /* [B][S]   S = dec_len                    */
+  int32_t* parents;  /* [B][S]   -1 for the root                */
+  int32_t* depths;   /* [B][S]                                  */
+  uint64_t* mask;    /* [B][S][W] W = ceil(S/64); bit j of row i = j is i or an ancestor */
+} sssd_draft_out;
+
+/* Optional lookup diagnostics for parity (any pointer may be NULL). */
+typedef struct sssd_lookup_out {
+  int64_t* ranges;   /* [B][P][2] (lo, hi) for every p <= min(P, L) (find_range)  */
+  int64_t* samples;  /* [B][P][M] corpus positions of the sampled ranks, -1 pad   */
+  int32_t* n_conts;  /* [B][P] non-empty continuations per p                      */
+  int32_t* p_cut;    /* [B] smallest evaluated p (get_conts shortening stop)      */
+} sssd_lookup_out;
+
+/* Workspace bytes for sssd_propose on this batch shape. */
+size_t sssd_propose_workspace(const sssd_cfg* cfg, int32_t B, int32_t max_len);
+
+/* One batched propose (GenerationSession.propose, draft.py:183-200, over B
+ * sessions): datastore range search + sampling + continuation lists
+ * (Datastore.get_conts datastore.py:156-218), input-cache trees
+ * (InputCache.get_conts input_cache.py:88-113), best-first fusion
+ * (merge fusion.py:209-261) and flatten + ancestor masks (draft.py:67-86). */
+int sssd_propose(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
+                 const sssd_draft_out* out, const sssd_lookup_out* lookup, void* workspace,
+                 size_t workspace_bytes, void* stream);
+
+/* Stage entry points (the single-request reference API is built on these). */
+
+/* Batched Datastore.find_range (datastore.py:156-183): pattern b =
+ * pat[pat_off[b] .. + pat_len[b]); lo_hi[b] = (lo, hi) global SA ranks. */
+int sssd_find_ranges(const sssd_ds* ds, const uint32_t* pat, const int64_t* pat_off,
+                     const int32_t* pat_len, int32_t B, int64_t* lo_hi, void* stream);
+
+/* Datastore.get_conts (datastore.py:185-218) for B prefixes (the last
+ * min(P, len) tokens of each sequence): continuation strings tab[B][P][M][BL],
+ * lengths lens[B][P][M], and the evaluated ones as elements el[B][P*M] sorted
+ * by (string, insertion order), n_el[B] of them (el.orig = insertion order). */
+int sssd_ds_lookup(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg, uint32_t* tab,
+                   uint8_t* lens, sssd_elem* el, int32_t* n_el, const sssd_lookup_out* lookup,
+                   void* stream);
+
+/* InputCache.get_conts (input_cache.py:88-113) for B sequences: every earlier
+ * occurrence e of the last token (m = backward match length >= 1), as elements
+ * el[B][max_len] sorted by (seq[e:e+len], e); n_el[B] of them.  Tree p holds
+ * the elements with m >= p (el.orig = e = insertion order). */
+size_t sssd_input_scan_workspace(int32_t B, int32_t max_len);
+int sssd_input_scan(const sssd_seqs* seqs, const sssd_cfg* cfg, sssd_elem* el, int32_t* n_el,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* Fusion of caller-provided source trees (merge fusion.py:209-261 + flatten).
+ * Each tree is given as its multiset of root-to-end paths in DFS order (first
+ * appearance order = the tree's child order): paths of request b / source s
+ * are elements el[el_off[b*(P+1)+s] .. + el_n[...]) over token buffer `tok`;
+ * source 0 = datastore tree, source s>=1 = input tree p=s.  The library sorts
+ * them on the device and runs the same fusion kernel as sssd_propose. */
+size_t sssd_merge_workspace(const sssd_cfg* cfg, int32_t B, int64_t total_elems);
+int sssd_merge(const uint32_t* tok, const sssd_elem* el, const int64_t* el_off,
+               const int32_t* el_n, int64_t total_elems, const uint32_t* root_tokens, int32_t B,
+               const sssd_cfg* cfg, const sssd_draft_out* out, void* workspace,
+               size_t workspace_bytes, void* stream);
+
+/* Synchronises `stream` and returns the device status word left in a propose
+ * (is_merge = 0) or merge (is_merge = 1) workspace: 0, or SSSD_E_WORKSPACE when
+ * the fusion arena overflowed (outputs are then invalid). */
+int sssd_workspace_status(const sssd_cfg* cfg, int32_t B, int32_t max_len, const void* workspace,
+                          int32_t is_merge, int64_t total_elems, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Verification (verify_greedy draft.py:114-138, step draft.py:202-216)      */
+/* ------------------------------------------------------------------------ */
+
+/* Teacher-forced node predictions (TeacherForcedOracle harness.py:49-67):
+ * pred[b][i] = ref[b][L_b - plen_b + depth[b][i]] or 0xFFFFFFFF. */
+int sssd_teacher_predict(const int32_t* depths, const int32_t* size, int32_t S,
+                         const uint32_t* ref, const int64_t* ref_off, const int32_t* ref_len,
+                         const int32_t* seq_len, const int32_t* prompt_len, int32_t B,
+                         uint32_t* pred, void* stream);
+
+/* Greedy accept + append: walks the draft with pred[b][*], writes the accepted
+ * node indices (path[b][0..n_acc)), the bonus token, and appends
+ * accepted tokens + bonus to the sequence buffer in place (seq_len updated,
+ * clipped to seq_cap[b]).  emitted[b] = n_acc + 1 before clipping. */
+int sssd_accept(const uint32_t* tokens, const int32_t* parents, const int32_t* size, int32_t S,
+                const uint32_t* pred, int32_t B, uint32_t* seq, const int64_t* seq_off,
+                int32_t* seq_len, const int32_t* seq_cap, int32_t* path, int32_t* n_acc,
+                uint32_t* bonus, int32_t* emitted, void* stream);
+
+/* KV compaction after acceptance: for each request, copy cache rows of the
+ * accepted draft nodes (positions base_b + path[b][k]) to base_b + 1 + k, for
+ * every layer / kv head: kv[layer][b][head][pos][d] layout (bf16). */
+int sssd_kv_compact(uint16_t* kv, int32_t n_layers, int32_t B, int32_t n_heads, int32_t max_pos,
+                    int32_t head_dim, const int32_t* base, const int32_t* path,
+                    const int32_t* n_acc, int32_t S, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Tree attention (verification forward; semantics draft.py:205-210)         */
+/* ------------------------------------------------------------------------ */
+/* q:  [B][S][Hq][D] bf16, k/v cache: [B][Hkv][max_pos][D] bf16 holding the
+ * prefix rows [0, ctx_len[b]) and the S tree rows at [ctx_len[b], +S);
+ * mask [B][S][W] u64 ancestor bitmask; o: [B][S][Hq][D] bf16.  D = 128. */
+int sssd_tree_attention(const uint16_t* q, const uint16_t* k, const uint16_t* v,
+                        const uint64_t* mask, const int32_t* ctx_len, int32_t B, int32_t S,
+                        int32_t Hq, int32_t Hkv, int32_t max_pos, int32_t head_dim, float scale,
+                        uint16_t* o, void* workspace, size_t workspace_bytes, void* stream);
+size_t sssd_tree_attention_workspace(int32_t B, int32_t S, int32_t Hq, int32_t max_pos);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSSD_H */

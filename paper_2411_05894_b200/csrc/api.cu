@@ -1,0 +1,395 @@
+// C-ABI entry points of libsssd.so (see include/sssd.h): argument validation,
+// workspace carving and kernel launches.  No allocation, no synchronisation
+// (except the explicit sssd_workspace_status).
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "common.cuh"
+#include "propose.cuh"
+
+namespace sssd {
+
+static thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return SSSD_OK;
+  return fail(SSSD_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Bump-carve a workspace; with base == nullptr it only measures.
+struct Carver {
+  uint8_t* base;
+  size_t off;
+  template <class T>
+  T* take(size_t n) {
+    off = align_up(off, 128);
+    // with base == nullptr the returned "pointer" is the byte offset
+    T* p = reinterpret_cast<T*>(reinterpret_cast<uintptr_t>(base) + off);
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+static int validate_cfg(const sssd_cfg* c) {
+  if (!c) return fail(SSSD_E_ARG, "cfg is NULL");
+  if (c->P < 1) return fail(SSSD_E_ARG, "P must be >= 1, got %d", c->P);
+  if (c->P > SSSD_MAX_P) return fail(SSSD_E_LIMIT, "P=%d exceeds the compiled limit %d", c->P, SSSD_MAX_P);
+  if (c->dec_len < 1) return fail(SSSD_E_ARG, "dec_len must be >= 1, got %d", c->dec_len);
+  if (c->dec_len > SSSD_MAX_DRAFT)
+    return fail(SSSD_E_LIMIT, "dec_len=%d exceeds the compiled limit %d", c->dec_len, SSSD_MAX_DRAFT);
+  if (c->branch_len < 1) return fail(SSSD_E_ARG, "branch_len must be >= 1, got %d", c->branch_len);
+  if (c->input_branch_len < 1)
+    return fail(SSSD_E_ARG, "input_branch_len must be >= 1, got %d", c->input_branch_len);
+  if (c->branch_len > SSSD_MAX_DEPTH || c->input_branch_len > SSSD_MAX_DEPTH)
+    return fail(SSSD_E_LIMIT, "branch lengths exceed the compiled limit %d", SSSD_MAX_DEPTH);
+  if (c->M < 1) return fail(SSSD_E_ARG, "M must be >= 1, got %d", c->M);
+  if (c->T < 1) return fail(SSSD_E_ARG, "T must be >= 1, got %d", c->T);
+  if (c->n_input_trees < 0 || c->n_input_trees > c->P)
+    return fail(SSSD_E_ARG, "got %d input trees for P=%d", c->n_input_trees, c->P);
+  const int md = c->branch_len > c->input_branch_len ? c->branch_len : c->input_branch_len;
+  if (c->disc_stride < md + 1) return fail(SSSD_E_ARG, "disc_stride %d < max depth + 1", c->disc_stride);
+  if (!c->disc) return fail(SSSD_E_ARG, "discount table is NULL");
+  return SSSD_OK;
+}
+
+static KCfg kcfg(const sssd_cfg* c) {
+  KCfg k;
+  k.P = c->P;
+  k.S = c->dec_len;
+  k.BL = c->branch_len;
+  k.IBL = c->input_branch_len;
+  k.M = c->M;
+  k.T = c->T;
+  k.use_ds = c->use_datastore;
+  k.use_in = c->use_input;
+  k.n_trees = c->n_input_trees;
+  k.has_sep = c->has_separator;
+  k.sep = c->separator;
+  k.disc_stride = c->disc_stride;
+  k.disc = c->disc;
+  return k;
+}
+
+constexpr uint32_t kSlabChildren = 1024;
+
+struct DraftWs {
+  SrcDesc* desc;
+  uint32_t* root;
+  Child* slabs;
+  Child* pool;
+  unsigned long long* cursor;
+  int32_t* err;
+  uint64_t pool_cap;
+};
+
+static DraftWs carve_draft(Carver& cv, int P, int B) {
+  DraftWs d;
+  d.desc = cv.take<SrcDesc>((size_t)B * (P + 1));
+  d.root = cv.take<uint32_t>((size_t)B);
+  d.slabs = reinterpret_cast<Child*>(cv.take<uint8_t>((size_t)B * kSlabChildren * kChildBytes));
+  d.pool_cap = (uint64_t)B * 2048 > (1u << 16) ? (uint64_t)B * 2048 : (1u << 16);
+  d.pool = reinterpret_cast<Child*>(cv.take<uint8_t>((size_t)d.pool_cap * kChildBytes));
+  d.cursor = cv.take<unsigned long long>(2);  // cursor + err (the status words)
+  d.err = reinterpret_cast<int32_t*>(d.cursor + 1);
+  return d;
+}
+
+struct PropWs {
+  uint32_t* ds_tab;
+  uint8_t* ds_len;
+  sssd_elem* ds_el;
+  int32_t* ds_n;
+  sssd_elem* in_raw;
+  sssd_elem* in_el;
+  int32_t* in_n;
+  uint32_t* idx;
+  int64_t cap, cap2;
+  DraftWs d;
+  size_t bytes;
+};
+
+static PropWs carve_propose(uint8_t* base, const sssd_cfg* c, int B, int max_len) {
+  Carver cv{base, 0};
+  PropWs w;
+  const size_t PM = (size_t)c->P * c->M;
+  w.ds_tab = cv.take<uint32_t>((size_t)B * PM * c->branch_len);
+  w.ds_len = cv.take<uint8_t>((size_t)B * PM);
+  w.ds_el = cv.take<sssd_elem>((size_t)B * PM);
+  w.ds_n = cv.take<int32_t>((size_t)B);
+  w.cap = max_len > 1 ? max_len : 1;
+  int64_t p2 = 1;
+  while (p2 < w.cap) p2 <<= 1;
+  w.cap2 = w.cap > 4096 ? p2 : 0;
+  w.in_raw = cv.take<sssd_elem>((size_t)B * w.cap);
+  w.in_el = cv.take<sssd_elem>((size_t)B * w.cap);
+  w.in_n = cv.take<int32_t>((size_t)B);
+  w.idx = cv.take<uint32_t>((size_t)B * (w.cap2 ? w.cap2 : 1));
+  w.d = carve_draft(cv, c->P, B);
+  w.bytes = align_up(cv.off, 256);
+  return w;
+}
+
+__global__ void propose_setup_kernel(sssd_seqs seqs, KCfg c, sssd_elem* ds_el, uint32_t* ds_tab,
+                                     const int32_t* ds_n, sssd_elem* in_el, const int32_t* in_n,
+                                     int64_t cap, SrcDesc* desc, uint32_t* root) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= seqs.B) return;
+  const int L = seqs.seq_len[b];
+  const uint32_t* seq = seqs.seq + seqs.seq_off[b];
+  root[b] = seq[L - 1];
+  SrcDesc* d = desc + (size_t)b * (c.P + 1);
+  const size_t PM = (size_t)c.P * c.M;
+  d[0].el = ds_el + b * PM;
+  d[0].tok = ds_tab + b * PM * c.BL;
+  d[0].n = c.use_ds ? ds_n[b] : 0;
+  d[0].thr = 0;
+  d[0].pad = 0;
+  for (int rk = 1; rk <= c.P; ++rk) {
+    const int p = c.P - rk + 1;
+    d[rk].el = in_el + (size_t)b * cap;
+    d[rk].tok = seq;
+    d[rk].n = (c.use_in && p <= c.n_trees) ? in_n[b] : 0;
+    d[rk].thr = p;
+    d[rk].pad = 0;
+  }
+}
+
+__global__ void merge_setup_kernel(const uint32_t* tok, const sssd_elem* sorted,
+                                   const int64_t* el_off, const int32_t* el_n,
+                                   const uint32_t* roots, int B, KCfg c, SrcDesc* desc,
+                                   uint32_t* root) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  root[b] = roots[b];
+  SrcDesc* d = desc + (size_t)b * (c.P + 1);
+  for (int rk = 0; rk <= c.P; ++rk) {
+    const int s = rk == 0 ? 0 : c.P - rk + 1;  // source slot: 0 = datastore, p = input tree p
+    const bool live = rk == 0 || s <= c.n_trees;
+    const size_t bs = (size_t)b * (c.P + 1) + s;
+    d[rk].el = sorted + (live ? el_off[bs] : 0);
+    d[rk].tok = tok;
+    d[rk].n = live ? el_n[bs] : 0;
+    d[rk].thr = 0;
+    d[rk].pad = 0;
+  }
+}
+
+static int launch_draft(const DraftWs& d, const KCfg& k, int B, const sssd_draft_out* out,
+                        cudaStream_t st) {
+  const int smem = draft_smem_bytes(k.P, k.S);
+  cudaError_t e = cudaFuncSetAttribute(draft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return cuda_check(e, "draft_kernel smem attribute");
+  draft_kernel<<<B, 32, smem, st>>>(d.desc, d.root, k, d.slabs, kSlabChildren, d.pool, d.cursor,
+                                    d.pool_cap, d.err, *out);
+  return cuda_check(cudaGetLastError(), "draft_kernel launch");
+}
+
+static int validate_out(const sssd_draft_out* out) {
+  if (!out || !out->size || !out->tokens || !out->parents || !out->depths || !out->mask)
+    return fail(SSSD_E_ARG, "draft output buffers must all be non-NULL");
+  return SSSD_OK;
+}
+
+}  // namespace sssd
+
+using namespace sssd;
+
+extern "C" {
+
+const char* sssd_error_string(int code) {
+  switch (code) {
+    case SSSD_OK: return "ok";
+    case SSSD_E_ARG: return "invalid argument";
+    case SSSD_E_LIMIT: return "compiled limit exceeded";
+    case SSSD_E_CUDA: return "CUDA error";
+    case SSSD_E_WORKSPACE: return "workspace too small";
+    default: return "unknown error";
+  }
+}
+
+const char* sssd_last_error(void) { return g_err.c_str(); }
+
+int sssd_version(void) { return 1; }
+
+size_t sssd_propose_workspace(const sssd_cfg* cfg, int32_t B, int32_t max_len) {
+  if (!cfg || B < 0) return 0;
+  return carve_propose(nullptr, cfg, B, max_len).bytes;
+}
+
+int sssd_propose(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
+                 const sssd_draft_out* out, const sssd_lookup_out* lookup, void* workspace,
+                 size_t workspace_bytes, void* stream) {
+  int rc = validate_cfg(cfg);
+  if (rc) return rc;
+  if ((rc = validate_out(out))) return rc;
+  if (!seqs || seqs->B < 0) return fail(SSSD_E_ARG, "bad sequence batch");
+  if (cfg->use_datastore) {
+    if (!ds || !ds->rows) return fail(SSSD_E_ARG, "use_datastore requires a datastore");
+    if (ds->n_rows == 0 || ds->n_tokens == 0) return fail(SSSD_E_ARG, "empty corpus");
+    if (ds->n_tokens >= 0xffffffffull) return fail(SSSD_E_LIMIT, "corpus longer than 2^32-1 tokens");
+    if (cfg->P + cfg->branch_len > SSSD_ROW_TOKENS && !ds->tokens)
+      return fail(SSSD_E_ARG, "P + branch_len > %d needs the token array", SSSD_ROW_TOKENS);
+  }
+  const int B = seqs->B;
+  if (B == 0) return SSSD_OK;
+  const PropWs w = carve_propose(static_cast<uint8_t*>(workspace), cfg, B, seqs->max_len);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(SSSD_E_WORKSPACE, "propose needs %zu workspace bytes, got %zu", w.bytes, workspace_bytes);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const KCfg k = kcfg(cfg);
+  sssd_lookup_out lk{};
+  if (lookup) lk = *lookup;
+  if ((rc = cuda_check(cudaMemsetAsync(w.d.cursor, 0, 16, st), "memset status"))) return rc;
+  if (cfg->use_datastore) {
+    ds_lookup_kernel<<<B, 32 * cfg->P, 0, st>>>(*ds, *seqs, k, w.ds_tab, w.ds_len, w.ds_el, w.ds_n, lk);
+    if ((rc = cuda_check(cudaGetLastError(), "ds_lookup_kernel launch"))) return rc;
+  }
+  if (cfg->use_input) {
+    input_scan_kernel<<<B, 256, 0, st>>>(*seqs, k, w.in_raw, w.in_el, w.in_n, w.idx, w.cap, w.cap2);
+    if ((rc = cuda_check(cudaGetLastError(), "input_scan_kernel launch"))) return rc;
+  }
+  propose_setup_kernel<<<(B + 127) / 128, 128, 0, st>>>(*seqs, k, w.ds_el, w.ds_tab, w.ds_n, w.in_el,
+                                                          w.in_n, w.cap, w.d.desc, w.d.root);
+  if ((rc = cuda_check(cudaGetLastError(), "propose_setup_kernel launch"))) return rc;
+  return launch_draft(w.d, k, B, out, st);
+}
+
+// Returns the device status word of the last propose / merge that used this
+// workspace (synchronising on `stream`): 0 or SSSD_E_WORKSPACE.
+int sssd_workspace_status(const sssd_cfg* cfg, int32_t B, int32_t max_len, const void* workspace,
+                          int32_t is_merge, int64_t total_elems, void* stream) {
+  size_t off;
+  if (is_merge) {
+    Carver cv{nullptr, 0};
+    cv.take<sssd_elem>((size_t)(total_elems > 0 ? total_elems : 1));
+    cv.take<uint32_t>((size_t)2 * (total_elems > 0 ? total_elems : 1));
+    DraftWs d = carve_draft(cv, cfg->P, B);
+    off = reinterpret_cast<size_t>(d.err);
+  } else {
+    PropWs w = carve_propose(nullptr, cfg, B, max_len);
+    off = reinterpret_cast<size_t>(w.d.err);
+  }
+  int32_t v = 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = cuda_check(cudaMemcpyAsync(&v, static_cast<const uint8_t*>(workspace) + off, 4,
+                                      cudaMemcpyDeviceToHost, st), "status copy");
+  if (rc) return rc;
+  if ((rc = cuda_check(cudaStreamSynchronize(st), "status sync"))) return rc;
+  if (v) return fail(v, "device workspace overflow (fusion arena)");
+  return SSSD_OK;
+}
+
+size_t sssd_merge_workspace(const sssd_cfg* cfg, int32_t B, int64_t total_elems) {
+  if (!cfg || B < 0) return 0;
+  Carver cv{nullptr, 0};
+  cv.take<sssd_elem>((size_t)(total_elems > 0 ? total_elems : 1));
+  cv.take<uint32_t>((size_t)2 * (total_elems > 0 ? total_elems : 1));
+  carve_draft(cv, cfg->P, B);
+  return align_up(cv.off, 256);
+}
+
+int sssd_merge(const uint32_t* tok, const sssd_elem* el, const int64_t* el_off,
+                const int32_t* el_n, int64_t total_elems, const uint32_t* root_tokens, int32_t B,
+                const sssd_cfg* cfg, const sssd_draft_out* out, void* workspace,
+                size_t workspace_bytes, void* stream) {
+  int rc = validate_cfg(cfg);
+  if (rc) return rc;
+  if ((rc = validate_out(out))) return rc;
+  if (B < 0) return fail(SSSD_E_ARG, "bad batch size %d", B);
+  if (B == 0) return SSSD_OK;
+  Carver cv{static_cast<uint8_t*>(workspace), 0};
+  const size_t te = (size_t)(total_elems > 0 ? total_elems : 1);
+  sssd_elem* sorted = cv.take<sssd_elem>(te);
+  uint32_t* idx = cv.take<uint32_t>(2 * te);
+  DraftWs d = carve_draft(cv, cfg->P, B);
+  const size_t need = align_up(cv.off, 256);
+  if (!workspace || workspace_bytes < need)
+    return fail(SSSD_E_WORKSPACE, "merge needs %zu workspace bytes, got %zu", need, workspace_bytes);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const KCfg k = kcfg(cfg);
+  if ((rc = cuda_check(cudaMemsetAsync(d.cursor, 0, 16, st), "memset status"))) return rc;
+  sort_sources_kernel<<<B * (cfg->P + 1), 256, 0, st>>>(tok, el, el_off, el_n, sorted, idx, 2 * te);
+  if ((rc = cuda_check(cudaGetLastError(), "sort_sources_kernel launch"))) return rc;
+  merge_setup_kernel<<<(B + 127) / 128, 128, 0, st>>>(tok, sorted, el_off, el_n, root_tokens, B, k,
+                                                        d.desc, d.root);
+  if ((rc = cuda_check(cudaGetLastError(), "merge_setup_kernel launch"))) return rc;
+  return launch_draft(d, k, B, out, st);
+}
+
+
+size_t sssd_ds_lookup_workspace(const sssd_cfg* cfg, int32_t B) {
+  (void)cfg;
+  (void)B;
+  return 0;
+}
+
+int sssd_ds_lookup(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg, uint32_t* tab,
+                   uint8_t* lens, sssd_elem* el, int32_t* n_el, const sssd_lookup_out* lookup,
+                   void* stream) {
+  int rc = validate_cfg(cfg);
+  if (rc) return rc;
+  if (!ds || !ds->rows || ds->n_rows == 0) return fail(SSSD_E_ARG, "empty corpus");
+  if (cfg->P + cfg->branch_len > SSSD_ROW_TOKENS && !ds->tokens)
+    return fail(SSSD_E_ARG, "P + branch_len > %d needs the token array", SSSD_ROW_TOKENS);
+  if (!seqs || seqs->B < 0) return fail(SSSD_E_ARG, "bad sequence batch");
+  if (seqs->B == 0) return SSSD_OK;
+  sssd_lookup_out lk{};
+  if (lookup) lk = *lookup;
+  ds_lookup_kernel<<<seqs->B, 32 * cfg->P, 0, static_cast<cudaStream_t>(stream)>>>(
+      *ds, *seqs, kcfg(cfg), tab, lens, el, n_el, lk);
+  return cuda_check(cudaGetLastError(), "ds_lookup_kernel launch");
+}
+
+size_t sssd_input_scan_workspace(int32_t B, int32_t max_len) {
+  const int64_t cap = max_len > 1 ? max_len : 1;
+  int64_t p2 = 1;
+  while (p2 < cap) p2 <<= 1;
+  return (size_t)B * cap * sizeof(sssd_elem) + (size_t)B * (cap > 4096 ? p2 : 1) * 4 + 256;
+}
+
+int sssd_input_scan(const sssd_seqs* seqs, const sssd_cfg* cfg, sssd_elem* el, int32_t* n_el,
+                    void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = validate_cfg(cfg);
+  if (rc) return rc;
+  if (!seqs || seqs->B < 0) return fail(SSSD_E_ARG, "bad sequence batch");
+  if (seqs->B == 0) return SSSD_OK;
+  const size_t need = sssd_input_scan_workspace(seqs->B, seqs->max_len);
+  if (!workspace || workspace_bytes < need)
+    return fail(SSSD_E_WORKSPACE, "input_scan needs %zu workspace bytes, got %zu", need, workspace_bytes);
+  const int64_t cap = seqs->max_len > 1 ? seqs->max_len : 1;
+  int64_t p2 = 1;
+  while (p2 < cap) p2 <<= 1;
+  sssd_elem* raw = static_cast<sssd_elem*>(workspace);
+  uint32_t* idx = reinterpret_cast<uint32_t*>(raw + (size_t)seqs->B * cap);
+  KCfg k = kcfg(cfg);
+  k.use_in = 1;
+  input_scan_kernel<<<seqs->B, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      *seqs, k, raw, el, n_el, idx, cap, cap > 4096 ? p2 : 0);
+  return cuda_check(cudaGetLastError(), "input_scan_kernel launch");
+}
+
+int sssd_find_ranges(const sssd_ds* ds, const uint32_t* pat, const int64_t* pat_off,
+                     const int32_t* pat_len, int32_t B, int64_t* lo_hi, void* stream) {
+  if (!ds || !ds->rows || ds->n_rows == 0) return fail(SSSD_E_ARG, "empty corpus");
+  if (B <= 0) return B == 0 ? SSSD_OK : fail(SSSD_E_ARG, "bad batch");
+  find_ranges_kernel<<<(B + 3) / 4, 128, 0, static_cast<cudaStream_t>(stream)>>>(*ds, pat, pat_off,
+                                                                                 pat_len, B, lo_hi);
+  return cuda_check(cudaGetLastError(), "find_ranges_kernel launch");
+}
+
+}  // extern "C"

@@ -1,0 +1,49 @@
+// Shared device helpers for libsssd (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sssd.h"
+
+#define SSSD_FULL 0xffffffffu
+
+namespace sssd {
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ uint4 ldg4(const uint4* p) { return __ldg(p); }
+
+__device__ __forceinline__ uint32_t el_len(uint32_t len_m) { return len_m & 0xffu; }
+__device__ __forceinline__ uint32_t el_m(uint32_t len_m) { return (len_m >> 8) & 0xffu; }
+
+// Lexicographic compare of two token strings with "shorter sorts first"
+// (a proper prefix precedes its extensions; ref datastore.py:129-141 and the
+// continuation-list order of A.3/A.4).  Returns -1/0/+1.
+__device__ __forceinline__ int cmp_str(const uint32_t* a, uint32_t la, const uint32_t* b,
+                                       uint32_t lb) {
+  const uint32_t l = la < lb ? la : lb;
+  for (uint32_t j = 0; j < l; ++j) {
+    const uint32_t x = a[j], y = b[j];
+    if (x != y) return x < y ? -1 : 1;
+  }
+  return la < lb ? -1 : (la > lb ? 1 : 0);
+}
+
+// Per-(request, source) view used by the fusion kernel: a sorted element
+// array over a token buffer; an element counts toward this source's tree when
+// its backward-match length m >= thr (input tree p: thr = p; datastore and
+// caller-provided trees: thr = 0).
+struct SrcDesc {
+  const sssd_elem* el;
+  const uint32_t* tok;
+  int32_t n;
+  int32_t thr;
+  int64_t pad;
+};
+
+}  // namespace sssd

@@ -1,0 +1,41 @@
+// Kernel-side configuration and launch declarations of the propose path.
+#pragma once
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace sssd {
+
+struct KCfg {
+  int P, S, BL, IBL, M, T, use_ds, use_in, n_trees, has_sep;
+  uint32_t sep;
+  int disc_stride;
+  const double* disc;
+};
+
+struct Child;
+
+__global__ void find_ranges_kernel(sssd_ds ds, const uint32_t* pat, const int64_t* pat_off,
+                                   const int32_t* pat_len, int32_t B, int64_t* lo_hi);
+
+__global__ void ds_lookup_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, uint32_t* ds_tab,
+                                 uint8_t* ds_len, sssd_elem* ds_el, int32_t* ds_n,
+                                 sssd_lookup_out lk);
+__global__ void input_scan_kernel(sssd_seqs seqs, KCfg c, sssd_elem* raw, sssd_elem* sorted,
+                                  int32_t* in_n, uint32_t* idx_ws, int64_t cap, int64_t cap2);
+__global__ void sort_sources_kernel(const uint32_t* tok, const sssd_elem* el,
+                                    const int64_t* el_off, const int32_t* el_n, sssd_elem* sorted,
+                                    uint32_t* idx_ws, int64_t idx_cap);
+__global__ void draft_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, Child* slabs,
+                             uint32_t slab_cap, Child* pool, unsigned long long* cursor,
+                             uint64_t pool_cap, int32_t* err, sssd_draft_out out);
+
+constexpr int kChildBytes = 32;
+constexpr int kGroupBytes = 40;
+
+inline int draft_smem_bytes(int P, int S) {
+  const int Gmax = (P + 1) * S + P + 1;
+  return Gmax * kGroupBytes + S * 4 + S * 2 * 8 + 16;
+}
+
+}  // namespace sssd

@@ -1,0 +1,229 @@
+"""GPU parity: the CUDA path (through the C ABI) against golden vectors made by
+the reference and against the CPU oracle.  Bit-exact for every integer output
+(suffix arrays, [lo, hi) ranges, sampled positions, ordered trees, flattened
+drafts, packed masks, per-step token counts)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import sssd_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2411_05894_b200 as G  # noqa: E402
+from paper_2411_05894_b200 import workload  # noqa: E402
+from paper_2411_05894_b200.draft import pack_mask  # noqa: E402
+
+
+def shape_of(tree) -> list:
+    def r(node):
+        return [node.count, [[int(k), r(v)] for k, v in node.children.items()]]
+
+    return [tree.root_count, [[int(k), r(v)] for k, v in tree.children.items()]]
+
+
+def flat_dict(f) -> dict:
+    return {"tokens": [int(x) for x in f.tokens], "parents": list(f.parents), "depths": list(f.depths),
+            "mask": pack_mask(f.mask).hex()}
+
+
+def test_sa_build_golden(golden):
+    for case in golden("sa.json"):
+        ds = G.build(case["corpus"])
+        assert ds.suffix_index.tolist() == case["sa"]
+
+
+def test_sa_build_phrase_and_random():
+    g = __import__("json").load(open(__import__("os").path.join(__import__("os").path.dirname(__file__),
+                                                                "golden", "phrase.json")))
+    corpus = workload.corpus(g["n"], g["vocab"])
+    ds = G.build(corpus, vocab_size=g["vocab"])
+    assert hashlib.sha256(ds.suffix_index.astype("<u8").tobytes()).hexdigest() == g["sa_sha256"]
+    rng = np.random.default_rng(5)
+    for alpha, n in [(2, 20000), (3, 50000), (1000, 200000), (2**32 - 1, 3000)]:
+        c = rng.integers(0, alpha, n, dtype=np.int64).astype(np.uint32)
+        assert np.array_equal(G.build(c).suffix_index, O.suffix_array(c))
+
+
+def test_lookup_golden(golden):
+    """find_range + sample_range positions + ordered get_conts trees."""
+    for case in golden("lookup.json"):
+        ds = G.build(case["corpus"])
+        c = case["cfg"]
+        qc = G.DatastoreQueryConfig(c["P"], c["M"], c["T"], c["branch_len"], c["separator"])
+        pats, want = [], []
+        for q in case["queries"]:
+            for p, lo, hi, pos in q["ranges"]:
+                pats.append(q["prefix"][len(q["prefix"]) - p:])
+                want.append((lo, hi))
+        assert ds.find_ranges(pats) == want
+        for q in case["queries"]:
+            assert shape_of(ds.get_conts(q["prefix"], qc)) == q["tree"]
+
+
+def test_lookup_samples_match_oracle():
+    """Sampled SA positions and per-p counts from the propose path itself."""
+    corpus = workload.corpus(200_000, 500)
+    ds = G.build(corpus)
+    sa = O.suffix_array(corpus)
+    ctxs = workload.contexts(48, 64, 500)
+    cfg = G.FusionConfig(dec_len=16, M=20, T=30)
+    eng = G.DraftEngine(ds, cfg)
+    drafts, out = eng.propose_host([c.tolist() for c in ctxs], lookup=True)
+    ranges = out.ranges.cpu().numpy()
+    samples = out.samples.cpu().numpy()
+    pcut = out.p_cut.cpu().numpy()
+    for b, ctx in enumerate(ctxs):
+        look = O.ds_lookup(corpus, sa, ctx[-4:].tolist(), cfg.P, cfg.M, cfg.T, cfg.branch_len)
+        for p in range(1, 5):
+            lo, hi = O.find_range(corpus, sa, ctx[-p:].tolist())
+            assert tuple(ranges[b, p - 1]) == (lo, hi)
+        assert pcut[b] == look.ranges[-1][0]
+        for p, pos in look.samples:
+            assert samples[b, p - 1, : len(pos)].tolist() == pos
+
+
+def test_input_golden(golden):
+    from paper_2411_05894_b200.input_cache import input_trees_batch
+
+    cases = golden("input.json")
+    for case in cases:
+        trees = input_trees_batch([case["seq"]], case["P"], case["ibl"])[0]
+        assert [shape_of(t) for t in trees] == case["trees"]
+
+
+def test_merge_golden(golden):
+    cases = golden("merge.json")
+    by_cfg: dict = {}
+    for case in cases:
+        by_cfg.setdefault(tuple(sorted(case["cfg"].items())), []).append(case)
+    for key, group in by_cfg.items():
+        cfg = G.FusionConfig(**dict(key))
+        reqs = [(G.tree_from_paths(cs["ds"]), [G.tree_from_paths(p) for p in cs["inputs"]], cs["root"])
+                for cs in group]
+        # requests with different numbers of input trees are fused separately
+        for n_in in sorted({len(r[1]) for r in reqs}):
+            sub = [(r, cs) for r, cs in zip(reqs, group) if len(r[1]) == n_in]
+            flats = G.merge_batch([r for r, _ in sub], cfg)
+            for f, (_, cs) in zip(flats, sub):
+                assert flat_dict(f) == cs["flat"]
+
+
+def test_propose_golden(golden):
+    for case in golden("propose.json"):
+        ds = G.build(case["corpus"])
+        cfg = G.FusionConfig(**case["cfg"])
+        src = case["sources"]
+        eng = G.DraftEngine(ds, cfg, case["separator"], src in ("both", "datastore"), src in ("both", "input"))
+        flats = eng.propose_host([r["seq"] for r in case["requests"]])
+        for f, r in zip(flats, case["requests"]):
+            assert flat_dict(f) == r["flat"]
+
+
+def test_phrase_golden_digests(golden):
+    g = golden("phrase.json")
+    ds = G.build(workload.corpus(g["n"], g["vocab"]), vocab_size=g["vocab"])
+    for case in g["cases"]:
+        cfg = G.FusionConfig(**case["cfg"])
+        if case["kind"] == "propose":
+            ctxs = [c.tolist() for c in workload.contexts(case["B"], case["ctx"], g["vocab"])]
+            flats = G.DraftEngine(ds, cfg).propose_host(ctxs)
+            assert [flat_dict(f) for f in flats] == case["flats"]
+            assert G.draft_digest(flats) == case["digest"]
+        else:
+            recs = [G.SimRecord(p, r) for p, r in workload.records(case["records"], case["prompt"], case["ref"],
+                                                                   g["vocab"])]
+            rep = G.simulate(recs, ds, cfg)
+            assert [r.per_step_tokens for r in rep.records] == case["per_step"]
+
+
+def test_simulate_golden(golden):
+    for case in golden("simulate.json"):
+        ds = G.build(case["corpus"])
+        st = G.run_record(0, G.SimRecord(case["prompt"], case["reference"]), ds, G.FusionConfig(**case["cfg"]))
+        assert st.per_step_tokens == case["per_step"]
+
+
+def test_simulate_batch_composition_invariant():
+    """Continuous batching: per-record stats independent of slot count."""
+    corpus = workload.corpus(100_000, 2000)
+    ds = G.build(corpus)
+    recs = [G.SimRecord(p, r) for p, r in workload.records(12, 64, 40, 2000)]
+    cfg = G.FusionConfig(dec_len=12)
+    a = G.simulate(recs, ds, cfg, slots=12).deterministic_dict()
+    b = G.simulate(recs, ds, cfg, slots=5).deterministic_dict()
+    assert a == b
+    store = O.Store(corpus, O.suffix_array(corpus))
+    oc = O.Cfg(dec_len=12)
+    for i, r in enumerate(recs):
+        assert a["records"][i]["per_step_tokens"] == O.run_record(store, r.prompt, r.reference, oc)
+
+
+def test_propose_vs_oracle_random_shapes():
+    """Random stores / configs / long contexts against the oracle (ordered)."""
+    rng = np.random.default_rng(11)
+    for trial in range(6):
+        V = int(rng.choice([3, 8, 50]))
+        corpus = rng.integers(0, V, int(rng.integers(500, 20000))).astype(np.uint32)
+        sa = O.suffix_array(corpus)
+        store = O.Store(corpus, sa)
+        ds = G.build(corpus)
+        cfg = G.FusionConfig(P=int(rng.integers(1, 6)), dec_len=int(rng.choice([8, 32, 64, 100])),
+                             input_branch_len=int(rng.integers(1, 9)), M=int(rng.choice([10, 100])),
+                             T=int(rng.choice([1, 16, 50])))
+        ctxs = [rng.integers(0, V, int(rng.integers(1, 3000))).tolist() for _ in range(16)]
+        flats = G.DraftEngine(ds, cfg).propose_host(ctxs)
+        oc = O.Cfg(**{k: getattr(cfg, k) for k in ("P", "dec_len", "branch_len", "input_branch_len", "M", "T",
+                                                    "alpha", "beta", "gamma_ds", "gamma_in")})
+        for f, ctx in zip(flats, ctxs):
+            d = O.propose(store, ctx, oc)
+            assert (f.tokens, f.parents, f.depths) == (d.tokens, d.parents, d.depths), trial
+            assert pack_mask(f.mask) == O.pack_mask_rows(d.masks, d.size)
+
+
+def test_long_context_input_sort_path():
+    """>4096 occurrences of the last token exercises the global-memory sort."""
+    rng = np.random.default_rng(3)
+    seq = rng.integers(0, 3, 20000).tolist()
+    corpus = rng.integers(0, 3, 5000).astype(np.uint32)
+    store = O.Store(corpus, O.suffix_array(corpus))
+    cfg = G.FusionConfig(dec_len=16)
+    f = G.DraftEngine(G.build(corpus), cfg).propose_host([seq])[0]
+    d = O.propose(store, seq, O.Cfg(dec_len=16))
+    assert (f.tokens, f.parents, f.depths) == (d.tokens, d.parents, d.depths)
+
+
+def test_verify_matches_oracle():
+    rng = np.random.default_rng(9)
+    corpus = workload.corpus(50_000, 50)
+    ds = G.build(corpus)
+    ctxs = [c.tolist() for c in workload.contexts(64, 100, 50)]
+    flats = G.DraftEngine(ds, G.FusionConfig(dec_len=24)).propose_host(ctxs)
+    preds = []
+    for f in flats:
+        p = []
+        for i in range(f.s_q):
+            kids = [f.tokens[j] for j in range(1, f.s_q) if f.parents[j] == i]
+            p.append(int(rng.choice(kids)) if kids and rng.random() < 0.7 else int(rng.integers(0, 50)))
+        preds.append(p)
+    got = G.verify_batch(flats, preds)
+    for f, p, r in zip(flats, preds, got):
+        d = O.Draft(f.tokens, f.parents, f.depths, [0] * f.s_q)
+        assert (r.accepted_path, r.bonus_token) == O.verify(d, p)
+
+
+def test_save_load_roundtrip(tmp_path):
+    corpus = np.random.default_rng(1).integers(0, 1000, 3000)
+    ds = G.build(corpus, vocab_size=1000)
+    path = tmp_path / "ds.bin"
+    ds.save(path)
+    back = G.load(path)
+    assert np.array_equal(back.suffix_index, ds.suffix_index)
+    assert back.vocab_size == 1000
+    assert back.find_range([int(corpus[5]), int(corpus[6])]) == ds.find_range([int(corpus[5]), int(corpus[6])])
