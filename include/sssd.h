@@ -159,9 +159,10 @@ int sssd_find_ranges(const sssd_ds* ds, const uint32_t* pat, const int64_t* pat_
  * min(P, len) tokens of each sequence): continuation strings tab[B][P][M][BL],
  * lengths lens[B][P][M], and the evaluated ones as elements el[B][P*M] sorted
  * by (string, insertion order), n_el[B] of them (el.orig = insertion order). */
+size_t sssd_ds_lookup_workspace(const sssd_cfg* cfg, int32_t B);
 int sssd_ds_lookup(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg, uint32_t* tab,
                    uint8_t* lens, sssd_elem* el, int32_t* n_el, const sssd_lookup_out* lookup,
-                   void* stream);
+                   void* workspace, size_t workspace_bytes, void* stream);
 
 /* InputCache.get_conts (input_cache.py:88-113) for B sequences: every earlier
  * occurrence e of the last token (m = backward match length >= 1), as elements

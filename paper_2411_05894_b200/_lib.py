@@ -73,8 +73,9 @@ _SIGS = {
     "sssd_workspace_status": (C.c_int, [C.POINTER(Cfg), C.c_int32, C.c_int32, vp, C.c_int32,
                                         C.c_int64, vp]),
     "sssd_find_ranges": (C.c_int, [C.POINTER(Ds), vp, vp, vp, C.c_int32, vp, vp]),
+    "sssd_ds_lookup_workspace": (C.c_size_t, [C.POINTER(Cfg), C.c_int32]),
     "sssd_ds_lookup": (C.c_int, [C.POINTER(Ds), C.POINTER(Seqs), C.POINTER(Cfg), vp, vp, vp, vp,
-                                 C.POINTER(LookupOut), vp]),
+                                 C.POINTER(LookupOut), vp, C.c_size_t, vp]),
     "sssd_input_scan_workspace": (C.c_size_t, [C.c_int32, C.c_int32]),
     "sssd_input_scan": (C.c_int, [C.POINTER(Seqs), C.POINTER(Cfg), vp, vp, vp, C.c_size_t, vp]),
     "sssd_merge_workspace": (C.c_size_t, [C.POINTER(Cfg), C.c_int32, C.c_int64]),

@@ -85,7 +85,7 @@ static KCfg kcfg(const sssd_cfg* c) {
   return k;
 }
 
-constexpr uint32_t kSlabChildren = 1024;
+constexpr uint32_t kSlabChildren = 2048;
 
 struct DraftWs {
   SrcDesc* desc;
@@ -97,12 +97,17 @@ struct DraftWs {
   uint64_t pool_cap;
 };
 
-static DraftWs carve_draft(Carver& cv, int P, int B) {
+// Fusion arena: a per-request slab (stack of sibling-group child lists) plus a
+// shared overflow pool.  An expansion reserves its element-range size and
+// returns the unused tail, so the slab holds the typical request; long
+// contexts (huge input-tree roots) spill into the pool, sized by max_len.
+static DraftWs carve_draft(Carver& cv, int P, int B, int64_t max_len = 0) {
   DraftWs d;
   d.desc = cv.take<SrcDesc>((size_t)B * (P + 1));
   d.root = cv.take<uint32_t>((size_t)B);
   d.slabs = reinterpret_cast<Child*>(cv.take<uint8_t>((size_t)B * kSlabChildren * kChildBytes));
-  d.pool_cap = (uint64_t)B * 2048 > (1u << 16) ? (uint64_t)B * 2048 : (1u << 16);
+  d.pool_cap = (1u << 16) + (uint64_t)B * 1024 +
+               (max_len > (int64_t)kSlabChildren ? (uint64_t)B * (P + 1) * (uint64_t)max_len : 0);
   d.pool = reinterpret_cast<Child*>(cv.take<uint8_t>((size_t)d.pool_cap * kChildBytes));
   d.cursor = cv.take<unsigned long long>(2);  // cursor + err (the status words)
   d.err = reinterpret_cast<int32_t*>(d.cursor + 1);
@@ -114,6 +119,9 @@ struct PropWs {
   uint8_t* ds_len;
   sssd_elem* ds_el;
   int32_t* ds_n;
+  sssd_elem* ds_raw;
+  uint32_t* ds_idx;
+  int64_t ds_idx_cap;
   sssd_elem* in_raw;
   sssd_elem* in_el;
   int32_t* in_n;
@@ -131,6 +139,10 @@ static PropWs carve_propose(uint8_t* base, const sssd_cfg* c, int B, int max_len
   w.ds_len = cv.take<uint8_t>((size_t)B * PM);
   w.ds_el = cv.take<sssd_elem>((size_t)B * PM);
   w.ds_n = cv.take<int32_t>((size_t)B);
+  const bool sep = c->has_separator != 0;
+  w.ds_idx_cap = ds_idx_cap(c->P, c->M);
+  w.ds_raw = cv.take<sssd_elem>(sep ? (size_t)B * PM : 1);
+  w.ds_idx = cv.take<uint32_t>(sep && w.ds_idx_cap > 4096 ? (size_t)B * w.ds_idx_cap : 1);
   w.cap = max_len > 1 ? max_len : 1;
   int64_t p2 = 1;
   while (p2 < w.cap) p2 <<= 1;
@@ -139,7 +151,7 @@ static PropWs carve_propose(uint8_t* base, const sssd_cfg* c, int B, int max_len
   w.in_el = cv.take<sssd_elem>((size_t)B * w.cap);
   w.in_n = cv.take<int32_t>((size_t)B);
   w.idx = cv.take<uint32_t>((size_t)B * (w.cap2 ? w.cap2 : 1));
-  w.d = carve_draft(cv, c->P, B);
+  w.d = carve_draft(cv, c->P, B, w.cap);
   w.bytes = align_up(cv.off, 256);
   return w;
 }
@@ -256,7 +268,8 @@ int sssd_propose(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
   if (lookup) lk = *lookup;
   if ((rc = cuda_check(cudaMemsetAsync(w.d.cursor, 0, 16, st), "memset status"))) return rc;
   if (cfg->use_datastore) {
-    ds_lookup_kernel<<<B, 32 * cfg->P, 0, st>>>(*ds, *seqs, k, w.ds_tab, w.ds_len, w.ds_el, w.ds_n, lk);
+    ds_lookup_kernel<<<B, 32 * cfg->P, 0, st>>>(*ds, *seqs, k, w.ds_tab, w.ds_len, w.ds_el, w.ds_n, lk,
+                                                 w.ds_raw, w.ds_idx, w.ds_idx_cap);
     if ((rc = cuda_check(cudaGetLastError(), "ds_lookup_kernel launch"))) return rc;
   }
   if (cfg->use_input) {
@@ -333,14 +346,14 @@ int sssd_merge(const uint32_t* tok, const sssd_elem* el, const int64_t* el_off,
 
 
 size_t sssd_ds_lookup_workspace(const sssd_cfg* cfg, int32_t B) {
-  (void)cfg;
-  (void)B;
-  return 0;
+  if (!cfg || B < 0) return 0;
+  const int64_t cap = ds_idx_cap(cfg->P, cfg->M);
+  return (size_t)B * cfg->P * cfg->M * sizeof(sssd_elem) + 256 + (size_t)B * cap * 4;
 }
 
 int sssd_ds_lookup(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg, uint32_t* tab,
                    uint8_t* lens, sssd_elem* el, int32_t* n_el, const sssd_lookup_out* lookup,
-                   void* stream) {
+                   void* workspace, size_t workspace_bytes, void* stream) {
   int rc = validate_cfg(cfg);
   if (rc) return rc;
   if (!ds || !ds->rows || ds->n_rows == 0) return fail(SSSD_E_ARG, "empty corpus");
@@ -348,10 +361,16 @@ int sssd_ds_lookup(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg
     return fail(SSSD_E_ARG, "P + branch_len > %d needs the token array", SSSD_ROW_TOKENS);
   if (!seqs || seqs->B < 0) return fail(SSSD_E_ARG, "bad sequence batch");
   if (seqs->B == 0) return SSSD_OK;
+  const size_t need = sssd_ds_lookup_workspace(cfg, seqs->B);
+  if (!workspace || workspace_bytes < need)
+    return fail(SSSD_E_WORKSPACE, "ds_lookup needs %zu workspace bytes, got %zu", need, workspace_bytes);
   sssd_lookup_out lk{};
   if (lookup) lk = *lookup;
+  sssd_elem* raw = static_cast<sssd_elem*>(workspace);
+  uint32_t* idx = reinterpret_cast<uint32_t*>(
+      align_up(reinterpret_cast<uintptr_t>(raw + (size_t)seqs->B * cfg->P * cfg->M), 256));
   ds_lookup_kernel<<<seqs->B, 32 * cfg->P, 0, static_cast<cudaStream_t>(stream)>>>(
-      *ds, *seqs, kcfg(cfg), tab, lens, el, n_el, lk);
+      *ds, *seqs, kcfg(cfg), tab, lens, el, n_el, lk, raw, idx, ds_idx_cap(cfg->P, cfg->M));
   return cuda_check(cudaGetLastError(), "ds_lookup_kernel launch");
 }
 

@@ -110,18 +110,25 @@ __device__ uint64_t warp_search(const sssd_ds& ds, const uint32_t* pat, int p, u
       bracket_update(gt, q, olo, ohi);
     }
   }
+  // final round: probe every rank of [lo, hi) (w <= 32); the answer is the
+  // first probe satisfying pred, or hi when none does
   const uint64_t w = hi - lo;
   const uint64_t q = lo + lane;
   const int c = (uint64_t)lane < w ? cmp_rank(ds, q, pat, p) : 2;
-  const uint32_t ge = __ballot_sync(SSSD_FULL, c >= 0 && c != 2) | (w < 32 ? (1u << w) : 0u);
-  const uint32_t gt = __ballot_sync(SSSD_FULL, c > 0 && c != 2) | (w < 32 ? (1u << w) : 0u);
+  const uint32_t ge = __ballot_sync(SSSD_FULL, c >= 0 && c != 2);
+  const uint32_t gt = __ballot_sync(SSSD_FULL, c > 0 && c != 2);
   const uint32_t use = kUpper ? gt : ge;
   const uint64_t ans = lo + (use ? (uint64_t)(__ffs(use) - 1) : w);
   if (!kUpper) {
-    const int jt = gt ? __ffs(gt) - 1 : 32;
-    const uint64_t tb = lo + (uint64_t)min((uint64_t)jt, w);
-    ohi = min(ohi, tb);
-    olo = max(olo, tb);
+    // these probes cover [lo, hi) completely, so they pin the upper bound when
+    // one of them is past the pattern, else only raise its floor
+    if (gt) {
+      const uint64_t tb = lo + (uint64_t)(__ffs(gt) - 1);
+      ohi = min(ohi, tb);
+      olo = max(olo, tb);
+    } else {
+      olo = max(olo, lo + w);
+    }
   }
   return ans;
 }
@@ -149,6 +156,52 @@ __global__ void find_ranges_kernel(sssd_ds ds, const uint32_t* pat, const int64_
     lo_hi[2 * b] = (int64_t)(lo + ds.rank_base);
     lo_hi[2 * b + 1] = (int64_t)(hi + ds.rank_base);
   }
+}
+
+// --------------------------------------------------------------------------
+// block bitonic sort of element indices by (string, orig)
+// --------------------------------------------------------------------------
+
+struct ElemLess {
+  const sssd_elem* el;
+  const uint32_t* tok;
+  int n;
+  __device__ __forceinline__ bool operator()(uint32_t a, uint32_t b) const {
+    if (b >= (uint32_t)n) return a < (uint32_t)n || a < b;  // padding sorts last
+    if (a >= (uint32_t)n) return false;
+    const sssd_elem ea = el[a], eb = el[b];
+    const int r = cmp_str(tok + ea.off, el_len(ea.len_m), tok + eb.off, el_len(eb.len_m));
+    if (r != 0) return r < 0;
+    return ea.orig < eb.orig;
+  }
+};
+
+__device__ void block_sort_elems(const sssd_elem* src, sssd_elem* dst, const uint32_t* tok, int n,
+                                 uint32_t* idx) {
+  int n2 = 1;
+  while (n2 < n) n2 <<= 1;
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) idx[i] = i;
+  __syncthreads();
+  const ElemLess less{src, tok, n};
+  for (int k = 2; k <= n2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const uint32_t a = idx[i], bb = idx[ixj];
+          const bool up = (i & k) == 0;
+          const bool sw = up ? less(bb, a) : less(a, bb);
+          if (sw) {
+            idx[i] = bb;
+            idx[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[idx[i]];
+  __syncthreads();
 }
 
 // --------------------------------------------------------------------------
@@ -210,7 +263,8 @@ __device__ int gather_p(const sssd_ds& ds, const KCfg& c, int p, uint64_t lo, ui
 
 __global__ void __launch_bounds__(32 * SSSD_MAX_P)
     ds_lookup_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, uint32_t* ds_tab, uint8_t* ds_len,
-                     sssd_elem* ds_el, int32_t* ds_n, sssd_lookup_out lk) {
+                     sssd_elem* ds_el, int32_t* ds_n, sssd_lookup_out lk, sssd_elem* ds_raw,
+                     uint32_t* ds_idx, int64_t idx_cap) {
   const int b = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = lane_id();
   __shared__ uint32_t s_pat[SSSD_MAX_P];
@@ -278,12 +332,35 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P)
   }
   if (pmax == 0) pcut = 1;
 
-  // Merge the included per-p runs (each sorted by string, ties by SA order)
-  // into one array sorted by (string, list position).
+  // Merge the included per-p runs into one array sorted by (string, list
+  // position).  Without a separator every run is already sorted (SA order of
+  // the suffixes = order of their cut continuations), so each element's rank
+  // is its index plus binary-search counts in the other runs.  A separator
+  // breaks that (suffixes [x,0,..] < [x,sep,..] but cut strings [x] < [x,0,..])
+  // and the included strings are block-sorted instead.
   int before = 0;  // list position of run p's first element
   for (int q = pmax; q > p; --q)
     if (q >= pcut) before += s_cnt[q - 1];
-  if (p >= pcut && p <= pmax) {
+  if (c.has_sep) {
+    sssd_elem* raw = ds_raw + (size_t)b * c.P * c.M;
+    if (p >= pcut && p <= pmax) {
+      for (int i = lane; i < s_cnt[warp]; i += 32) {
+        sssd_elem e;
+        e.off = (uint32_t)(((size_t)(p - 1) * c.M + i) * c.BL);
+        e.orig = (uint32_t)(before + i);
+        e.len_m = (uint32_t)lens[(size_t)(p - 1) * c.M + i] | (255u << 8);
+        e.pad = 0;
+        raw[before + i] = e;
+      }
+    }
+    __syncthreads();
+    int n = 0;
+    for (int q = pcut; q <= pmax; ++q) n += s_cnt[q - 1];
+    if (n > 0) {
+      uint32_t* idx = (n <= SSSD_MAX_P * 32 * kRowStride) ? s_rows : ds_idx + (size_t)b * idx_cap;
+      block_sort_elems(raw, ds_el + (size_t)b * c.P * c.M, tab, n, idx);
+    }
+  } else if (p >= pcut && p <= pmax) {
     const int cnt = s_cnt[warp];
     for (int i = lane; i < cnt; i += 32) {
       const uint32_t* si = tab + ((size_t)(p - 1) * c.M + i) * c.BL;
@@ -320,52 +397,6 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P)
     const int q = threadIdx.x + 1;
     lk.n_conts[(size_t)b * c.P + threadIdx.x] = (q <= pmax && s_cnt[threadIdx.x] >= 0) ? s_cnt[threadIdx.x] : -1;
   }
-}
-
-// --------------------------------------------------------------------------
-// block bitonic sort of element indices by (string, orig)
-// --------------------------------------------------------------------------
-
-struct ElemLess {
-  const sssd_elem* el;
-  const uint32_t* tok;
-  int n;
-  __device__ __forceinline__ bool operator()(uint32_t a, uint32_t b) const {
-    if (b >= (uint32_t)n) return a < (uint32_t)n || a < b;  // padding sorts last
-    if (a >= (uint32_t)n) return false;
-    const sssd_elem ea = el[a], eb = el[b];
-    const int r = cmp_str(tok + ea.off, el_len(ea.len_m), tok + eb.off, el_len(eb.len_m));
-    if (r != 0) return r < 0;
-    return ea.orig < eb.orig;
-  }
-};
-
-__device__ void block_sort_elems(const sssd_elem* src, sssd_elem* dst, const uint32_t* tok, int n,
-                                 uint32_t* idx) {
-  int n2 = 1;
-  while (n2 < n) n2 <<= 1;
-  for (int i = threadIdx.x; i < n2; i += blockDim.x) idx[i] = i;
-  __syncthreads();
-  const ElemLess less{src, tok, n};
-  for (int k = 2; k <= n2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const uint32_t a = idx[i], bb = idx[ixj];
-          const bool up = (i & k) == 0;
-          const bool sw = up ? less(bb, a) : less(a, bb);
-          if (sw) {
-            idx[i] = bb;
-            idx[ixj] = a;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[idx[i]];
-  __syncthreads();
 }
 
 // --------------------------------------------------------------------------
@@ -490,8 +521,9 @@ struct Arena {
     }
     return pool + at;
   }
-  __device__ void release(Child* p, uint32_t n) {
-    if (p == slab + used - n) used -= n;
+  // return the unused tail [p + keep, p + n) of the latest slab allocation
+  __device__ void shrink(Child* p, uint32_t n, uint32_t keep) {
+    if (p + n == slab + used) used -= n - keep;
   }
 };
 
@@ -619,10 +651,8 @@ __device__ void expand(const SrcDesc& sd, uint32_t rank, uint32_t D, uint32_t a,
     }
   }
   if (c_open) emit(lane == 0, c_tok, c_cnt, c_first, c_start, z);
-  if (nch == 0) {
-    ar.release(ch, z - a);
-    return;
-  }
+  ar.shrink(ch, z - a, nch);
+  if (nch == 0) return;
   warp_best(bp, bf, bi);
   if (lane == 0) {
     Group g;

@@ -20,7 +20,15 @@ __global__ void find_ranges_kernel(sssd_ds ds, const uint32_t* pat, const int64_
 
 __global__ void ds_lookup_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, uint32_t* ds_tab,
                                  uint8_t* ds_len, sssd_elem* ds_el, int32_t* ds_n,
-                                 sssd_lookup_out lk);
+                                 sssd_lookup_out lk, sssd_elem* ds_raw, uint32_t* ds_idx,
+                                 int64_t idx_cap);
+
+// scratch of the datastore lookup when a separator forces a block sort
+inline int64_t ds_idx_cap(int P, int M) {
+  int64_t n = (int64_t)P * M, p2 = 1;
+  while (p2 < n) p2 <<= 1;
+  return p2;
+}
 __global__ void input_scan_kernel(sssd_seqs seqs, KCfg c, sssd_elem* raw, sssd_elem* sorted,
                                   int32_t* in_n, uint32_t* idx_ws, int64_t cap, int64_t cap2);
 __global__ void sort_sources_kernel(const uint32_t* tok, const sssd_elem* el,

@@ -196,8 +196,9 @@ def ds_paths(store: Datastore, prefixes: list[list[int]], c) -> list[list[list[i
     el = torch.zeros(B * P * M * 4, dtype=torch.int32, device=dev)
     n_el = torch.zeros(B, dtype=torch.int32, device=dev)
     view = store.c_view()
+    ws = _workspace(lib().sssd_ds_lookup_workspace(c, B), dev)
     check(lib().sssd_ds_lookup(view, seqs, c, ptr(tab), ptr(lens), ptr(el), ptr(n_el), None,
-                               stream_ptr(dev)))
+                               ptr(ws), ws.numel(), stream_ptr(dev)))
     tab_h = tab.cpu().numpy().view("<u4")
     el_h = el.cpu().numpy().view("<u4").reshape(B, P * M, 4)
     n_h = n_el.cpu().tolist()
