@@ -1,0 +1,418 @@
+"""Benchmark of the SSSD drafting hot path on B200 (BASELINE.json metric
+"draft lookups/s at B=64"; workload = configs[1] / cfg2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+One *step* = one batched propose (datastore range search + sampling +
+continuations, input-cache scan, best-first fusion, flatten + masks) over
+R independent B=64 batches of live 2048-token contexts (R*64 lookups) against
+a 100M-token phrase-model datastore resident in HBM, dec_len = 64.  `value` is
+whole-job lookups/s with inputs already in HBM (device time, CUDA events,
+max over ranks); `e2e` is the same through the public API with the contexts
+copied H2D from pinned memory and the drafts copied back D2H every step.
+Multi-GPU: every rank drafts its own R*64 requests against a replicated
+datastore (weak scaling, no data-path collective).
+
+`--impl reference` times the reference algorithm on the host cores (the CPU
+oracle port, process-parallel over all cores, one B=64 batch per step).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_TOKENS = 100_000_000
+VOCAB = 32000
+CTX = 2048
+BATCH = 64
+DEC_LEN = 64
+METRIC = "draft lookups/s at B=64"
+UNIT = "lookups/s"
+WORKLOAD = ("cfg2: batched lookup + draft-tree build (B=64 batches), 100M-token phrase-model "
+            "datastore, ctx 2048, dec_len 64, P=4 M=100 T=16")
+
+
+def peaks() -> tuple[float, str]:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def algorithmic_bytes(ranges: np.ndarray, p_cut: np.ndarray, sizes: np.ndarray, ctx_lens: np.ndarray,
+                      n: int, P: int, M: int) -> np.ndarray:
+    """SURVEY.md 8(d) sector-granular algorithmic bytes per lookup:
+    sum over evaluated p of 2*ceil(log2(n+1))*64 B (search probes: SA sector +
+    token sector) + s_p * 96 B (SA sector + 2 token sectors per sample)
+    + 4 * L_ctx (input scan) + 20 * s_q (outputs)."""
+    probes = 2 * int(np.ceil(np.log2(n + 1))) * 64
+    B = ranges.shape[0]
+    out = np.zeros(B, dtype=np.float64)
+    pmax = np.minimum(P, ctx_lens)
+    for b in range(B):
+        tot = 0.0
+        for p in range(int(pmax[b]), int(p_cut[b]) - 1, -1):
+            lo, hi = ranges[b, p - 1]
+            tot += probes + min(M, hi - lo) * 96
+        out[b] = tot + 4 * ctx_lens[b] + 20 * sizes[b]
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int) -> None:
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(n_gpus: int):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world: int) -> None:
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def allreduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_baseline(tokens: np.ndarray, sa: np.ndarray, ctxs: list, budget_s: float = 12.0) -> dict:
+    """The CPU oracle port, single thread, on a bounded sample of the step's contexts."""
+    from oracle import sssd_oracle as O
+
+    store = O.Store(tokens, sa)
+    cfg = O.Cfg(dec_len=DEC_LEN)
+    disc = cfg.disc()
+    t0 = time.perf_counter()
+    done = 0
+    for c in ctxs:
+        O.propose(store, c, cfg, disc=disc)
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{done} cfg2 lookups (oracle/sssd_oracle.py propose, 1 thread) on the same 100M datastore"}
+
+
+def run_ours(args) -> None:
+    import torch
+
+    import paper_2411_05894_b200 as G
+    from paper_2411_05894_b200 import workload
+
+    world, rank, local = dist_setup(args.gpus)
+    dev = torch.device("cuda", local)
+    R = args.batches
+    B = R * BATCH
+    # identical corpus on every rank (replicated datastore), distinct requests per rank
+    corpus = workload.corpus(N_TOKENS, VOCAB)
+    t0 = time.perf_counter()
+    ds = G.build(corpus, vocab_size=VOCAB, device=dev)
+    torch.cuda.synchronize(dev)
+    build_s = time.perf_counter() - t0
+    stream_all = workload.phrase_stream(B * CTX * world, VOCAB, workload.HELDOUT_SEED)
+    mine = stream_all[rank * B * CTX:(rank + 1) * B * CTX]
+    cfg = G.FusionConfig(dec_len=DEC_LEN)
+    eng = G.DraftEngine(ds, cfg, device=dev)
+
+    ctx_h = torch.from_numpy(mine.view(np.int32)).pin_memory()
+    seq = ctx_h.to(dev)
+    off = (torch.arange(B, dtype=torch.int64) * CTX).to(dev)
+    ln = torch.full((B,), CTX, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream(dev)
+
+    # correctness spot check + algorithmic bytes (untimed pass with lookup diagnostics)
+    out_lk = eng.propose(seq, off, ln, CTX, lookup=True)
+    eng.check_status()
+    lk_bytes = algorithmic_bytes(out_lk.ranges.cpu().numpy(), out_lk.p_cut.cpu().numpy(),
+                                 out_lk.size.cpu().numpy(), ln.cpu().numpy(), N_TOKENS, cfg.P, cfg.M)
+    bytes_per_step = float(lk_bytes.sum())
+    mean_size = float(out_lk.size.float().mean().item())
+
+    for _ in range(args.warmup):
+        eng.propose(seq, off, ln, CTX)
+    torch.cuda.synchronize(dev)
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush between timed iterations (outside the events)
+            evs[i][0].record(st)
+            eng.propose(seq, off, ln, CTX)
+            evs[i][1].record(st)
+        torch.cuda.synchronize(dev)
+    barrier(world)
+    eng.check_status()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms_local = float(np.sum(step_ms))
+    ms_total = allreduce_max(ms_local, world)
+    ms_per_step = ms_total / args.steps
+    value = B * world * args.steps / (ms_total / 1e3)
+
+    # per-kernel device time (profiled pass, outside the timed region)
+    prof = np.zeros(4)
+    for _ in range(3):
+        flush.zero_()
+        prof += np.asarray(eng.propose_profile(seq, off, ln, CTX))
+    prof /= 3
+    names = ["ds_lookup_kernel", "input_scan_kernel", "propose_setup_kernel", "draft_kernel"]
+    dom = int(np.argmax(prof))
+
+    # single-batch latency at B=64
+    seq64, off64, ln64 = seq, off[:BATCH], ln[:BATCH]
+    for _ in range(5):
+        eng.propose(seq64, off64, ln64, CTX)
+    lat = []
+    for _ in range(20):
+        flush.zero_()
+        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        eng.propose(seq64, off64, ln64, CTX)
+        b_.record(st)
+        torch.cuda.synchronize(dev)
+        lat.append(a.elapsed_time(b_))
+    lat_ms = float(np.median(lat))
+
+    # e2e through the public API with host buffers (H2D contexts, D2H drafts)
+    S, W = eng.S, eng.W
+    h_size = torch.empty(B, dtype=torch.int32).pin_memory()
+    h_tok = torch.empty((B, S), dtype=torch.int32).pin_memory()
+    h_par = torch.empty((B, S), dtype=torch.int32).pin_memory()
+    h_dep = torch.empty((B, S), dtype=torch.int32).pin_memory()
+    h_mask = torch.empty((B, S, W), dtype=torch.int64).pin_memory()
+    seq_e = torch.empty_like(seq)
+    h2d = ctx_h.numel() * 4
+    d2h = B * 4 + 3 * B * S * 4 + B * S * W * 8
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        seq_e.copy_(ctx_h, non_blocking=True)
+        o = eng.propose(seq_e, off, ln, CTX)
+        h_size.copy_(o.size, non_blocking=True)
+        h_tok.copy_(o.tokens, non_blocking=True)
+        h_par.copy_(o.parents, non_blocking=True)
+        h_dep.copy_(o.depths, non_blocking=True)
+        h_mask.copy_(o.mask, non_blocking=True)
+        b_.record(st)
+        torch.cuda.synchronize(dev)
+        if i >= args.warmup:
+            e2e_ms.append(a.elapsed_time(b_))
+    e2e_total = allreduce_max(float(np.sum(e2e_ms)), world)
+    e2e_value = B * world * args.steps / (e2e_total / 1e3)
+
+    peak, peak_src = peaks()
+    achieved = bytes_per_step / (ms_per_step / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_step")
+        except Exception:
+            traffic = None
+
+    base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        tokens_h = corpus
+        sa_h = ds.suffix_index
+        ctxs = [mine[i * CTX:(i + 1) * CTX].tolist() for i in range(min(B, 256))]
+        base = cpu_baseline(tokens_h, sa_h, ctxs)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32 tokens / f64 fusion keys",
+            "data": "synthetic (seeded phrase-model corpus + held-out contexts, SURVEY App. B)",
+            "config": {"workload": WORKLOAD, "batch": BATCH, "batches_per_step": R, "lookups_per_step": B,
+                       "n_tokens": N_TOKENS, "vocab": VOCAB, "ctx": CTX, "dec_len": DEC_LEN,
+                       "parallelism": f"replicated datastore x{world}, requests partitioned",
+                       "l2": "inputs > L2 (6.4 GB suffix rows, 134 MB contexts) + 256 MB flush between steps",
+                       "b64_latency_ms": round(lat_ms, 4), "b64_lookups_per_s": round(BATCH / lat_ms * 1e3, 1),
+                       "mean_draft_size": round(mean_size, 2), "gpu_sa_build_s": round(build_s, 2)},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "scope": "whole propose step (SURVEY 8(d) algorithmic bytes of lookup + tree build)",
+                         "algorithmic_bytes_per_lookup": round(bytes_per_step / B, 1), "peak_source": peak_src,
+                         "kernel_ms": {n: round(float(x), 4) for n, x in zip(names, prof)},
+                         "dominant_kernel": names[dom],
+                         "dominant_share": round(float(prof[dom] / prof.sum()), 3)},
+            "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": 4 * args.steps,
+            "clocks": clk.summary(),
+        }
+        if base is not None:
+            line["cpu_baseline"] = base
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def _ref_worker(args):
+    from oracle import sssd_oracle as O
+
+    ctxs = args
+    cfg = O.Cfg(dec_len=DEC_LEN)
+    disc = cfg.disc()
+    for c in ctxs:
+        O.propose(_REF_STORE, c, cfg, disc=disc)
+    return len(ctxs)
+
+
+_REF_STORE = None
+
+
+def run_reference(args) -> None:
+    """Reference CPU path: the oracle port of the reference algorithm, fork-parallel
+    over all host cores, one B=64 batch per step."""
+    global _REF_STORE
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    from oracle import sssd_oracle as O
+    from paper_2411_05894_b200 import workload
+
+    corpus = workload.corpus(N_TOKENS, VOCAB)
+    cache = os.environ.get("SSSD_REF_SA_CACHE", "/tmp/sssd_sa100m.npy")
+    if os.path.exists(cache):
+        sa = np.load(cache)
+    else:
+        sa = O.suffix_array(corpus).astype(np.uint32)
+        try:
+            np.save(cache, sa)
+        except OSError:
+            pass
+    _REF_STORE = O.Store(corpus, sa)
+    stream = workload.phrase_stream(BATCH * CTX, VOCAB, workload.HELDOUT_SEED)
+    ctxs = [stream[i * CTX:(i + 1) * CTX].tolist() for i in range(BATCH)]
+    cores = os.cpu_count() or 1
+    chunks = [ctxs[i::cores] for i in range(cores)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        for _ in range(args.warmup):
+            pool.map(_ref_worker, chunks)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            pool.map(_ref_worker, chunks)
+        dt = time.perf_counter() - t0
+    value = BATCH * args.steps / dt
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 tokens / f64 fusion keys",
+            "data": "synthetic (seeded phrase-model corpus + held-out contexts, SURVEY App. B)",
+            "config": {"workload": WORKLOAD, "batch": BATCH, "batches_per_step": 1, "n_tokens": N_TOKENS,
+                       "ctx": CTX, "dec_len": DEC_LEN},
+            "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"one B=64 batch per step, oracle port fork-parallel over {cores} processes"},
+            "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batches", type=int, default=256, help="independent B=64 batches per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

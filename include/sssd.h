@@ -172,6 +172,13 @@ size_t sssd_input_scan_workspace(int32_t B, int32_t max_len);
 int sssd_input_scan(const sssd_seqs* seqs, const sssd_cfg* cfg, sssd_elem* el, int32_t* n_el,
                     void* workspace, size_t workspace_bytes, void* stream);
 
+/* sssd_propose with CUDA events between its launches; synchronises and writes
+ * the device time of each stage: [0] ds_lookup_kernel, [1] input_scan_kernel,
+ * [2] propose_setup_kernel, [3] draft_kernel (ms).  Measurement aid only. */
+int sssd_propose_profile(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
+                         const sssd_draft_out* out, void* workspace, size_t workspace_bytes,
+                         void* stream, float* stage_ms);
+
 /* Fusion of caller-provided source trees (merge fusion.py:209-261 + flatten).
  * Each tree is given as its multiset of root-to-end paths in DFS order (first
  * appearance order = the tree's child order): paths of request b / source s

@@ -243,9 +243,32 @@ size_t sssd_propose_workspace(const sssd_cfg* cfg, int32_t B, int32_t max_len) {
   return carve_propose(nullptr, cfg, B, max_len).bytes;
 }
 
+static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
+                        const sssd_draft_out* out, const sssd_lookup_out* lookup, void* workspace,
+                        size_t workspace_bytes, void* stream, cudaEvent_t* ev);
+
 int sssd_propose(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
                  const sssd_draft_out* out, const sssd_lookup_out* lookup, void* workspace,
                  size_t workspace_bytes, void* stream) {
+  return propose_impl(ds, seqs, cfg, out, lookup, workspace, workspace_bytes, stream, nullptr);
+}
+
+int sssd_propose_profile(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
+                         const sssd_draft_out* out, void* workspace, size_t workspace_bytes,
+                         void* stream, float* stage_ms) {
+  cudaEvent_t ev[5];
+  for (auto& e : ev) cudaEventCreate(&e);
+  int rc = propose_impl(ds, seqs, cfg, out, nullptr, workspace, workspace_bytes, stream, ev);
+  if (!rc) rc = cuda_check(cudaEventSynchronize(ev[4]), "profile sync");
+  if (!rc)
+    for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&stage_ms[i], ev[i], ev[i + 1]);
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
+}
+
+static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
+                        const sssd_draft_out* out, const sssd_lookup_out* lookup, void* workspace,
+                        size_t workspace_bytes, void* stream, cudaEvent_t* ev) {
   int rc = validate_cfg(cfg);
   if (rc) return rc;
   if ((rc = validate_out(out))) return rc;
@@ -267,19 +290,25 @@ int sssd_propose(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
   sssd_lookup_out lk{};
   if (lookup) lk = *lookup;
   if ((rc = cuda_check(cudaMemsetAsync(w.d.cursor, 0, 16, st), "memset status"))) return rc;
+  if (ev) cudaEventRecord(ev[0], st);
   if (cfg->use_datastore) {
     ds_lookup_kernel<<<B, 32 * cfg->P, 0, st>>>(*ds, *seqs, k, w.ds_tab, w.ds_len, w.ds_el, w.ds_n, lk,
                                                  w.ds_raw, w.ds_idx, w.ds_idx_cap);
     if ((rc = cuda_check(cudaGetLastError(), "ds_lookup_kernel launch"))) return rc;
   }
+  if (ev) cudaEventRecord(ev[1], st);
   if (cfg->use_input) {
     input_scan_kernel<<<B, 256, 0, st>>>(*seqs, k, w.in_raw, w.in_el, w.in_n, w.idx, w.cap, w.cap2);
     if ((rc = cuda_check(cudaGetLastError(), "input_scan_kernel launch"))) return rc;
   }
+  if (ev) cudaEventRecord(ev[2], st);
   propose_setup_kernel<<<(B + 127) / 128, 128, 0, st>>>(*seqs, k, w.ds_el, w.ds_tab, w.ds_n, w.in_el,
                                                           w.in_n, w.cap, w.d.desc, w.d.root);
   if ((rc = cuda_check(cudaGetLastError(), "propose_setup_kernel launch"))) return rc;
-  return launch_draft(w.d, k, B, out, st);
+  if (ev) cudaEventRecord(ev[3], st);
+  rc = launch_draft(w.d, k, B, out, st);
+  if (ev) cudaEventRecord(ev[4], st);
+  return rc;
 }
 
 // Returns the device status word of the last propose / merge that used this

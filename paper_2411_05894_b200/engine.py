@@ -113,6 +113,20 @@ class DraftEngine:
         check(lib().sssd_propose(ds, seqs, self.c, d_out, lk, ptr(ws), ws.numel(), stream_ptr(self.device)))
         return out
 
+    def propose_profile(self, seq, seq_off, seq_len, max_len) -> list[float]:
+        """Device ms of [ds_lookup, input_scan, setup, draft] for one propose (synchronises)."""
+        import ctypes as C
+
+        B = int(seq_len.shape[0])
+        out = self.outputs(B)
+        ws = self.workspace(B, max_len)
+        seqs = _lib.Seqs(ptr(seq), ptr(seq_off), ptr(seq_len), B, int(max_len))
+        d_out = _lib.DraftOut(ptr(out.size), ptr(out.tokens), ptr(out.parents), ptr(out.depths), ptr(out.mask))
+        ds = self.store.c_view() if (self.use_datastore and self.store is not None) else self._null_ds
+        ms = (C.c_float * 4)()
+        check(lib().sssd_propose_profile(ds, seqs, self.c, d_out, ptr(ws), ws.numel(), stream_ptr(self.device), ms))
+        return list(ms)
+
     def check_status(self) -> None:
         """Synchronise and raise if the device fusion arena overflowed."""
         if self._ws is not None:
