@@ -88,6 +88,8 @@ static KCfg kcfg(const sssd_cfg* c) {
 constexpr uint32_t kSlabChildren = 2048;
 
 struct DraftWs {
+  Group* gover;
+  int gover_cap;
   SrcDesc* desc;
   uint32_t* root;
   Child* slabs;
@@ -101,8 +103,10 @@ struct DraftWs {
 // shared overflow pool.  An expansion reserves its element-range size and
 // returns the unused tail, so the slab holds the typical request; long
 // contexts (huge input-tree roots) spill into the pool, sized by max_len.
-static DraftWs carve_draft(Carver& cv, int P, int B, int64_t max_len = 0) {
+static DraftWs carve_draft(Carver& cv, int P, int S, int B, int64_t max_len = 0) {
   DraftWs d;
+  d.gover_cap = draft_group_overflow(P, S);
+  d.gover = reinterpret_cast<Group*>(cv.take<uint8_t>((size_t)B * (d.gover_cap ? d.gover_cap : 1) * kGroupBytes));
   d.desc = cv.take<SrcDesc>((size_t)B * (P + 1));
   d.root = cv.take<uint32_t>((size_t)B);
   d.slabs = reinterpret_cast<Child*>(cv.take<uint8_t>((size_t)B * kSlabChildren * kChildBytes));
@@ -151,7 +155,7 @@ static PropWs carve_propose(uint8_t* base, const sssd_cfg* c, int B, int max_len
   w.in_el = cv.take<sssd_elem>((size_t)B * w.cap);
   w.in_n = cv.take<int32_t>((size_t)B);
   w.idx = cv.take<uint32_t>((size_t)B * (w.cap2 ? w.cap2 : 1));
-  w.d = carve_draft(cv, c->P, B, w.cap);
+  w.d = carve_draft(cv, c->P, c->dec_len, B, w.cap);
   w.bytes = align_up(cv.off, 256);
   return w;
 }
@@ -207,7 +211,7 @@ static int launch_draft(const DraftWs& d, const KCfg& k, int B, const sssd_draft
   cudaError_t e = cudaFuncSetAttribute(draft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return cuda_check(e, "draft_kernel smem attribute");
   draft_kernel<<<B, 32, smem, st>>>(d.desc, d.root, k, d.slabs, kSlabChildren, d.pool, d.cursor,
-                                    d.pool_cap, d.err, *out);
+                                    d.pool_cap, d.err, d.gover, d.gover_cap, *out);
   return cuda_check(cudaGetLastError(), "draft_kernel launch");
 }
 
@@ -320,7 +324,7 @@ int sssd_workspace_status(const sssd_cfg* cfg, int32_t B, int32_t max_len, const
     Carver cv{nullptr, 0};
     cv.take<sssd_elem>((size_t)(total_elems > 0 ? total_elems : 1));
     cv.take<uint32_t>((size_t)2 * (total_elems > 0 ? total_elems : 1));
-    DraftWs d = carve_draft(cv, cfg->P, B);
+    DraftWs d = carve_draft(cv, cfg->P, cfg->dec_len, B);
     off = reinterpret_cast<size_t>(d.err);
   } else {
     PropWs w = carve_propose(nullptr, cfg, B, max_len);
@@ -341,7 +345,7 @@ size_t sssd_merge_workspace(const sssd_cfg* cfg, int32_t B, int64_t total_elems)
   Carver cv{nullptr, 0};
   cv.take<sssd_elem>((size_t)(total_elems > 0 ? total_elems : 1));
   cv.take<uint32_t>((size_t)2 * (total_elems > 0 ? total_elems : 1));
-  carve_draft(cv, cfg->P, B);
+  carve_draft(cv, cfg->P, cfg->dec_len, B);
   return align_up(cv.off, 256);
 }
 
@@ -358,7 +362,7 @@ int sssd_merge(const uint32_t* tok, const sssd_elem* el, const int64_t* el_off,
   const size_t te = (size_t)(total_elems > 0 ? total_elems : 1);
   sssd_elem* sorted = cv.take<sssd_elem>(te);
   uint32_t* idx = cv.take<uint32_t>(2 * te);
-  DraftWs d = carve_draft(cv, cfg->P, B);
+  DraftWs d = carve_draft(cv, cfg->P, cfg->dec_len, B);
   const size_t need = align_up(cv.off, 256);
   if (!workspace || workspace_bytes < need)
     return fail(SSSD_E_WORKSPACE, "merge needs %zu workspace bytes, got %zu", need, workspace_bytes);

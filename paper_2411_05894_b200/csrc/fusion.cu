@@ -1,0 +1,459 @@
+// K5: best-first fusion + DFS flatten for SSSD drafts (sm_100a).
+// Replaces ref fusion.py:209-261 (merge) and draft.py:67-86 (flatten); the
+// tie-break and float semantics follow SURVEY.md A.5 / A.6 exactly.
+//
+// One warp per request.  Source tries are never materialised: a trie node is
+// a range [a, z) of its source's element array sorted by (string, insertion
+// order), so a node's children are the runs of equal token at its depth.
+//
+// Frontier.  The reference heap orders candidates by (-priority, depth, rank,
+// ticket).  Children pushed by one pop share depth, rank and parent and hold
+// consecutive tickets, so the frontier is kept as *sibling groups*: the heap
+// minimum is the minimum over group heads of (-priority, depth, rank, group
+// creation order), and inside a group candidates pop in (priority desc,
+// first-appearance asc) order.  Keys are compared as 96-bit integers
+// (~bits(priority) is monotone for priorities >= 0) with three REDUX
+// (__reduce_min_sync) steps instead of shuffle trees; groups of <= 32
+// children are stored in pop order at creation so advancing a head is O(1).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "propose.cuh"
+
+namespace sssd {
+
+struct Child {  // one candidate (32 B, global arena)
+  double pp;       // path probability (ref fusion.py:244,259)
+  uint32_t first;  // first-appearance position = reference child order
+  uint32_t count;  // node count in its source trie
+  uint32_t token;
+  uint32_t a, b;   // element range of the candidate node in the source array
+  uint32_t pad;
+};
+
+struct Group {  // sibling group header (32 B; shared memory, global overflow)
+  uint32_t khi, klo;  // head key = ~bits(priority of the head child)
+  Child* ch;
+  uint32_t head;  // head child index; == nch when exhausted
+  uint32_t nch;
+  uint32_t meta;      // depth << 26 | rank << 22 | creation sequence
+  uint16_t dparent;   // draft node the children hang under
+  uint16_t sorted;    // children stored in pop order
+};
+static_assert(sizeof(Child) == kChildBytes, "Child layout");
+static_assert(sizeof(Group) == kGroupBytes, "Group layout");
+
+__device__ __forceinline__ uint32_t g_depth(uint32_t meta) { return meta >> 26; }
+__device__ __forceinline__ uint32_t g_rank(uint32_t meta) { return (meta >> 22) & 0xf; }
+
+__device__ __forceinline__ void prio_key(double pr, uint32_t& hi, uint32_t& lo) {
+  const uint64_t k = ~(uint64_t)__double_as_longlong(pr);
+  hi = (uint32_t)(k >> 32);
+  lo = (uint32_t)k;
+}
+
+__device__ __forceinline__ bool key_less(uint32_t ah, uint32_t al, uint32_t at, uint32_t bh,
+                                         uint32_t bl, uint32_t bt) {
+  return ah < bh || (ah == bh && (al < bl || (al == bl && at < bt)));
+}
+
+// Lane holding the minimum (hi, lo, tie) among valid lanes (ties are unique),
+// or -1 when no lane is valid.
+__device__ __forceinline__ int warp_argmin3(bool valid, uint32_t hi, uint32_t lo, uint32_t tie) {
+  if (!__ballot_sync(SSSD_FULL, valid)) return -1;
+  if (!valid) hi = lo = tie = 0xffffffffu;
+  const uint32_t mh = __reduce_min_sync(SSSD_FULL, hi);
+  bool c = valid && hi == mh;
+  const uint32_t ml = __reduce_min_sync(SSSD_FULL, c ? lo : 0xffffffffu);
+  c = c && lo == ml;
+  const uint32_t mt = __reduce_min_sync(SSSD_FULL, c ? tie : 0xffffffffu);
+  c = c && tie == mt;
+  return __ffs(__ballot_sync(SSSD_FULL, c)) - 1;
+}
+
+struct Arena {
+  Child* slab;
+  uint32_t used, cap;
+  Child* pool;
+  unsigned long long* cursor;
+  uint64_t pool_cap;
+  int32_t* err;
+  __device__ Child* alloc(uint32_t n) {  // warp-uniform
+    if (used + n <= cap) {
+      Child* p = slab + used;
+      used += n;
+      return p;
+    }
+    unsigned long long at = 0;
+    if (lane_id() == 0) at = atomicAdd(cursor, (unsigned long long)n);
+    at = __shfl_sync(SSSD_FULL, at, 0);
+    if (at + n > pool_cap) {
+      if (lane_id() == 0) atomicExch(err, SSSD_E_WORKSPACE);
+      return nullptr;
+    }
+    return pool + at;
+  }
+  // give back the unused tail [p + keep, p + n) of the latest slab allocation
+  __device__ void shrink(Child* p, uint32_t n, uint32_t keep) {
+    if (p + n == slab + used) used -= n - keep;
+  }
+};
+
+struct Frontier {
+  Group* sg;  // first kGroupSmem groups (shared memory)
+  Group* gg;  // overflow groups (global)
+  int G;
+  __device__ __forceinline__ Group* at(int i) const { return i < kGroupSmem ? sg + i : gg + (i - kGroupSmem); }
+};
+
+// Expand the node covering [a, z) of source sd at depth D-1 into the group of
+// its depth-D children (runs of equal token index D-1).  seed: the node is the
+// source root (path prob = count / root_count, ref fusion.py:244); otherwise
+// path prob = ppar * (count / pcount) (ref fusion.py:259).
+__device__ void expand(const SrcDesc& sd, uint32_t rank, uint32_t D, uint32_t a, uint32_t z,
+                       bool seed, double ppar, uint32_t pcount, uint32_t dparent, double disc,
+                       Frontier& fr, Arena& ar) {
+  const int lane = lane_id();
+  const double dpc = (double)pcount;
+  const uint32_t n = z - a;
+  Child* ch = nullptr;
+  uint32_t nch = 0;
+
+  if (n == 1) {  // single element: at most one child, count 1
+    const sssd_elem e = sd.el[a];
+    if (el_len(e.len_m) < D || (int)el_m(e.len_m) < sd.thr) return;
+    ch = ar.alloc(1);
+    if (!ch) return;
+    if (lane == 0) {
+      const double ratio = __ddiv_rn(1.0, dpc);
+      Child c;
+      c.pp = seed ? ratio : __dmul_rn(ppar, ratio);
+      c.first = e.orig;
+      c.count = 1;
+      c.token = sd.tok[e.off + D - 1];
+      c.a = a;
+      c.b = z;
+      c.pad = 0;
+      ch[0] = c;
+    }
+    nch = 1;
+  } else {
+    ch = ar.alloc(n);
+    if (!ch) return;
+    auto emit = [&](bool pred, uint32_t tok, uint32_t cnt, uint32_t first, uint32_t s, uint32_t e) {
+      const bool live = pred && cnt > 0;
+      const uint32_t bal = __ballot_sync(SSSD_FULL, live);
+      if (live) {
+        const double ratio = __ddiv_rn((double)cnt, dpc);
+        Child c;
+        c.pp = seed ? ratio : __dmul_rn(ppar, ratio);
+        c.first = first;
+        c.count = cnt;
+        c.token = tok;
+        c.a = s;
+        c.b = e;
+        c.pad = 0;
+        ch[nch + __popc(bal & lanemask_lt())] = c;
+      }
+      nch += __popc(bal);
+    };
+    bool c_open = false;
+    uint32_t c_tok = 0, c_cnt = 0, c_first = 0xffffffffu, c_start = 0;
+    for (uint32_t base = a; base < z; base += 32) {
+      const uint32_t i = base + lane;
+      bool has = false;
+      uint32_t t = 0, orig = 0xffffffffu;
+      bool w = false;
+      if (i < z) {
+        const sssd_elem e = sd.el[i];
+        if (el_len(e.len_m) >= D) {
+          has = true;
+          t = sd.tok[e.off + D - 1];
+          if ((int)el_m(e.len_m) >= sd.thr) {
+            w = true;
+            orig = e.orig;
+          }
+        }
+      }
+      const uint32_t hasm = __ballot_sync(SSSD_FULL, has);
+      if (!hasm) continue;
+      // runs of equal token are contiguous (the range is sorted); lanes without
+      // a token at this depth get a private key
+      const unsigned long long key = has ? (0x100000000ull | t) : (0x200000000ull + (unsigned)lane);
+      const uint32_t gm = __match_any_sync(SSSD_FULL, key);
+      const uint32_t wm = __ballot_sync(SSSD_FULL, w);
+      uint32_t cnt = __popc(gm & wm);
+      uint32_t fm = __reduce_min_sync(gm, orig);
+      const int lo_l = __ffs(gm) - 1, hi_l = 31 - __clz(gm);
+      const uint32_t t0 = __shfl_sync(SSSD_FULL, t, 0);
+      if (c_open && !((hasm & 1u) && t0 == c_tok)) {  // the carried run ended at the chunk edge
+        emit(lane == 0, c_tok, c_cnt, c_first, c_start, base);
+        c_open = false;
+      }
+      uint32_t start = base + lo_l;
+      if (c_open && has && lo_l == 0) {  // continuation of the carried run
+        cnt += c_cnt;
+        fm = min(fm, c_first);
+        start = c_start;
+      }
+      const bool to_next = has && hi_l == 31 && base + 32 < z;
+      emit(has && lane == hi_l && !to_next, t, cnt, fm, start, base + hi_l + 1);
+      if (__ballot_sync(SSSD_FULL, lane == 31 && to_next)) {
+        c_tok = __shfl_sync(SSSD_FULL, t, 31);
+        c_cnt = __shfl_sync(SSSD_FULL, cnt, 31);
+        c_first = __shfl_sync(SSSD_FULL, fm, 31);
+        c_start = __shfl_sync(SSSD_FULL, start, 31);
+        c_open = true;
+      } else {
+        c_open = false;
+      }
+    }
+    if (c_open) emit(lane == 0, c_tok, c_cnt, c_first, c_start, z);
+    ar.shrink(ch, n, nch);
+    if (nch == 0) return;
+  }
+  __syncwarp();
+
+  uint32_t head = 0, kh = 0xffffffffu, kl = 0xffffffffu;
+  uint16_t sorted = 1;
+  if (nch <= 32) {
+    // store the group in pop order: rank of each child by (priority desc, first asc)
+    const bool v = (uint32_t)lane < nch;
+    Child cc;
+    uint32_t h = 0xffffffffu, l = 0xffffffffu, f = 0xffffffffu;
+    if (v) {
+      cc = ch[lane];
+      prio_key(__dmul_rn(cc.pp, disc), h, l);
+      f = cc.first;
+    }
+    uint32_t r = 0;
+    for (uint32_t j = 0; j < nch; ++j) {
+      const uint32_t jh = __shfl_sync(SSSD_FULL, h, j), jl = __shfl_sync(SSSD_FULL, l, j),
+                     jf = __shfl_sync(SSSD_FULL, f, j);
+      r += key_less(jh, jl, jf, h, l, f) ? 1u : 0u;
+    }
+    __syncwarp();
+    if (v) ch[r] = cc;
+    const int src = __ffs(__ballot_sync(SSSD_FULL, v && r == 0)) - 1;
+    kh = __shfl_sync(SSSD_FULL, h, src);
+    kl = __shfl_sync(SSSD_FULL, l, src);
+    __syncwarp();
+  } else {
+    // large group: keep emission order, find heads by scanning
+    sorted = 0;
+    uint32_t bh = 0xffffffffu, bl = 0xffffffffu, bf = 0xffffffffu, bi = 0;
+    bool bv = false;
+    for (uint32_t k = lane; k < nch; k += 32) {
+      const Child c = ch[k];
+      uint32_t h, l;
+      prio_key(__dmul_rn(c.pp, disc), h, l);
+      if (!bv || key_less(h, l, c.first, bh, bl, bf)) {
+        bh = h;
+        bl = l;
+        bf = c.first;
+        bi = k;
+        bv = true;
+      }
+    }
+    const int win = warp_argmin3(bv, bh, bl, bf);
+    head = __shfl_sync(SSSD_FULL, bi, win);
+    kh = __shfl_sync(SSSD_FULL, bh, win);
+    kl = __shfl_sync(SSSD_FULL, bl, win);
+  }
+  if (lane == 0) {
+    Group g;
+    g.khi = kh;
+    g.klo = kl;
+    g.ch = ch;
+    g.head = head;
+    g.nch = nch;
+    g.meta = (D << 26) | (rank << 22) | (uint32_t)fr.G;
+    g.dparent = (uint16_t)dparent;
+    g.sorted = sorted;
+    *fr.at(fr.G) = g;
+  }
+  ++fr.G;
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(32)
+    draft_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, Child* slabs,
+                 uint32_t slab_cap, Child* pool, unsigned long long* cursor, uint64_t pool_cap,
+                 int32_t* err, Group* gover, int gover_cap, sssd_draft_out out) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int b = blockIdx.x;
+  const int lane = lane_id();
+  const int S = c.S;
+  const int W = (S + 63) >> 6;
+  const int Gs = min(draft_max_groups(c.P, S), kGroupSmem);
+  Group* sg = reinterpret_cast<Group*>(smem);
+  uint32_t* d_tok = reinterpret_cast<uint32_t*>(sg + Gs);
+  int16_t* d_par = reinterpret_cast<int16_t*>(d_tok + S);
+  int16_t* d_fc = d_par + S;  // first child
+  int16_t* d_lc = d_fc + S;   // last child
+  int16_t* d_ps = d_lc + S;   // previous sibling
+  int16_t* d_dep = d_ps + S;
+  int16_t* pre = d_dep + S;   // pre-order position -> node
+  int16_t* n2p = pre + S;     // node -> pre-order position
+  int16_t* stk = n2p + S;
+
+  Arena ar{slabs + (size_t)b * slab_cap, 0, slab_cap, pool, cursor, pool_cap, err};
+  Frontier fr{sg, gover + (size_t)b * gover_cap, 0};
+  if (lane == 0) {
+    d_tok[0] = root_tok[b];
+    d_par[0] = -1;
+    d_fc[0] = d_lc[0] = d_ps[0] = -1;
+    d_dep[0] = 0;
+  }
+  __syncwarp();
+  int size = 1;
+  const SrcDesc* sds = desc + (size_t)b * (c.P + 1);
+
+  // seeds: datastore (rank 0), then input trees p = n_trees..1 (rank P-p+1)
+  if (S > 1) {
+    for (int rk = 0; rk <= c.P; ++rk) {
+      const SrcDesc sd = sds[rk];
+      if (sd.n <= 0) continue;
+      uint32_t rc = 0;
+      for (int i = lane; i < sd.n; i += 32) rc += (int)el_m(sd.el[i].len_m) >= sd.thr ? 1u : 0u;
+      rc = __reduce_add_sync(SSSD_FULL, rc);
+      if (rc == 0) continue;
+      expand(sd, rk, 1, 0, sd.n, true, 0.0, rc, 0, c.disc[rk * c.disc_stride + 1], fr, ar);
+    }
+  }
+
+  while (size < S) {
+    // pop: minimum over group heads of (~prio, depth|rank|sequence)
+    bool v = false;
+    uint32_t bh = 0, bl = 0, bm = 0;
+    int bg = -1;
+    for (int gi = lane; gi < fr.G; gi += 32) {
+      const Group* g = fr.at(gi);
+      if (g->head >= g->nch) continue;
+      const uint32_t h = g->khi, l = g->klo, m = g->meta;
+      if (!v || key_less(h, l, m, bh, bl, bm)) {
+        bh = h;
+        bl = l;
+        bm = m;
+        bg = gi;
+        v = true;
+      }
+    }
+    const int win = warp_argmin3(v, bh, bl, bm);
+    if (win < 0) break;
+    const int gi = __shfl_sync(SSSD_FULL, bg, win);
+    Group* gp = fr.at(gi);
+    const Group g = *gp;
+    const Child h = g.ch[g.head];
+    const uint32_t D = g_depth(g.meta), rk = g_rank(g.meta);
+    const double dsc = c.disc[rk * c.disc_stride + D];
+
+    // draft insert: an existing (parent, token) keeps the first node (ref fusion.py:185-198)
+    const int par = g.dparent;
+    int nid = -1;
+    if (d_fc[par] >= 0) {
+      for (int i0 = 1; i0 < size; i0 += 32) {
+        const int i = i0 + lane;
+        const uint32_t hb = __ballot_sync(SSSD_FULL, i < size && d_par[i] == par && d_tok[i] == h.token);
+        if (hb) {
+          nid = i0 + __ffs(hb) - 1;
+          break;
+        }
+      }
+    }
+    if (nid < 0) {
+      nid = size++;
+      if (lane == 0) {
+        d_tok[nid] = h.token;
+        d_par[nid] = (int16_t)par;
+        d_fc[nid] = d_lc[nid] = -1;
+        d_dep[nid] = (int16_t)(d_dep[par] + 1);
+        d_ps[nid] = d_lc[par];
+        if (d_lc[par] < 0) d_fc[par] = (int16_t)nid;
+        d_lc[par] = (int16_t)nid;
+      }
+    }
+
+    // advance the popped group's head
+    {
+      uint32_t nh = g.nch, kh = 0xffffffffu, kl = 0xffffffffu;
+      if (g.sorted) {
+        nh = g.head + 1;
+        if (nh < g.nch) prio_key(__dmul_rn(g.ch[nh].pp, dsc), kh, kl);
+      } else {
+        uint32_t bh2 = 0xffffffffu, bl2 = 0xffffffffu, bf2 = 0xffffffffu, bi2 = 0;
+        bool bv2 = false;
+        for (uint32_t k = lane; k < g.nch; k += 32) {
+          const Child ck = g.ch[k];
+          uint32_t hh, ll;
+          prio_key(__dmul_rn(ck.pp, dsc), hh, ll);
+          if (key_less(g.khi, g.klo, h.first, hh, ll, ck.first) &&
+              (!bv2 || key_less(hh, ll, ck.first, bh2, bl2, bf2))) {
+            bh2 = hh;
+            bl2 = ll;
+            bf2 = ck.first;
+            bi2 = k;
+            bv2 = true;
+          }
+        }
+        const int w2 = warp_argmin3(bv2, bh2, bl2, bf2);
+        if (w2 >= 0) {
+          nh = __shfl_sync(SSSD_FULL, bi2, w2);
+          kh = __shfl_sync(SSSD_FULL, bh2, w2);
+          kl = __shfl_sync(SSSD_FULL, bl2, w2);
+        }
+      }
+      if (lane == 0) {
+        gp->head = nh;
+        gp->khi = kh;
+        gp->klo = kl;
+      }
+    }
+    __syncwarp();
+    // push the popped source node's children (ref fusion.py:258-259)
+    if (D + 1 < (uint32_t)c.disc_stride)
+      expand(sds[rk], rk, D + 1, h.a, h.b, false, h.pp, h.count, (uint32_t)nid,
+             c.disc[rk * c.disc_stride + D + 1], fr, ar);
+  }
+
+  // DFS pre-order flatten, children in insertion order (ref draft.py:67-86)
+  if (lane == 0) {
+    int sp = 0, k = 0;
+    stk[sp++] = 0;
+    while (sp > 0) {
+      const int nid = stk[--sp];
+      pre[k] = (int16_t)nid;
+      n2p[nid] = (int16_t)k;
+      ++k;
+      for (int ch = d_lc[nid]; ch >= 0; ch = d_ps[ch]) stk[sp++] = (int16_t)ch;  // reverse push
+    }
+  }
+  __syncwarp();
+  uint32_t* o_tok = out.tokens + (size_t)b * S;
+  int32_t* o_par = out.parents + (size_t)b * S;
+  int32_t* o_dep = out.depths + (size_t)b * S;
+  uint64_t* o_mask = out.mask + (size_t)b * S * W;
+  for (int k = lane; k < S; k += 32) {
+    if (k < size) {
+      const int nid = pre[k];
+      o_tok[k] = d_tok[nid];
+      o_par[k] = nid == 0 ? -1 : (int32_t)n2p[d_par[nid]];
+      o_dep[k] = d_dep[nid];
+      uint64_t mw[SSSD_MAX_DRAFT / 64] = {0, 0, 0, 0};
+      for (int x = nid; x >= 0; x = d_par[x]) {
+        const int pk = n2p[x];
+        mw[pk >> 6] |= 1ull << (pk & 63);
+      }
+      for (int w = 0; w < W; ++w) o_mask[(size_t)k * W + w] = mw[w];
+    } else {
+      o_tok[k] = 0;
+      o_par[k] = -1;
+      o_dep[k] = -1;
+      for (int w = 0; w < W; ++w) o_mask[(size_t)k * W + w] = 0;
+    }
+  }
+  if (lane == 0) out.size[b] = size;
+}
+
+}  // namespace sssd

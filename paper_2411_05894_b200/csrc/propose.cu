@@ -11,12 +11,7 @@
 //                      live sequence, occurrence compaction and a
 //                      block bitonic sort of the continuation strings.  Replaces
 //                      InputCache.get_conts (ref input_cache.py:88-121).
-//   draft_kernel       one warp per request: best-first fusion over tries that
-//                      are never materialised — a trie node is a range of its
-//                      source's sorted element array and is expanded lazily into
-//                      a sibling group when popped — followed by DFS
-//                      flattening and u64 ancestor masks.  Replaces merge /
-//                      flatten (ref fusion.py:209-261, draft.py:67-86).
+//   (draft_kernel, the fusion + flatten stage, lives in fusion.cu)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -470,382 +465,6 @@ __global__ void __launch_bounds__(256)
   uint32_t* idx = (n <= kSortSmem) ? s_idx : idx_ws + o * 2;  // idx_ws holds 2*total entries
   (void)idx_cap;
   block_sort_elems(el + o, sorted + o, tok, n, idx);
-}
-
-// --------------------------------------------------------------------------
-// K5: fusion + flatten (ref fusion.py:209-261, draft.py:67-86; A.5, A.6)
-// --------------------------------------------------------------------------
-
-struct Child {  // one candidate of a sibling group (32 B, global arena)
-  double pp;       // path probability (ref fusion.py:244,259)
-  uint32_t first;  // first-appearance position = reference child order
-  uint32_t count;  // node count in its source trie
-  uint32_t token;
-  uint32_t a, b;   // element range [a, b) of the node in the source array
-  uint32_t pad;
-};
-
-struct Group {  // sibling group header (40 B, shared memory)
-  double prio;    // head priority
-  Child* ch;
-  uint32_t first;  // head first-appearance
-  int32_t head;    // head child index, -1 when exhausted
-  uint32_t nch;
-  uint32_t meta;     // depth << 26 | rank << 22 | sequence
-  uint32_t dparent;  // draft node the children hang under
-  uint32_t pad;
-};
-
-__device__ __forceinline__ uint32_t g_depth(uint32_t meta) { return meta >> 26; }
-__device__ __forceinline__ uint32_t g_rank(uint32_t meta) { return (meta >> 22) & 0xf; }
-
-struct Arena {
-  Child* slab;
-  uint32_t used, cap;
-  Child* pool;
-  unsigned long long* cursor;
-  uint64_t pool_cap;
-  int32_t* err;
-  __device__ Child* alloc(uint32_t n) {  // warp-uniform
-    if (used + n <= cap) {
-      Child* p = slab + used;
-      used += n;
-      return p;
-    }
-    unsigned long long at = 0;
-    if (lane_id() == 0) at = atomicAdd(cursor, (unsigned long long)n);
-    at = __shfl_sync(SSSD_FULL, at, 0);
-    if (at + n > pool_cap) {
-      if (lane_id() == 0) atomicExch(err, SSSD_E_WORKSPACE);
-      return nullptr;
-    }
-    return pool + at;
-  }
-  // return the unused tail [p + keep, p + n) of the latest slab allocation
-  __device__ void shrink(Child* p, uint32_t n, uint32_t keep) {
-    if (p + n == slab + used) used -= n - keep;
-  }
-};
-
-// better(a, b): higher priority first, then smaller first-appearance (ticket)
-__device__ __forceinline__ bool child_better(double pa, uint32_t fa, double pb, uint32_t fb) {
-  return pa > pb || (pa == pb && fa < fb);
-}
-
-__device__ __forceinline__ void warp_best(double& p, uint32_t& f, int& i) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double op = __shfl_xor_sync(SSSD_FULL, p, o);
-    const uint32_t of = __shfl_xor_sync(SSSD_FULL, f, o);
-    const int oi = __shfl_xor_sync(SSSD_FULL, i, o);
-    if (oi >= 0 && (i < 0 || child_better(op, of, p, f))) {
-      p = op;
-      f = of;
-      i = oi;
-    }
-  }
-}
-
-// Expand the node covering [a, z) of source sd at depth D-1 into the sibling
-// group of its depth-D children (sub-runs by token index D-1).  Creates a
-// group (appended at *G) when the node has at least one child.
-__device__ void expand(const SrcDesc& sd, uint32_t rank, uint32_t D, uint32_t a, uint32_t z,
-                       bool seed, double ppar, uint32_t pcount, uint32_t dparent, double disc,
-                       Group* groups, int& G, Arena& ar) {
-  const int lane = lane_id();
-  Child* ch = ar.alloc(z - a);
-  if (!ch) return;
-  uint32_t nch = 0;
-  double bp = -1.0;
-  uint32_t bf = 0xffffffffu;
-  int bi = -1;
-  bool c_open = false;
-  uint32_t c_tok = 0, c_cnt = 0, c_first = 0xffffffffu, c_start = 0;
-  const double dpc = (double)pcount;
-
-  auto emit = [&](bool pred, uint32_t tok, uint32_t cnt, uint32_t first, uint32_t s, uint32_t e) {
-    const bool live = pred && cnt > 0;
-    const uint32_t bal = __ballot_sync(SSSD_FULL, live);
-    if (live) {
-      const uint32_t k = nch + __popc(bal & lanemask_lt());
-      const double ratio = __ddiv_rn((double)cnt, dpc);
-      const double pp = seed ? ratio : __dmul_rn(ppar, ratio);
-      const double pr = __dmul_rn(pp, disc);
-      Child cc;
-      cc.pp = pp;
-      cc.first = first;
-      cc.count = cnt;
-      cc.token = tok;
-      cc.a = s;
-      cc.b = e;
-      cc.pad = 0;
-      ch[k] = cc;
-      if (bi < 0 || child_better(pr, first, bp, bf)) {
-        bp = pr;
-        bf = first;
-        bi = (int)k;
-      }
-    }
-    nch += __popc(bal);
-  };
-
-  for (uint32_t base = a; base < z; base += 32) {
-    const uint32_t i = base + lane;
-    bool has = false;
-    uint32_t t = 0, wgt = 0, orig = 0xffffffffu;
-    if (i < z) {
-      const sssd_elem e = sd.el[i];
-      if (el_len(e.len_m) >= D) {
-        has = true;
-        t = sd.tok[e.off + D - 1];
-        if ((int)el_m(e.len_m) >= sd.thr) {
-          wgt = 1;
-          orig = e.orig;
-        }
-      }
-    }
-    const uint32_t hasm = __ballot_sync(SSSD_FULL, has);
-    if (!hasm) continue;
-    const uint32_t tprev = __shfl_up_sync(SSSD_FULL, t, 1);
-    bool head;
-    if (lane == 0) head = has && !(c_open && c_tok == t);
-    else head = has && (!((hasm >> (lane - 1)) & 1u) || tprev != t);
-    const uint32_t headm = __ballot_sync(SSSD_FULL, head);
-    // a pending carry run ends where this chunk starts a new run
-    if (c_open && (headm & 1u)) {
-      emit(lane == 0, c_tok, c_cnt, c_first, c_start, base);
-      c_open = false;
-    }
-    const uint32_t le = headm & (lanemask_lt() | (1u << lane));
-    const int seg = le ? 31 - __clz(le) : -1;
-    uint32_t cnt = wgt, fm = orig;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t oc = __shfl_up_sync(SSSD_FULL, cnt, o);
-      const uint32_t of = __shfl_up_sync(SSSD_FULL, fm, o);
-      if (lane >= o && lane - o >= seg) {
-        cnt += oc;
-        fm = min(fm, of);
-      }
-    }
-    uint32_t start = base + (seg < 0 ? 0 : seg);
-    if (seg < 0) {  // continuation of the carried run
-      cnt += c_cnt;
-      fm = min(fm, c_first);
-      start = c_start;
-    }
-    const bool nxt_has = lane < 31 ? ((hasm >> (lane + 1)) & 1u) : false;
-    const bool nxt_head = lane < 31 ? ((headm >> (lane + 1)) & 1u) : false;
-    const bool tail = has && (lane == 31 || !nxt_has || nxt_head);
-    const bool open = tail && lane == 31 && i + 1 < z;
-    emit(tail && !open, t, cnt, fm, start, i + 1);
-    const uint32_t ob = __ballot_sync(SSSD_FULL, open);
-    if (ob) {
-      c_tok = __shfl_sync(SSSD_FULL, t, 31);
-      c_cnt = __shfl_sync(SSSD_FULL, cnt, 31);
-      c_first = __shfl_sync(SSSD_FULL, fm, 31);
-      c_start = __shfl_sync(SSSD_FULL, start, 31);
-      c_open = true;
-    } else {
-      c_open = false;
-    }
-  }
-  if (c_open) emit(lane == 0, c_tok, c_cnt, c_first, c_start, z);
-  ar.shrink(ch, z - a, nch);
-  if (nch == 0) return;
-  warp_best(bp, bf, bi);
-  if (lane == 0) {
-    Group g;
-    g.prio = bp;
-    g.ch = ch;
-    g.first = bf;
-    g.head = bi;
-    g.nch = nch;
-    g.meta = (D << 26) | (rank << 22) | (uint32_t)G;
-    g.dparent = dparent;
-    g.pad = 0;
-    groups[G] = g;
-  }
-  ++G;
-  __syncwarp();
-}
-
-__global__ void __launch_bounds__(32)
-    draft_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, Child* slabs,
-                 uint32_t slab_cap, Child* pool, unsigned long long* cursor, uint64_t pool_cap,
-                 int32_t* err, sssd_draft_out out) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const int b = blockIdx.x;
-  const int lane = lane_id();
-  const int S = c.S;
-  const int W = (S + 63) >> 6;
-  const int Gmax = (c.P + 1) * S + c.P + 1;
-  Group* groups = reinterpret_cast<Group*>(smem);
-  uint32_t* d_tok = reinterpret_cast<uint32_t*>(groups + Gmax);
-  int16_t* d_par = reinterpret_cast<int16_t*>(d_tok + S);
-  int16_t* d_fc = d_par + S;
-  int16_t* d_ns = d_fc + S;
-  int16_t* d_lc = d_ns + S;
-  int16_t* d_dep = d_lc + S;
-  int16_t* pre = d_dep + S;
-  int16_t* n2p = pre + S;
-  int16_t* stk = n2p + S;
-
-  Arena ar{slabs + (size_t)b * slab_cap, 0, slab_cap, pool, cursor, pool_cap, err};
-  if (lane == 0) {
-    d_tok[0] = root_tok[b];
-    d_par[0] = -1;
-    d_fc[0] = d_ns[0] = d_lc[0] = -1;
-    d_dep[0] = 0;
-  }
-  __syncwarp();
-  int G = 0;
-  int size = 1;
-  const SrcDesc* sds = desc + (size_t)b * (c.P + 1);
-
-  // Seeds: datastore (rank 0), then input trees p = n_trees..1 (rank P-p+1).
-  if (S > 1) {
-    for (int rk = 0; rk <= c.P; ++rk) {
-      const SrcDesc sd = sds[rk];
-      if (sd.n <= 0) continue;
-      uint32_t rc = 0;
-      for (int i = lane; i < sd.n; i += 32) rc += (int)el_m(sd.el[i].len_m) >= sd.thr ? 1u : 0u;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) rc += __shfl_xor_sync(SSSD_FULL, rc, o);
-      if (rc == 0) continue;
-      expand(sd, rk, 1, 0, sd.n, true, 0.0, rc, 0, c.disc[rk * c.disc_stride + 1], groups, G, ar);
-    }
-  }
-
-  while (size < S) {
-    // pop: min over group heads of (-prio, depth, rank, sequence)
-    double bp = -1.0;
-    uint32_t bm = 0xffffffffu;
-    int bg = -1;
-    for (int gi = lane; gi < G; gi += 32) {
-      const Group& g = groups[gi];
-      if (g.head < 0) continue;
-      if (bg < 0 || g.prio > bp || (g.prio == bp && g.meta < bm)) {
-        bp = g.prio;
-        bm = g.meta;
-        bg = gi;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double op = __shfl_xor_sync(SSSD_FULL, bp, o);
-      const uint32_t om = __shfl_xor_sync(SSSD_FULL, bm, o);
-      const int og = __shfl_xor_sync(SSSD_FULL, bg, o);
-      if (og >= 0 && (bg < 0 || op > bp || (op == bp && om < bm))) {
-        bp = op;
-        bm = om;
-        bg = og;
-      }
-    }
-    if (bg < 0) break;
-    const Group g = groups[bg];
-    const Child h = g.ch[g.head];
-    const uint32_t D = g_depth(g.meta), rk = g_rank(g.meta);
-    const double dsc = c.disc[rk * c.disc_stride + D];
-    // draft insert: an existing (parent, token) keeps the first node (ref fusion.py:185-198)
-    const int par = (int)g.dparent;
-    int found = -1;
-    for (int i0 = 1; i0 < size; i0 += 32) {
-      const int i = i0 + lane;
-      const bool hit = i < size && d_par[i] == par && d_tok[i] == h.token;
-      const uint32_t hb = __ballot_sync(SSSD_FULL, hit);
-      if (hb) {
-        found = i0 + __ffs(hb) - 1;
-        break;
-      }
-    }
-    int nid = found;
-    if (found < 0) {
-      nid = size++;
-      if (lane == 0) {
-        d_tok[nid] = h.token;
-        d_par[nid] = (int16_t)par;
-        d_fc[nid] = d_ns[nid] = d_lc[nid] = -1;
-        d_dep[nid] = (int16_t)(d_dep[par] + 1);
-        if (d_lc[par] < 0) d_fc[par] = (int16_t)nid;
-        else d_ns[d_lc[par]] = (int16_t)nid;
-        d_lc[par] = (int16_t)nid;
-      }
-    }
-    // advance the popped group's head: best child strictly after (h.prio, h.first)
-    {
-      const double hp = __dmul_rn(h.pp, dsc);
-      double np = -1.0;
-      uint32_t nf = 0xffffffffu;
-      int ni = -1;
-      for (uint32_t k = lane; k < g.nch; k += 32) {
-        const Child ck = g.ch[k];
-        const double pk = __dmul_rn(ck.pp, dsc);
-        if (child_better(hp, h.first, pk, ck.first) && (ni < 0 || child_better(pk, ck.first, np, nf))) {
-          np = pk;
-          nf = ck.first;
-          ni = (int)k;
-        }
-      }
-      warp_best(np, nf, ni);
-      if (lane == 0) {
-        groups[bg].head = ni;
-        groups[bg].prio = np;
-        groups[bg].first = nf;
-      }
-    }
-    __syncwarp();
-    // push the popped source node's children (ref fusion.py:258-259)
-    if (h.b - h.a > 0) {
-      const SrcDesc sd = sds[rk];
-      if (D + 1 < (uint32_t)c.disc_stride)
-        expand(sd, rk, D + 1, h.a, h.b, false, h.pp, h.count, (uint32_t)nid,
-               c.disc[rk * c.disc_stride + D + 1], groups, G, ar);
-    }
-    __syncwarp();
-  }
-
-  // DFS pre-order flatten, children in insertion order (ref draft.py:67-86)
-  if (lane == 0) {
-    int sp = 0, k = 0;
-    stk[sp++] = 0;
-    while (sp > 0) {
-      const int nid = stk[--sp];
-      pre[k] = (int16_t)nid;
-      n2p[nid] = (int16_t)k;
-      ++k;
-      int cnt = 0;
-      for (int ch = d_fc[nid]; ch >= 0; ch = d_ns[ch]) ++cnt;
-      int j = 0;
-      for (int ch = d_fc[nid]; ch >= 0; ch = d_ns[ch], ++j) stk[sp + cnt - 1 - j] = (int16_t)ch;
-      sp += cnt;
-    }
-  }
-  __syncwarp();
-  uint32_t* o_tok = out.tokens + (size_t)b * S;
-  int32_t* o_par = out.parents + (size_t)b * S;
-  int32_t* o_dep = out.depths + (size_t)b * S;
-  uint64_t* o_mask = out.mask + (size_t)b * S * W;
-  for (int k = lane; k < S; k += 32) {
-    if (k < size) {
-      const int nid = pre[k];
-      o_tok[k] = d_tok[nid];
-      o_par[k] = nid == 0 ? -1 : (int32_t)n2p[d_par[nid]];
-      o_dep[k] = d_dep[nid];
-      uint64_t mw[SSSD_MAX_DRAFT / 64] = {0, 0, 0, 0};
-      for (int x = nid; x >= 0; x = d_par[x]) {
-        const int pk = n2p[x];
-        mw[pk >> 6] |= 1ull << (pk & 63);
-      }
-      for (int w = 0; w < W; ++w) o_mask[(size_t)k * W + w] = mw[w];
-    } else {
-      o_tok[k] = 0;
-      o_par[k] = -1;
-      o_dep[k] = -1;
-      for (int w = 0; w < W; ++w) o_mask[(size_t)k * W + w] = 0;
-    }
-  }
-  if (lane == 0) out.size[b] = size;
 }
 
 }  // namespace sssd

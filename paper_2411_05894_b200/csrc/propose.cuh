@@ -34,16 +34,29 @@ __global__ void input_scan_kernel(sssd_seqs seqs, KCfg c, sssd_elem* raw, sssd_e
 __global__ void sort_sources_kernel(const uint32_t* tok, const sssd_elem* el,
                                     const int64_t* el_off, const int32_t* el_n, sssd_elem* sorted,
                                     uint32_t* idx_ws, int64_t idx_cap);
+struct Group;
 __global__ void draft_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, Child* slabs,
                              uint32_t slab_cap, Child* pool, unsigned long long* cursor,
-                             uint64_t pool_cap, int32_t* err, sssd_draft_out out);
+                             uint64_t pool_cap, int32_t* err, Group* gover, int gover_cap,
+                             sssd_draft_out out);
 
 constexpr int kChildBytes = 32;
-constexpr int kGroupBytes = 40;
+constexpr int kGroupBytes = 32;
+constexpr int kGroupSmem = 192;  // groups kept in shared memory; the rest spill to global
+
+// Upper bound on sibling groups: one per source seed plus one per pop, and a
+// draft node can be popped at most once per source.
+__host__ __device__ inline int draft_max_groups(int P, int S) { return (P + 1) * S + P + 1; }
 
 inline int draft_smem_bytes(int P, int S) {
-  const int Gmax = (P + 1) * S + P + 1;
-  return Gmax * kGroupBytes + S * 4 + S * 2 * 8 + 16;
+  const int G = draft_max_groups(P, S);
+  const int Gs = G < kGroupSmem ? G : kGroupSmem;
+  return Gs * kGroupBytes + S * 4 + S * 2 * 8 + 16;
+}
+
+inline int draft_group_overflow(int P, int S) {
+  const int G = draft_max_groups(P, S);
+  return G > kGroupSmem ? G - kGroupSmem : 0;
 }
 
 }  // namespace sssd
