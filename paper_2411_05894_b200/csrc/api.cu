@@ -67,6 +67,8 @@ static int validate_cfg(const sssd_cfg* c) {
   return SSSD_OK;
 }
 
+static int merge_depth(const sssd_cfg* cfg) { return cfg->disc_stride - 1; }
+
 static KCfg kcfg(const sssd_cfg* c) {
   KCfg k;
   k.P = c->P;
@@ -88,8 +90,8 @@ static KCfg kcfg(const sssd_cfg* c) {
 constexpr uint32_t kSlabChildren = 2048;
 
 struct DraftWs {
-  Group* gover;
-  int gover_cap;
+  uint8_t* gover;
+  int64_t gover_bytes;
   SrcDesc* desc;
   uint32_t* root;
   Child* slabs;
@@ -105,8 +107,8 @@ struct DraftWs {
 // contexts (huge input-tree roots) spill into the pool, sized by max_len.
 static DraftWs carve_draft(Carver& cv, int P, int S, int B, int64_t max_len = 0) {
   DraftWs d;
-  d.gover_cap = draft_group_overflow(P, S);
-  d.gover = reinterpret_cast<Group*>(cv.take<uint8_t>((size_t)B * (d.gover_cap ? d.gover_cap : 1) * kGroupBytes));
+  d.gover_bytes = draft_group_overflow_bytes(P, S);
+  d.gover = cv.take<uint8_t>((size_t)B * (d.gover_bytes ? d.gover_bytes : 1));
   d.desc = cv.take<SrcDesc>((size_t)B * (P + 1));
   d.root = cv.take<uint32_t>((size_t)B);
   d.slabs = reinterpret_cast<Child*>(cv.take<uint8_t>((size_t)B * kSlabChildren * kChildBytes));
@@ -130,6 +132,7 @@ struct PropWs {
   sssd_elem* in_el;
   int32_t* in_n;
   uint32_t* idx;
+  Cols ds_cols, in_cols;
   int64_t cap, cap2;
   DraftWs d;
   size_t bytes;
@@ -155,38 +158,44 @@ static PropWs carve_propose(uint8_t* base, const sssd_cfg* c, int B, int max_len
   w.in_el = cv.take<sssd_elem>((size_t)B * w.cap);
   w.in_n = cv.take<int32_t>((size_t)B);
   w.idx = cv.take<uint32_t>((size_t)B * (w.cap2 ? w.cap2 : 1));
+  w.ds_cols.stride = (int64_t)PM;
+  w.ds_cols.meta = cv.take<uint32_t>((size_t)B * PM);
+  w.ds_cols.orig = cv.take<uint32_t>((size_t)B * PM);
+  w.ds_cols.tok = cv.take<uint32_t>((size_t)B * PM * c->branch_len);
+  w.in_cols.stride = w.cap;
+  w.in_cols.meta = cv.take<uint32_t>((size_t)B * w.cap);
+  w.in_cols.orig = cv.take<uint32_t>((size_t)B * w.cap);
+  w.in_cols.tok = cv.take<uint32_t>((size_t)B * w.cap * c->input_branch_len);
   w.d = carve_draft(cv, c->P, c->dec_len, B, w.cap);
   w.bytes = align_up(cv.off, 256);
   return w;
 }
 
-__global__ void propose_setup_kernel(sssd_seqs seqs, KCfg c, sssd_elem* ds_el, uint32_t* ds_tab,
-                                     const int32_t* ds_n, sssd_elem* in_el, const int32_t* in_n,
-                                     int64_t cap, SrcDesc* desc, uint32_t* root) {
+__global__ void propose_setup_kernel(sssd_seqs seqs, KCfg c, Cols dsc, const int32_t* ds_n,
+                                     Cols inc, const int32_t* in_n, SrcDesc* desc, uint32_t* root) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= seqs.B) return;
   const int L = seqs.seq_len[b];
-  const uint32_t* seq = seqs.seq + seqs.seq_off[b];
-  root[b] = seq[L - 1];
+  root[b] = seqs.seq[seqs.seq_off[b] + L - 1];
   SrcDesc* d = desc + (size_t)b * (c.P + 1);
-  const size_t PM = (size_t)c.P * c.M;
-  d[0].el = ds_el + b * PM;
-  d[0].tok = ds_tab + b * PM * c.BL;
+  d[0].meta = dsc.meta + (size_t)b * dsc.stride;
+  d[0].orig = dsc.orig + (size_t)b * dsc.stride;
+  d[0].tok = dsc.tok + (size_t)b * dsc.stride * c.BL;
+  d[0].stride = dsc.stride;
   d[0].n = c.use_ds ? ds_n[b] : 0;
   d[0].thr = 0;
-  d[0].pad = 0;
   for (int rk = 1; rk <= c.P; ++rk) {
     const int p = c.P - rk + 1;
-    d[rk].el = in_el + (size_t)b * cap;
-    d[rk].tok = seq;
+    d[rk].meta = inc.meta + (size_t)b * inc.stride;
+    d[rk].orig = inc.orig + (size_t)b * inc.stride;
+    d[rk].tok = inc.tok + (size_t)b * inc.stride * c.IBL;
+    d[rk].stride = inc.stride;
     d[rk].n = (c.use_in && p <= c.n_trees) ? in_n[b] : 0;
     d[rk].thr = p;
-    d[rk].pad = 0;
   }
 }
 
-__global__ void merge_setup_kernel(const uint32_t* tok, const sssd_elem* sorted,
-                                   const int64_t* el_off, const int32_t* el_n,
+__global__ void merge_setup_kernel(Cols cols, const int64_t* el_off, const int32_t* el_n,
                                    const uint32_t* roots, int B, KCfg c, SrcDesc* desc,
                                    uint32_t* root) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -197,11 +206,13 @@ __global__ void merge_setup_kernel(const uint32_t* tok, const sssd_elem* sorted,
     const int s = rk == 0 ? 0 : c.P - rk + 1;  // source slot: 0 = datastore, p = input tree p
     const bool live = rk == 0 || s <= c.n_trees;
     const size_t bs = (size_t)b * (c.P + 1) + s;
-    d[rk].el = sorted + (live ? el_off[bs] : 0);
-    d[rk].tok = tok;
+    const int64_t o = live ? el_off[bs] : 0;
+    d[rk].meta = cols.meta + o;
+    d[rk].orig = cols.orig + o;
+    d[rk].tok = cols.tok + o;
+    d[rk].stride = cols.stride;
     d[rk].n = live ? el_n[bs] : 0;
     d[rk].thr = 0;
-    d[rk].pad = 0;
   }
 }
 
@@ -211,7 +222,7 @@ static int launch_draft(const DraftWs& d, const KCfg& k, int B, const sssd_draft
   cudaError_t e = cudaFuncSetAttribute(draft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return cuda_check(e, "draft_kernel smem attribute");
   draft_kernel<<<B, 32, smem, st>>>(d.desc, d.root, k, d.slabs, kSlabChildren, d.pool, d.cursor,
-                                    d.pool_cap, d.err, d.gover, d.gover_cap, *out);
+                                    d.pool_cap, d.err, d.gover, d.gover_bytes, *out);
   return cuda_check(cudaGetLastError(), "draft_kernel launch");
 }
 
@@ -297,17 +308,18 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
   if (ev) cudaEventRecord(ev[0], st);
   if (cfg->use_datastore) {
     ds_lookup_kernel<<<B, 32 * cfg->P, 0, st>>>(*ds, *seqs, k, w.ds_tab, w.ds_len, w.ds_el, w.ds_n, lk,
-                                                 w.ds_raw, w.ds_idx, w.ds_idx_cap);
+                                                 w.ds_raw, w.ds_idx, w.ds_idx_cap, w.ds_cols);
     if ((rc = cuda_check(cudaGetLastError(), "ds_lookup_kernel launch"))) return rc;
   }
   if (ev) cudaEventRecord(ev[1], st);
   if (cfg->use_input) {
-    input_scan_kernel<<<B, 256, 0, st>>>(*seqs, k, w.in_raw, w.in_el, w.in_n, w.idx, w.cap, w.cap2);
+    input_scan_kernel<<<B, 256, 0, st>>>(*seqs, k, w.in_raw, w.in_el, w.in_n, w.idx, w.cap, w.cap2,
+                                         w.in_cols);
     if ((rc = cuda_check(cudaGetLastError(), "input_scan_kernel launch"))) return rc;
   }
   if (ev) cudaEventRecord(ev[2], st);
-  propose_setup_kernel<<<(B + 127) / 128, 128, 0, st>>>(*seqs, k, w.ds_el, w.ds_tab, w.ds_n, w.in_el,
-                                                          w.in_n, w.cap, w.d.desc, w.d.root);
+  propose_setup_kernel<<<(B + 127) / 128, 128, 0, st>>>(*seqs, k, w.ds_cols, w.ds_n, w.in_cols, w.in_n,
+                                                          w.d.desc, w.d.root);
   if ((rc = cuda_check(cudaGetLastError(), "propose_setup_kernel launch"))) return rc;
   if (ev) cudaEventRecord(ev[3], st);
   rc = launch_draft(w.d, k, B, out, st);
@@ -322,8 +334,10 @@ int sssd_workspace_status(const sssd_cfg* cfg, int32_t B, int32_t max_len, const
   size_t off;
   if (is_merge) {
     Carver cv{nullptr, 0};
-    cv.take<sssd_elem>((size_t)(total_elems > 0 ? total_elems : 1));
-    cv.take<uint32_t>((size_t)2 * (total_elems > 0 ? total_elems : 1));
+    const size_t te = (size_t)(total_elems > 0 ? total_elems : 1);
+    cv.take<sssd_elem>(te);
+    cv.take<uint32_t>(2 * te);
+    cv.take<uint32_t>(te * (2 + merge_depth(cfg)));
     DraftWs d = carve_draft(cv, cfg->P, cfg->dec_len, B);
     off = reinterpret_cast<size_t>(d.err);
   } else {
@@ -343,8 +357,10 @@ int sssd_workspace_status(const sssd_cfg* cfg, int32_t B, int32_t max_len, const
 size_t sssd_merge_workspace(const sssd_cfg* cfg, int32_t B, int64_t total_elems) {
   if (!cfg || B < 0) return 0;
   Carver cv{nullptr, 0};
-  cv.take<sssd_elem>((size_t)(total_elems > 0 ? total_elems : 1));
-  cv.take<uint32_t>((size_t)2 * (total_elems > 0 ? total_elems : 1));
+  const size_t te = (size_t)(total_elems > 0 ? total_elems : 1);
+  cv.take<sssd_elem>(te);
+  cv.take<uint32_t>(2 * te);
+  cv.take<uint32_t>(te * (2 + merge_depth(cfg)));
   carve_draft(cv, cfg->P, cfg->dec_len, B);
   return align_up(cv.off, 256);
 }
@@ -362,6 +378,8 @@ int sssd_merge(const uint32_t* tok, const sssd_elem* el, const int64_t* el_off,
   const size_t te = (size_t)(total_elems > 0 ? total_elems : 1);
   sssd_elem* sorted = cv.take<sssd_elem>(te);
   uint32_t* idx = cv.take<uint32_t>(2 * te);
+  uint32_t* colbuf = cv.take<uint32_t>(te * (2 + merge_depth(cfg)));
+  Cols cols{colbuf, colbuf + te, colbuf + 2 * te, (int64_t)te};
   DraftWs d = carve_draft(cv, cfg->P, cfg->dec_len, B);
   const size_t need = align_up(cv.off, 256);
   if (!workspace || workspace_bytes < need)
@@ -369,10 +387,9 @@ int sssd_merge(const uint32_t* tok, const sssd_elem* el, const int64_t* el_off,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const KCfg k = kcfg(cfg);
   if ((rc = cuda_check(cudaMemsetAsync(d.cursor, 0, 16, st), "memset status"))) return rc;
-  sort_sources_kernel<<<B * (cfg->P + 1), 256, 0, st>>>(tok, el, el_off, el_n, sorted, idx, 2 * te);
+  sort_sources_kernel<<<B * (cfg->P + 1), 256, 0, st>>>(tok, el, el_off, el_n, sorted, idx, 2 * te, cols);
   if ((rc = cuda_check(cudaGetLastError(), "sort_sources_kernel launch"))) return rc;
-  merge_setup_kernel<<<(B + 127) / 128, 128, 0, st>>>(tok, sorted, el_off, el_n, root_tokens, B, k,
-                                                        d.desc, d.root);
+  merge_setup_kernel<<<(B + 127) / 128, 128, 0, st>>>(cols, el_off, el_n, root_tokens, B, k, d.desc, d.root);
   if ((rc = cuda_check(cudaGetLastError(), "merge_setup_kernel launch"))) return rc;
   return launch_draft(d, k, B, out, st);
 }
@@ -403,7 +420,7 @@ int sssd_ds_lookup(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg
   uint32_t* idx = reinterpret_cast<uint32_t*>(
       align_up(reinterpret_cast<uintptr_t>(raw + (size_t)seqs->B * cfg->P * cfg->M), 256));
   ds_lookup_kernel<<<seqs->B, 32 * cfg->P, 0, static_cast<cudaStream_t>(stream)>>>(
-      *ds, *seqs, kcfg(cfg), tab, lens, el, n_el, lk, raw, idx, ds_idx_cap(cfg->P, cfg->M));
+      *ds, *seqs, kcfg(cfg), tab, lens, el, n_el, lk, raw, idx, ds_idx_cap(cfg->P, cfg->M), Cols{});
   return cuda_check(cudaGetLastError(), "ds_lookup_kernel launch");
 }
 
@@ -431,7 +448,7 @@ int sssd_input_scan(const sssd_seqs* seqs, const sssd_cfg* cfg, sssd_elem* el, i
   KCfg k = kcfg(cfg);
   k.use_in = 1;
   input_scan_kernel<<<seqs->B, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      *seqs, k, raw, el, n_el, idx, cap, cap > 4096 ? p2 : 0);
+      *seqs, k, raw, el, n_el, idx, cap, cap > 4096 ? p2 : 0, Cols{});
   return cuda_check(cudaGetLastError(), "input_scan_kernel launch");
 }
 

@@ -34,16 +34,35 @@ __device__ __forceinline__ int cmp_str(const uint32_t* a, uint32_t la, const uin
   return la < lb ? -1 : (la > lb ? 1 : 0);
 }
 
-// Per-(request, source) view used by the fusion kernel: a sorted element
-// array over a token buffer; an element counts toward this source's tree when
-// its backward-match length m >= thr (input tree p: thr = p; datastore and
-// caller-provided trees: thr = 0).
+// Depth-major columns of one sorted source array (the fusion kernel's input):
+// element i's metadata, insertion position and token at depth d live at
+// meta[i], orig[i], tok[d * stride + i], so the lanes of a warp expanding a
+// trie node read 3 coalesced, mutually independent words per element.
+struct Cols {
+  uint32_t* meta;  // len | m << 8
+  uint32_t* orig;
+  uint32_t* tok;
+  int64_t stride;
+};
+
+__device__ __forceinline__ void write_cols(const Cols& c, int64_t i, const sssd_elem& e,
+                                           const uint32_t* tokbuf) {
+  const uint32_t len = el_len(e.len_m);
+  c.meta[i] = e.len_m & 0xffffu;
+  c.orig[i] = e.orig;
+  for (uint32_t d = 0; d < len; ++d) c.tok[d * c.stride + i] = tokbuf[e.off + d];
+}
+
+// Per-(request, source) view used by the fusion kernel: n sorted elements in
+// columns; an element counts toward this source's tree when its backward-match
+// length m >= thr (input tree p: thr = p; datastore and caller trees: thr = 0).
 struct SrcDesc {
-  const sssd_elem* el;
+  const uint32_t* meta;
+  const uint32_t* orig;
   const uint32_t* tok;
+  int64_t stride;
   int32_t n;
   int32_t thr;
-  int64_t pad;
 };
 
 }  // namespace sssd

@@ -32,17 +32,17 @@ struct Child {  // one candidate (32 B, global arena)
   uint32_t pad;
 };
 
-struct Group {  // sibling group header (32 B; shared memory, global overflow)
-  uint32_t khi, klo;  // head key = ~bits(priority of the head child)
+// A sibling group is split into a hot key (always in shared memory, scanned
+// every pop) and a cold record (children pointer and cursor; shared memory for
+// the first kGroupSmem groups, global overflow after).
+struct Group {  // cold record (16 B)
   Child* ch;
-  uint32_t head;  // head child index; == nch when exhausted
-  uint32_t nch;
-  uint32_t meta;      // depth << 26 | rank << 22 | creation sequence
-  uint16_t dparent;   // draft node the children hang under
-  uint16_t sorted;    // children stored in pop order
+  uint32_t head;  // head child index (low 24 bits) | draft parent << 24
+  uint32_t nch;   // children (low 31 bits) | stored-in-pop-order flag << 31
 };
 static_assert(sizeof(Child) == kChildBytes, "Child layout");
 static_assert(sizeof(Group) == kGroupBytes, "Group layout");
+constexpr uint32_t kExhausted = 0xffffffffu;  // meta of a group with no candidates left
 
 __device__ __forceinline__ uint32_t g_depth(uint32_t meta) { return meta >> 26; }
 __device__ __forceinline__ uint32_t g_rank(uint32_t meta) { return (meta >> 22) & 0xf; }
@@ -73,6 +73,10 @@ __device__ __forceinline__ int warp_argmin3(bool valid, uint32_t hi, uint32_t lo
 }
 
 struct Arena {
+  // child lists: a shared-memory slab first, then the request's global slab,
+  // then the shared overflow pool
+  Child* sslab;
+  uint32_t sused, scap;
   Child* slab;
   uint32_t used, cap;
   Child* pool;
@@ -80,6 +84,11 @@ struct Arena {
   uint64_t pool_cap;
   int32_t* err;
   __device__ Child* alloc(uint32_t n) {  // warp-uniform
+    if (sused + n <= scap) {
+      Child* p = sslab + sused;
+      sused += n;
+      return p;
+    }
     if (used + n <= cap) {
       Child* p = slab + used;
       used += n;
@@ -94,17 +103,24 @@ struct Arena {
     }
     return pool + at;
   }
-  // give back the unused tail [p + keep, p + n) of the latest slab allocation
+  // give back the unused tail [p + keep, p + n) of the latest allocation
   __device__ void shrink(Child* p, uint32_t n, uint32_t keep) {
-    if (p + n == slab + used) used -= n - keep;
+    if (p + n == sslab + sused) sused -= n - keep;
+    else if (p + n == slab + used) used -= n - keep;
   }
 };
 
+// Frontier: hot keys of the *live* groups form a compact list in shared memory
+// (an exhausted group is swapped out), so a pop scans only groups that still
+// hold candidates.  Cold records are indexed by group id: ids < kGroupSmem in
+// shared memory, later ids in the request's global overflow area.
 struct Frontier {
-  Group* sg;  // first kGroupSmem groups (shared memory)
-  Group* gg;  // overflow groups (global)
-  int G;
-  __device__ __forceinline__ Group* at(int i) const { return i < kGroupSmem ? sg + i : gg + (i - kGroupSmem); }
+  uint32_t *kh, *kl, *km;  // live list: ~bits(prio) hi / lo, meta (group id in low 22 bits)
+  Group* sc;
+  Group* gc;
+  int G;  // groups created
+  int A;  // live groups
+  __device__ __forceinline__ Group* cold(int i) const { return i < kGroupSmem ? sc + i : gc + (i - kGroupSmem); }
 };
 
 // Expand the node covering [a, z) of source sd at depth D-1 into the group of
@@ -117,21 +133,22 @@ __device__ void expand(const SrcDesc& sd, uint32_t rank, uint32_t D, uint32_t a,
   const int lane = lane_id();
   const double dpc = (double)pcount;
   const uint32_t n = z - a;
+  const uint32_t* tokD = sd.tok + (int64_t)(D - 1) * sd.stride;
   Child* ch = nullptr;
   uint32_t nch = 0;
 
   if (n == 1) {  // single element: at most one child, count 1
-    const sssd_elem e = sd.el[a];
-    if (el_len(e.len_m) < D || (int)el_m(e.len_m) < sd.thr) return;
+    const uint32_t lm = sd.meta[a], t = tokD[a], o = sd.orig[a];
+    if (el_len(lm) < D || (int)el_m(lm) < sd.thr) return;
     ch = ar.alloc(1);
     if (!ch) return;
     if (lane == 0) {
       const double ratio = __ddiv_rn(1.0, dpc);
       Child c;
       c.pp = seed ? ratio : __dmul_rn(ppar, ratio);
-      c.first = e.orig;
+      c.first = o;
       c.count = 1;
-      c.token = sd.tok[e.off + D - 1];
+      c.token = t;
       c.a = a;
       c.b = z;
       c.pad = 0;
@@ -162,17 +179,16 @@ __device__ void expand(const SrcDesc& sd, uint32_t rank, uint32_t D, uint32_t a,
     uint32_t c_tok = 0, c_cnt = 0, c_first = 0xffffffffu, c_start = 0;
     for (uint32_t base = a; base < z; base += 32) {
       const uint32_t i = base + lane;
-      bool has = false;
+      bool has = false, w = false;
       uint32_t t = 0, orig = 0xffffffffu;
-      bool w = false;
       if (i < z) {
-        const sssd_elem e = sd.el[i];
-        if (el_len(e.len_m) >= D) {
+        const uint32_t lm = sd.meta[i], tv = tokD[i], ov = sd.orig[i];
+        if (el_len(lm) >= D) {
           has = true;
-          t = sd.tok[e.off + D - 1];
-          if ((int)el_m(e.len_m) >= sd.thr) {
+          t = tv;
+          if ((int)el_m(lm) >= sd.thr) {
             w = true;
-            orig = e.orig;
+            orig = ov;
           }
         }
       }
@@ -183,9 +199,17 @@ __device__ void expand(const SrcDesc& sd, uint32_t rank, uint32_t D, uint32_t a,
       const unsigned long long key = has ? (0x100000000ull | t) : (0x200000000ull + (unsigned)lane);
       const uint32_t gm = __match_any_sync(SSSD_FULL, key);
       const uint32_t wm = __ballot_sync(SSSD_FULL, w);
-      uint32_t cnt = __popc(gm & wm);
-      uint32_t fm = __reduce_min_sync(gm, orig);
       const int lo_l = __ffs(gm) - 1, hi_l = 31 - __clz(gm);
+      // run minimum of orig: segmented down-scan (lane lo_l ends with the
+      // minimum over [lo_l, hi_l]); runs are contiguous lane intervals
+      uint32_t fm = orig;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_down_sync(SSSD_FULL, fm, o);
+        if (lane + o <= hi_l) fm = min(fm, x);
+      }
+      fm = __shfl_sync(SSSD_FULL, fm, lo_l);
+      uint32_t cnt = __popc(gm & wm);
       const uint32_t t0 = __shfl_sync(SSSD_FULL, t, 0);
       if (c_open && !((hasm & 1u) && t0 == c_tok)) {  // the carried run ended at the chunk edge
         emit(lane == 0, c_tok, c_cnt, c_first, c_start, base);
@@ -216,8 +240,10 @@ __device__ void expand(const SrcDesc& sd, uint32_t rank, uint32_t D, uint32_t a,
   __syncwarp();
 
   uint32_t head = 0, kh = 0xffffffffu, kl = 0xffffffffu;
-  uint16_t sorted = 1;
-  if (nch <= 32) {
+  uint32_t sorted = 1;
+  if (nch == 1) {
+    prio_key(__dmul_rn(ch[0].pp, disc), kh, kl);
+  } else if (nch <= 32) {
     // store the group in pop order: rank of each child by (priority desc, first asc)
     const bool v = (uint32_t)lane < nch;
     Child cc;
@@ -263,32 +289,36 @@ __device__ void expand(const SrcDesc& sd, uint32_t rank, uint32_t D, uint32_t a,
   }
   if (lane == 0) {
     Group g;
-    g.khi = kh;
-    g.klo = kl;
     g.ch = ch;
-    g.head = head;
-    g.nch = nch;
-    g.meta = (D << 26) | (rank << 22) | (uint32_t)fr.G;
-    g.dparent = (uint16_t)dparent;
-    g.sorted = sorted;
-    *fr.at(fr.G) = g;
+    g.head = head | (dparent << 24);
+    g.nch = nch | (sorted << 31);
+    *fr.cold(fr.G) = g;
+    fr.kh[fr.A] = kh;
+    fr.kl[fr.A] = kl;
+    fr.km[fr.A] = (D << 26) | (rank << 22) | (uint32_t)fr.G;
   }
   ++fr.G;
+  ++fr.A;
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(32)
+__global__ void __launch_bounds__(32, 32)
     draft_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, Child* slabs,
                  uint32_t slab_cap, Child* pool, unsigned long long* cursor, uint64_t pool_cap,
-                 int32_t* err, Group* gover, int gover_cap, sssd_draft_out out) {
+                 int32_t* err, uint8_t* gover, int64_t gover_bytes, sssd_draft_out out) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int b = blockIdx.x;
   const int lane = lane_id();
   const int S = c.S;
   const int W = (S + 63) >> 6;
-  const int Gs = min(draft_max_groups(c.P, S), kGroupSmem);
-  Group* sg = reinterpret_cast<Group*>(smem);
-  uint32_t* d_tok = reinterpret_cast<uint32_t*>(sg + Gs);
+  const int Gmax = draft_max_groups(c.P, S);
+  const int Gs = min(Gmax, kGroupSmem);
+  Child* sslab = reinterpret_cast<Child*>(smem);
+  Group* sc = reinterpret_cast<Group*>(sslab + kChildSmem);
+  uint32_t* skh = reinterpret_cast<uint32_t*>(sc + Gs);
+  uint32_t* skl = skh + Gmax;
+  uint32_t* skm = skl + Gmax;
+  uint32_t* d_tok = skm + Gmax;
   int16_t* d_par = reinterpret_cast<int16_t*>(d_tok + S);
   int16_t* d_fc = d_par + S;  // first child
   int16_t* d_lc = d_fc + S;   // last child
@@ -298,8 +328,10 @@ __global__ void __launch_bounds__(32)
   int16_t* n2p = pre + S;     // node -> pre-order position
   int16_t* stk = n2p + S;
 
-  Arena ar{slabs + (size_t)b * slab_cap, 0, slab_cap, pool, cursor, pool_cap, err};
-  Frontier fr{sg, gover + (size_t)b * gover_cap, 0};
+  Group* gc = reinterpret_cast<Group*>(gover + (size_t)b * gover_bytes);  // cold overflow
+
+  Arena ar{sslab, 0, kChildSmem, slabs + (size_t)b * slab_cap, 0, slab_cap, pool, cursor, pool_cap, err};
+  Frontier fr{skh, skl, skm, sc, gc, 0, 0};
   if (lane == 0) {
     d_tok[0] = root_tok[b];
     d_par[0] = -1;
@@ -316,7 +348,7 @@ __global__ void __launch_bounds__(32)
       const SrcDesc sd = sds[rk];
       if (sd.n <= 0) continue;
       uint32_t rc = 0;
-      for (int i = lane; i < sd.n; i += 32) rc += (int)el_m(sd.el[i].len_m) >= sd.thr ? 1u : 0u;
+      for (int i = lane; i < sd.n; i += 32) rc += (int)el_m(sd.meta[i]) >= sd.thr ? 1u : 0u;
       rc = __reduce_add_sync(SSSD_FULL, rc);
       if (rc == 0) continue;
       expand(sd, rk, 1, 0, sd.n, true, 0.0, rc, 0, c.disc[rk * c.disc_stride + 1], fr, ar);
@@ -324,33 +356,34 @@ __global__ void __launch_bounds__(32)
   }
 
   while (size < S) {
-    // pop: minimum over group heads of (~prio, depth|rank|sequence)
-    bool v = false;
-    uint32_t bh = 0, bl = 0, bm = 0;
-    int bg = -1;
-    for (int gi = lane; gi < fr.G; gi += 32) {
-      const Group* g = fr.at(gi);
-      if (g->head >= g->nch) continue;
-      const uint32_t h = g->khi, l = g->klo, m = g->meta;
-      if (!v || key_less(h, l, m, bh, bl, bm)) {
+    // pop: minimum over group heads of (~prio, depth|rank|sequence); exhausted
+    // groups carry meta = kExhausted and lose every comparison
+    uint32_t bh = 0xffffffffu, bl = 0xffffffffu, bm = kExhausted;
+    int bp = 0;
+    for (int q = lane; q < fr.A; q += 32) {
+      const uint32_t h = skh[q], l = skl[q], m = skm[q];
+      if (key_less(h, l, m, bh, bl, bm)) {
         bh = h;
         bl = l;
         bm = m;
-        bg = gi;
-        v = true;
+        bp = q;
       }
     }
-    const int win = warp_argmin3(v, bh, bl, bm);
+    const int win = warp_argmin3(bm != kExhausted, bh, bl, bm);
     if (win < 0) break;
-    const int gi = __shfl_sync(SSSD_FULL, bg, win);
-    Group* gp = fr.at(gi);
+    const uint32_t meta = __shfl_sync(SSSD_FULL, bm, win);
+    const uint32_t pkh = __shfl_sync(SSSD_FULL, bh, win), pkl = __shfl_sync(SSSD_FULL, bl, win);
+    const int pos = __shfl_sync(SSSD_FULL, bp, win);  // live-list slot of the popped group
+    const int gi = (int)(meta & 0x3fffffu);
+    Group* gp = fr.cold(gi);
     const Group g = *gp;
-    const Child h = g.ch[g.head];
-    const uint32_t D = g_depth(g.meta), rk = g_rank(g.meta);
+    const uint32_t ghead = g.head & 0xffffffu, gnch = g.nch & 0x7fffffffu;
+    const Child h = g.ch[ghead];
+    const uint32_t D = g_depth(meta), rk = g_rank(meta);
     const double dsc = c.disc[rk * c.disc_stride + D];
 
     // draft insert: an existing (parent, token) keeps the first node (ref fusion.py:185-198)
-    const int par = g.dparent;
+    const int par = (int)(g.head >> 24);
     int nid = -1;
     if (d_fc[par] >= 0) {
       for (int i0 = 1; i0 < size; i0 += 32) {
@@ -377,18 +410,18 @@ __global__ void __launch_bounds__(32)
 
     // advance the popped group's head
     {
-      uint32_t nh = g.nch, kh = 0xffffffffu, kl = 0xffffffffu;
-      if (g.sorted) {
-        nh = g.head + 1;
-        if (nh < g.nch) prio_key(__dmul_rn(g.ch[nh].pp, dsc), kh, kl);
+      uint32_t nh = gnch, kh = 0xffffffffu, kl = 0xffffffffu;
+      if (g.nch >> 31) {
+        nh = ghead + 1;
+        if (nh < gnch) prio_key(__dmul_rn(g.ch[nh].pp, dsc), kh, kl);
       } else {
         uint32_t bh2 = 0xffffffffu, bl2 = 0xffffffffu, bf2 = 0xffffffffu, bi2 = 0;
         bool bv2 = false;
-        for (uint32_t k = lane; k < g.nch; k += 32) {
+        for (uint32_t k = lane; k < gnch; k += 32) {
           const Child ck = g.ch[k];
           uint32_t hh, ll;
           prio_key(__dmul_rn(ck.pp, dsc), hh, ll);
-          if (key_less(g.khi, g.klo, h.first, hh, ll, ck.first) &&
+          if (key_less(pkh, pkl, h.first, hh, ll, ck.first) &&
               (!bv2 || key_less(hh, ll, ck.first, bh2, bl2, bf2))) {
             bh2 = hh;
             bl2 = ll;
@@ -405,10 +438,18 @@ __global__ void __launch_bounds__(32)
         }
       }
       if (lane == 0) {
-        gp->head = nh;
-        gp->khi = kh;
-        gp->klo = kl;
+        gp->head = (g.head & 0xff000000u) | nh;
+        if (nh < gnch) {
+          skh[pos] = kh;
+          skl[pos] = kl;
+        } else {  // exhausted: move the last live group into this slot
+          const int last = fr.A - 1;
+          skh[pos] = skh[last];
+          skl[pos] = skl[last];
+          skm[pos] = skm[last];
+        }
       }
+      if (nh >= gnch) --fr.A;
     }
     __syncwarp();
     // push the popped source node's children (ref fusion.py:258-259)

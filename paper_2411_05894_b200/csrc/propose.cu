@@ -259,7 +259,7 @@ __device__ int gather_p(const sssd_ds& ds, const KCfg& c, int p, uint64_t lo, ui
 __global__ void __launch_bounds__(32 * SSSD_MAX_P)
     ds_lookup_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, uint32_t* ds_tab, uint8_t* ds_len,
                      sssd_elem* ds_el, int32_t* ds_n, sssd_lookup_out lk, sssd_elem* ds_raw,
-                     uint32_t* ds_idx, int64_t idx_cap) {
+                     uint32_t* ds_idx, int64_t idx_cap, Cols cols) {
   const int b = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = lane_id();
   __shared__ uint32_t s_pat[SSSD_MAX_P];
@@ -353,7 +353,13 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P)
     for (int q = pcut; q <= pmax; ++q) n += s_cnt[q - 1];
     if (n > 0) {
       uint32_t* idx = (n <= SSSD_MAX_P * 32 * kRowStride) ? s_rows : ds_idx + (size_t)b * idx_cap;
-      block_sort_elems(raw, ds_el + (size_t)b * c.P * c.M, tab, n, idx);
+      sssd_elem* sorted = ds_el + (size_t)b * c.P * c.M;
+      block_sort_elems(raw, sorted, tab, n, idx);
+      if (cols.meta) {
+        const Cols cb{cols.meta + (size_t)b * cols.stride, cols.orig + (size_t)b * cols.stride,
+                      cols.tok + (size_t)b * cols.stride * c.BL, cols.stride};
+        for (int i = threadIdx.x; i < n; i += blockDim.x) write_cols(cb, i, sorted[i], tab);
+      }
     }
   } else if (p >= pcut && p <= pmax) {
     const int cnt = s_cnt[warp];
@@ -380,6 +386,11 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P)
       e.len_m = li | (255u << 8);
       e.pad = 0;
       ds_el[(size_t)b * c.P * c.M + rank] = e;
+      if (cols.meta) {
+        const Cols cb{cols.meta + (size_t)b * cols.stride, cols.orig + (size_t)b * cols.stride,
+                      cols.tok + (size_t)b * cols.stride * c.BL, cols.stride};
+        write_cols(cb, rank, e, tab);
+      }
     }
   }
   if (threadIdx.x == 0) {
@@ -402,7 +413,7 @@ constexpr int kSortSmem = 4096;
 
 __global__ void __launch_bounds__(256)
     input_scan_kernel(sssd_seqs seqs, KCfg c, sssd_elem* raw, sssd_elem* sorted, int32_t* in_n,
-                      uint32_t* idx_ws, int64_t cap, int64_t cap2) {
+                      uint32_t* idx_ws, int64_t cap, int64_t cap2, Cols cols) {
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   __shared__ uint32_t s_tail[SSSD_MAX_P];
@@ -451,12 +462,18 @@ __global__ void __launch_bounds__(256)
   if (base == 0) return;
   uint32_t* idx = (base <= kSortSmem) ? s_idx : idx_ws + (size_t)b * cap2;
   block_sort_elems(r, out, seq, base, idx);
+  if (cols.meta) {
+    const Cols cb{cols.meta + (size_t)b * cols.stride, cols.orig + (size_t)b * cols.stride,
+                  cols.tok + (size_t)b * cols.stride * c.IBL, cols.stride};
+    for (int i = tid; i < base; i += blockDim.x) write_cols(cb, i, out[i], seq);
+  }
 }
 
 // Sort caller-provided source paths (sssd_merge): one CTA per (request, source).
 __global__ void __launch_bounds__(256)
     sort_sources_kernel(const uint32_t* tok, const sssd_elem* el, const int64_t* el_off,
-                        const int32_t* el_n, sssd_elem* sorted, uint32_t* idx_ws, int64_t idx_cap) {
+                        const int32_t* el_n, sssd_elem* sorted, uint32_t* idx_ws, int64_t idx_cap,
+                        Cols cols) {
   __shared__ uint32_t s_idx[kSortSmem];
   const int bs = blockIdx.x;
   const int n = el_n[bs];
@@ -465,6 +482,7 @@ __global__ void __launch_bounds__(256)
   uint32_t* idx = (n <= kSortSmem) ? s_idx : idx_ws + o * 2;  // idx_ws holds 2*total entries
   (void)idx_cap;
   block_sort_elems(el + o, sorted + o, tok, n, idx);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) write_cols(cols, o + i, sorted[o + i], tok);
 }
 
 }  // namespace sssd

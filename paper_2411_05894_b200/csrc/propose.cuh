@@ -21,7 +21,7 @@ __global__ void find_ranges_kernel(sssd_ds ds, const uint32_t* pat, const int64_
 __global__ void ds_lookup_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, uint32_t* ds_tab,
                                  uint8_t* ds_len, sssd_elem* ds_el, int32_t* ds_n,
                                  sssd_lookup_out lk, sssd_elem* ds_raw, uint32_t* ds_idx,
-                                 int64_t idx_cap);
+                                 int64_t idx_cap, Cols cols);
 
 // scratch of the datastore lookup when a separator forces a block sort
 inline int64_t ds_idx_cap(int P, int M) {
@@ -30,19 +30,21 @@ inline int64_t ds_idx_cap(int P, int M) {
   return p2;
 }
 __global__ void input_scan_kernel(sssd_seqs seqs, KCfg c, sssd_elem* raw, sssd_elem* sorted,
-                                  int32_t* in_n, uint32_t* idx_ws, int64_t cap, int64_t cap2);
+                                  int32_t* in_n, uint32_t* idx_ws, int64_t cap, int64_t cap2,
+                                  Cols cols);
 __global__ void sort_sources_kernel(const uint32_t* tok, const sssd_elem* el,
                                     const int64_t* el_off, const int32_t* el_n, sssd_elem* sorted,
-                                    uint32_t* idx_ws, int64_t idx_cap);
+                                    uint32_t* idx_ws, int64_t idx_cap, Cols cols);
 struct Group;
 __global__ void draft_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, Child* slabs,
                              uint32_t slab_cap, Child* pool, unsigned long long* cursor,
-                             uint64_t pool_cap, int32_t* err, Group* gover, int gover_cap,
+                             uint64_t pool_cap, int32_t* err, uint8_t* gover, int64_t gover_bytes,
                              sssd_draft_out out);
 
 constexpr int kChildBytes = 32;
-constexpr int kGroupBytes = 32;
-constexpr int kGroupSmem = 192;  // groups kept in shared memory; the rest spill to global
+constexpr int kGroupBytes = 16;  // cold group record
+constexpr int kGroupSmem = 128;  // groups kept in shared memory; later ones spill to global
+constexpr int kChildSmem = 96;   // child records in the shared-memory slab
 
 // Upper bound on sibling groups: one per source seed plus one per pop, and a
 // draft node can be popped at most once per source.
@@ -51,12 +53,14 @@ __host__ __device__ inline int draft_max_groups(int P, int S) { return (P + 1) *
 inline int draft_smem_bytes(int P, int S) {
   const int G = draft_max_groups(P, S);
   const int Gs = G < kGroupSmem ? G : kGroupSmem;
-  return Gs * kGroupBytes + S * 4 + S * 2 * 8 + 16;
+  return kChildSmem * kChildBytes + Gs * kGroupBytes + G * 12 + S * 4 + S * 2 * 8 + 16;
 }
 
-inline int draft_group_overflow(int P, int S) {
+// global overflow bytes per request: cold records of groups >= kGroupSmem
+inline int64_t draft_group_overflow_bytes(int P, int S) {
   const int G = draft_max_groups(P, S);
-  return G > kGroupSmem ? G - kGroupSmem : 0;
+  const int Go = G > kGroupSmem ? G - kGroupSmem : 0;
+  return ((int64_t)Go * kGroupBytes + 127) / 128 * 128;
 }
 
 }  // namespace sssd
