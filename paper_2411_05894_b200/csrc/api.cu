@@ -71,6 +71,8 @@ static int merge_depth(const sssd_cfg* cfg) { return cfg->disc_stride - 1; }
 
 static KCfg kcfg(const sssd_cfg* c) {
   KCfg k;
+  k.b0 = 0;
+  k.b1 = 0;
   k.P = c->P;
   k.S = c->dec_len;
   k.BL = c->branch_len;
@@ -173,8 +175,8 @@ static PropWs carve_propose(uint8_t* base, const sssd_cfg* c, int B, int max_len
 
 __global__ void propose_setup_kernel(sssd_seqs seqs, KCfg c, Cols dsc, const int32_t* ds_n,
                                      Cols inc, const int32_t* in_n, SrcDesc* desc, uint32_t* root) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= seqs.B) return;
+  const int b = c.b0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= c.b1) return;
   const int L = seqs.seq_len[b];
   root[b] = seqs.seq[seqs.seq_off[b] + L - 1];
   SrcDesc* d = desc + (size_t)b * (c.P + 1);
@@ -258,6 +260,32 @@ size_t sssd_propose_workspace(const sssd_cfg* cfg, int32_t B, int32_t max_len) {
   return carve_propose(nullptr, cfg, B, max_len).bytes;
 }
 
+// Library-internal streams used to fork the independent propose stages off the
+// caller's stream (joined back with events, so the caller sees stream order).
+struct Aux {
+  cudaStream_t s[2];
+  cudaEvent_t fork;
+  cudaEvent_t done[2][8];
+};
+
+static Aux* aux_streams() {
+  static Aux aux[16];
+  static bool ready[16] = {false};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+  if (!ready[dev]) {
+    Aux& x = aux[dev];
+    for (auto& s : x.s)
+      if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    if (cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    for (auto& row : x.done)
+      for (auto& e : row)
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    ready[dev] = true;
+  }
+  return &aux[dev];
+}
+
 static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
                         const sssd_draft_out* out, const sssd_lookup_out* lookup, void* workspace,
                         size_t workspace_bytes, void* stream, cudaEvent_t* ev);
@@ -301,30 +329,79 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
   if (!workspace || workspace_bytes < w.bytes)
     return fail(SSSD_E_WORKSPACE, "propose needs %zu workspace bytes, got %zu", w.bytes, workspace_bytes);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const KCfg k = kcfg(cfg);
+  KCfg k = kcfg(cfg);
   sssd_lookup_out lk{};
   if (lookup) lk = *lookup;
   if ((rc = cuda_check(cudaMemsetAsync(w.d.cursor, 0, 16, st), "memset status"))) return rc;
-  if (ev) cudaEventRecord(ev[0], st);
-  if (cfg->use_datastore) {
-    ds_lookup_kernel<<<B, 32 * cfg->P, 0, st>>>(*ds, *seqs, k, w.ds_tab, w.ds_len, w.ds_el, w.ds_n, lk,
-                                                 w.ds_raw, w.ds_idx, w.ds_idx_cap, w.ds_cols);
-    if ((rc = cuda_check(cudaGetLastError(), "ds_lookup_kernel launch"))) return rc;
+  const int smem = draft_smem_bytes(k.P, k.S);
+  if ((rc = cuda_check(cudaFuncSetAttribute(draft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                       "draft_kernel smem attribute")))
+    return rc;
+
+  auto launch_lookup = [&](cudaStream_t s, int b0, int b1) {
+    KCfg kk = k;
+    kk.b0 = b0;
+    kk.b1 = b1;
+    ds_lookup_kernel<<<b1 - b0, 32 * cfg->P, 0, s>>>(*ds, *seqs, kk, w.ds_tab, w.ds_len, w.ds_el, w.ds_n, lk,
+                                                       w.ds_raw, w.ds_idx, w.ds_idx_cap, w.ds_cols);
+  };
+  auto launch_scan = [&](cudaStream_t s, int b0, int b1) {
+    KCfg kk = k;
+    kk.b0 = b0;
+    kk.b1 = b1;
+    input_scan_kernel<<<b1 - b0, 256, 0, s>>>(*seqs, kk, w.in_raw, w.in_el, w.in_n, w.idx, w.cap, w.cap2,
+                                               w.in_cols);
+  };
+  auto launch_fuse = [&](cudaStream_t s, int b0, int b1) {
+    KCfg kk = k;
+    kk.b0 = b0;
+    kk.b1 = b1;
+    propose_setup_kernel<<<(b1 - b0 + 127) / 128, 128, 0, s>>>(*seqs, kk, w.ds_cols, w.ds_n, w.in_cols,
+                                                                 w.in_n, w.d.desc, w.d.root);
+    draft_kernel<<<b1 - b0, 32, smem, s>>>(w.d.desc, w.d.root, kk, w.d.slabs, kSlabChildren, w.d.pool,
+                                           w.d.cursor, w.d.pool_cap, w.d.err, w.d.gover, w.d.gover_bytes, *out);
+  };
+
+  if (ev) {  // profiling: stages back to back on the caller's stream
+    cudaEventRecord(ev[0], st);
+    if (cfg->use_datastore) launch_lookup(st, 0, B);
+    cudaEventRecord(ev[1], st);
+    if (cfg->use_input) launch_scan(st, 0, B);
+    cudaEventRecord(ev[2], st);
+    KCfg kk = k;
+    kk.b0 = 0;
+    kk.b1 = B;
+    propose_setup_kernel<<<(B + 127) / 128, 128, 0, st>>>(*seqs, kk, w.ds_cols, w.ds_n, w.in_cols, w.in_n,
+                                                            w.d.desc, w.d.root);
+    cudaEventRecord(ev[3], st);
+    draft_kernel<<<B, 32, smem, st>>>(w.d.desc, w.d.root, kk, w.d.slabs, kSlabChildren, w.d.pool, w.d.cursor,
+                                      w.d.pool_cap, w.d.err, w.d.gover, w.d.gover_bytes, *out);
+    cudaEventRecord(ev[4], st);
+    return cuda_check(cudaGetLastError(), "propose launch");
   }
-  if (ev) cudaEventRecord(ev[1], st);
-  if (cfg->use_input) {
-    input_scan_kernel<<<B, 256, 0, st>>>(*seqs, k, w.in_raw, w.in_el, w.in_n, w.idx, w.cap, w.cap2,
-                                         w.in_cols);
-    if ((rc = cuda_check(cudaGetLastError(), "input_scan_kernel launch"))) return rc;
+
+  // The lookup and the input scan are independent and both latency-bound: run
+  // them on two forked streams, chunk the batch, and let the fusion kernel of
+  // chunk i (caller's stream) overlap the lookup / scan of chunk i+1.
+  Aux* ax = aux_streams();
+  if (!ax) return fail(SSSD_E_CUDA, "could not create auxiliary streams");
+  const int chunks = 1;  // chunked pipelining measured slower: each chunk pays a fusion-kernel tail
+  const int per = (B + chunks - 1) / chunks;
+  cudaEventRecord(ax->fork, st);
+  cudaStreamWaitEvent(ax->s[0], ax->fork, 0);
+  cudaStreamWaitEvent(ax->s[1], ax->fork, 0);
+  for (int ci = 0; ci < chunks; ++ci) {
+    const int b0 = ci * per, b1 = min(B, b0 + per);
+    if (b0 >= b1) break;
+    if (cfg->use_datastore) launch_lookup(ax->s[0], b0, b1);
+    if (cfg->use_input) launch_scan(ax->s[1], b0, b1);
+    cudaEventRecord(ax->done[0][ci], ax->s[0]);
+    cudaEventRecord(ax->done[1][ci], ax->s[1]);
+    cudaStreamWaitEvent(st, ax->done[0][ci], 0);
+    cudaStreamWaitEvent(st, ax->done[1][ci], 0);
+    launch_fuse(st, b0, b1);
   }
-  if (ev) cudaEventRecord(ev[2], st);
-  propose_setup_kernel<<<(B + 127) / 128, 128, 0, st>>>(*seqs, k, w.ds_cols, w.ds_n, w.in_cols, w.in_n,
-                                                          w.d.desc, w.d.root);
-  if ((rc = cuda_check(cudaGetLastError(), "propose_setup_kernel launch"))) return rc;
-  if (ev) cudaEventRecord(ev[3], st);
-  rc = launch_draft(w.d, k, B, out, st);
-  if (ev) cudaEventRecord(ev[4], st);
-  return rc;
+  return cuda_check(cudaGetLastError(), "propose launch");
 }
 
 // Returns the device status word of the last propose / merge that used this

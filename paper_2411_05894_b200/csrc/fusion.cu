@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(32, 32)
                  uint32_t slab_cap, Child* pool, unsigned long long* cursor, uint64_t pool_cap,
                  int32_t* err, uint8_t* gover, int64_t gover_bytes, sssd_draft_out out) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int b = blockIdx.x;
+  const int b = c.b0 + blockIdx.x;
   const int lane = lane_id();
   const int S = c.S;
   const int W = (S + 63) >> 6;

@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P)
     ds_lookup_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, uint32_t* ds_tab, uint8_t* ds_len,
                      sssd_elem* ds_el, int32_t* ds_n, sssd_lookup_out lk, sssd_elem* ds_raw,
                      uint32_t* ds_idx, int64_t idx_cap, Cols cols) {
-  const int b = blockIdx.x;
+  const int b = c.b0 + blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = lane_id();
   __shared__ uint32_t s_pat[SSSD_MAX_P];
   __shared__ uint64_t s_lo[SSSD_MAX_P], s_hi[SSSD_MAX_P];
@@ -414,7 +414,7 @@ constexpr int kSortSmem = 4096;
 __global__ void __launch_bounds__(256)
     input_scan_kernel(sssd_seqs seqs, KCfg c, sssd_elem* raw, sssd_elem* sorted, int32_t* in_n,
                       uint32_t* idx_ws, int64_t cap, int64_t cap2, Cols cols) {
-  const int b = blockIdx.x;
+  const int b = c.b0 + blockIdx.x;
   const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   __shared__ uint32_t s_tail[SSSD_MAX_P];
   __shared__ int s_wsum[8];

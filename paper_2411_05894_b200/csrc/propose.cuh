@@ -7,6 +7,7 @@
 namespace sssd {
 
 struct KCfg {
+  int b0, b1;  // request range [b0, b1) handled by this launch (blockIdx.x is relative to b0)
   int P, S, BL, IBL, M, T, use_ds, use_in, n_trees, has_sep;
   uint32_t sep;
   int disc_stride;
