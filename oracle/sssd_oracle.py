@@ -498,3 +498,40 @@ def hash_oracle_next(ctx, alphabet: int, salt: int = 0) -> int:
     for tok in list(ctx[-3:]):
         h = (h * 31 + int(tok) + 7) & 0xFFFFFFFF
     return h % alphabet
+
+
+# ---------------------------------------------------------------------------
+# C restatement of the SA build (oracle/sa_oracle.c), for host-side baselines
+# ---------------------------------------------------------------------------
+
+_HERE = __import__("os").path.dirname(__import__("os").path.abspath(__file__))
+_SA_LIB = __import__("os").path.join(_HERE, "_build", "libsa_oracle.so")
+
+
+def build_c_oracle() -> str:
+    """Compile oracle/sa_oracle.c with gcc (called by __graft_entry__.build())."""
+    import os
+    import subprocess
+
+    src = os.path.join(_HERE, "sa_oracle.c")
+    os.makedirs(os.path.dirname(_SA_LIB), exist_ok=True)
+    if not os.path.exists(_SA_LIB) or os.path.getmtime(_SA_LIB) < os.path.getmtime(src):
+        subprocess.run(["gcc", "-O3", "-shared", "-fPIC", "-o", _SA_LIB, src], check=True)
+    return _SA_LIB
+
+
+def suffix_array_c(tokens) -> np.ndarray:
+    """Same result as suffix_array(), via the C oracle (u32 positions)."""
+    import ctypes
+
+    t = np.ascontiguousarray(np.asarray(tokens), dtype=np.uint32)
+    n = int(t.size)
+    if n == 0:
+        raise ValueError("empty corpus")
+    lib = ctypes.CDLL(build_c_oracle())
+    out = np.empty(n, dtype=np.uint32)
+    rc = lib.sa_oracle_build(t.ctypes.data_as(ctypes.c_void_p), ctypes.c_uint64(n),
+                             out.ctypes.data_as(ctypes.c_void_p))
+    if rc != 0:
+        raise RuntimeError(f"sa_oracle_build failed ({rc})")
+    return out
