@@ -94,6 +94,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   }
 }
 
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -140,26 +146,32 @@ struct Params {
   float* part_ml;        // [splits][B][Hq][S][2]
   int B, S, Hq, Hkv, G, max_pos, W, splits, split_len;
   float scale_log2;
-  int dbg;  // debug early exit stage (0 = off)
 };
 
-// stage rows [0, nrows) of a 128 x 128 bf16 tile; rows >= nrows are zeroed
-__device__ __forceinline__ void stage_tile(uint8_t* tile, const uint16_t* src, int64_t row_stride, int nrows) {
+// asynchronous staging of rows [0, nrows) of a 128 x 128 bf16 tile into the
+// core-matrix layout (cp.async, 16 B per op, all in flight); rows >= nrows are
+// zero-filled (src-size 0) so masked keys contribute 0 * 0 to P V
+__device__ __forceinline__ void stage_tile_async(uint8_t* tile, const uint16_t* src, int64_t row_stride,
+                                                 int nrows) {
+#pragma unroll 4
   for (int idx = threadIdx.x; idx < kM * 16; idx += kThreads) {
     const int r = idx >> 4, c8 = idx & 15;
-    uint4 val = make_uint4(0, 0, 0, 0);
-    if (r < nrows) val = __ldg(reinterpret_cast<const uint4*>(src + (int64_t)r * row_stride) + c8);
-    *reinterpret_cast<uint4*>(tile + tile_off(r, c8)) = val;
+    const uint16_t* g = src + (int64_t)(r < nrows ? r : 0) * row_stride + c8 * 8;
+    const uint32_t bytes = r < nrows ? 16u : 0u;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(tile + tile_off(r, c8))), "l"(g),
+                 "r"(bytes)
+                 : "memory");
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 __global__ void __launch_bounds__(kThreads, 1) tree_attn_kernel(Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem;
-  uint8_t* sK = smem + kTile;
-  uint8_t* sV = smem + 2 * kTile;
-  uint8_t* sP = smem + 3 * kTile;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 4 * kTile);
+  uint8_t* sKb[2] = {smem + kTile, smem + 2 * kTile};
+  uint8_t* sVb[2] = {smem + 3 * kTile, smem + 4 * kTile};
+  uint8_t* sP = smem + 5 * kTile;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 6 * kTile);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -201,18 +213,12 @@ __global__ void __launch_bounds__(kThreads, 1) tree_attn_kernel(Params p) {
   fence_after();
   const uint32_t tbase = *tslot;
   const uint32_t tS = tbase, tO = tbase + 128;
-  if (p.dbg == 1) {
-    if (tid == 0) printf("dbg1 tbase=%u\n", tbase);
-    __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(256));
-    return;
-  }
+
   const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-  const uint64_t mrow = row_ok ? p.mask[((int64_t)b * p.S + qi) * p.W] : 0;  // S <= 64 per word
   const uint64_t* mrow_all = p.mask + ((int64_t)b * p.S + qi) * p.W;
 
   const uint32_t id_qk = idesc_bf16(false), id_pv = idesc_bf16(true);
-  const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV), aP = smem_u32(sP);
+  const uint32_t aQ = smem_u32(sQ), aP = smem_u32(sP);
   const int64_t kv_stride = (int64_t)p.max_pos * kD;
   const uint16_t* kbase = p.k + ((int64_t)b * p.Hkv + kvh) * kv_stride;
   const uint16_t* vbase = p.v + ((int64_t)b * p.Hkv + kvh) * kv_stride;
@@ -220,10 +226,24 @@ __global__ void __launch_bounds__(kThreads, 1) tree_attn_kernel(Params p) {
   float m_run = -INFINITY, l_run = 0.f;
   uint32_t phase = 0;
   bool first = true;
-  for (int k0 = kv0; k0 < kv1; k0 += kN) {
-    const int nk = min(kN, kv1 - k0);
-    stage_tile(sK, kbase + (int64_t)k0 * kD, kD, nk);
-    stage_tile(sV, vbase + (int64_t)k0 * kD, kD, nk);
+  if (kv0 < kv1) {  // prefetch block 0
+    const int nk = min(kN, kv1 - kv0);
+    stage_tile_async(sKb[0], kbase + (int64_t)kv0 * kD, kD, nk);
+    stage_tile_async(sVb[0], vbase + (int64_t)kv0 * kD, kD, nk);
+  }
+  int buf = 0;
+  for (int k0 = kv0; k0 < kv1; k0 += kN, buf ^= 1) {
+    // prefetch the next block into the other buffer (its last readers, the
+    // MMAs of the previous block, completed before this iteration)
+    if (k0 + kN < kv1) {
+      const int nk2 = min(kN, kv1 - (k0 + kN));
+      stage_tile_async(sKb[buf ^ 1], kbase + (int64_t)(k0 + kN) * kD, kD, nk2);
+      stage_tile_async(sVb[buf ^ 1], vbase + (int64_t)(k0 + kN) * kD, kD, nk2);
+      asm volatile("cp.async.wait_group 2;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    const uint32_t aK = smem_u32(sKb[buf]), aV = smem_u32(sVb[buf]);
     fence_async_smem();
     __syncthreads();
     if (tid == 0) {
@@ -233,54 +253,59 @@ __global__ void __launch_bounds__(kThreads, 1) tree_attn_kernel(Params p) {
         mma_bf16(tS, smem_desc(aQ + ks * 256, 128, 2048), smem_desc(aK + ks * 256, 128, 2048), id_qk, ks > 0);
       mma_commit(bar);
     }
-    if (p.dbg == 2 && tid == 0) printf("dbg2 issued S mma\n");
     mbar_wait(bar, phase);
     phase ^= 1;
     fence_after();
-    if (p.dbg == 2) {
-      if (tid == 0) printf("dbg2 S done\n");
-      break;
-    }
 
-    // online softmax over this block (one thread per query row)
+    // online softmax over this block (one thread per query row).  Visibility of
+    // the 32 keys of chunk c is one word: prefix keys are all visible, tree key
+    // t is visible iff bit t of this row's ancestor mask is set.
+    uint32_t visw[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int key0 = k0 + c * 32;
+      uint32_t w = 0;
+      if (row_ok) {
+        const int lim = min(32, kv1 - key0);  // keys past the range are invisible
+        w = lim >= 32 ? 0xffffffffu : (lim > 0 ? (1u << lim) - 1u : 0u);
+        if (key0 + 32 > ctx) {  // chunk overlaps the tree region
+          uint32_t tree = 0;
+#pragma unroll 1
+          for (int jj = max(0, ctx - key0); jj < 32; ++jj) {
+            const int t = key0 + jj - ctx;
+            if (t < p.S && ((mrow_all[t >> 6] >> (t & 63)) & 1ull)) tree |= 1u << jj;
+          }
+          const uint32_t pref = ctx - key0 >= 32 ? 0xffffffffu : (ctx > key0 ? (1u << (ctx - key0)) - 1u : 0u);
+          w &= pref | tree;
+        }
+      }
+      visw[c] = w;
+    }
     float sv[32];
     float bmax = -INFINITY;
-#pragma unroll
+#pragma unroll 1
     for (int c = 0; c < 4; ++c) {
       tmem_ld32(tS + lane_off + c * 32, sv);
+      const uint32_t w = visw[c];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int key = k0 + c * 32 + j;
-        bool vis = key < kv1;
-        if (key >= ctx) {
-          const int t = key - ctx;
-          vis = vis && (((t < 64 ? mrow : mrow_all[t >> 6]) >> (t & 63)) & 1ull);
-        }
-        if (vis && row_ok) bmax = fmaxf(bmax, sv[j] * p.scale_log2);
-      }
+      for (int j = 0; j < 32; ++j)
+        if ((w >> j) & 1u) bmax = fmaxf(bmax, sv[j]);
     }
+    bmax = (bmax == -INFINITY) ? bmax : bmax * p.scale_log2;
     const float m_new = fmaxf(m_run, bmax);
-    const float corr = (m_run == -INFINITY) ? 0.f : exp2f(m_run - m_new);
+    const float corr = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - m_new);
     float psum = 0.f;
-#pragma unroll
+#pragma unroll 1
     for (int c = 0; c < 4; ++c) {
       tmem_ld32(tS + lane_off + c * 32, sv);
+      const uint32_t w = (m_new == -INFINITY) ? 0u : visw[c];
       uint32_t pk[16];
 #pragma unroll
       for (int j = 0; j < 32; j += 2) {
-        float e[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int key = k0 + c * 32 + j + u;
-          bool vis = key < kv1 && row_ok;
-          if (key >= ctx) {
-            const int t = key - ctx;
-            vis = vis && (((t < 64 ? mrow : mrow_all[t >> 6]) >> (t & 63)) & 1ull);
-          }
-          e[u] = (vis && m_new != -INFINITY) ? exp2f(sv[j + u] * p.scale_log2 - m_new) : 0.f;
-          psum += e[u];
-        }
-        const __nv_bfloat162 h2 = __floats2bfloat162_rn(e[0], e[1]);
+        const float e0 = ((w >> j) & 1u) ? fast_exp2(fmaf(sv[j], p.scale_log2, -m_new)) : 0.f;
+        const float e1 = ((w >> (j + 1)) & 1u) ? fast_exp2(fmaf(sv[j + 1], p.scale_log2, -m_new)) : 0.f;
+        psum += e0 + e1;
+        const __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
         pk[j >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
       }
 #pragma unroll
@@ -293,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) tree_attn_kernel(Params p) {
     // whole warp takes the branch when any of its rows needs it
     if (!first && __any_sync(SSSD_FULL, corr != 1.f)) {
       float ov[32];
-#pragma unroll
+#pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         tmem_ld32(tO + lane_off + c * 32, ov);
 #pragma unroll
@@ -391,7 +416,7 @@ __global__ void tree_attn_combine_kernel(Params p) {
   p.o[(((int64_t)b * p.S + i) * p.Hq + head) * kD + d] = __bfloat16_as_ushort(__float2bfloat16_rn(out));
 }
 
-constexpr int kSmem = 4 * kTile + 64;
+constexpr int kSmem = 6 * kTile + 64;
 
 }  // namespace attn
 }  // namespace sssd
@@ -439,10 +464,7 @@ int sssd_tree_attention(const uint16_t* q, const uint16_t* k, const uint16_t* v,
   p.max_pos = max_pos;
   p.W = (S + 63) / 64;
   p.scale_log2 = scale * 1.4426950408889634f;
-  {
-    const char* e = getenv("SSSD_ATTN_DBG");
-    p.dbg = e ? atoi(e) : 0;
-  }
+
   p.splits = attn_splits(B, Hq, Hkv, S, max_pos);
   p.split_len = ((max_pos + p.splits - 1) / p.splits + attn::kN - 1) / attn::kN * attn::kN;
   const size_t need = (size_t)p.splits * B * Hq * S * (attn::kD + 2) * sizeof(float) + 256;
