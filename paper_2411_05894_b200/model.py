@@ -1,0 +1,156 @@
+"""Random-init Llama-style decoders for the verification forward.
+
+The reference has no model; its oracle protocol (ref draft.py:29-32,
+205-210) asks, for every draft node i, the greedy next token after
+``sequence + path(i)``.  ``Decoder.verify`` answers all nodes of a batch of
+drafts in ONE forward: the draft tokens are run at positions L-1+depth, their
+K/V rows are written to the cache at [ctx, ctx+S), and attention is the
+tcgen05 tree kernel (prefix + ancestor-or-self mask).  Dense projections use
+cuBLAS through torch (plain library GEMMs); RMSNorm / RoPE / SwiGLU are
+elementwise torch ops.
+
+Specs:
+  TINY       2 layers, h=1024, n_q=8, n_kv=2, d=128, SwiGLU 2816, V=32000
+  LLAMA3_8B  32 layers, h=4096, n_q=32, n_kv=8, d=128, SwiGLU 14336, V=128256
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from .verify import kv_compact, tree_attention
+
+
+@dataclass(frozen=True)
+class ModelSpec:
+    n_layers: int
+    hidden: int
+    n_q: int
+    n_kv: int
+    mlp: int
+    vocab: int
+    head_dim: int = 128
+    rope_theta: float = 500000.0
+    eps: float = 1e-5
+
+
+TINY = ModelSpec(2, 1024, 8, 2, 2816, 32000)
+LLAMA3_8B = ModelSpec(32, 4096, 32, 8, 14336, 128256)
+
+
+def _rope(x: torch.Tensor, pos: torch.Tensor, theta: float) -> torch.Tensor:
+    """x [..., S, H, D] (any float), pos [..., S] int -> rotated (float32 math)."""
+    D = x.shape[-1]
+    inv = 1.0 / (theta ** (torch.arange(0, D, 2, device=x.device, dtype=torch.float32) / D))
+    ang = pos.to(torch.float32)[..., None] * inv  # [..., S, D/2]
+    cos, sin = ang.cos()[..., None, :], ang.sin()[..., None, :]
+    xf = x.float()
+    x1, x2 = xf[..., : D // 2], xf[..., D // 2:]
+    return torch.cat([x1 * cos - x2 * sin, x1 * sin + x2 * cos], dim=-1)
+
+
+def _rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
+    xf = x.float()
+    return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps) * w.float()).to(x.dtype)
+
+
+class Decoder:
+    """bf16 weights (seeded random init), KV cache [layers, B, n_kv, max_pos, d]."""
+
+    def __init__(self, spec: ModelSpec, batch: int, max_pos: int, device="cuda", seed: int = 0,
+                 dtype=torch.bfloat16) -> None:
+        self.spec, self.B, self.max_pos, self.device, self.dtype = spec, batch, max_pos, torch.device(device), dtype
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        h, d = spec.hidden, spec.head_dim
+
+        def w(*shape, scale):
+            return (torch.randn(*shape, generator=g) * scale).to(dtype).to(self.device)
+
+        self.embed = w(spec.vocab, h, scale=1.0)
+        self.layers = []
+        for _ in range(spec.n_layers):
+            self.layers.append({
+                "n1": torch.ones(h, dtype=dtype, device=self.device),
+                "wq": w(h, spec.n_q * d, scale=1 / math.sqrt(h)),
+                "wk": w(h, spec.n_kv * d, scale=1 / math.sqrt(h)),
+                "wv": w(h, spec.n_kv * d, scale=1 / math.sqrt(h)),
+                "wo": w(spec.n_q * d, h, scale=1 / math.sqrt(spec.n_q * d)),
+                "n2": torch.ones(h, dtype=dtype, device=self.device),
+                "wg": w(h, spec.mlp, scale=1 / math.sqrt(h)),
+                "wu": w(h, spec.mlp, scale=1 / math.sqrt(h)),
+                "wd": w(spec.mlp, h, scale=1 / math.sqrt(spec.mlp)),
+            })
+        self.norm = torch.ones(h, dtype=dtype, device=self.device)
+        self.lm_head = w(h, spec.vocab, scale=1 / math.sqrt(h))
+        self.k_cache = torch.zeros(spec.n_layers, batch, spec.n_kv, max_pos, d, dtype=dtype, device=self.device)
+        self.v_cache = torch.zeros_like(self.k_cache)
+        self.scale = 1.0 / math.sqrt(d)
+
+    def forward(self, tokens: torch.Tensor, positions: torch.Tensor, mask: torch.Tensor,
+                ctx_len: torch.Tensor, rows: torch.Tensor | None = None) -> torch.Tensor:
+        """Tree forward: tokens / positions [b, S] (rows = cache rows of these b
+        requests, default all), mask [b, S, W] int64, ctx_len [b] int32 = committed
+        tokens already in the cache.  Writes K/V of the S tokens to cache
+        positions ctx..ctx+S-1 and returns logits [b, S, V] (fp32)."""
+        sp = self.spec
+        b, S = tokens.shape
+        rows = torch.arange(self.B, device=self.device) if rows is None else rows
+        d = sp.head_dim
+        x = self.embed[tokens.long()]  # [b, S, h]
+        slot = ctx_len.long()[:, None] + torch.arange(S, device=self.device)[None, :]  # [b, S]
+        bi = rows.long()[:, None].expand(b, S)
+        for li, L in enumerate(self.layers):
+            hN = _rmsnorm(x, L["n1"], sp.eps)
+            q = (hN @ L["wq"]).view(b, S, sp.n_q, d)
+            k = (hN @ L["wk"]).view(b, S, sp.n_kv, d)
+            v = (hN @ L["wv"]).view(b, S, sp.n_kv, d)
+            q = _rope(q, positions, sp.rope_theta).to(self.dtype).contiguous()
+            k = _rope(k, positions, sp.rope_theta).to(self.dtype)
+            kc, vc = self.k_cache[li], self.v_cache[li]
+            kc[bi, :, slot] = k
+            vc[bi, :, slot] = v
+            if rows.numel() == self.B:
+                o = tree_attention(q, kc, vc, mask, ctx_len.to(torch.int32), self.scale)
+            else:
+                o = tree_attention(q, kc[rows].contiguous(), vc[rows].contiguous(), mask,
+                                   ctx_len.to(torch.int32), self.scale)
+            x = x + o.view(b, S, sp.n_q * d) @ L["wo"]
+            hN = _rmsnorm(x, L["n2"], sp.eps)
+            x = x + (torch.nn.functional.silu(hN @ L["wg"]) * (hN @ L["wu"])) @ L["wd"]
+        return (_rmsnorm(x, self.norm, sp.eps) @ self.lm_head).float()
+
+    def prefill(self, prompts: list, chunk: int = 256) -> None:
+        """Write the cache for prompts[b][:-1] (the last prompt token is the first
+        draft root) through the tree kernel with causal chain masks."""
+        B = len(prompts)
+        assert B == self.B
+        n = [len(p) - 1 for p in prompts]
+        done = [0] * B
+        while any(done[b] < n[b] for b in range(B)):
+            S = min(chunk, max(n[b] - done[b] for b in range(B)))
+            S = max(S, 1)
+            toks = torch.zeros(B, S, dtype=torch.int64)
+            for b in range(B):
+                seg = prompts[b][done[b]: min(n[b], done[b] + S)]
+                toks[b, : len(seg)] = torch.tensor([int(t) for t in seg])
+            W = (S + 63) // 64
+            bits = torch.tril(torch.ones(S, S, dtype=torch.bool))
+            mask = torch.zeros(S, W, dtype=torch.int64)
+            for w in range(W):
+                blk = bits[:, 64 * w: 64 * (w + 1)].to(torch.int64)
+                sh = torch.arange(blk.shape[1], dtype=torch.int64)
+                mask[:, w] = (blk << sh).sum(-1)
+            ctx = torch.tensor(done, dtype=torch.int32, device=self.device)
+            pos = ctx.long()[:, None] + torch.arange(S, device=self.device)[None, :]
+            self.forward(toks.to(self.device), pos, mask[None].expand(B, S, W).contiguous().to(self.device), ctx)
+            for b in range(B):
+                done[b] = min(n[b], done[b] + S)
+
+    def compact(self, ctx_len: torch.Tensor, path: torch.Tensor, n_acc: torch.Tensor) -> None:
+        """Move the K/V rows of accepted draft nodes (cache slot ctx + node) to
+        ctx + 1 + k, all layers, in one launch each for K and V."""
+        kv_compact(self.k_cache, ctx_len, path, n_acc)
+        kv_compact(self.v_cache, ctx_len, path, n_acc)
