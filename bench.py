@@ -313,6 +313,24 @@ def run_ours(args) -> None:
         ctxs = [mine[i * CTX:(i + 1) * CTX].tolist() for i in range(min(B, 256))]
         base = cpu_baseline(tokens_h, sa_h, ctxs)
 
+    extra = {}
+    if rank == 0 and world == 1 and not args.no_extra:
+        pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0}
+        try:
+            extra["verify_attention"] = bench_verify(peak, float(pk.get("bf16_tflops", 1590.0)))
+        except Exception as exc:  # report, never hide
+            extra["verify_attention"] = {"error": repr(exc)}
+        try:
+            extra["decode_cfg1"] = bench_decode_cfg1()
+        except Exception as exc:
+            extra["decode_cfg1"] = {"error": repr(exc)}
+        if args.decode_8b:
+            try:
+                extra["decode_cfg3"] = bench_decode_cfg3()
+            except Exception as exc:
+                extra["decode_cfg3"] = {"error": repr(exc)}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -339,11 +357,129 @@ def run_ours(args) -> None:
         }
         if base is not None:
             line["cpu_baseline"] = base
+        line.update(extra)
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def bench_verify(peak: float, peak_tf: float) -> dict:
+    """Tree-attention kernel (tcgen05) at the cfg3 / cfg4 shapes, one layer:
+    SURVEY 8(d) bytes = 2*b*n_kv*(s_kv+s_q)*d*2 + 2*b*n_q*s_q*d*2 + 8*b*s_q,
+    flops = 4*b*s_q*(s_kv+s_q)*n_q*d."""
+    import torch
+
+    from paper_2411_05894_b200.verify import tree_attention
+
+    out = {}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for name, (B, S, Hq, Hkv, ctx) in {"cfg3": (32, 32, 32, 8, 4096), "cfg4": (8, 16, 32, 8, 32768)}.items():
+        q = torch.randn(B, S, Hq, 128, device="cuda").bfloat16()
+        k = torch.randn(B, Hkv, ctx + S, 128, device="cuda").bfloat16()
+        v = torch.randn(B, Hkv, ctx + S, 128, device="cuda").bfloat16()
+        mask = torch.full((B, S, 1), -1, dtype=torch.int64, device="cuda")
+        c = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
+        for _ in range(3):
+            tree_attention(q, k, v, mask, c)
+        ts = []
+        for _ in range(10):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            tree_attention(q, k, v, mask, c)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        ms = float(np.median(ts))
+        byt = 2 * B * Hkv * (ctx + S) * 128 * 2 + 2 * B * Hq * S * 128 * 2 + 8 * B * S
+        fl = 4 * B * S * (ctx + S) * Hq * 128
+        out[name] = {"shape": f"b={B} s_q={S} s_kv={ctx} n_q={Hq} n_kv={Hkv} d=128", "ms_per_layer": round(ms, 4),
+                     "achieved_GBps": round(byt / ms / 1e6, 1), "hbm_frac": round(byt / ms / 1e6 / peak, 4),
+                     "achieved_TFLOPs": round(fl / ms / 1e9, 1), "tensor_frac": round(fl / ms / 1e9 / peak_tf, 4)}
+        del q, k, v
+    return out
+
+
+def bench_decode_cfg1(budget_s: float = 60.0) -> dict:
+    """cfg1: B=8, 1M-token datastore, tiny random-init decoder; speculative vs
+    autoregressive decode on the GPU, plus teacher-forced accepted tokens/step
+    (GPU simulate == CPU oracle, bit-exact) with the CPU oracle's time."""
+    import torch
+
+    import paper_2411_05894_b200 as G
+    from oracle import sssd_oracle as O
+    from paper_2411_05894_b200 import model as Mo
+    from paper_2411_05894_b200 import workload
+    from paper_2411_05894_b200.serving import SpecDecoder
+
+    corpus = workload.corpus(1_000_000, VOCAB)
+    ds = G.build(corpus, vocab_size=VOCAB)
+    recs = workload.records(8, 512, 256, VOCAB)
+    cfg = G.FusionConfig()  # dec_len 30 (reference default)
+    prompts = [p.tolist() for p, _ in recs]
+    spec = SpecDecoder(G.DraftEngine(ds, cfg), Mo.Decoder(Mo.TINY, 8, 1024, seed=0), prompts, 256)
+    r_spec = spec.run()
+    ar = SpecDecoder(None, Mo.Decoder(Mo.TINY, 8, 1024, seed=0), prompts, 256)
+    r_ar = ar.run()
+    same = sum(a == b for a, b in zip(spec.sequences(), ar.sequences()))
+    # teacher-forced acceptance on the GPU decode loop vs the CPU oracle
+    t0 = time.perf_counter()
+    rep = G.simulate([G.SimRecord(p, r) for p, r in recs], ds, cfg)
+    gpu_s = time.perf_counter() - t0
+    store = O.Store(corpus, ds.suffix_index)
+    oc = O.Cfg()
+    t0 = time.perf_counter()
+    cpu_steps = [O.run_record(store, p, r, oc) for p, r in recs[:2]]
+    cpu_s = time.perf_counter() - t0
+    bitexact = [r.per_step_tokens for r in rep.records[:2]] == cpu_steps
+    return {"workload": "cfg1: B=8, 1M-token datastore, TINY decoder (2L h1024 GQA 8/2 d128 V32000, random init), "
+                        "prompt 512, 256 new tokens, dec_len 30",
+            "spec_tokens_per_s": round(r_spec["tokens_per_s"], 1), "spec_steps": r_spec["steps"],
+            "spec_accepted_per_step": round(r_spec["accepted_per_step"], 3),
+            "autoregressive_tokens_per_s": round(r_ar["tokens_per_s"], 1),
+            "sequences_identical_to_autoregressive": f"{same}/8",
+            "teacher_forced": {"mean_accepted_per_step": round(rep.mean_accepted_per_step, 4),
+                               "gpu_simulate_s": round(gpu_s, 3),
+                               "cpu_oracle_s_per_record": round(cpu_s / 2, 3),
+                               "per_step_tokens_bitexact_vs_cpu_oracle": bitexact}}
+
+
+def bench_decode_cfg3(steps: int = 5) -> dict:
+    """cfg3: Llama-3-8B-shaped random-init verify, B=32, ctx 4k, tree budget 32:
+    device time of full speculative decode steps (propose + 32-layer tree
+    forward + accept + KV compaction)."""
+    import torch
+
+    import paper_2411_05894_b200 as G
+    from paper_2411_05894_b200 import model as Mo
+    from paper_2411_05894_b200 import workload
+    from paper_2411_05894_b200.serving import SpecDecoder
+
+    corpus = workload.corpus(10_000_000, 128256)
+    ds = G.build(corpus, vocab_size=128256)
+    prompts = [c.tolist() for c in workload.contexts(32, 4096, 128256)]
+    dec = Mo.Decoder(Mo.LLAMA3_8B, 32, 4096 + 2 * 32 + steps * 33 + 64, seed=0, init_on_device=True)
+    sd = SpecDecoder(G.DraftEngine(ds, G.FusionConfig(dec_len=32)), dec, prompts, steps * 33)
+    sd.step()  # warm
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    before = sd.seq_len.clone()
+    a.record()
+    for _ in range(steps):
+        sd.step()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    toks = int((sd.seq_len - before).sum())
+    out = {"workload": "cfg3: Llama-3-8B-shaped (32L h4096 GQA 32/8 d128 mlp14336 V128256, random init), B=32, "
+                       "ctx 4096, dec_len 32, 10M-token datastore",
+           "ms_per_step": round(ms, 3), "tokens_per_s": round(toks / (a.elapsed_time(b) / 1e3), 1),
+           "accepted_per_step": round(toks / (steps * 32), 3)}
+    del dec, sd
+    torch.cuda.empty_cache()
+    return out
 
 
 def _ref_worker(args):
@@ -403,11 +539,15 @@ def run_reference(args) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batches", type=int, default=256, help="independent B=64 batches per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip verify/decode sub-benchmarks")
+    ap.add_argument("--decode-8b", action="store_true", default=True,
+                    help="include the Llama-3-8B-shaped cfg3 decode step (default on)")
+    ap.add_argument("--no-decode-8b", dest="decode_8b", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

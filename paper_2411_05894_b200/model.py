@@ -61,13 +61,15 @@ class Decoder:
     """bf16 weights (seeded random init), KV cache [layers, B, n_kv, max_pos, d]."""
 
     def __init__(self, spec: ModelSpec, batch: int, max_pos: int, device="cuda", seed: int = 0,
-                 dtype=torch.bfloat16) -> None:
+                 dtype=torch.bfloat16, init_on_device: bool = False) -> None:
         self.spec, self.B, self.max_pos, self.device, self.dtype = spec, batch, max_pos, torch.device(device), dtype
-        g = torch.Generator(device="cpu").manual_seed(seed)
+        # seeded init; large models draw on the device (same seed -> same weights on the same torch/GPU)
+        gdev = self.device if init_on_device else torch.device("cpu")
+        g = torch.Generator(device=gdev).manual_seed(seed)
         h, d = spec.hidden, spec.head_dim
 
         def w(*shape, scale):
-            return (torch.randn(*shape, generator=g) * scale).to(dtype).to(self.device)
+            return (torch.randn(*shape, generator=g, device=gdev, dtype=torch.float32) * scale).to(dtype).to(self.device)
 
         self.embed = w(spec.vocab, h, scale=1.0)
         self.layers = []
