@@ -204,7 +204,19 @@ def run_ours(args) -> None:
     stream_all = workload.phrase_stream(B * CTX * world, VOCAB, workload.HELDOUT_SEED)
     mine = stream_all[rank * B * CTX:(rank + 1) * B * CTX]
     cfg = G.FusionConfig(dec_len=DEC_LEN)
-    eng = G.DraftEngine(ds, cfg, device=dev)
+    if args.shard and world > 1:
+        # SA-range sharding: keep only this rank's contiguous slice of suffix rows
+        from paper_2411_05894_b200.sharded import Collective, ShardedDraftEngine, shard_bounds
+
+        a, b_ = shard_bounds(ds.n_rows, world, rank)
+        shard = G.Datastore(ds.token_tensor, ds.rows[a:b_].clone(), b_ - a, VOCAB, rank_base=a,
+                            n_tokens=ds.n_tokens)
+        del ds
+        torch.cuda.empty_cache()
+        ds = shard
+        eng = ShardedDraftEngine(shard, cfg, Collective(), device=dev)
+    else:
+        eng = G.DraftEngine(ds, cfg, device=dev)
 
     ctx_h = torch.from_numpy(mine.view(np.int32)).pin_memory()
     seq = ctx_h.to(dev)
@@ -339,7 +351,9 @@ def run_ours(args) -> None:
             "data": "synthetic (seeded phrase-model corpus + held-out contexts, SURVEY App. B)",
             "config": {"workload": WORKLOAD, "batch": BATCH, "batches_per_step": R, "lookups_per_step": B,
                        "n_tokens": N_TOKENS, "vocab": VOCAB, "ctx": CTX, "dec_len": DEC_LEN,
-                       "parallelism": f"replicated datastore x{world}, requests partitioned",
+                       "parallelism": (f"SA-range sharded x{world} (NCCL all-gather + sum all-reduce + "
+                                       f"reduce-scatter per step), requests partitioned") if (args.shard and world > 1)
+                       else f"replicated datastore x{world}, requests partitioned",
                        "l2": "inputs > L2 (6.4 GB suffix rows, 134 MB contexts) + 256 MB flush between steps",
                        "b64_latency_ms": round(lat_ms, 4), "b64_lookups_per_s": round(BATCH / lat_ms * 1e3, 1),
                        "mean_draft_size": round(mean_size, 2), "gpu_sa_build_s": round(build_s, 2)},
@@ -545,6 +559,7 @@ def main() -> None:
     ap.add_argument("--batches", type=int, default=256, help="independent B=64 batches per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip verify/decode sub-benchmarks")
+    ap.add_argument("--shard", action="store_true", help="N>1: shard the suffix rows by rank range")
     ap.add_argument("--decode-8b", action="store_true", default=True,
                     help="include the Llama-3-8B-shaped cfg3 decode step (default on)")
     ap.add_argument("--no-decode-8b", dest="decode_8b", action="store_false")

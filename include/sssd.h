@@ -179,6 +179,25 @@ int sssd_propose_profile(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cf
                          const sssd_draft_out* out, void* workspace, size_t workspace_bytes,
                          void* stream, float* stage_ms);
 
+/* SA-range sharding.  A shard is an sssd_ds over global
+ * ranks [rank_base, rank_base + n_rows) with n_tokens = the global corpus
+ * length.  Per step:
+ *   sssd_shard_search   local bounds[b][p-1] = (#shard rows < pattern, <=) of the
+ *                       last p tokens of each tail sequence;  SUM over shards =
+ *                       global [lo, hi) exactly (A.2)          -> NCCL all-reduce
+ *   sssd_shard_gather   xrows[b][p-1][k][16] = suffix row of sampled global rank
+ *                       k of [lo, hi) if this shard owns it, else 0
+ *                                                   -> NCCL reduce-scatter (sum)
+ *   sssd_propose_pre    sssd_propose for this rank's requests with the global
+ *                       bounds and assembled rows instead of a local search. */
+int sssd_shard_search(const sssd_ds* ds, const sssd_seqs* tails, const sssd_cfg* cfg, int64_t* bounds,
+                      void* stream);
+int sssd_shard_gather(const sssd_ds* ds, const sssd_cfg* cfg, int32_t B, const int64_t* gbounds, uint32_t* xrows,
+                      void* stream);
+int sssd_propose_pre(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg, const int64_t* gbounds,
+                     const uint32_t* rows, const sssd_draft_out* out, const sssd_lookup_out* lookup,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
 /* Fusion of caller-provided source trees (merge fusion.py:209-261 + flatten).
  * Each tree is given as its multiset of root-to-end paths in DFS order (first
  * appearance order = the tree's child order): paths of request b / source s

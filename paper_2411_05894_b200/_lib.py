@@ -83,6 +83,10 @@ _SIGS = {
     "sssd_merge_workspace": (C.c_size_t, [C.POINTER(Cfg), C.c_int32, C.c_int64]),
     "sssd_merge": (C.c_int, [vp, vp, vp, vp, C.c_int64, vp, C.c_int32, C.POINTER(Cfg),
                              C.POINTER(DraftOut), vp, C.c_size_t, vp]),
+    "sssd_shard_search": (C.c_int, [C.POINTER(Ds), C.POINTER(Seqs), C.POINTER(Cfg), vp, vp]),
+    "sssd_shard_gather": (C.c_int, [C.POINTER(Ds), C.POINTER(Cfg), C.c_int32, vp, vp, vp]),
+    "sssd_propose_pre": (C.c_int, [C.POINTER(Ds), C.POINTER(Seqs), C.POINTER(Cfg), vp, vp, C.POINTER(DraftOut),
+                                   C.POINTER(LookupOut), vp, C.c_size_t, vp]),
     "sssd_teacher_predict": (C.c_int, [vp, vp, C.c_int32, vp, vp, vp, vp, vp, C.c_int32, vp, vp]),
     "sssd_accept": (C.c_int, [vp, vp, vp, C.c_int32, vp, C.c_int32, vp, vp, vp, vp, vp, vp, vp, vp,
                               vp]),

@@ -288,7 +288,8 @@ static Aux* aux_streams() {
 
 static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
                         const sssd_draft_out* out, const sssd_lookup_out* lookup, void* workspace,
-                        size_t workspace_bytes, void* stream, cudaEvent_t* ev);
+                        size_t workspace_bytes, void* stream, cudaEvent_t* ev,
+                        const int64_t* pre_bounds = nullptr, const uint32_t* pre_rows = nullptr);
 
 int sssd_propose(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
                  const sssd_draft_out* out, const sssd_lookup_out* lookup, void* workspace,
@@ -311,7 +312,8 @@ int sssd_propose_profile(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cf
 
 static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
                         const sssd_draft_out* out, const sssd_lookup_out* lookup, void* workspace,
-                        size_t workspace_bytes, void* stream, cudaEvent_t* ev) {
+                        size_t workspace_bytes, void* stream, cudaEvent_t* ev, const int64_t* pre_bounds,
+                        const uint32_t* pre_rows) {
   int rc = validate_cfg(cfg);
   if (rc) return rc;
   if ((rc = validate_out(out))) return rc;
@@ -343,7 +345,8 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
     kk.b0 = b0;
     kk.b1 = b1;
     ds_lookup_kernel<<<b1 - b0, 32 * cfg->P, 0, s>>>(*ds, *seqs, kk, w.ds_tab, w.ds_len, w.ds_el, w.ds_n, lk,
-                                                       w.ds_raw, w.ds_idx, w.ds_idx_cap, w.ds_cols);
+                                                       w.ds_raw, w.ds_idx, w.ds_idx_cap, w.ds_cols, pre_bounds,
+                                                       pre_rows);
   };
   auto launch_scan = [&](cudaStream_t s, int b0, int b1) {
     KCfg kk = k;
@@ -497,7 +500,8 @@ int sssd_ds_lookup(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg
   uint32_t* idx = reinterpret_cast<uint32_t*>(
       align_up(reinterpret_cast<uintptr_t>(raw + (size_t)seqs->B * cfg->P * cfg->M), 256));
   ds_lookup_kernel<<<seqs->B, 32 * cfg->P, 0, static_cast<cudaStream_t>(stream)>>>(
-      *ds, *seqs, kcfg(cfg), tab, lens, el, n_el, lk, raw, idx, ds_idx_cap(cfg->P, cfg->M), Cols{});
+      *ds, *seqs, kcfg(cfg), tab, lens, el, n_el, lk, raw, idx, ds_idx_cap(cfg->P, cfg->M), Cols{}, nullptr,
+      nullptr);
   return cuda_check(cudaGetLastError(), "ds_lookup_kernel launch");
 }
 
@@ -536,6 +540,42 @@ int sssd_find_ranges(const sssd_ds* ds, const uint32_t* pat, const int64_t* pat_
   find_ranges_kernel<<<(B + 3) / 4, 128, 0, static_cast<cudaStream_t>(stream)>>>(*ds, pat, pat_off,
                                                                                  pat_len, B, lo_hi);
   return cuda_check(cudaGetLastError(), "find_ranges_kernel launch");
+}
+
+
+int sssd_shard_search(const sssd_ds* ds, const sssd_seqs* tails, const sssd_cfg* cfg, int64_t* bounds,
+                      void* stream) {
+  int rc = validate_cfg(cfg);
+  if (rc) return rc;
+  if (!ds || !ds->rows) return fail(SSSD_E_ARG, "shard has no rows");
+  if (!tails || tails->B < 0) return fail(SSSD_E_ARG, "bad sequence batch");
+  if (tails->B == 0) return SSSD_OK;
+  if (ds->n_rows == 0)
+    return cuda_check(cudaMemsetAsync(bounds, 0, sizeof(int64_t) * 2 * tails->B * cfg->P,
+                                      static_cast<cudaStream_t>(stream)), "bounds memset");
+  shard_search_kernel<<<tails->B, 32 * cfg->P, 0, static_cast<cudaStream_t>(stream)>>>(*ds, *tails, kcfg(cfg),
+                                                                                       bounds);
+  return cuda_check(cudaGetLastError(), "shard_search_kernel launch");
+}
+
+int sssd_shard_gather(const sssd_ds* ds, const sssd_cfg* cfg, int32_t B, const int64_t* gbounds, uint32_t* xrows,
+                      void* stream) {
+  int rc = validate_cfg(cfg);
+  if (rc) return rc;
+  if (B <= 0) return B == 0 ? SSSD_OK : fail(SSSD_E_ARG, "bad batch");
+  const int64_t total = (int64_t)B * cfg->P * cfg->M * 4;
+  shard_gather_kernel<<<(unsigned)((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      *ds, kcfg(cfg), B, gbounds, xrows);
+  return cuda_check(cudaGetLastError(), "shard_gather_kernel launch");
+}
+
+int sssd_propose_pre(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg, const int64_t* gbounds,
+                     const uint32_t* rows, const sssd_draft_out* out, const sssd_lookup_out* lookup,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+  if (!gbounds || !rows) return fail(SSSD_E_ARG, "sharded propose needs global bounds and assembled rows");
+  if (cfg && cfg->P + cfg->branch_len > SSSD_ROW_TOKENS)
+    return fail(SSSD_E_LIMIT, "sharded lookup needs P + branch_len <= %d", SSSD_ROW_TOKENS);
+  return propose_impl(ds, seqs, cfg, out, lookup, workspace, workspace_bytes, stream, nullptr, gbounds, rows);
 }
 
 }  // extern "C"

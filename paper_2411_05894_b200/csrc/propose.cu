@@ -208,7 +208,8 @@ constexpr int kRowStride = 16;  // u32 per staged row in smem
 // Gather the sampled continuations of prefix length p into this request's
 // string table (non-empty ones compacted, SA order kept).  Returns the count.
 __device__ int gather_p(const sssd_ds& ds, const KCfg& c, int p, uint64_t lo, uint64_t hi,
-                        uint32_t* tab, uint8_t* lens, int64_t* samples, uint32_t* srows) {
+                        uint32_t* tab, uint8_t* lens, int64_t* samples, uint32_t* srows,
+                        const uint32_t* pre_rows) {
   const int lane = lane_id();
   const uint64_t w = hi - lo;
   const int s = (int)min(w, (uint64_t)c.M);
@@ -223,7 +224,9 @@ __device__ int gather_p(const sssd_ds& ds, const KCfg& c, int p, uint64_t lo, ui
     if (valid) {
       const uint64_t r =
           lo + (w <= (uint64_t)c.M ? (uint64_t)k : ((uint64_t)k * w) / (uint64_t)c.M);
-      const uint4* row = reinterpret_cast<const uint4*>(ds.rows) + (r - ds.rank_base) * 4;
+      // sharded mode: the row was fetched by its owning shard into pre_rows[k]
+      const uint4* row = pre_rows ? reinterpret_cast<const uint4*>(pre_rows) + (uint64_t)k * 4
+                                  : reinterpret_cast<const uint4*>(ds.rows) + (r - ds.rank_base) * 4;
       uint4* sr = reinterpret_cast<uint4*>(srow);
       sr[0] = ldg4(row);
       sr[1] = ldg4(row + 1);
@@ -259,7 +262,8 @@ __device__ int gather_p(const sssd_ds& ds, const KCfg& c, int p, uint64_t lo, ui
 __global__ void __launch_bounds__(32 * SSSD_MAX_P)
     ds_lookup_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, uint32_t* ds_tab, uint8_t* ds_len,
                      sssd_elem* ds_el, int32_t* ds_n, sssd_lookup_out lk, sssd_elem* ds_raw,
-                     uint32_t* ds_idx, int64_t idx_cap, Cols cols) {
+                     uint32_t* ds_idx, int64_t idx_cap, Cols cols, const int64_t* pre_bounds,
+                     const uint32_t* pre_rows) {
   const int b = c.b0 + blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = lane_id();
   __shared__ uint32_t s_pat[SSSD_MAX_P];
@@ -276,7 +280,12 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P)
   const int p = warp + 1;
   if (p <= pmax) {
     uint64_t lo, hi;
-    warp_bounds(ds, s_pat + (pmax - p), p, lo, hi);
+    if (pre_bounds) {  // sharded mode: global bounds = sum of the shards' local bounds (A.2)
+      lo = (uint64_t)pre_bounds[((size_t)b * c.P + warp) * 2] - ds.rank_base;
+      hi = (uint64_t)pre_bounds[((size_t)b * c.P + warp) * 2 + 1] - ds.rank_base;
+    } else {
+      warp_bounds(ds, s_pat + (pmax - p), p, lo, hi);
+    }
     if (lane == 0) {
       s_lo[warp] = lo + ds.rank_base;
       s_hi[warp] = hi + ds.rank_base;
@@ -308,7 +317,8 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P)
     const int blo = max(q, 1);
     if (p >= blo && p <= next) {
       const int n = gather_p(ds, c, p, s_lo[warp], s_hi[warp], tab, lens,
-                             smp ? smp + (size_t)warp * c.M : nullptr, s_rows + warp * 32 * kRowStride);
+                             smp ? smp + (size_t)warp * c.M : nullptr, s_rows + warp * 32 * kRowStride,
+                             pre_rows ? pre_rows + (((size_t)b * c.P + warp) * c.M) * 16 : nullptr);
       if (lane == 0) s_cnt[warp] = n;
     }
     __syncthreads();
@@ -403,6 +413,53 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P)
     const int q = threadIdx.x + 1;
     lk.n_conts[(size_t)b * c.P + threadIdx.x] = (q <= pmax && s_cnt[threadIdx.x] >= 0) ? s_cnt[threadIdx.x] : -1;
   }
+}
+
+// --------------------------------------------------------------------------
+// SA-range sharding: local bounds per shard, then the
+// owning shard copies each sampled suffix row into an exchange buffer
+// --------------------------------------------------------------------------
+
+// bounds[b][p-1] = (#rows < pattern, #rows <= pattern) within this shard;
+// patterns are the last p tokens of each (tail) sequence; p > len -> (0, 0)
+__global__ void __launch_bounds__(32 * SSSD_MAX_P)
+    shard_search_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, int64_t* bounds) {
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  __shared__ uint32_t s_pat[SSSD_MAX_P];
+  const int L = seqs.seq_len[b];
+  const uint32_t* seq = seqs.seq + seqs.seq_off[b];
+  const int pmax = min(c.P, L);
+  if (threadIdx.x < pmax) s_pat[threadIdx.x] = seq[L - pmax + threadIdx.x];
+  __syncthreads();
+  const int p = warp + 1;
+  uint64_t lo = 0, hi = 0;
+  if (p <= pmax) warp_bounds(ds, s_pat + (pmax - p), p, lo, hi);
+  if (lane == 0) {
+    bounds[((size_t)b * c.P + warp) * 2] = (int64_t)lo;
+    bounds[((size_t)b * c.P + warp) * 2 + 1] = (int64_t)hi;
+  }
+}
+
+// xrows[b][p-1][k][16] = suffix row of the k-th sampled global rank when this
+// shard owns it, zeros otherwise (so a sum over shards assembles every row)
+__global__ void shard_gather_kernel(sssd_ds ds, KCfg c, int B, const int64_t* gbounds, uint32_t* xrows) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16B quarter-row per thread
+  const int64_t total = (int64_t)B * c.P * c.M * 4;
+  if (t >= total) return;
+  const int q = (int)(t & 3);
+  const int64_t s = t >> 2;
+  const int k = (int)(s % c.M);
+  const int64_t bp = s / c.M;
+  const uint64_t lo = (uint64_t)gbounds[bp * 2], hi = (uint64_t)gbounds[bp * 2 + 1];
+  const uint64_t w = hi - lo;
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if ((uint64_t)k < min(w, (uint64_t)c.M)) {
+    const uint64_t r = lo + (w <= (uint64_t)c.M ? (uint64_t)k : ((uint64_t)k * w) / (uint64_t)c.M);
+    if (r >= ds.rank_base && r < ds.rank_base + ds.n_rows)
+      v = ldg4(reinterpret_cast<const uint4*>(ds.rows) + (r - ds.rank_base) * 4 + q);
+  }
+  reinterpret_cast<uint4*>(xrows)[t] = v;
 }
 
 // --------------------------------------------------------------------------

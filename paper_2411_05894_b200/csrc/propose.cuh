@@ -22,7 +22,10 @@ __global__ void find_ranges_kernel(sssd_ds ds, const uint32_t* pat, const int64_
 __global__ void ds_lookup_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, uint32_t* ds_tab,
                                  uint8_t* ds_len, sssd_elem* ds_el, int32_t* ds_n,
                                  sssd_lookup_out lk, sssd_elem* ds_raw, uint32_t* ds_idx,
-                                 int64_t idx_cap, Cols cols);
+                                 int64_t idx_cap, Cols cols, const int64_t* pre_bounds,
+                                 const uint32_t* pre_rows);
+__global__ void shard_search_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, int64_t* bounds);
+__global__ void shard_gather_kernel(sssd_ds ds, KCfg c, int B, const int64_t* gbounds, uint32_t* xrows);
 
 // scratch of the datastore lookup when a separator forces a block sort
 inline int64_t ds_idx_cap(int P, int M) {

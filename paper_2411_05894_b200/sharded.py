@@ -1,0 +1,166 @@
+"""SA-range sharded drafting across GPUs.
+
+The suffix rows are split into W contiguous global-rank ranges, one per GPU;
+decode requests are partitioned (each rank drafts its own B_local).  Per step:
+
+1. all-gather the last P tokens of every request              (u32 [W*B, P])
+2. ``sssd_shard_search`` on every request against the local shard -> local
+   bounds; SUM all-reduce -> the global ``[lo, hi)`` exactly (A.2: a shard's
+   lower/upper bound counts sum to the global ones)            (i64 [W*B, P, 2])
+3. ``sssd_shard_gather``: each sampled global rank's 64 B suffix row is
+   written by the one shard that owns it, zeros elsewhere; SUM reduce-scatter
+   hands each rank the rows of its own requests                (i32 [B, P, M, 16])
+4. ``sssd_propose_pre``: the unchanged lookup-finish / input-scan / fusion
+   kernels run locally on the assembled rows.
+
+Drafts are bit-identical to a single-GPU run because shards are rank-ordered
+(A.2/A.3).  Collectives go through ``Collective`` so the same protocol runs on
+NCCL (GPUs), gloo (CPU tests) or in-process emulation (one-GPU tests).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, lib, ptr, stream_ptr
+from .datastore import Datastore
+from .engine import DraftBatch, DraftEngine
+from .fusion import FusionConfig
+
+
+def shard_bounds(n_rows: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous global-rank range [a, b) of shard `rank` (sizes differ by <= 1)."""
+    base, extra = divmod(n_rows, world)
+    a = rank * base + min(rank, extra)
+    return a, a + base + (1 if rank < extra else 0)
+
+
+def shard_view(full: Datastore, world: int, rank: int) -> Datastore:
+    """A shard as a Datastore view over rows [a, b) of a full index (global
+    n_tokens kept).  On a real multi-GPU run each rank keeps only its slice."""
+    a, b = shard_bounds(full.n_rows, world, rank)
+    return Datastore(full.token_tensor, full.rows[a:b], b - a, full.vocab_size, rank_base=a,
+                     n_tokens=full.n_tokens)
+
+
+class Collective:
+    """torch.distributed collectives (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None) -> None:
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def all_gather(self, x: torch.Tensor) -> torch.Tensor:
+        out = torch.empty((self.world * x.shape[0],) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        self.dist.all_gather_into_tensor(out, x.contiguous(), group=self.group)
+        return out
+
+    def all_reduce_sum(self, x: torch.Tensor) -> torch.Tensor:
+        self.dist.all_reduce(x, op=self.dist.ReduceOp.SUM, group=self.group)
+        return x
+
+    def reduce_scatter_sum(self, x: torch.Tensor) -> torch.Tensor:
+        n = x.shape[0] // self.world
+        if self.dist.get_backend(self.group) == "gloo":  # gloo has no reduce_scatter
+            self.all_reduce_sum(x)
+            return x[self.rank * n:(self.rank + 1) * n].clone()
+        out = torch.empty((n,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        self.dist.reduce_scatter_tensor(out, x.contiguous(), op=self.dist.ReduceOp.SUM, group=self.group)
+        return out
+
+
+def tails_of(seq: torch.Tensor, off: torch.Tensor, ln: torch.Tensor, P: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """Last min(P, L) tokens of each sequence, right-aligned in [B, P] (+ lengths)."""
+    B = ln.shape[0]
+    idx = (off + ln.long())[:, None] - P + torch.arange(P, device=seq.device)[None, :]
+    valid = idx >= off[:, None]
+    t = torch.where(valid, seq[idx.clamp(min=0)], torch.zeros((), dtype=seq.dtype, device=seq.device))
+    return t.contiguous(), torch.clamp(ln, max=P).to(torch.int32)
+
+
+def search(shard: Datastore, cfg_c, tails: torch.Tensor, tlen: torch.Tensor) -> torch.Tensor:
+    """Local bounds of every tail against one shard: int64 [B, P, 2]."""
+    B, P = tails.shape
+    dev = tails.device
+    off = (torch.arange(B, dtype=torch.int64, device=dev) * P) + (P - tlen.long())
+    seqs = _lib.Seqs(ptr(tails), ptr(off), ptr(tlen), B, P)
+    out = torch.empty(B, P, 2, dtype=torch.int64, device=dev)
+    check(lib().sssd_shard_search(shard.c_view(), seqs, cfg_c, ptr(out), stream_ptr(dev)))
+    return out
+
+
+def gather(shard: Datastore, cfg_c, gbounds: torch.Tensor, M: int) -> torch.Tensor:
+    """Owned sampled rows: int32 [B, P, M, 16] (zeros where another shard owns the rank)."""
+    B, P, _ = gbounds.shape
+    out = torch.empty(B, P, M, 16, dtype=torch.int32, device=gbounds.device)
+    check(lib().sssd_shard_gather(shard.c_view(), cfg_c, B, ptr(gbounds), ptr(out), stream_ptr(gbounds.device)))
+    return out
+
+
+class ShardedDraftEngine(DraftEngine):
+    """DraftEngine over one SA-range shard; ``propose`` runs the collective protocol."""
+
+    def __init__(self, shard: Datastore, cfg: FusionConfig, coll: Collective, separator=None,
+                 use_input: bool = True, device=None) -> None:
+        super().__init__(shard, cfg, separator, True, use_input, device)
+        if cfg.P + cfg.branch_len > _lib.SSSD_ROW_TOKENS:
+            raise ValueError(f"sharded lookup needs P + branch_len <= {_lib.SSSD_ROW_TOKENS}")
+        self.coll = coll
+
+    def propose(self, seq, seq_off, seq_len, max_len, lookup: bool = False, out: DraftBatch | None = None):
+        B = int(seq_len.shape[0])
+        out = out or self.outputs(B, lookup)
+        P, M = self.cfg.P, self.cfg.M
+        tails, tlen = tails_of(seq, seq_off, seq_len, P)
+        all_tails = self.coll.all_gather(tails)
+        all_tlen = self.coll.all_gather(tlen)
+        gb = self.coll.all_reduce_sum(search(self.store, self.c, all_tails, all_tlen))
+        rows = self.coll.reduce_scatter_sum(gather(self.store, self.c, gb, M))
+        mine = gb[self.coll.rank * B:(self.coll.rank + 1) * B].contiguous()
+        ws = self.workspace(B, max_len)
+        seqs = _lib.Seqs(ptr(seq), ptr(seq_off), ptr(seq_len), B, int(max_len))
+        d_out = _lib.DraftOut(ptr(out.size), ptr(out.tokens), ptr(out.parents), ptr(out.depths), ptr(out.mask))
+        lk = _lib.LookupOut(ptr(out.ranges), ptr(out.samples), ptr(out.n_conts), ptr(out.p_cut)) if lookup else None
+        check(lib().sssd_propose_pre(self.store.c_view(), seqs, self.c, ptr(mine), ptr(rows), d_out, lk, ptr(ws),
+                                     ws.numel(), stream_ptr(self.device)))
+        return out
+
+
+class LocalShards:
+    """In-process emulation of W ranks for one-GPU tests: the collectives are sums /
+    concatenations over per-rank tensors."""
+
+    def __init__(self, full: Datastore, world: int, cfg: FusionConfig, separator=None) -> None:
+        self.world = world
+        self.shards = [shard_view(full, world, r) for r in range(world)]
+        self.engines = [DraftEngine(s, cfg, separator) for s in self.shards]
+        self.cfg = cfg
+
+    def propose(self, per_rank: list) -> list:
+        """per_rank[r] = (seq, off, len, max_len) device tensors; returns DraftBatch per rank."""
+        P, M = self.cfg.P, self.cfg.M
+        tails = [tails_of(s, o, l, P) for s, o, l, _ in per_rank]
+        all_tails = torch.cat([t for t, _ in tails])
+        all_tlen = torch.cat([n for _, n in tails])
+        gb = sum(search(s, self.engines[0].c, all_tails, all_tlen) for s in self.shards)
+        rows = sum(gather(s, self.engines[0].c, gb, M) for s in self.shards)
+        outs, b0 = [], 0
+        for r, (seq, off, ln, mx) in enumerate(per_rank):
+            B = int(ln.shape[0])
+            eng = self.engines[r]
+            out = eng.outputs(B)
+            ws = eng.workspace(B, mx)
+            seqs = _lib.Seqs(ptr(seq), ptr(off), ptr(ln), B, int(mx))
+            d_out = _lib.DraftOut(ptr(out.size), ptr(out.tokens), ptr(out.parents), ptr(out.depths), ptr(out.mask))
+            mine, rr = gb[b0:b0 + B].contiguous(), rows[b0:b0 + B].contiguous()
+            check(lib().sssd_propose_pre(self.shards[r].c_view(), seqs, eng.c, ptr(mine), ptr(rr), d_out, None,
+                                         ptr(ws), ws.numel(), stream_ptr(seq.device)))
+            outs.append(out)
+            b0 += B
+        return outs
