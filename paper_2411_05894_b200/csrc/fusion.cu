@@ -115,12 +115,21 @@ struct Arena {
 // hold candidates.  Cold records are indexed by group id: ids < kGroupSmem in
 // shared memory, later ids in the request's global overflow area.
 struct Frontier {
-  uint32_t *kh, *kl, *km;  // live list: ~bits(prio) hi / lo, meta (group id in low 22 bits)
+  uint32_t *kh, *kl, *km;     // live list slots [0, kGroupSmem): ~bits(prio) hi / lo, meta
+  uint32_t *gkh, *gkl, *gkm;  // live list slots >= kGroupSmem (global, rare)
   Group* sc;
   Group* gc;
   int G;  // groups created
   int A;  // live groups
   __device__ __forceinline__ Group* cold(int i) const { return i < kGroupSmem ? sc + i : gc + (i - kGroupSmem); }
+  __device__ __forceinline__ void put(int q, uint32_t h, uint32_t l, uint32_t m) {
+    if (q < kGroupSmem) { kh[q] = h; kl[q] = l; km[q] = m; }
+    else { gkh[q - kGroupSmem] = h; gkl[q - kGroupSmem] = l; gkm[q - kGroupSmem] = m; }
+  }
+  __device__ __forceinline__ void get(int q, uint32_t& h, uint32_t& l, uint32_t& m) const {
+    if (q < kGroupSmem) { h = kh[q]; l = kl[q]; m = km[q]; }
+    else { h = gkh[q - kGroupSmem]; l = gkl[q - kGroupSmem]; m = gkm[q - kGroupSmem]; }
+  }
 };
 
 // Expand the node covering [a, z) of source sd at depth D-1 into the group of
@@ -143,7 +152,7 @@ __device__ void expand(const SrcDesc& sd, uint32_t rank, uint32_t D, uint32_t a,
     ch = ar.alloc(1);
     if (!ch) return;
     if (lane == 0) {
-      const double ratio = __ddiv_rn(1.0, dpc);
+      const double ratio = pcount == 1 ? 1.0 : __ddiv_rn(1.0, dpc);  // c/c == 1.0 exactly
       Child c;
       c.pp = seed ? ratio : __dmul_rn(ppar, ratio);
       c.first = o;
@@ -162,7 +171,7 @@ __device__ void expand(const SrcDesc& sd, uint32_t rank, uint32_t D, uint32_t a,
       const bool live = pred && cnt > 0;
       const uint32_t bal = __ballot_sync(SSSD_FULL, live);
       if (live) {
-        const double ratio = __ddiv_rn((double)cnt, dpc);
+        const double ratio = cnt == pcount ? 1.0 : __ddiv_rn((double)cnt, dpc);  // exact shortcut
         Child c;
         c.pp = seed ? ratio : __dmul_rn(ppar, ratio);
         c.first = first;
@@ -293,9 +302,7 @@ __device__ void expand(const SrcDesc& sd, uint32_t rank, uint32_t D, uint32_t a,
     g.head = head | (dparent << 24);
     g.nch = nch | (sorted << 31);
     *fr.cold(fr.G) = g;
-    fr.kh[fr.A] = kh;
-    fr.kl[fr.A] = kl;
-    fr.km[fr.A] = (D << 26) | (rank << 22) | (uint32_t)fr.G;
+    fr.put(fr.A, kh, kl, (D << 26) | (rank << 22) | (uint32_t)fr.G);
   }
   ++fr.G;
   ++fr.A;
@@ -316,9 +323,9 @@ __global__ void __launch_bounds__(32, 32)
   Child* sslab = reinterpret_cast<Child*>(smem);
   Group* sc = reinterpret_cast<Group*>(sslab + kChildSmem);
   uint32_t* skh = reinterpret_cast<uint32_t*>(sc + Gs);
-  uint32_t* skl = skh + Gmax;
-  uint32_t* skm = skl + Gmax;
-  uint32_t* d_tok = skm + Gmax;
+  uint32_t* skl = skh + Gs;
+  uint32_t* skm = skl + Gs;
+  uint32_t* d_tok = skm + Gs;
   int16_t* d_par = reinterpret_cast<int16_t*>(d_tok + S);
   int16_t* d_fc = d_par + S;  // first child
   int16_t* d_lc = d_fc + S;   // last child
@@ -328,10 +335,14 @@ __global__ void __launch_bounds__(32, 32)
   int16_t* n2p = pre + S;     // node -> pre-order position
   int16_t* stk = n2p + S;
 
+  const int Go = Gmax - Gs;
   Group* gc = reinterpret_cast<Group*>(gover + (size_t)b * gover_bytes);  // cold overflow
+  uint32_t* gkh = reinterpret_cast<uint32_t*>(gc + (Go > 0 ? Go : 0));     // live-list overflow
+  uint32_t* gkl = gkh + (Go > 0 ? Go : 0);
+  uint32_t* gkm = gkl + (Go > 0 ? Go : 0);
 
   Arena ar{sslab, 0, kChildSmem, slabs + (size_t)b * slab_cap, 0, slab_cap, pool, cursor, pool_cap, err};
-  Frontier fr{skh, skl, skm, sc, gc, 0, 0};
+  Frontier fr{skh, skl, skm, gkh, gkl, gkm, sc, gc, 0, 0};
   if (lane == 0) {
     d_tok[0] = root_tok[b];
     d_par[0] = -1;
@@ -360,8 +371,19 @@ __global__ void __launch_bounds__(32, 32)
     // groups carry meta = kExhausted and lose every comparison
     uint32_t bh = 0xffffffffu, bl = 0xffffffffu, bm = kExhausted;
     int bp = 0;
-    for (int q = lane; q < fr.A; q += 32) {
+    const int A1 = min(fr.A, kGroupSmem);
+    for (int q = lane; q < A1; q += 32) {
       const uint32_t h = skh[q], l = skl[q], m = skm[q];
+      if (key_less(h, l, m, bh, bl, bm)) {
+        bh = h;
+        bl = l;
+        bm = m;
+        bp = q;
+      }
+    }
+    for (int q = kGroupSmem + lane; q < fr.A; q += 32) {
+      const int o = q - kGroupSmem;
+      const uint32_t h = gkh[o], l = gkl[o], m = gkm[o];
       if (key_less(h, l, m, bh, bl, bm)) {
         bh = h;
         bl = l;
@@ -440,13 +462,11 @@ __global__ void __launch_bounds__(32, 32)
       if (lane == 0) {
         gp->head = (g.head & 0xff000000u) | nh;
         if (nh < gnch) {
-          skh[pos] = kh;
-          skl[pos] = kl;
+          fr.put(pos, kh, kl, meta);
         } else {  // exhausted: move the last live group into this slot
-          const int last = fr.A - 1;
-          skh[pos] = skh[last];
-          skl[pos] = skl[last];
-          skm[pos] = skm[last];
+          uint32_t h2, l2, m2;
+          fr.get(fr.A - 1, h2, l2, m2);
+          fr.put(pos, h2, l2, m2);
         }
       }
       if (nh >= gnch) --fr.A;
@@ -458,18 +478,41 @@ __global__ void __launch_bounds__(32, 32)
              c.disc[rk * c.disc_stride + D + 1], fr, ar);
   }
 
-  // DFS pre-order flatten, children in insertion order (ref draft.py:67-86)
-  if (lane == 0) {
-    int sp = 0, k = 0;
-    stk[sp++] = 0;
-    while (sp > 0) {
-      const int nid = stk[--sp];
-      pre[k] = (int16_t)nid;
-      n2p[nid] = (int16_t)k;
-      ++k;
-      for (int ch = d_lc[nid]; ch >= 0; ch = d_ps[ch]) stk[sp++] = (int16_t)ch;  // reverse push
-    }
+  // DFS pre-order flatten, children in insertion order (ref draft.py:67-86),
+  // level-parallel: subtree sizes bottom-up, then pre-order positions top-down
+  // (a child's subtree ends where its next sibling's starts); each lane
+  // owns the parents of one level and walks their child lists
+  int16_t* sub = stk;  // subtree sizes
+  int maxd = 0;
+  for (int v = lane; v < size; v += 32) {
+    sub[v] = 1;
+    maxd = max(maxd, (int)d_dep[v]);
   }
+  maxd = __reduce_max_sync(SSSD_FULL, maxd);
+  __syncwarp();
+  for (int dd = maxd - 1; dd >= 0; --dd) {
+    for (int v = lane; v < size; v += 32) {
+      if (d_dep[v] != dd) continue;
+      int t = 1;
+      for (int ch = d_lc[v]; ch >= 0; ch = d_ps[ch]) t += sub[ch];
+      sub[v] = (int16_t)t;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) n2p[0] = 0;
+  __syncwarp();
+  for (int dd = 0; dd < maxd; ++dd) {
+    for (int v = lane; v < size; v += 32) {
+      if (d_dep[v] != dd) continue;
+      int end = n2p[v] + sub[v];  // children fill the subtree right to left
+      for (int ch = d_lc[v]; ch >= 0; ch = d_ps[ch]) {
+        end -= sub[ch];
+        n2p[ch] = (int16_t)end;
+      }
+    }
+    __syncwarp();
+  }
+  for (int v = lane; v < size; v += 32) pre[n2p[v]] = (int16_t)v;
   __syncwarp();
   uint32_t* o_tok = out.tokens + (size_t)b * S;
   int32_t* o_par = out.parents + (size_t)b * S;

@@ -48,7 +48,7 @@ __global__ void draft_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg
 constexpr int kChildBytes = 32;
 constexpr int kGroupBytes = 16;  // cold group record
 constexpr int kGroupSmem = 128;  // groups kept in shared memory; later ones spill to global
-constexpr int kChildSmem = 96;   // child records in the shared-memory slab
+constexpr int kChildSmem = 48;   // child records in the shared-memory slab
 
 // Upper bound on sibling groups: one per source seed plus one per pop, and a
 // draft node can be popped at most once per source.
@@ -57,14 +57,14 @@ __host__ __device__ inline int draft_max_groups(int P, int S) { return (P + 1) *
 inline int draft_smem_bytes(int P, int S) {
   const int G = draft_max_groups(P, S);
   const int Gs = G < kGroupSmem ? G : kGroupSmem;
-  return kChildSmem * kChildBytes + Gs * kGroupBytes + G * 12 + S * 4 + S * 2 * 8 + 16;
+  return kChildSmem * kChildBytes + Gs * (kGroupBytes + 12) + S * 4 + S * 2 * 8 + 16;
 }
 
-// global overflow bytes per request: cold records of groups >= kGroupSmem
+// global overflow bytes per request: cold records + live-list slots beyond kGroupSmem
 inline int64_t draft_group_overflow_bytes(int P, int S) {
   const int G = draft_max_groups(P, S);
   const int Go = G > kGroupSmem ? G - kGroupSmem : 0;
-  return ((int64_t)Go * kGroupBytes + 127) / 128 * 128;
+  return ((int64_t)Go * (kGroupBytes + 12) + 127) / 128 * 128;
 }
 
 }  // namespace sssd
