@@ -198,6 +198,10 @@ int sssd_propose_pre(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* c
                      const uint32_t* rows, const sssd_draft_out* out, const sssd_lookup_out* lookup,
                      void* workspace, size_t workspace_bytes, void* stream);
 
+/* Measurement aid: device int64[B] receiving per-request fusion-kernel cycles
+ * of subsequent sssd_propose calls; NULL disables. */
+void sssd_set_cycle_probe(long long* cycles);
+
 /* Fusion of caller-provided source trees (merge fusion.py:209-261 + flatten).
  * Each tree is given as its multiset of root-to-end paths in DFS order (first
  * appearance order = the tree's child order): paths of request b / source s

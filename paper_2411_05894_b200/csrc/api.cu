@@ -13,6 +13,7 @@
 namespace sssd {
 
 static thread_local std::string g_err;
+static long long* g_cycles = nullptr;  // optional per-request fusion-kernel cycle counts
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -92,6 +93,7 @@ static KCfg kcfg(const sssd_cfg* c) {
 constexpr uint32_t kSlabChildren = 2048;
 
 struct DraftWs {
+  int32_t* order;
   uint8_t* gover;
   int64_t gover_bytes;
   SrcDesc* desc;
@@ -109,6 +111,7 @@ struct DraftWs {
 // contexts (huge input-tree roots) spill into the pool, sized by max_len.
 static DraftWs carve_draft(Carver& cv, int P, int S, int B, int64_t max_len = 0) {
   DraftWs d;
+  d.order = cv.take<int32_t>((size_t)B);
   d.gover_bytes = draft_group_overflow_bytes(P, S);
   d.gover = cv.take<uint8_t>((size_t)B * (d.gover_bytes ? d.gover_bytes : 1));
   d.desc = cv.take<SrcDesc>((size_t)B * (P + 1));
@@ -224,7 +227,7 @@ static int launch_draft(const DraftWs& d, const KCfg& k, int B, const sssd_draft
   cudaError_t e = cudaFuncSetAttribute(draft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return cuda_check(e, "draft_kernel smem attribute");
   draft_kernel<<<B, 32, smem, st>>>(d.desc, d.root, k, d.slabs, kSlabChildren, d.pool, d.cursor,
-                                    d.pool_cap, d.err, d.gover, d.gover_bytes, *out);
+                                    d.pool_cap, d.err, d.gover, d.gover_bytes, *out, nullptr, nullptr);
   return cuda_check(cudaGetLastError(), "draft_kernel launch");
 }
 
@@ -361,8 +364,11 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
     kk.b1 = b1;
     propose_setup_kernel<<<(b1 - b0 + 127) / 128, 128, 0, s>>>(*seqs, kk, w.ds_cols, w.ds_n, w.in_cols,
                                                                  w.in_n, w.d.desc, w.d.root);
+    const bool lpt = b0 == 0 && b1 == B && B >= 2048;  // order only pays with several waves
+    if (lpt) lpt_order_kernel<<<1, 1024, 0, s>>>(w.d.desc, k.P, B, w.d.order);
     draft_kernel<<<b1 - b0, 32, smem, s>>>(w.d.desc, w.d.root, kk, w.d.slabs, kSlabChildren, w.d.pool,
-                                           w.d.cursor, w.d.pool_cap, w.d.err, w.d.gover, w.d.gover_bytes, *out);
+                                           w.d.cursor, w.d.pool_cap, w.d.err, w.d.gover, w.d.gover_bytes, *out,
+                                           g_cycles, lpt ? w.d.order : nullptr);
   };
 
   if (ev) {  // profiling: stages back to back on the caller's stream
@@ -376,9 +382,12 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
     kk.b1 = B;
     propose_setup_kernel<<<(B + 127) / 128, 128, 0, st>>>(*seqs, kk, w.ds_cols, w.ds_n, w.in_cols, w.in_n,
                                                             w.d.desc, w.d.root);
+    const bool lpt = B >= 2048;
+    if (lpt) lpt_order_kernel<<<1, 1024, 0, st>>>(w.d.desc, k.P, B, w.d.order);
     cudaEventRecord(ev[3], st);
     draft_kernel<<<B, 32, smem, st>>>(w.d.desc, w.d.root, kk, w.d.slabs, kSlabChildren, w.d.pool, w.d.cursor,
-                                      w.d.pool_cap, w.d.err, w.d.gover, w.d.gover_bytes, *out);
+                                      w.d.pool_cap, w.d.err, w.d.gover, w.d.gover_bytes, *out, g_cycles,
+                                      lpt ? w.d.order : nullptr);
     cudaEventRecord(ev[4], st);
     return cuda_check(cudaGetLastError(), "propose launch");
   }
@@ -577,5 +586,9 @@ int sssd_propose_pre(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* c
     return fail(SSSD_E_LIMIT, "sharded lookup needs P + branch_len <= %d", SSSD_ROW_TOKENS);
   return propose_impl(ds, seqs, cfg, out, lookup, workspace, workspace_bytes, stream, nullptr, gbounds, rows);
 }
+
+// Measurement aid: when set (device pointer, [B] int64), the fusion kernel
+// records clock64 cycles per request; NULL disables.
+void sssd_set_cycle_probe(long long* cycles) { g_cycles = cycles; }
 
 }  // extern "C"

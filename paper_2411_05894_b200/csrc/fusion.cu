@@ -312,9 +312,11 @@ __device__ void expand(const SrcDesc& sd, uint32_t rank, uint32_t D, uint32_t a,
 __global__ void __launch_bounds__(32, 32)
     draft_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, Child* slabs,
                  uint32_t slab_cap, Child* pool, unsigned long long* cursor, uint64_t pool_cap,
-                 int32_t* err, uint8_t* gover, int64_t gover_bytes, sssd_draft_out out) {
+                 int32_t* err, uint8_t* gover, int64_t gover_bytes, sssd_draft_out out,
+                 long long* cycles, const int32_t* order) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int b = c.b0 + blockIdx.x;
+  const long long t_start = clock64();
+  const int b = order ? order[c.b0 + blockIdx.x] : c.b0 + blockIdx.x;  // longest-first launch order
   const int lane = lane_id();
   const int S = c.S;
   const int W = (S + 63) >> 6;
@@ -537,7 +539,41 @@ __global__ void __launch_bounds__(32, 32)
       for (int w = 0; w < W; ++w) o_mask[(size_t)k * W + w] = 0;
     }
   }
-  if (lane == 0) out.size[b] = size;
+  if (lane == 0) {
+    out.size[b] = size;
+    if (cycles) cycles[b] = clock64() - t_start;  // per-request profile (optional)
+  }
+}
+
+// Longest-processing-time-first launch order for the fusion kernel: requests
+// are bucketed by log2 of their element count (datastore elements + input
+// occurrences x trees, a proxy for expansion work) and emitted in descending
+// bucket order, so the long requests start in the first wave instead of
+// forming the tail.  One CTA; order within a bucket is arbitrary (requests are
+// independent, outputs are indexed by request).
+__global__ void __launch_bounds__(1024) lpt_order_kernel(const SrcDesc* desc, int P, int B, int32_t* order) {
+  __shared__ int hist[64], cur[64];
+  if (threadIdx.x < 64) hist[threadIdx.x] = 0;
+  __syncthreads();
+  auto bucket = [&](int b) {
+    const SrcDesc* d = desc + (size_t)b * (P + 1);
+    long long cost = d[0].n;
+    for (int r = 1; r <= P; ++r) cost += d[r].n;
+    int lg = 0;
+    while (lg < 60 && (cost >> (lg / 2 + 1)) > 0 && (1ll << (lg / 2 + 1)) <= cost) ++lg;  // ~2 buckets per octave
+    return 63 - min(lg, 63);
+  };
+  for (int b = threadIdx.x; b < B; b += blockDim.x) atomicAdd(&hist[bucket(b)], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int i = 0; i < 64; ++i) {
+      cur[i] = acc;
+      acc += hist[i];
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < B; b += blockDim.x) order[atomicAdd(&cur[bucket(b)], 1)] = b;
 }
 
 }  // namespace sssd

@@ -43,7 +43,8 @@ struct Group;
 __global__ void draft_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, Child* slabs,
                              uint32_t slab_cap, Child* pool, unsigned long long* cursor,
                              uint64_t pool_cap, int32_t* err, uint8_t* gover, int64_t gover_bytes,
-                             sssd_draft_out out);
+                             sssd_draft_out out, long long* cycles, const int32_t* order);
+__global__ void lpt_order_kernel(const SrcDesc* desc, int P, int B, int32_t* order);
 
 constexpr int kChildBytes = 32;
 constexpr int kGroupBytes = 16;  // cold group record
