@@ -94,6 +94,8 @@ constexpr uint32_t kSlabChildren = 2048;
 
 struct DraftWs {
   int32_t* order;
+  uint8_t* bucket;
+  int32_t* hist;  // [64] histogram + [64] fill cursors (zeroed with the status words)
   uint8_t* gover;
   int64_t gover_bytes;
   SrcDesc* desc;
@@ -112,6 +114,7 @@ struct DraftWs {
 static DraftWs carve_draft(Carver& cv, int P, int S, int B, int64_t max_len = 0) {
   DraftWs d;
   d.order = cv.take<int32_t>((size_t)B);
+  d.bucket = cv.take<uint8_t>((size_t)B);
   d.gover_bytes = draft_group_overflow_bytes(P, S);
   d.gover = cv.take<uint8_t>((size_t)B * (d.gover_bytes ? d.gover_bytes : 1));
   d.desc = cv.take<SrcDesc>((size_t)B * (P + 1));
@@ -120,8 +123,9 @@ static DraftWs carve_draft(Carver& cv, int P, int S, int B, int64_t max_len = 0)
   d.pool_cap = (1u << 16) + (uint64_t)B * 1024 +
                (max_len > (int64_t)kSlabChildren ? (uint64_t)B * (P + 1) * (uint64_t)max_len : 0);
   d.pool = reinterpret_cast<Child*>(cv.take<uint8_t>((size_t)d.pool_cap * kChildBytes));
-  d.cursor = cv.take<unsigned long long>(2);  // cursor + err (the status words)
+  d.cursor = cv.take<unsigned long long>(2 + 64);  // cursor + err (status words) + LPT histogram
   d.err = reinterpret_cast<int32_t*>(d.cursor + 1);
+  d.hist = reinterpret_cast<int32_t*>(d.cursor + 2);
   return d;
 }
 
@@ -177,7 +181,8 @@ static PropWs carve_propose(uint8_t* base, const sssd_cfg* c, int B, int max_len
 }
 
 __global__ void propose_setup_kernel(sssd_seqs seqs, KCfg c, Cols dsc, const int32_t* ds_n,
-                                     Cols inc, const int32_t* in_n, SrcDesc* desc, uint32_t* root) {
+                                     Cols inc, const int32_t* in_n, SrcDesc* desc, uint32_t* root,
+                                     uint8_t* bucket, int32_t* hist) {
   const int b = c.b0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= c.b1) return;
   const int L = seqs.seq_len[b];
@@ -197,6 +202,11 @@ __global__ void propose_setup_kernel(sssd_seqs seqs, KCfg c, Cols dsc, const int
     d[rk].stride = inc.stride;
     d[rk].n = (c.use_in && p <= c.n_trees) ? in_n[b] : 0;
     d[rk].thr = p;
+  }
+  if (bucket) {
+    const int k = lpt_bucket(d, c.P);
+    bucket[b] = (uint8_t)k;
+    atomicAdd(&hist[k], 1);
   }
 }
 
@@ -337,7 +347,7 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
   KCfg k = kcfg(cfg);
   sssd_lookup_out lk{};
   if (lookup) lk = *lookup;
-  if ((rc = cuda_check(cudaMemsetAsync(w.d.cursor, 0, 16, st), "memset status"))) return rc;
+  if ((rc = cuda_check(cudaMemsetAsync(w.d.cursor, 0, 16 + 512, st), "memset status"))) return rc;
   const int smem = draft_smem_bytes(k.P, k.S);
   if ((rc = cuda_check(cudaFuncSetAttribute(draft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                        "draft_kernel smem attribute")))
@@ -362,10 +372,11 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
     KCfg kk = k;
     kk.b0 = b0;
     kk.b1 = b1;
-    propose_setup_kernel<<<(b1 - b0 + 127) / 128, 128, 0, s>>>(*seqs, kk, w.ds_cols, w.ds_n, w.in_cols,
-                                                                 w.in_n, w.d.desc, w.d.root);
     const bool lpt = b0 == 0 && b1 == B && B >= 2048;  // order only pays with several waves
-    if (lpt) lpt_order_kernel<<<1, 1024, 0, s>>>(w.d.desc, k.P, B, w.d.order);
+    propose_setup_kernel<<<(b1 - b0 + 127) / 128, 128, 0, s>>>(*seqs, kk, w.ds_cols, w.ds_n, w.in_cols,
+                                                                 w.in_n, w.d.desc, w.d.root,
+                                                                 lpt ? w.d.bucket : nullptr, w.d.hist);
+    if (lpt) lpt_scatter_kernel<<<(B + 255) / 256, 256, 0, s>>>(w.d.bucket, w.d.hist, w.d.hist + 64, B, w.d.order);
     draft_kernel<<<b1 - b0, 32, smem, s>>>(w.d.desc, w.d.root, kk, w.d.slabs, kSlabChildren, w.d.pool,
                                            w.d.cursor, w.d.pool_cap, w.d.err, w.d.gover, w.d.gover_bytes, *out,
                                            g_cycles, lpt ? w.d.order : nullptr);
@@ -380,10 +391,11 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
     KCfg kk = k;
     kk.b0 = 0;
     kk.b1 = B;
-    propose_setup_kernel<<<(B + 127) / 128, 128, 0, st>>>(*seqs, kk, w.ds_cols, w.ds_n, w.in_cols, w.in_n,
-                                                            w.d.desc, w.d.root);
     const bool lpt = B >= 2048;
-    if (lpt) lpt_order_kernel<<<1, 1024, 0, st>>>(w.d.desc, k.P, B, w.d.order);
+    propose_setup_kernel<<<(B + 127) / 128, 128, 0, st>>>(*seqs, kk, w.ds_cols, w.ds_n, w.in_cols, w.in_n,
+                                                            w.d.desc, w.d.root, lpt ? w.d.bucket : nullptr,
+                                                            w.d.hist);
+    if (lpt) lpt_scatter_kernel<<<(B + 255) / 256, 256, 0, st>>>(w.d.bucket, w.d.hist, w.d.hist + 64, B, w.d.order);
     cudaEventRecord(ev[3], st);
     draft_kernel<<<B, 32, smem, st>>>(w.d.desc, w.d.root, kk, w.d.slabs, kSlabChildren, w.d.pool, w.d.cursor,
                                       w.d.pool_cap, w.d.err, w.d.gover, w.d.gover_bytes, *out, g_cycles,

@@ -547,33 +547,24 @@ __global__ void __launch_bounds__(32, 32)
 
 // Longest-processing-time-first launch order for the fusion kernel: requests
 // are bucketed by log2 of their element count (datastore elements + input
-// occurrences x trees, a proxy for expansion work) and emitted in descending
-// bucket order, so the long requests start in the first wave instead of
-// forming the tail.  One CTA; order within a bucket is arbitrary (requests are
-// independent, outputs are indexed by request).
-__global__ void __launch_bounds__(1024) lpt_order_kernel(const SrcDesc* desc, int P, int B, int32_t* order) {
-  __shared__ int hist[64], cur[64];
-  if (threadIdx.x < 64) hist[threadIdx.x] = 0;
-  __syncthreads();
-  auto bucket = [&](int b) {
-    const SrcDesc* d = desc + (size_t)b * (P + 1);
-    long long cost = d[0].n;
-    for (int r = 1; r <= P; ++r) cost += d[r].n;
-    int lg = 0;
-    while (lg < 60 && (cost >> (lg / 2 + 1)) > 0 && (1ll << (lg / 2 + 1)) <= cost) ++lg;  // ~2 buckets per octave
-    return 63 - min(lg, 63);
-  };
-  for (int b = threadIdx.x; b < B; b += blockDim.x) atomicAdd(&hist[bucket(b)], 1);
-  __syncthreads();
-  if (threadIdx.x == 0) {
+// occurrences x trees, a proxy for expansion work; propose_setup_kernel fills
+// bucket[] and the 64-bin histogram) and emitted in descending bucket order,
+// so long requests start in the first wave instead of forming the tail.
+// Order within a bucket is arbitrary: requests are independent and every
+// output is indexed by request.
+__global__ void lpt_scatter_kernel(const uint8_t* bucket, const int32_t* hist, int32_t* fill, int B,
+                                   int32_t* order) {
+  __shared__ int start[64];
+  if (threadIdx.x < 64) {
     int acc = 0;
-    for (int i = 0; i < 64; ++i) {
-      cur[i] = acc;
-      acc += hist[i];
-    }
+    for (int i = 0; i < (int)threadIdx.x; ++i) acc += hist[i];
+    start[threadIdx.x] = acc;
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < B; b += blockDim.x) order[atomicAdd(&cur[bucket(b)], 1)] = b;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int k = bucket[b];
+  order[start[k] + atomicAdd(&fill[k], 1)] = b;
 }
 
 }  // namespace sssd

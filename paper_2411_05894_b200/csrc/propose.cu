@@ -486,43 +486,71 @@ __global__ void __launch_bounds__(256)
   if (tid < jm) s_tail[tid] = seq[L - 1 - tid];
   __syncthreads();
   sssd_elem* r = raw + (size_t)b * cap;
-  int base = 0;
-  for (int e0 = 1; e0 < L; e0 += blockDim.x) {
-    const int e = e0 + tid;
+  // Each warp owns one contiguous segment of end positions e in [1, L): pass 1
+  // counts its occurrences, one block prefix gives every warp its output base,
+  // pass 2 recomputes the (L1-resident) matches and writes them in e order.
+  const int nw = blockDim.x >> 5;
+  const int seg = ((L - 1 + nw - 1) / nw + 31) & ~31;
+  const int e_lo = 1 + warp * seg, e_hi = min(L, e_lo + seg);
+  auto match = [&](int e) {
     int m = 0;
-    if (e < L) {
+    if (e < e_hi) {
       const int lim = min(jm, e);
       while (m < lim && seq[e - 1 - m] == s_tail[m]) ++m;
     }
-    const bool f = m > 0;
-    const uint32_t bal = __ballot_sync(SSSD_FULL, f);
-    if (lane == 0) s_wsum[warp] = __popc(bal);
-    __syncthreads();
-    int off = 0, tot = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      if (w < warp) off += s_wsum[w];
-      tot += s_wsum[w];
-    }
-    if (f) {
+    return m;
+  };
+  int mine = 0;
+  for (int e0 = e_lo; e0 < e_hi; e0 += 32) mine += __popc(__ballot_sync(SSSD_FULL, match(e0 + lane) > 0));
+  if (lane == 0) s_wsum[warp] = mine;
+  __syncthreads();
+  int base = 0, total = 0;
+  for (int w = 0; w < nw; ++w) {
+    if (w < warp) base += s_wsum[w];
+    total += s_wsum[w];
+  }
+  for (int e0 = e_lo; e0 < e_hi; e0 += 32) {
+    const int e = e0 + lane;
+    const int m = match(e);
+    const uint32_t bal = __ballot_sync(SSSD_FULL, m > 0);
+    if (m > 0) {
       sssd_elem el;
       el.off = (uint32_t)e;
       el.orig = (uint32_t)e;
       el.len_m = (uint32_t)min(c.IBL, L - e) | ((uint32_t)m << 8);
       el.pad = 0;
-      r[base + off + __popc(bal & lanemask_lt())] = el;
+      r[base + __popc(bal & lanemask_lt())] = el;
     }
-    base += tot;
-    __syncthreads();
+    base += __popc(bal);
   }
-  if (tid == 0) in_n[b] = base;
+  if (tid == 0) in_n[b] = total;
   sssd_elem* out = sorted + (size_t)b * cap;
-  if (base == 0) return;
-  uint32_t* idx = (base <= kSortSmem) ? s_idx : idx_ws + (size_t)b * cap2;
-  block_sort_elems(r, out, seq, base, idx);
+  if (total == 0) return;
+  __syncthreads();
+  if (total <= 32) {
+    // small occurrence sets (the common case): rank sort inside warp 0, no barriers
+    if (warp == 0) {
+      const ElemLess less{r, seq, total};
+      if (lane < total) {
+        int rank = 0;
+        for (int jj = 0; jj < total; ++jj) rank += less((uint32_t)jj, (uint32_t)lane) ? 1 : 0;
+        out[rank] = r[lane];
+      }
+      __syncwarp();
+      if (cols.meta && lane < total) {
+        const Cols cb{cols.meta + (size_t)b * cols.stride, cols.orig + (size_t)b * cols.stride,
+                      cols.tok + (size_t)b * cols.stride * c.IBL, cols.stride};
+        write_cols(cb, lane, out[lane], seq);
+      }
+    }
+    return;
+  }
+  uint32_t* idx = (total <= kSortSmem) ? s_idx : idx_ws + (size_t)b * cap2;
+  block_sort_elems(r, out, seq, total, idx);
   if (cols.meta) {
     const Cols cb{cols.meta + (size_t)b * cols.stride, cols.orig + (size_t)b * cols.stride,
                   cols.tok + (size_t)b * cols.stride * c.IBL, cols.stride};
-    for (int i = tid; i < base; i += blockDim.x) write_cols(cb, i, out[i], seq);
+    for (int i = tid; i < total; i += blockDim.x) write_cols(cb, i, out[i], seq);
   }
 }
 

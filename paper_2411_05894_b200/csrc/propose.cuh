@@ -44,7 +44,13 @@ __global__ void draft_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg
                              uint32_t slab_cap, Child* pool, unsigned long long* cursor,
                              uint64_t pool_cap, int32_t* err, uint8_t* gover, int64_t gover_bytes,
                              sssd_draft_out out, long long* cycles, const int32_t* order);
-__global__ void lpt_order_kernel(const SrcDesc* desc, int P, int B, int32_t* order);
+__device__ __forceinline__ int lpt_bucket(const SrcDesc* d, int P) {
+  long long cost = d[0].n;
+  for (int r = 1; r <= P; ++r) cost += d[r].n;
+  return 63 - min(63, 2 * (63 - __clzll(cost + 1)));  // 2 buckets per octave, largest first
+}
+__global__ void lpt_scatter_kernel(const uint8_t* bucket, const int32_t* hist, int32_t* fill, int B,
+                                   int32_t* order);
 
 constexpr int kChildBytes = 32;
 constexpr int kGroupBytes = 16;  // cold group record
