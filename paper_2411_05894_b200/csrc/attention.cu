@@ -1,25 +1,29 @@
 // Tree-attention verification on B200: tcgen05.mma (kind::f16, bf16 inputs,
-// fp32 accumulators in TMEM), semantics of ref draft.py:205-210 — every draft
-// node i attends to the committed prefix [0, ctx) and to its ancestors-or-self
-// among the S tree keys [ctx, ctx + S) (u64 ancestor rows from the fusion
-// kernel), so one forward gives all s_q greedy predictions.
+// fp32 accumulators in TMEM) fed by TMA.  Semantics of ref draft.py:205-210 —
+// every draft node i attends to the committed prefix [0, ctx) and to its
+// ancestors-or-self among the S tree keys [ctx, ctx + S) (u64 ancestor rows
+// from the fusion kernel), so one forward gives all s_q greedy predictions.
 //
 // One CTA = (row tile of 128 query rows, batch * kv-head, KV split).  The
 // G = Hq/Hkv query heads sharing a kv head are packed with the S tree queries
-// into the MMA M dimension (row r = head_in_group * S + i), so K/V are read
-// once per kv head (GQA).  Per 128-key block:
-//   stage K, V (global -> smem, core-matrix layout)          all threads
-//   S = Q K^T        8 x tcgen05.mma M128 N128 K16 -> TMEM    thread 0
-//   online softmax   tcgen05.ld S rows, mask, exp2, P -> smem  1 thread / row
-//   O *= corr        tcgen05.ld/st of the O accumulator rows
-//   O += P V         8 x tcgen05.mma (V as an MN-major operand)
-// Splits write unnormalised partial O + (max, sum); a combine kernel merges
-// them with the log-sum-exp rule.
+// into the MMA M dimension (row r = head_in_group * S + i): K/V are read once
+// per kv head (GQA).  Warp roles (6 warps):
+//   warps 0-3  softmax: one thread per query row; online softmax over S rows
+//              read with tcgen05.ld, P (bf16) written to smem in the 128B-
+//              swizzled K-major layout, O rows rescaled in TMEM
+//   warp 4     TMA producer: K and V blocks of 128 keys (2 stages, 128B
+//              swizzle, 64 KB per stage) into smem, mbarrier complete_tx
+//   warp 5     MMA issuer: S[j%2] = Q K_j^T (M128 N128 K16 x 8) as soon as the
+//              stage lands, so Q K^T of block j+1 overlaps the softmax of j;
+//              O += P_j V_j (V as an MN-major operand) after P_j is ready
+// TMEM: S0 | S1 | O (3 x 128 fp32 columns).  Split-KV partials (unnormalised O,
+// row max, row sum) are merged by the log-sum-exp combine kernel.
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <stdint.h>
 #include <stdio.h>
-#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -29,25 +33,30 @@ int cuda_check(cudaError_t e, const char* what);
 
 namespace attn {
 
-constexpr int kD = 128;       // head dim
-constexpr int kM = 128;       // rows per tile (UMMA M)
-constexpr int kN = 128;       // keys per block (UMMA N of QK^T, K of PV)
+constexpr int kD = 128;             // head dim
+constexpr int kM = 128;             // rows per tile (UMMA M)
+constexpr int kN = 128;             // keys per block (UMMA N of QK^T, K of PV)
 constexpr int kTile = kM * kD * 2;  // 32 KB per bf16 128x128 tile
-constexpr int kThreads = 128;
+constexpr int kHalf = kTile / 2;    // 16 KB: 128 rows x 64 columns (one 128B-swizzled TMA box)
+constexpr int kStages = 2;
+constexpr int kSoftmaxThreads = 128;
+constexpr int kThreads = 192;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// Core-matrix ("interleave", no swizzle) layout of a 128 x 128 bf16 tile:
-// element (r, c) lives at (r/8)*2048 + (c/8)*128 + (r%8)*16 + (c%8)*2.
-// As a K-major operand (rows = M or N, c = K): LBO = 128 B, SBO = 2048 B.
-// As an MN-major operand (rows = K, c = N):    LBO = 2048 B, SBO = 128 B.
-__device__ __forceinline__ uint32_t tile_off(int r, int c8) { return (r >> 3) * 2048 + c8 * 128 + (r & 7) * 16; }
+// 128B-swizzled K-major tile of 128 rows x 128 bf16 columns, stored as two
+// [128 x 64] halves (16 KB each, = the TMA SWIZZLE_128B box layout): element
+// (r, c) at half(c/64) + r*128 + (((c%64)/8) ^ (r%8))*16 + (c%8)*2.
+__device__ __forceinline__ uint32_t sw_off(int r, int c8) {
+  return (uint32_t)((c8 >> 3) * kHalf + r * 128 + (((c8 & 7) ^ (r & 7)) << 4));
+}
 
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory descriptor, SWIZZLE_128B (layout type 2), version 1
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((addr >> 4) & 0x3fff) | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | (1ull << 46);  // version 1, no swizzle
+         ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | (1ull << 46) | (2ull << 61);
 }
 
 // kind::f16 instruction descriptor: bf16 x bf16 -> f32, M = 128, N = 128
@@ -72,6 +81,14 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t phase) {
   uint32_t ok;
   asm volatile(
@@ -84,14 +101,23 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t phase) {
   return ok != 0;
 }
 
-// bounded wait: a tensor-core op that never completes traps instead of hanging
+// bounded wait: a pipeline stage that never completes traps instead of hanging
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   for (uint32_t it = 0; !mbar_try(bar, phase); ++it) {
-    if (it > (1u << 24)) {
-      printf("sssd tree_attn: mbarrier timeout block (%d,%d,%d) phase %u\n", blockIdx.x, blockIdx.y, blockIdx.z, phase);
+    if (it > (1u << 26)) {
+      printf("sssd tree_attn: mbarrier timeout block (%d,%d,%d) thread %d phase %u\n", blockIdx.x, blockIdx.y,
+             blockIdx.z, threadIdx.x, phase);
       __trap();
     }
   }
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ float fast_exp2(float x) {
@@ -136,9 +162,7 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
 }
 
 struct Params {
-  const uint16_t* q;   // [B][S][Hq][D]
-  const uint16_t* k;   // [B][Hkv][max_pos][D]
-  const uint16_t* v;
+  const uint16_t* q;     // [B][S][Hq][D]
   const uint64_t* mask;  // [B][S][W]
   const int32_t* ctx;    // [B]
   uint16_t* o;           // [B][S][Hq][D]
@@ -148,249 +172,258 @@ struct Params {
   float scale_log2;
 };
 
-// asynchronous staging of rows [0, nrows) of a 128 x 128 bf16 tile into the
-// core-matrix layout (cp.async, 16 B per op, all in flight); rows >= nrows are
-// zero-filled (src-size 0) so masked keys contribute 0 * 0 to P V
-__device__ __forceinline__ void stage_tile_async(uint8_t* tile, const uint16_t* src, int64_t row_stride,
-                                                 int nrows) {
-#pragma unroll 4
-  for (int idx = threadIdx.x; idx < kM * 16; idx += kThreads) {
-    const int r = idx >> 4, c8 = idx & 15;
-    const uint16_t* g = src + (int64_t)(r < nrows ? r : 0) * row_stride + c8 * 8;
-    const uint32_t bytes = r < nrows ? 16u : 0u;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(tile + tile_off(r, c8))), "l"(g),
-                 "r"(bytes)
-                 : "memory");
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
+struct Smem {  // 1024-aligned dynamic shared memory layout
+  uint8_t q[kTile];
+  uint8_t k[kStages][kTile];
+  uint8_t v[kStages][kTile];
+  uint8_t p[kTile];
+  uint64_t full[kStages], empty[kStages], s_full[2], s_free[2], p_ready, pv_done;
+  uint32_t tmem;
+};
 
-__global__ void __launch_bounds__(kThreads, 1) tree_attn_kernel(Params p) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sQ = smem;
-  uint8_t* sKb[2] = {smem + kTile, smem + 2 * kTile};
-  uint8_t* sVb[2] = {smem + 3 * kTile, smem + 4 * kTile};
-  uint8_t* sP = smem + 5 * kTile;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 6 * kTile);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
-
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int tile = blockIdx.x;               // row tile
-  const int bh = blockIdx.y;                 // b * Hkv + kvh
-  const int split = blockIdx.z;
+__global__ void __launch_bounds__(kThreads, 1)
+    tree_attn_kernel(Params p, const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tile = blockIdx.x, bh = blockIdx.y, split = blockIdx.z;
   const int b = bh / p.Hkv, kvh = bh % p.Hkv;
   const int rows = p.G * p.S;
-  const int r = tile * kM + tid;             // this thread's query row
-  const bool row_ok = r < rows;
-  const int hl = row_ok ? r / p.S : 0, qi = row_ok ? r % p.S : 0;
-  const int head = kvh * p.G + hl;
   const int ctx = p.ctx[b];
   const int total = ctx + p.S;
   const int kv0 = split * p.split_len;
   const int kv1 = min(total, kv0 + p.split_len);
+  const int nblk = kv1 > kv0 ? (kv1 - kv0 + kN - 1) / kN : 0;
 
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(256));
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem)),
+                 "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    mbar_init(bar, 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&sm.s_full[s], 1);
+      mbar_init(&sm.s_free[s], kSoftmaxThreads);
+    }
+    mbar_init(&sm.p_ready, kSoftmaxThreads);
+    mbar_init(&sm.pv_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // Q tile: row r = (head_in_group, query i) -> q[b][i][kvh*G + hl][:]
-  for (int idx = tid; idx < kM * 16; idx += kThreads) {
-    const int rr = idx >> 4, c8 = idx & 15;
-    const int gr = tile * kM + rr;
-    uint4 val = make_uint4(0, 0, 0, 0);
-    if (gr < rows) {
-      const int h2 = kvh * p.G + gr / p.S, i2 = gr % p.S;
-      val = __ldg(reinterpret_cast<const uint4*>(p.q + (((int64_t)b * p.S + i2) * p.Hq + h2) * kD) + c8);
+  // Q tile (swizzled K-major): row r = (head_in_group, query i) -> q[b][i][kvh*G + hl][:]
+  if (warp < 4) {
+    for (int idx = tid; idx < kM * 16; idx += kSoftmaxThreads) {
+      const int rr = idx >> 4, c8 = idx & 15;
+      const int gr = tile * kM + rr;
+      uint4 val = make_uint4(0, 0, 0, 0);
+      if (gr < rows) {
+        const int h2 = kvh * p.G + gr / p.S, i2 = gr % p.S;
+        val = __ldg(reinterpret_cast<const uint4*>(p.q + (((int64_t)b * p.S + i2) * p.Hq + h2) * kD) + c8);
+      }
+      *reinterpret_cast<uint4*>(sm.q + sw_off(rr, c8)) = val;
     }
-    *reinterpret_cast<uint4*>(sQ + tile_off(rr, c8)) = val;
+    fence_async_smem();
   }
   fence_before();
   __syncthreads();
   fence_after();
-  const uint32_t tbase = *tslot;
-  const uint32_t tS = tbase, tO = tbase + 128;
+  const uint32_t tbase = sm.tmem;
+  const uint32_t tS0 = tbase, tS1 = tbase + 128, tO = tbase + 256;
+  const int64_t row0 = (int64_t)(b * p.Hkv + kvh) * p.max_pos;  // first K/V row of this (b, kv head)
 
-  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-  const uint64_t* mrow_all = p.mask + ((int64_t)b * p.S + qi) * p.W;
-
-  const uint32_t id_qk = idesc_bf16(false), id_pv = idesc_bf16(true);
-  const uint32_t aQ = smem_u32(sQ), aP = smem_u32(sP);
-  const int64_t kv_stride = (int64_t)p.max_pos * kD;
-  const uint16_t* kbase = p.k + ((int64_t)b * p.Hkv + kvh) * kv_stride;
-  const uint16_t* vbase = p.v + ((int64_t)b * p.Hkv + kvh) * kv_stride;
-
-  float m_run = -INFINITY, l_run = 0.f;
-  uint32_t phase = 0;
-  bool first = true;
-  if (kv0 < kv1) {  // prefetch block 0
-    const int nk = min(kN, kv1 - kv0);
-    stage_tile_async(sKb[0], kbase + (int64_t)kv0 * kD, kD, nk);
-    stage_tile_async(sVb[0], vbase + (int64_t)kv0 * kD, kD, nk);
-  }
-  int buf = 0;
-  for (int k0 = kv0; k0 < kv1; k0 += kN, buf ^= 1) {
-    // prefetch the next block into the other buffer (its last readers, the
-    // MMAs of the previous block, completed before this iteration)
-    if (k0 + kN < kv1) {
-      const int nk2 = min(kN, kv1 - (k0 + kN));
-      stage_tile_async(sKb[buf ^ 1], kbase + (int64_t)(k0 + kN) * kD, kD, nk2);
-      stage_tile_async(sVb[buf ^ 1], vbase + (int64_t)(k0 + kN) * kD, kD, nk2);
-      asm volatile("cp.async.wait_group 2;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (warp == 4) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      for (int j = 0; j < nblk; ++j) {
+        const int st = j % kStages;
+        if (j >= kStages) mbar_wait(&sm.empty[st], ((j / kStages) - 1) & 1);
+        mbar_expect_tx(&sm.full[st], 2 * kTile);
+        const int y = (int)(row0 + kv0 + j * kN);
+        tma_load_2d(sm.k[st], &kmap, 0, y, &sm.full[st]);
+        tma_load_2d(sm.k[st] + kHalf, &kmap, 64, y, &sm.full[st]);
+        tma_load_2d(sm.v[st], &vmap, 0, y, &sm.full[st]);
+        tma_load_2d(sm.v[st] + kHalf, &vmap, 64, y, &sm.full[st]);
+      }
     }
-    const uint32_t aK = smem_u32(sKb[buf]), aV = smem_u32(sVb[buf]);
-    fence_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      fence_after();
+  } else if (warp == 5) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t id_qk = idesc_bf16(false), id_pv = idesc_bf16(true);
+      const uint32_t aQ = smem_u32(sm.q), aP = smem_u32(sm.p);
+      for (int j = -1; j < nblk; ++j) {
+        const int jn = j + 1;  // Q K^T of the next block goes first so it overlaps softmax(j)
+        if (jn < nblk) {
+          const int st = jn % kStages, sb = jn & 1;
+          mbar_wait(&sm.full[st], (jn / kStages) & 1);
+          if (jn >= 2) mbar_wait(&sm.s_free[sb], ((jn - 2) / 2) & 1);
+          fence_after();
+          const uint32_t aK = smem_u32(sm.k[st]);
+          const uint32_t tS = sb ? tS1 : tS0;
 #pragma unroll
-      for (int ks = 0; ks < kD / 16; ++ks)
-        mma_bf16(tS, smem_desc(aQ + ks * 256, 128, 2048), smem_desc(aK + ks * 256, 128, 2048), id_qk, ks > 0);
-      mma_commit(bar);
-    }
-    mbar_wait(bar, phase);
-    phase ^= 1;
-    fence_after();
-
-    // online softmax over this block (one thread per query row).  Visibility of
-    // the 32 keys of chunk c is one word: prefix keys are all visible, tree key
-    // t is visible iff bit t of this row's ancestor mask is set.
-    uint32_t visw[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int key0 = k0 + c * 32;
-      uint32_t w = 0;
-      if (row_ok) {
-        const int lim = min(32, kv1 - key0);  // keys past the range are invisible
-        w = lim >= 32 ? 0xffffffffu : (lim > 0 ? (1u << lim) - 1u : 0u);
-        if (key0 + 32 > ctx) {  // chunk overlaps the tree region
-          uint32_t tree = 0;
-#pragma unroll 1
-          for (int jj = max(0, ctx - key0); jj < 32; ++jj) {
-            const int t = key0 + jj - ctx;
-            if (t < p.S && ((mrow_all[t >> 6] >> (t & 63)) & 1ull)) tree |= 1u << jj;
+          for (int ks = 0; ks < kD / 16; ++ks) {
+            const uint32_t off = (ks >> 2) * kHalf + (ks & 3) * 32;  // K step of 16 columns
+            mma_bf16(tS, sw128_desc(aQ + off, 16, 1024), sw128_desc(aK + off, 16, 1024), id_qk, ks > 0);
           }
-          const uint32_t pref = ctx - key0 >= 32 ? 0xffffffffu : (ctx > key0 ? (1u << (ctx - key0)) - 1u : 0u);
-          w &= pref | tree;
+          mma_commit(&sm.s_full[sb]);
         }
-      }
-      visw[c] = w;
-    }
-    float sv[32];
-    float bmax = -INFINITY;
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      tmem_ld32(tS + lane_off + c * 32, sv);
-      const uint32_t w = visw[c];
+        if (j < 0) continue;
+        mbar_wait(&sm.p_ready, j & 1);
+        fence_after();
+        const uint32_t aV = smem_u32(sm.v[j % kStages]);
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if ((w >> j) & 1u) bmax = fmaxf(bmax, sv[j]);
-    }
-    bmax = (bmax == -INFINITY) ? bmax : bmax * p.scale_log2;
-    const float m_new = fmaxf(m_run, bmax);
-    const float corr = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - m_new);
-    float psum = 0.f;
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      tmem_ld32(tS + lane_off + c * 32, sv);
-      const uint32_t w = (m_new == -INFINITY) ? 0u : visw[c];
-      uint32_t pk[16];
-#pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        const float e0 = ((w >> j) & 1u) ? fast_exp2(fmaf(sv[j], p.scale_log2, -m_new)) : 0.f;
-        const float e1 = ((w >> (j + 1)) & 1u) ? fast_exp2(fmaf(sv[j + 1], p.scale_log2, -m_new)) : 0.f;
-        psum += e0 + e1;
-        const __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
-        pk[j >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
-      }
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4)
-        *reinterpret_cast<uint4*>(sP + tile_off(tid, c * 4 + q4)) =
-            make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
-    }
-    l_run = l_run * corr + psum;
-    // rescale the running O rows; tcgen05.ld/st are warp-collective, so the
-    // whole warp takes the branch when any of its rows needs it
-    if (!first && __any_sync(SSSD_FULL, corr != 1.f)) {
-      float ov[32];
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        tmem_ld32(tO + lane_off + c * 32, ov);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) ov[j] *= corr;
-        tmem_st32(tO + lane_off + c * 32, ov);
-      }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    }
-    m_run = m_new;
-    fence_async_smem();
-    fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      fence_after();
-#pragma unroll
-      for (int ks = 0; ks < kN / 16; ++ks)
-        mma_bf16(tO, smem_desc(aP + ks * 256, 128, 2048), smem_desc(aV + ks * 4096, 2048, 128), id_pv,
-                 (!first || ks > 0) ? 1u : 0u);
-      mma_commit(bar);
-    }
-    mbar_wait(bar, phase);
-    phase ^= 1;
-    fence_after();
-    first = false;
-  }
-
-  // epilogue: O row from TMEM
-  float ov[32];
-  if (p.splits == 1) {
-    const float inv = (l_run > 0.f) ? 1.f / l_run : 0.f;
-    for (int c = 0; c < 4; ++c) {
-      if (first) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) ov[j] = 0.f;
-      } else {
-        tmem_ld32(tO + lane_off + c * 32, ov);
-      }
-      if (row_ok) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          const __nv_bfloat162 h2 = __floats2bfloat162_rn(ov[j] * inv, ov[j + 1] * inv);
-          pk[j >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
+        for (int ks = 0; ks < kN / 16; ++ks) {
+          // P: K-major over keys (two 64-key halves); V: MN-major, 8-key groups of 1024 B
+          const uint32_t poff = (ks >> 2) * kHalf + (ks & 3) * 32;
+          mma_bf16(tO, sw128_desc(aP + poff, 16, 1024), sw128_desc(aV + ks * 2048, kHalf, 1024), id_pv,
+                   (j > 0 || ks > 0) ? 1u : 0u);
         }
-        uint4* dst = reinterpret_cast<uint4*>(p.o + (((int64_t)b * p.S + qi) * p.Hq + head) * kD + c * 32);
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) dst[q4] = make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+        mma_commit(&sm.pv_done);
+        mma_commit(&sm.empty[j % kStages]);
       }
     }
   } else {
-    const int64_t prow = (((int64_t)split * p.B + b) * p.Hq + head) * p.S + qi;
-    for (int c = 0; c < 4; ++c) {
-      if (first) {
+    // ---------------- softmax (one thread per query row) ----------------
+    const int r = tile * kM + tid;
+    const bool row_ok = r < rows;
+    const int hl = row_ok ? r / p.S : 0, qi = row_ok ? r % p.S : 0;
+    const int head = kvh * p.G + hl;
+    const uint64_t* mrow = p.mask + ((int64_t)b * p.S + qi) * p.W;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < nblk; ++j) {
+      const int k0 = kv0 + j * kN, sb = j & 1;
+      const uint32_t tS = sb ? tS1 : tS0;
+      // visibility of the 32 keys of chunk c: prefix keys visible, tree key t iff bit t
+      uint32_t visw[4];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) ov[j] = 0.f;
-      } else {
-        tmem_ld32(tO + lane_off + c * 32, ov);
+      for (int c = 0; c < 4; ++c) {
+        const int key0 = k0 + c * 32;
+        uint32_t w = 0;
+        if (row_ok) {
+          const int lim = min(32, kv1 - key0);
+          w = lim >= 32 ? 0xffffffffu : (lim > 0 ? (1u << lim) - 1u : 0u);
+          if (key0 + 32 > ctx) {
+            uint32_t tree = 0;
+#pragma unroll 1
+            for (int jj = max(0, ctx - key0); jj < 32; ++jj) {
+              const int t = key0 + jj - ctx;
+              if (t < p.S && ((mrow[t >> 6] >> (t & 63)) & 1ull)) tree |= 1u << jj;
+            }
+            const uint32_t pref = ctx - key0 >= 32 ? 0xffffffffu : (ctx > key0 ? (1u << (ctx - key0)) - 1u : 0u);
+            w &= pref | tree;
+          }
+        }
+        visw[c] = w;
+      }
+      mbar_wait(&sm.s_full[sb], (j >> 1) & 1);
+      fence_after();
+      float sv[32];
+      float bmax = -INFINITY;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        tmem_ld32(tS + lane_off + c * 32, sv);
+        const uint32_t w = visw[c];
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj)
+          if ((w >> jj) & 1u) bmax = fmaxf(bmax, sv[jj]);
+      }
+      bmax = (bmax == -INFINITY) ? bmax : bmax * p.scale_log2;
+      const float m_new = fmaxf(m_run, bmax);
+      const float corr = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - m_new);
+      // P and the O accumulator are free once P_{j-1} V_{j-1} completed
+      if (j > 0) mbar_wait(&sm.pv_done, (j - 1) & 1);
+      fence_after();
+      float psum = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        tmem_ld32(tS + lane_off + c * 32, sv);
+        const uint32_t w = (m_new == -INFINITY) ? 0u : visw[c];
+        uint32_t pk[16];
+#pragma unroll
+        for (int jj = 0; jj < 32; jj += 2) {
+          const float e0 = ((w >> jj) & 1u) ? fast_exp2(fmaf(sv[jj], p.scale_log2, -m_new)) : 0.f;
+          const float e1 = ((w >> (jj + 1)) & 1u) ? fast_exp2(fmaf(sv[jj + 1], p.scale_log2, -m_new)) : 0.f;
+          psum += e0 + e1;
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
+          pk[jj >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4)
+          *reinterpret_cast<uint4*>(sm.p + sw_off(tid, c * 4 + q4)) =
+              make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+      }
+      fence_before();
+      mbar_arrive(&sm.s_free[sb]);  // S[sb] fully read
+      l_run = l_run * corr + psum;
+      if (j > 0 && __any_sync(SSSD_FULL, corr != 1.f)) {  // warp-collective TMEM ld/st
+        float ov[32];
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          tmem_ld32(tO + lane_off + c * 32, ov);
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) ov[jj] *= corr;
+          tmem_st32(tO + lane_off + c * 32, ov);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+      m_run = m_new;
+      fence_async_smem();
+      fence_before();
+      mbar_arrive(&sm.p_ready);
+    }
+    // epilogue: O rows from TMEM after the last P V
+    if (nblk > 0) mbar_wait(&sm.pv_done, (nblk - 1) & 1);
+    fence_after();
+    float ov[32];
+    if (p.splits == 1) {
+      const float inv = (l_run > 0.f) ? 1.f / l_run : 0.f;
+      for (int c = 0; c < 4; ++c) {
+        if (nblk == 0) {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) ov[jj] = 0.f;
+        } else {
+          tmem_ld32(tO + lane_off + c * 32, ov);
+        }
+        if (row_ok) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int jj = 0; jj < 32; jj += 2) {
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(ov[jj] * inv, ov[jj + 1] * inv);
+            pk[jj >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
+          }
+          uint4* dst = reinterpret_cast<uint4*>(p.o + (((int64_t)b * p.S + qi) * p.Hq + head) * kD + c * 32);
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) dst[q4] = make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+        }
+      }
+    } else {
+      const int64_t prow = (((int64_t)split * p.B + b) * p.Hq + head) * p.S + qi;
+      for (int c = 0; c < 4; ++c) {
+        if (nblk == 0) {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) ov[jj] = 0.f;
+        } else {
+          tmem_ld32(tO + lane_off + c * 32, ov);
+        }
+        if (row_ok) {
+          float4* dst = reinterpret_cast<float4*>(p.part_o + prow * kD + c * 32);
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4) dst[q4] = make_float4(ov[q4 * 4], ov[q4 * 4 + 1], ov[q4 * 4 + 2], ov[q4 * 4 + 3]);
+        }
       }
       if (row_ok) {
-        float4* dst = reinterpret_cast<float4*>(p.part_o + prow * kD + c * 32);
-#pragma unroll
-        for (int q4 = 0; q4 < 8; ++q4) dst[q4] = make_float4(ov[q4 * 4], ov[q4 * 4 + 1], ov[q4 * 4 + 2], ov[q4 * 4 + 3]);
+        p.part_ml[prow * 2] = m_run;
+        p.part_ml[prow * 2 + 1] = l_run;
       }
-    }
-    if (row_ok) {
-      p.part_ml[prow * 2] = m_run;
-      p.part_ml[prow * 2 + 1] = l_run;
     }
   }
   fence_before();
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(256));
+  if (warp == 5) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
 }
 
 // merge split-KV partials: O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s
@@ -416,7 +449,29 @@ __global__ void tree_attn_combine_kernel(Params p) {
   p.o[(((int64_t)b * p.S + i) * p.Hq + head) * kD + d] = __bfloat16_as_ushort(__float2bfloat16_rn(out));
 }
 
-constexpr int kSmem = 6 * kTile + 64;
+constexpr int kSmem = (int)sizeof(Smem) + 1024;
+
+// TMA descriptor over a [rows][128] bf16 cache viewed as 2D, box 64 x 128, 128B swizzle
+static int make_kv_map(CUtensorMap* map, const void* base, uint64_t rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(SSSD_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)kD, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)kD * 2};
+  const cuuint32_t box[2] = {64, (cuuint32_t)kN};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SSSD_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return SSSD_OK;
+}
 
 }  // namespace attn
 }  // namespace sssd
@@ -435,8 +490,7 @@ static int attn_splits(int32_t B, int32_t Hq, int32_t Hkv, int32_t S, int32_t ma
 }
 
 size_t sssd_tree_attention_workspace(int32_t B, int32_t S, int32_t Hq, int32_t max_pos) {
-  // worst case over Hkv: splits chosen for Hkv = 1
-  int splits = 1;
+  int splits = 1;  // worst case over Hkv: splits chosen for Hkv = 1
   while (splits < 64 && (max_pos / (splits * 2)) >= 1024) splits *= 2;
   return (size_t)splits * B * Hq * S * (attn::kD + 2) * sizeof(float) + 256;
 }
@@ -451,8 +505,6 @@ int sssd_tree_attention(const uint16_t* q, const uint16_t* k, const uint16_t* v,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   attn::Params p;
   p.q = q;
-  p.k = k;
-  p.v = v;
   p.mask = mask;
   p.ctx = ctx_len;
   p.o = o;
@@ -464,7 +516,6 @@ int sssd_tree_attention(const uint16_t* q, const uint16_t* k, const uint16_t* v,
   p.max_pos = max_pos;
   p.W = (S + 63) / 64;
   p.scale_log2 = scale * 1.4426950408889634f;
-
   p.splits = attn_splits(B, Hq, Hkv, S, max_pos);
   p.split_len = ((max_pos + p.splits - 1) / p.splits + attn::kN - 1) / attn::kN * attn::kN;
   const size_t need = (size_t)p.splits * B * Hq * S * (attn::kD + 2) * sizeof(float) + 256;
@@ -477,12 +528,17 @@ int sssd_tree_attention(const uint16_t* q, const uint16_t* k, const uint16_t* v,
     p.part_o = nullptr;
     p.part_ml = nullptr;
   }
-  const int tiles = (p.G * S + attn::kM - 1) / attn::kM;
-  int rc = cuda_check(cudaFuncSetAttribute(attn::tree_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           attn::kSmem),
-                      "tree_attn smem attribute");
+  CUtensorMap kmap, vmap;
+  const uint64_t rows = (uint64_t)B * Hkv * max_pos;
+  int rc = attn::make_kv_map(&kmap, k, rows);
+  if (!rc) rc = attn::make_kv_map(&vmap, v, rows);
   if (rc) return rc;
-  attn::tree_attn_kernel<<<dim3(tiles, B * Hkv, p.splits), attn::kThreads, attn::kSmem, st>>>(p);
+  const int tiles = (p.G * S + attn::kM - 1) / attn::kM;
+  rc = cuda_check(cudaFuncSetAttribute(attn::tree_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       attn::kSmem),
+                  "tree_attn smem attribute");
+  if (rc) return rc;
+  attn::tree_attn_kernel<<<dim3(tiles, B * Hkv, p.splits), attn::kThreads, attn::kSmem, st>>>(p, kmap, vmap);
   if ((rc = cuda_check(cudaGetLastError(), "tree_attn_kernel launch"))) return rc;
   if (p.splits > 1) {
     attn::tree_attn_combine_kernel<<<B * Hq * S, attn::kD, 0, st>>>(p);
