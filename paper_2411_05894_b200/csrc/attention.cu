@@ -7,17 +7,22 @@
 // One CTA = (row tile of 128 query rows, batch * kv-head, KV split).  The
 // G = Hq/Hkv query heads sharing a kv head are packed with the S tree queries
 // into the MMA M dimension (row r = head_in_group * S + i): K/V are read once
-// per kv head (GQA).  Warp roles (6 warps):
-//   warps 0-3  softmax: one thread per query row; online softmax over S rows
-//              read with tcgen05.ld, P (bf16) written to smem in the 128B-
-//              swizzled K-major layout, O rows rescaled in TMEM
-//   warp 4     TMA producer: K and V blocks of 128 keys (2 stages, 128B
+// per kv head (GQA).  Warp roles (10 warps):
+//   warps 0-7  softmax, two warpgroups: warpgroup g takes key blocks j = g,
+//              g+2, ... with its own online-softmax state (m, l) and its own O
+//              accumulator O[g] in TMEM — an intra-CTA split of the keys that
+//              doubles softmax issue width without a per-block cross-warpgroup
+//              sync; one thread per query row reads S with tcgen05.ld, writes P
+//              (bf16, 128B-swizzled K-major) over K_j, rescales O[g] lazily
+//              (only when the running max grows by > 2^8); the epilogue merges
+//              (m0, l0, O[0]) and (m1, l1, O[1])
+//   warp 8     TMA producer: K and V blocks of 128 keys (3 stages, 128B
 //              swizzle, 64 KB per stage) into smem, mbarrier complete_tx
-//   warp 5     MMA issuer: S[j%2] = Q K_j^T (M128 N128 K16 x 8) as soon as the
+//   warp 9     MMA issuer: S[j%2] = Q K_j^T (M128 N128 K16 x 8) as soon as the
 //              stage lands, so Q K^T of block j+1 overlaps the softmax of j;
-//              O += P_j V_j (V as an MN-major operand) after P_j is ready
-// TMEM: S0 | S1 | O (3 x 128 fp32 columns).  Split-KV partials (unnormalised O,
-// row max, row sum) are merged by the log-sum-exp combine kernel.
+//              O[j%2] += P_j V_j (V as an MN-major operand) once P_j is ready
+// TMEM: S0 | S1 | O0 | O1 (4 x 128 fp32 columns).  Split-KV partials
+// (unnormalised O, row max, row sum) are merged by the log-sum-exp combine kernel.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -38,9 +43,12 @@ constexpr int kM = 128;             // rows per tile (UMMA M)
 constexpr int kN = 128;             // keys per block (UMMA N of QK^T, K of PV)
 constexpr int kTile = kM * kD * 2;  // 32 KB per bf16 128x128 tile
 constexpr int kHalf = kTile / 2;    // 16 KB: 128 rows x 64 columns (one 128B-swizzled TMA box)
-constexpr int kStages = 2;
-constexpr int kSoftmaxThreads = 128;
-constexpr int kThreads = 192;
+constexpr int kStages = 3;
+constexpr int kWgWarps = 4;                  // one softmax warpgroup = 128 rows
+constexpr int kWgThreads = 32 * kWgWarps;
+constexpr int kTmaWarp = 2 * kWgWarps;       // warp 8
+constexpr int kMmaWarp = 2 * kWgWarps + 1;   // warp 9
+constexpr int kThreads = 32 * (kMmaWarp + 1);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -172,14 +180,17 @@ struct Params {
   float scale_log2;
 };
 
-struct Smem {  // 1024-aligned dynamic shared memory layout
-  uint8_t q[kTile];
-  uint8_t k[kStages][kTile];
+struct Smem {  // 1024-aligned dynamic shared memory layout (224 KB)
+  uint8_t q[kTile];           // Q tile; reused for the warpgroup merge once all MMAs completed
+  uint8_t k[kStages][kTile];  // K_j, then P_j once Q K_j^T has completed
   uint8_t v[kStages][kTile];
-  uint8_t p[kTile];
-  uint64_t full[kStages], empty[kStages], s_full[2], s_free[2], p_ready, pv_done;
+  uint64_t full[kStages], empty[kStages], s_full[2], s_free[2], p_ready[2], pv_done[2];
   uint32_t tmem;
 };
+
+__device__ __forceinline__ void wg_bar() {  // both softmax warpgroups (256 threads)
+  asm volatile("bar.sync 1, %0;" ::"n"(2 * kWgThreads) : "memory");
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
     tree_attn_kernel(Params p, const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap) {
@@ -196,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kv1 = min(total, kv0 + p.split_len);
   const int nblk = kv1 > kv0 ? (kv1 - kv0 + kN - 1) / kN : 0;
 
-  if (warp == 5) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem)),
                  "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -208,15 +219,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.s_full[s], 1);
-      mbar_init(&sm.s_free[s], kSoftmaxThreads);
+      mbar_init(&sm.s_free[s], kWgThreads);
+      mbar_init(&sm.p_ready[s], kWgThreads);
+      mbar_init(&sm.pv_done[s], 1);
     }
-    mbar_init(&sm.p_ready, kSoftmaxThreads);
-    mbar_init(&sm.pv_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // Q tile (swizzled K-major): row r = (head_in_group, query i) -> q[b][i][kvh*G + hl][:]
-  if (warp < 4) {
-    for (int idx = tid; idx < kM * 16; idx += kSoftmaxThreads) {
+  if (warp < 2 * kWgWarps) {
+    for (int idx = tid; idx < kM * 16; idx += 2 * kWgThreads) {
       const int rr = idx >> 4, c8 = idx & 15;
       const int gr = tile * kM + rr;
       uint4 val = make_uint4(0, 0, 0, 0);
@@ -232,10 +243,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   fence_after();
   const uint32_t tbase = sm.tmem;
-  const uint32_t tS0 = tbase, tS1 = tbase + 128, tO = tbase + 256;
   const int64_t row0 = (int64_t)(b * p.Hkv + kvh) * p.max_pos;  // first K/V row of this (b, kv head)
 
-  if (warp == 4) {
+  if (warp == kTmaWarp) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       for (int j = 0; j < nblk; ++j) {
@@ -249,54 +259,62 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(sm.v[st] + kHalf, &vmap, 64, y, &sm.full[st]);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == kMmaWarp) {
     // ---------------- MMA issuer ----------------
+    // block j: S[j&1] = Q K_j^T, O[j&1] += P_j V_j (warpgroup j&1 owns S/O[j&1])
     if (lane == 0) {
       const uint32_t id_qk = idesc_bf16(false), id_pv = idesc_bf16(true);
-      const uint32_t aQ = smem_u32(sm.q), aP = smem_u32(sm.p);
+      const uint32_t aQ = smem_u32(sm.q);
       for (int j = -1; j < nblk; ++j) {
         const int jn = j + 1;  // Q K^T of the next block goes first so it overlaps softmax(j)
         if (jn < nblk) {
-          const int st = jn % kStages, sb = jn & 1;
+          const int st = jn % kStages, g = jn & 1;
           mbar_wait(&sm.full[st], (jn / kStages) & 1);
-          if (jn >= 2) mbar_wait(&sm.s_free[sb], ((jn - 2) / 2) & 1);
+          if (jn >= 2) mbar_wait(&sm.s_free[g], ((jn >> 1) - 1) & 1);
           fence_after();
           const uint32_t aK = smem_u32(sm.k[st]);
-          const uint32_t tS = sb ? tS1 : tS0;
+          const uint32_t tS = tbase + g * kN;
 #pragma unroll
           for (int ks = 0; ks < kD / 16; ++ks) {
             const uint32_t off = (ks >> 2) * kHalf + (ks & 3) * 32;  // K step of 16 columns
             mma_bf16(tS, sw128_desc(aQ + off, 16, 1024), sw128_desc(aK + off, 16, 1024), id_qk, ks > 0);
           }
-          mma_commit(&sm.s_full[sb]);
+          mma_commit(&sm.s_full[g]);
         }
         if (j < 0) continue;
-        mbar_wait(&sm.p_ready, j & 1);
+        const int g = j & 1;
+        mbar_wait(&sm.p_ready[g], (j >> 1) & 1);
         fence_after();
-        const uint32_t aV = smem_u32(sm.v[j % kStages]);
+        const uint32_t aV = smem_u32(sm.v[j % kStages]), aP = smem_u32(sm.k[j % kStages]);
+        const uint32_t tO = tbase + 2 * kN + g * kD;
 #pragma unroll
         for (int ks = 0; ks < kN / 16; ++ks) {
           // P: K-major over keys (two 64-key halves); V: MN-major, 8-key groups of 1024 B
           const uint32_t poff = (ks >> 2) * kHalf + (ks & 3) * 32;
           mma_bf16(tO, sw128_desc(aP + poff, 16, 1024), sw128_desc(aV + ks * 2048, kHalf, 1024), id_pv,
-                   (j > 0 || ks > 0) ? 1u : 0u);
+                   (j >= 2 || ks > 0) ? 1u : 0u);
         }
-        mma_commit(&sm.pv_done);
+        mma_commit(&sm.pv_done[g]);
         mma_commit(&sm.empty[j % kStages]);
       }
     }
   } else {
-    // ---------------- softmax (one thread per query row) ----------------
-    const int r = tile * kM + tid;
+    // ---------------- softmax: warpgroup g takes blocks j = g, g+2, ... ----------------
+    // one thread per query row; each warpgroup keeps its own (m, l, O[g]) — an
+    // intra-CTA split of the keys merged in the epilogue
+    const int g = warp / kWgWarps, rt = tid - g * kWgThreads;
+    const int r = tile * kM + rt;
     const bool row_ok = r < rows;
     const int hl = row_ok ? r / p.S : 0, qi = row_ok ? r % p.S : 0;
     const int head = kvh * p.G + hl;
     const uint64_t* mrow = p.mask + ((int64_t)b * p.S + qi) * p.W;
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const uint32_t lane_off = (uint32_t)((warp % kWgWarps) * 32) << 16;
+    const uint32_t tS = tbase + g * kN + lane_off, tO = tbase + 2 * kN + g * kD + lane_off;
+    const float sl2 = p.scale_log2;
     float m_run = -INFINITY, l_run = 0.f;
-    for (int j = 0; j < nblk; ++j) {
-      const int k0 = kv0 + j * kN, sb = j & 1;
-      const uint32_t tS = sb ? tS1 : tS0;
+    int it = 0;
+    for (int j = g; j < nblk; j += 2, ++it) {
+      const int k0 = kv0 + j * kN;
       // visibility of the 32 keys of chunk c: prefix keys visible, tree key t iff bit t
       uint32_t visw[4];
 #pragma unroll
@@ -319,111 +337,123 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         visw[c] = w;
       }
-      mbar_wait(&sm.s_full[sb], (j >> 1) & 1);
+      mbar_wait(&sm.s_full[g], it & 1);
       fence_after();
       float sv[32];
       float bmax = -INFINITY;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
-        tmem_ld32(tS + lane_off + c * 32, sv);
+        tmem_ld32(tS + c * 32, sv);
         const uint32_t w = visw[c];
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj)
-          if ((w >> jj) & 1u) bmax = fmaxf(bmax, sv[jj]);
+        for (int jj = 0; jj < 32; ++jj) bmax = fmaxf(bmax, ((w >> jj) & 1u) ? sv[jj] : -INFINITY);
       }
-      bmax = (bmax == -INFINITY) ? bmax : bmax * p.scale_log2;
-      const float m_new = fmaxf(m_run, bmax);
-      const float corr = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - m_new);
-      // P and the O accumulator are free once P_{j-1} V_{j-1} completed
-      if (j > 0) mbar_wait(&sm.pv_done, (j - 1) & 1);
-      fence_after();
+      bmax = (bmax == -INFINITY) ? bmax : bmax * sl2;
+      // lazy rescale: keep the running max unless the block max exceeds it by
+      // more than 2^8 (P <= 256 stays exact in bf16 range; O / l is unchanged)
+      float m_use = m_run, corr = 1.f;
+      if (bmax > m_run + 8.f) {
+        corr = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - bmax);
+        m_use = bmax;
+      }
+      // P_j overwrites K_j (stage j%3), dead since Q K_j^T completed (s_full)
+      uint8_t* pbuf = sm.k[j % kStages];
       float psum = 0.f;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
-        tmem_ld32(tS + lane_off + c * 32, sv);
-        const uint32_t w = (m_new == -INFINITY) ? 0u : visw[c];
+        tmem_ld32(tS + c * 32, sv);
+        const uint32_t w = (m_use == -INFINITY) ? 0u : visw[c];
         uint32_t pk[16];
 #pragma unroll
         for (int jj = 0; jj < 32; jj += 2) {
-          const float e0 = ((w >> jj) & 1u) ? fast_exp2(fmaf(sv[jj], p.scale_log2, -m_new)) : 0.f;
-          const float e1 = ((w >> (jj + 1)) & 1u) ? fast_exp2(fmaf(sv[jj + 1], p.scale_log2, -m_new)) : 0.f;
+          float e0 = fast_exp2(fmaf(sv[jj], sl2, -m_use));
+          float e1 = fast_exp2(fmaf(sv[jj + 1], sl2, -m_use));
+          e0 = ((w >> jj) & 1u) ? e0 : 0.f;
+          e1 = ((w >> (jj + 1)) & 1u) ? e1 : 0.f;
           psum += e0 + e1;
           const __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
           pk[jj >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
         }
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4)
-          *reinterpret_cast<uint4*>(sm.p + sw_off(tid, c * 4 + q4)) =
+          *reinterpret_cast<uint4*>(pbuf + sw_off(rt, c * 4 + q4)) =
               make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
       }
       fence_before();
-      mbar_arrive(&sm.s_free[sb]);  // S[sb] fully read
+      mbar_arrive(&sm.s_free[g]);  // S[g] fully read
       l_run = l_run * corr + psum;
-      if (j > 0 && __any_sync(SSSD_FULL, corr != 1.f)) {  // warp-collective TMEM ld/st
-        float ov[32];
+      // O[g] is stable once this warpgroup's previous P V completed
+      if (it > 0) {
+        mbar_wait(&sm.pv_done[g], (it - 1) & 1);
+        fence_after();
+        if (__any_sync(SSSD_FULL, corr != 1.f)) {  // warp-collective TMEM ld/st
+          float ov[32];
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          tmem_ld32(tO + lane_off + c * 32, ov);
+          for (int c = 0; c < 4; ++c) {
+            tmem_ld32(tO + c * 32, ov);
 #pragma unroll
-          for (int jj = 0; jj < 32; ++jj) ov[jj] *= corr;
-          tmem_st32(tO + lane_off + c * 32, ov);
+            for (int jj = 0; jj < 32; ++jj) ov[jj] *= corr;
+            tmem_st32(tO + c * 32, ov);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
-      m_run = m_new;
+      m_run = m_use;
       fence_async_smem();
       fence_before();
-      mbar_arrive(&sm.p_ready);
+      mbar_arrive(&sm.p_ready[g]);
     }
-    // epilogue: O rows from TMEM after the last P V
-    if (nblk > 0) mbar_wait(&sm.pv_done, (nblk - 1) & 1);
+    if (it > 0) mbar_wait(&sm.pv_done[g], (it - 1) & 1);
+    // ---------------- epilogue: merge the two warpgroups ----------------
+    // every MMA has completed once both warpgroups passed their last pv_done
+    // (commit tracks all earlier tcgen05 ops), so the Q tile is free for (m, l)
+    float* xm = reinterpret_cast<float*>(sm.q);  // [2][kM] m, then [2][kM] l
+    wg_bar();
+    xm[g * kM + rt] = m_run;
+    xm[2 * kM + g * kM + rt] = l_run;
+    wg_bar();
     fence_after();
-    float ov[32];
-    if (p.splits == 1) {
-      const float inv = (l_run > 0.f) ? 1.f / l_run : 0.f;
-      for (int c = 0; c < 4; ++c) {
-        if (nblk == 0) {
+    const float m0 = xm[rt], m1 = xm[kM + rt];
+    const float mm = fmaxf(m0, m1);
+    const float w0 = (m0 == -INFINITY) ? 0.f : fast_exp2(m0 - mm);
+    const float w1 = (m1 == -INFINITY) ? 0.f : fast_exp2(m1 - mm);
+    const float l = w0 * xm[2 * kM + rt] + w1 * xm[3 * kM + rt];
+    const bool has0 = nblk > 0, has1 = nblk > 1;  // warpgroup 1 owns no block when nblk == 1
+    const uint32_t tO0 = tbase + 2 * kN + lane_off, tO1 = tO0 + kD;
+    // warpgroup g writes output columns [64 g, 64 g + 64)
+    const int64_t prow = (((int64_t)split * p.B + b) * p.Hq + head) * p.S + qi;
+    const float inv = (l > 0.f) ? 1.f / l : 0.f;
+    for (int c = 2 * g; c < 2 * g + 2; ++c) {
+      float o0[32], o1[32];
+      if (has0) tmem_ld32(tO0 + c * 32, o0);
+      if (has1) tmem_ld32(tO1 + c * 32, o1);
 #pragma unroll
-          for (int jj = 0; jj < 32; ++jj) ov[jj] = 0.f;
-        } else {
-          tmem_ld32(tO + lane_off + c * 32, ov);
+      for (int jj = 0; jj < 32; ++jj) o0[jj] = (has0 ? w0 * o0[jj] : 0.f) + (has1 ? w1 * o1[jj] : 0.f);
+      if (!row_ok) continue;
+      if (p.splits == 1) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int jj = 0; jj < 32; jj += 2) {
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(o0[jj] * inv, o0[jj + 1] * inv);
+          pk[jj >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
         }
-        if (row_ok) {
-          uint32_t pk[16];
+        uint4* dst = reinterpret_cast<uint4*>(p.o + (((int64_t)b * p.S + qi) * p.Hq + head) * kD + c * 32);
 #pragma unroll
-          for (int jj = 0; jj < 32; jj += 2) {
-            const __nv_bfloat162 h2 = __floats2bfloat162_rn(ov[jj] * inv, ov[jj + 1] * inv);
-            pk[jj >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
-          }
-          uint4* dst = reinterpret_cast<uint4*>(p.o + (((int64_t)b * p.S + qi) * p.Hq + head) * kD + c * 32);
+        for (int q4 = 0; q4 < 4; ++q4) dst[q4] = make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+      } else {
+        float4* dst = reinterpret_cast<float4*>(p.part_o + prow * kD + c * 32);
 #pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) dst[q4] = make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
-        }
+        for (int q4 = 0; q4 < 8; ++q4) dst[q4] = make_float4(o0[q4 * 4], o0[q4 * 4 + 1], o0[q4 * 4 + 2], o0[q4 * 4 + 3]);
       }
-    } else {
-      const int64_t prow = (((int64_t)split * p.B + b) * p.Hq + head) * p.S + qi;
-      for (int c = 0; c < 4; ++c) {
-        if (nblk == 0) {
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj) ov[jj] = 0.f;
-        } else {
-          tmem_ld32(tO + lane_off + c * 32, ov);
-        }
-        if (row_ok) {
-          float4* dst = reinterpret_cast<float4*>(p.part_o + prow * kD + c * 32);
-#pragma unroll
-          for (int q4 = 0; q4 < 8; ++q4) dst[q4] = make_float4(ov[q4 * 4], ov[q4 * 4 + 1], ov[q4 * 4 + 2], ov[q4 * 4 + 3]);
-        }
-      }
-      if (row_ok) {
-        p.part_ml[prow * 2] = m_run;
-        p.part_ml[prow * 2 + 1] = l_run;
-      }
+    }
+    if (p.splits > 1 && row_ok && g == 0) {
+      p.part_ml[prow * 2] = mm;
+      p.part_ml[prow * 2 + 1] = l;
     }
   }
   fence_before();
   __syncthreads();
-  if (warp == 5) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
+  if (warp == kMmaWarp) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
 }
 
 // merge split-KV partials: O = sum_s 2^(m_s - M) O_s / sum_s 2^(m_s - M) l_s
@@ -480,18 +510,40 @@ using namespace sssd;
 
 extern "C" {
 
+static int attn_max_splits(int32_t max_pos) {  // every split keeps >= 1024 keys (bounds the workspace)
+  int cap = 1;
+  while (cap < 64 && (max_pos / (cap * 2)) >= 1024) cap *= 2;
+  return cap;
+}
+
+// Split count minimising waves x (key blocks per CTA + fixed per-CTA cost).
+// The fixed cost (TMEM alloc, Q tile, pipeline fill, epilogue, partial
+// write-back) was measured at ~4.5 key blocks on B200 (cfg3: 1 split beats 2;
+// cfg4: 2 beat 4 and 8).
 static int attn_splits(int32_t B, int32_t Hq, int32_t Hkv, int32_t S, int32_t max_pos) {
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n_sm <= 0) n_sm = 148;
+  }
   const int G = Hq / Hkv;
   const int tiles = (G * S + attn::kM - 1) / attn::kM;
-  const int ctas = tiles * B * Hkv;
-  int splits = 1;
-  while (ctas * splits < 2 * 148 && (max_pos / (splits * 2)) >= 1024) splits *= 2;
-  return splits;
+  const int64_t ctas = (int64_t)tiles * B * Hkv;
+  const int nb = (max_pos + attn::kN - 1) / attn::kN;
+  const int cap = attn_max_splits(max_pos);
+  int best = 1;
+  double best_cost = 1e300;
+  for (int s = 1; s <= cap; ++s) {
+    const double waves = (double)((ctas * s + n_sm - 1) / n_sm);
+    const double cost = waves * ((nb + s - 1) / s + 4.5);
+    if (cost < best_cost * 0.999) best_cost = cost, best = s;
+  }
+  return best;
 }
 
 size_t sssd_tree_attention_workspace(int32_t B, int32_t S, int32_t Hq, int32_t max_pos) {
-  int splits = 1;  // worst case over Hkv: splits chosen for Hkv = 1
-  while (splits < 64 && (max_pos / (splits * 2)) >= 1024) splits *= 2;
+  const int splits = attn_max_splits(max_pos);  // upper bound of attn_splits
   return (size_t)splits * B * Hq * S * (attn::kD + 2) * sizeof(float) + 256;
 }
 

@@ -79,3 +79,28 @@ def test_tree_attention_matches_fp32_reference(B, S, Hq, Hkv, ctx_max, max_pos):
     want = ref_tree_attention(q, k, v, mask, ctx, scale)
     err = (got - want).abs().max().item()
     assert err <= 1e-2 * want.abs().max().item(), err
+
+
+@pytest.mark.parametrize("B,S,Hq,Hkv,ctx_max,max_pos", [
+    (2, 32, 32, 8, 1500, 1600),   # odd/even block split between the two softmax warpgroups
+    (1, 16, 8, 2, 200, 256),      # 2 blocks: one per warpgroup
+])
+def test_tree_attention_growing_max(B, S, Hq, Hkv, ctx_max, max_pos):
+    """Scores that rise along the keys force the running max up block after block
+    (the lazy-rescale path: rescale only when the max grows by > 2^8)."""
+    torch.manual_seed(3)
+    rng = np.random.default_rng(4)
+    D = 128
+    q = (torch.randn(B, S, Hq, D, device="cuda") * 2).to(torch.bfloat16)
+    ramp = torch.linspace(0.2, 3.0, max_pos, device="cuda")[None, None, :, None]
+    k = (torch.randn(B, Hkv, max_pos, D, device="cuda") * ramp).to(torch.bfloat16)
+    v = torch.randn(B, Hkv, max_pos, D, device="cuda").to(torch.bfloat16)
+    ctx = torch.tensor([int(rng.integers(ctx_max // 2, ctx_max + 1)) for _ in range(B)],
+                       dtype=torch.int32, device="cuda")
+    mask = random_tree_masks(B, S, rng)
+    scale = 1.0 / math.sqrt(D)
+    got = tree_attention(q, k, v, mask, ctx, scale).float()
+    torch.cuda.synchronize()
+    want = ref_tree_attention(q, k, v, mask, ctx, scale)
+    err = (got - want).abs().max().item()
+    assert err <= 1e-2 * want.abs().max().item(), err
