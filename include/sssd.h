@@ -198,8 +198,11 @@ int sssd_propose_pre(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* c
                      const uint32_t* rows, const sssd_draft_out* out, const sssd_lookup_out* lookup,
                      void* workspace, size_t workspace_bytes, void* stream);
 
-/* Measurement aid: device int64[B] receiving per-request fusion-kernel cycles
- * of subsequent sssd_propose calls; NULL disables. */
+/* Measurement aid: device int64[B][8] receiving, per request of subsequent
+ * sssd_propose calls, the fusion kernel's {total cycles, seeding cycles,
+ * best-first loop cycles, flatten cycles, pops, elements scanned by
+ * expansions, peak live sibling groups, allocations spilled out of shared
+ * memory}; NULL disables. */
 void sssd_set_cycle_probe(long long* cycles);
 
 /* Fusion of caller-provided source trees (merge fusion.py:209-261 + flatten).
@@ -215,8 +218,12 @@ int sssd_merge(const uint32_t* tok, const sssd_elem* el, const int64_t* el_off,
                size_t workspace_bytes, void* stream);
 
 /* Synchronises `stream` and returns the device status word left in a propose
- * (is_merge = 0) or merge (is_merge = 1) workspace: 0, or SSSD_E_WORKSPACE when
- * the fusion arena overflowed (outputs are then invalid). */
+ * or merge workspace by the last call that used it: 0, or SSSD_E_WORKSPACE
+ * when the fusion arena overflowed (outputs are then invalid).  The word is an
+ * int32 at byte offset SSSD_STATUS_OFFSET of every workspace (callers that
+ * pipeline several proposes through one workspace copy it after each call);
+ * the size arguments are ignored. */
+#define SSSD_STATUS_OFFSET 8
 int sssd_workspace_status(const sssd_cfg* cfg, int32_t B, int32_t max_len, const void* workspace,
                           int32_t is_merge, int64_t total_elems, void* stream);
 

@@ -13,12 +13,13 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsssd.so")
+LIB_PATH = os.environ.get("SSSD_LIB") or os.path.join(_HERE, "libsssd.so")  # override: A/B builds
 
 SSSD_MAX_P = 8
 SSSD_MAX_DEPTH = 32
 SSSD_MAX_DRAFT = 256
 SSSD_ROW_TOKENS = 15
+SSSD_STATUS_OFFSET = 8  # int32 status word in every propose / merge workspace
 E_WORKSPACE = -4
 
 u32p = C.POINTER(C.c_uint32)

@@ -111,7 +111,14 @@ struct DraftWs {
 // shared overflow pool.  An expansion reserves its element-range size and
 // returns the unused tail, so the slab holds the typical request; long
 // contexts (huge input-tree roots) spill into the pool, sized by max_len.
-static DraftWs carve_draft(Carver& cv, int P, int S, int B, int64_t max_len = 0) {
+// Status block (cursor, err, LPT histogram): always the first 528 bytes of a
+// propose or merge workspace, so the status word sits at a fixed offset
+// (kStatusErrOffset) whatever B / max_len the workspace was carved for.
+constexpr size_t kStatusWords = 2 + 64;
+constexpr size_t kStatusErrOffset = 8;
+static unsigned long long* carve_status(Carver& cv) { return cv.take<unsigned long long>(kStatusWords); }
+
+static DraftWs carve_draft(Carver& cv, unsigned long long* status, int P, int S, int B, int64_t max_len = 0) {
   DraftWs d;
   d.order = cv.take<int32_t>((size_t)B);
   d.bucket = cv.take<uint8_t>((size_t)B);
@@ -123,7 +130,7 @@ static DraftWs carve_draft(Carver& cv, int P, int S, int B, int64_t max_len = 0)
   d.pool_cap = (1u << 16) + (uint64_t)B * 1024 +
                (max_len > (int64_t)kSlabChildren ? (uint64_t)B * (P + 1) * (uint64_t)max_len : 0);
   d.pool = reinterpret_cast<Child*>(cv.take<uint8_t>((size_t)d.pool_cap * kChildBytes));
-  d.cursor = cv.take<unsigned long long>(2 + 64);  // cursor + err (status words) + LPT histogram
+  d.cursor = status;  // cursor + err (status words) + LPT histogram
   d.err = reinterpret_cast<int32_t*>(d.cursor + 1);
   d.hist = reinterpret_cast<int32_t*>(d.cursor + 2);
   return d;
@@ -149,6 +156,7 @@ struct PropWs {
 
 static PropWs carve_propose(uint8_t* base, const sssd_cfg* c, int B, int max_len) {
   Carver cv{base, 0};
+  unsigned long long* status = carve_status(cv);
   PropWs w;
   const size_t PM = (size_t)c->P * c->M;
   w.ds_tab = cv.take<uint32_t>((size_t)B * PM * c->branch_len);
@@ -175,7 +183,7 @@ static PropWs carve_propose(uint8_t* base, const sssd_cfg* c, int B, int max_len
   w.in_cols.meta = cv.take<uint32_t>((size_t)B * w.cap);
   w.in_cols.orig = cv.take<uint32_t>((size_t)B * w.cap);
   w.in_cols.tok = cv.take<uint32_t>((size_t)B * w.cap * c->input_branch_len);
-  w.d = carve_draft(cv, c->P, c->dec_len, B, w.cap);
+  w.d = carve_draft(cv, status, c->P, c->dec_len, B, w.cap);
   w.bytes = align_up(cv.off, 256);
   return w;
 }
@@ -194,6 +202,8 @@ __global__ void propose_setup_kernel(sssd_seqs seqs, KCfg c, Cols dsc, const int
   d[0].stride = dsc.stride;
   d[0].n = c.use_ds ? ds_n[b] : 0;
   d[0].thr = 0;
+  d[0].depth = c.BL;
+  d[0].pad = 0;
   for (int rk = 1; rk <= c.P; ++rk) {
     const int p = c.P - rk + 1;
     d[rk].meta = inc.meta + (size_t)b * inc.stride;
@@ -202,6 +212,8 @@ __global__ void propose_setup_kernel(sssd_seqs seqs, KCfg c, Cols dsc, const int
     d[rk].stride = inc.stride;
     d[rk].n = (c.use_in && p <= c.n_trees) ? in_n[b] : 0;
     d[rk].thr = p;
+    d[rk].depth = c.IBL;
+    d[rk].pad = 0;
   }
   if (bucket) {
     const int k = lpt_bucket(d, c.P);
@@ -228,6 +240,8 @@ __global__ void merge_setup_kernel(Cols cols, const int64_t* el_off, const int32
     d[rk].stride = cols.stride;
     d[rk].n = live ? el_n[bs] : 0;
     d[rk].thr = 0;
+    d[rk].depth = (int32_t)(c.disc_stride - 1);
+    d[rk].pad = 0;
   }
 }
 
@@ -429,25 +443,16 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
 }
 
 // Returns the device status word of the last propose / merge that used this
-// workspace (synchronising on `stream`): 0 or SSSD_E_WORKSPACE.
+// workspace (synchronising on `stream`): 0 or SSSD_E_WORKSPACE.  The word sits
+// at a fixed offset (status block first), so cfg / B / max_len / is_merge /
+// total_elems are accepted for ABI stability but no longer needed.
 int sssd_workspace_status(const sssd_cfg* cfg, int32_t B, int32_t max_len, const void* workspace,
                           int32_t is_merge, int64_t total_elems, void* stream) {
-  size_t off;
-  if (is_merge) {
-    Carver cv{nullptr, 0};
-    const size_t te = (size_t)(total_elems > 0 ? total_elems : 1);
-    cv.take<sssd_elem>(te);
-    cv.take<uint32_t>(2 * te);
-    cv.take<uint32_t>(te * (2 + merge_depth(cfg)));
-    DraftWs d = carve_draft(cv, cfg->P, cfg->dec_len, B);
-    off = reinterpret_cast<size_t>(d.err);
-  } else {
-    PropWs w = carve_propose(nullptr, cfg, B, max_len);
-    off = reinterpret_cast<size_t>(w.d.err);
-  }
+  (void)cfg, (void)B, (void)max_len, (void)is_merge, (void)total_elems;
+  if (!workspace) return fail(SSSD_E_ARG, "null workspace");
   int32_t v = 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int rc = cuda_check(cudaMemcpyAsync(&v, static_cast<const uint8_t*>(workspace) + off, 4,
+  int rc = cuda_check(cudaMemcpyAsync(&v, static_cast<const uint8_t*>(workspace) + kStatusErrOffset, 4,
                                       cudaMemcpyDeviceToHost, st), "status copy");
   if (rc) return rc;
   if ((rc = cuda_check(cudaStreamSynchronize(st), "status sync"))) return rc;
@@ -458,11 +463,12 @@ int sssd_workspace_status(const sssd_cfg* cfg, int32_t B, int32_t max_len, const
 size_t sssd_merge_workspace(const sssd_cfg* cfg, int32_t B, int64_t total_elems) {
   if (!cfg || B < 0) return 0;
   Carver cv{nullptr, 0};
+  unsigned long long* status = carve_status(cv);
   const size_t te = (size_t)(total_elems > 0 ? total_elems : 1);
   cv.take<sssd_elem>(te);
   cv.take<uint32_t>(2 * te);
   cv.take<uint32_t>(te * (2 + merge_depth(cfg)));
-  carve_draft(cv, cfg->P, cfg->dec_len, B);
+  carve_draft(cv, status, cfg->P, cfg->dec_len, B);
   return align_up(cv.off, 256);
 }
 
@@ -476,12 +482,13 @@ int sssd_merge(const uint32_t* tok, const sssd_elem* el, const int64_t* el_off,
   if (B < 0) return fail(SSSD_E_ARG, "bad batch size %d", B);
   if (B == 0) return SSSD_OK;
   Carver cv{static_cast<uint8_t*>(workspace), 0};
+  unsigned long long* status = carve_status(cv);
   const size_t te = (size_t)(total_elems > 0 ? total_elems : 1);
   sssd_elem* sorted = cv.take<sssd_elem>(te);
   uint32_t* idx = cv.take<uint32_t>(2 * te);
   uint32_t* colbuf = cv.take<uint32_t>(te * (2 + merge_depth(cfg)));
   Cols cols{colbuf, colbuf + te, colbuf + 2 * te, (int64_t)te};
-  DraftWs d = carve_draft(cv, cfg->P, cfg->dec_len, B);
+  DraftWs d = carve_draft(cv, status, cfg->P, cfg->dec_len, B);
   const size_t need = align_up(cv.off, 256);
   if (!workspace || workspace_bytes < need)
     return fail(SSSD_E_WORKSPACE, "merge needs %zu workspace bytes, got %zu", need, workspace_bytes);

@@ -63,6 +63,8 @@ struct SrcDesc {
   int64_t stride;
   int32_t n;
   int32_t thr;
+  int32_t depth;  // token columns (no element is longer): nodes at this depth have no children
+  int32_t pad;
 };
 
 }  // namespace sssd

@@ -83,12 +83,16 @@ struct Arena {
   unsigned long long* cursor;
   uint64_t pool_cap;
   int32_t* err;
+  uint32_t spill = 0;    // probe: allocations served outside shared memory
+  uint32_t scanned = 0;  // probe: elements scanned by expansions
   __device__ Child* alloc(uint32_t n) {  // warp-uniform
+    scanned += n;
     if (sused + n <= scap) {
       Child* p = sslab + sused;
       sused += n;
       return p;
     }
+    ++spill;
     if (used + n <= cap) {
       Child* p = slab + used;
       used += n;
@@ -309,7 +313,11 @@ __device__ void expand(const SrcDesc& sd, uint32_t rank, uint32_t D, uint32_t a,
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(32, 32)
+#ifndef SSSD_DRAFT_MINB
+#define SSSD_DRAFT_MINB 24  // resident requests per SM the register budget is sized for (24: best measured)
+#endif
+
+__global__ void __launch_bounds__(32, SSSD_DRAFT_MINB)
     draft_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, Child* slabs,
                  uint32_t slab_cap, Child* pool, unsigned long long* cursor, uint64_t pool_cap,
                  int32_t* err, uint8_t* gover, int64_t gover_bytes, sssd_draft_out out,
@@ -368,7 +376,11 @@ __global__ void __launch_bounds__(32, 32)
     }
   }
 
+  const long long t_seeded = clock64();
+  uint32_t pops = 0, max_live = fr.A;
   while (size < S) {
+    ++pops;
+    max_live = max(max_live, (uint32_t)fr.A);
     // pop: minimum over group heads of (~prio, depth|rank|sequence); exhausted
     // groups carry meta = kExhausted and lose every comparison
     uint32_t bh = 0xffffffffu, bl = 0xffffffffu, bm = kExhausted;
@@ -475,11 +487,13 @@ __global__ void __launch_bounds__(32, 32)
     }
     __syncwarp();
     // push the popped source node's children (ref fusion.py:258-259)
-    if (D + 1 < (uint32_t)c.disc_stride)
+    // (a node at its source's column depth has no children: skip the scan)
+    if (D + 1 < (uint32_t)c.disc_stride && (int)D < sds[rk].depth)
       expand(sds[rk], rk, D + 1, h.a, h.b, false, h.pp, h.count, (uint32_t)nid,
              c.disc[rk * c.disc_stride + D + 1], fr, ar);
   }
 
+  const long long t_popped = clock64();
   // DFS pre-order flatten, children in insertion order (ref draft.py:67-86),
   // level-parallel: subtree sizes bottom-up, then pre-order positions top-down
   // (a child's subtree ends where its next sibling's starts); each lane
@@ -541,7 +555,18 @@ __global__ void __launch_bounds__(32, 32)
   }
   if (lane == 0) {
     out.size[b] = size;
-    if (cycles) cycles[b] = clock64() - t_start;  // per-request profile (optional)
+    if (cycles) {  // per-request profile (optional): see sssd_set_cycle_probe
+      long long* st = cycles + (size_t)b * 8;
+      const long long t_end = clock64();
+      st[0] = t_end - t_start;
+      st[1] = t_seeded - t_start;
+      st[2] = t_popped - t_seeded;
+      st[3] = t_end - t_popped;
+      st[4] = pops;
+      st[5] = ar.scanned;
+      st[6] = max_live;
+      st[7] = ar.spill;
+    }
   }
 }
 

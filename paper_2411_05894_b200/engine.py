@@ -98,19 +98,24 @@ class DraftEngine:
         return out
 
     def propose(self, seq: torch.Tensor, seq_off: torch.Tensor, seq_len: torch.Tensor, max_len: int,
-                lookup: bool = False, out: DraftBatch | None = None) -> DraftBatch:
+                lookup: bool = False, out: DraftBatch | None = None, ws: torch.Tensor | None = None,
+                stream: torch.cuda.Stream | None = None) -> DraftBatch:
         """Draft for B device-resident sequences: seq (int32 view of u32),
-        seq_off [B] int64, seq_len [B] int32 (each >= 1)."""
+        seq_off [B] int64, seq_len [B] int32 (each >= 1).  Runs on ``stream``
+        (default: the current stream) with workspace ``ws`` (default: the
+        engine's own; concurrent calls on different streams need their own)."""
         B = int(seq_len.shape[0])
         out = out or self.outputs(B, lookup)
         if B == 0:
             return out
-        ws = self.workspace(B, max_len)
+        if ws is None:
+            ws = self.workspace(B, max_len)
         seqs = _lib.Seqs(ptr(seq), ptr(seq_off), ptr(seq_len), B, int(max_len))
         d_out = _lib.DraftOut(ptr(out.size), ptr(out.tokens), ptr(out.parents), ptr(out.depths), ptr(out.mask))
         lk = _lib.LookupOut(ptr(out.ranges), ptr(out.samples), ptr(out.n_conts), ptr(out.p_cut)) if lookup else None
         ds = self.store.c_view() if (self.use_datastore and self.store is not None) else self._null_ds
-        check(lib().sssd_propose(ds, seqs, self.c, d_out, lk, ptr(ws), ws.numel(), stream_ptr(self.device)))
+        sp = stream.cuda_stream if stream is not None else stream_ptr(self.device)
+        check(lib().sssd_propose(ds, seqs, self.c, d_out, lk, ptr(ws), ws.numel(), sp))
         return out
 
     def propose_profile(self, seq, seq_off, seq_len, max_len) -> list[float]:
@@ -126,6 +131,94 @@ class DraftEngine:
         ms = (C.c_float * 4)()
         check(lib().sssd_propose_profile(ds, seqs, self.c, d_out, ptr(ws), ws.numel(), stream_ptr(self.device), ms))
         return list(ms)
+
+    def propose_pinned(self, seq_h: torch.Tensor, off_h: torch.Tensor, len_h: torch.Tensor, max_len: int,
+                       out_h: DraftBatch | None = None, chunks: int = 8) -> DraftBatch:
+        """Host-buffer entry point for a large batch: contexts in pinned host
+        memory (seq_h int32, off_h int64 [B], len_h int32 [B], CPU tensors),
+        drafts returned in pinned host tensors (``out_h``, allocated if None —
+        pass it back in to reuse the pinned buffers).
+
+        The batch is cut into ``chunks`` request ranges.  Uploads run on an H2D
+        copy stream, drafting alternates between two compute streams with one
+        workspace each (so the fusion-kernel tail of range c overlaps the lookup
+        and drafting of range c+1), downloads run on a D2H copy stream: PCIe
+        both ways and the kernels all run concurrently.  Blocks until the drafts
+        are on the host; raises if any range overflowed the fusion arena."""
+        B = int(len_h.shape[0])
+        dev = self.device
+        S, W = self.S, self.W
+        if out_h is None:
+            out_h = DraftBatch(
+                size=torch.empty(B, dtype=torch.int32).pin_memory(),
+                tokens=torch.empty((B, S), dtype=torch.int32).pin_memory(),
+                parents=torch.empty((B, S), dtype=torch.int32).pin_memory(),
+                depths=torch.empty((B, S), dtype=torch.int32).pin_memory(),
+                mask=torch.empty((B, S, W), dtype=torch.int64).pin_memory())
+        if B == 0:
+            return out_h
+        offs, lens = off_h.numpy(), len_h.numpy()
+        if (lens < 1).any():
+            raise ValueError("empty prompt: the draft root is the last context token")
+        chunks = max(1, min(int(chunks), B))
+        cuts = [B * c // chunks for c in range(chunks + 1)]
+        bc = max(cuts[c + 1] - cuts[c] for c in range(chunks))
+        n_tok = int(seq_h.shape[0])
+        st = getattr(self, "_pin", None)
+        if st is None:
+            st = self._pin = {"streams": [torch.cuda.Stream(dev) for _ in range(4)], "key": None, "ws_key": None}
+        if st["key"] != (n_tok, B):
+            st["seq"] = torch.empty(n_tok, dtype=torch.int32, device=dev)
+            st["off"] = torch.empty(B, dtype=torch.int64, device=dev)
+            st["len"] = torch.empty(B, dtype=torch.int32, device=dev)
+            st["key"] = (n_tok, B)
+        if st["ws_key"] is None or st["ws_key"][0] < bc or st["ws_key"][1] < max_len:
+            nbytes = lib().sssd_propose_workspace(self.c, bc, int(max_len))
+            st["ws"] = [torch.empty(nbytes, dtype=torch.uint8, device=dev) for _ in range(2)]
+            st["ws_key"] = (bc, int(max_len))
+        if st.get("status") is None or st["status"].numel() < chunks:
+            st["status"] = torch.zeros(chunks, dtype=torch.int32, device=dev)
+        up, down, c0, c1 = st["streams"]
+        comp = (c0, c1)
+        seq_d, off_d, len_d, status = st["seq"], st["off"], st["len"], st["status"]
+        err = [w[_lib.SSSD_STATUS_OFFSET:_lib.SSSD_STATUS_OFFSET + 4].view(torch.int32) for w in st["ws"]]
+        main = torch.cuda.current_stream(dev)
+        out = self.outputs(B)
+        for s_ in st["streams"]:
+            s_.wait_stream(main)
+        with torch.cuda.stream(up):
+            off_d.copy_(off_h, non_blocking=True)
+            len_d.copy_(len_h, non_blocking=True)
+            uploaded = []
+            for c in range(chunks):  # every upload enqueued up front: the copy engine runs ahead
+                r0, r1 = cuts[c], cuts[c + 1]
+                t0 = int(offs[r0:r1].min())
+                t1 = int((offs[r0:r1] + lens[r0:r1]).max())
+                seq_d[t0:t1].copy_(seq_h[t0:t1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(up)
+                uploaded.append(ev)
+        for c in range(chunks):
+            r0, r1 = cuts[c], cuts[c + 1]
+            cs = comp[c & 1]
+            cs.wait_event(uploaded[c])
+            view = DraftBatch(out.size[r0:r1], out.tokens[r0:r1], out.parents[r0:r1], out.depths[r0:r1],
+                              out.mask[r0:r1])
+            with torch.cuda.stream(cs):
+                self.propose(seq_d, off_d[r0:r1], len_d[r0:r1], max_len, out=view, ws=st["ws"][c & 1], stream=cs)
+                status[c:c + 1].copy_(err[c & 1])
+                ev = torch.cuda.Event()
+                ev.record(cs)
+            down.wait_event(ev)
+            with torch.cuda.stream(down):
+                for dst, src in ((out_h.size, out.size), (out_h.tokens, out.tokens), (out_h.parents, out.parents),
+                                 (out_h.depths, out.depths), (out_h.mask, out.mask)):
+                    dst[r0:r1].copy_(src[r0:r1], non_blocking=True)
+        for s_ in (c0, c1, down):
+            main.wait_stream(s_)
+        if int(status[:chunks].max().item()) != 0:  # synchronises the current stream
+            raise _lib.SSSDError("device workspace overflow (fusion arena) in propose_pinned")
+        return out_h
 
     def check_status(self) -> None:
         """Synchronise and raise if the device fusion arena overflowed."""

@@ -227,3 +227,42 @@ def test_save_load_roundtrip(tmp_path):
     assert np.array_equal(back.suffix_index, ds.suffix_index)
     assert back.vocab_size == 1000
     assert back.find_range([int(corpus[5]), int(corpus[6])]) == ds.find_range([int(corpus[5]), int(corpus[6])])
+
+
+def test_propose_pinned_equals_resident_propose():
+    """The pipelined host-buffer entry point (chunked H2D / draft / D2H on three
+    streams) returns exactly the drafts of one device-resident propose, for
+    ragged lengths and offsets in shuffled order; the engine's workspace status
+    stays readable after calls of different batch sizes."""
+    rng = np.random.default_rng(21)
+    corpus = workload.corpus(300_000, 500)
+    ds = G.build(corpus, vocab_size=500)
+    eng = G.DraftEngine(ds, G.FusionConfig(dec_len=48))
+    B = 37
+    ctxs = [rng.integers(0, 500, int(rng.integers(1, 900))).astype(np.uint32) for _ in range(B)]
+    order = rng.permutation(B)  # request r stored at a shuffled position in the flat buffer
+    flat, offs, pos = [], np.zeros(B, np.int64), 0
+    for r in order:
+        offs[r] = pos
+        flat.append(ctxs[r])
+        pos += len(ctxs[r])
+    seq_h = torch.from_numpy(np.concatenate(flat).view(np.int32)).pin_memory()
+    off_h = torch.from_numpy(offs)
+    len_h = torch.tensor([len(c) for c in ctxs], dtype=torch.int32)
+    mx = int(len_h.max())
+    want = eng.propose(seq_h.cuda(), off_h.cuda(), len_h.cuda(), mx)
+    want = {k: getattr(want, k).cpu().clone() for k in ("size", "tokens", "parents", "depths", "mask")}
+    eng.check_status()
+    for chunks in (1, 3, 8):
+        got = eng.propose_pinned(seq_h, off_h, len_h, mx, chunks=chunks)
+        for k, v in want.items():
+            g = getattr(got, k)
+            assert not g.is_cuda and g.is_pinned()
+            if k == "size":
+                assert torch.equal(g, v), (chunks, k)
+            else:  # entries past size are unspecified
+                for b in range(B):
+                    n = int(want["size"][b])
+                    assert torch.equal(g[b, :n], v[b, :n]), (chunks, k, b)
+    eng.propose_host([c.tolist() for c in ctxs[:3]])  # smaller call through a larger workspace
+    eng.check_status()

@@ -27,6 +27,18 @@ def test_library_exports_every_declared_symbol():
     assert set(declared) == set(_lib.EXPORTED)
 
 
+def test_header_constants_match_python():
+    """Every #define SSSD_* integer constant the Python side mirrors equals the header's."""
+    from paper_2411_05894_b200 import _lib
+
+    text = open(os.path.join(ROOT, "include", "sssd.h")).read()
+    defs = {k: int(v) for k, v in re.findall(r"#define\s+(SSSD_[A-Z0-9_]+)\s+\(?(-?\d+)\)?", text)}
+    mirrored = [k for k in defs if hasattr(_lib, k)]
+    assert {"SSSD_MAX_DRAFT", "SSSD_ROW_TOKENS", "SSSD_STATUS_OFFSET"} <= set(mirrored)
+    for k in mirrored:
+        assert getattr(_lib, k) == defs[k], k
+
+
 def test_library_is_sm100a():
     import subprocess
 

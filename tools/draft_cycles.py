@@ -12,13 +12,25 @@ seq = torch.from_numpy(ctx.view(np.int32)).cuda()
 off = (torch.arange(B, dtype=torch.int64) * 2048).cuda()
 ln = torch.full((B,), 2048, dtype=torch.int32, device="cuda")
 eng = G.DraftEngine(ds, G.FusionConfig(dec_len=64))
-cyc = torch.zeros(B, dtype=torch.int64, device="cuda")
+cyc = torch.zeros(B, 8, dtype=torch.int64, device="cuda")
 eng.propose(seq, off, ln, 2048)
 _lib.lib().sssd_set_cycle_probe(cyc.data_ptr())
 eng.propose(seq, off, ln, 2048)
 torch.cuda.synchronize()
 _lib.lib().sssd_set_cycle_probe(None)
-c = cyc.cpu().numpy() / 1.965e3  # us at 1965 MHz
+st = cyc.cpu().numpy()
+c = st[:, 0] / 1.965e3  # us at 1965 MHz
+names = ["total_us", "seed_us", "loop_us", "flatten_us", "pops", "scanned", "max_live", "spill"]
+conv = [1.965e3] * 4 + [1] * 4
+for k, (nm, cv) in enumerate(zip(names, conv)):
+    x = st[:, k] / cv
+    print("%-10s mean %9.1f p50 %9.1f p99 %9.1f max %9.1f corr(total) %.3f" % (
+        nm, x.mean(), *np.percentile(x, [50, 99]), x.max(), np.corrcoef(x, c)[0, 1]))
+slow = np.argsort(-c)[:12]
+print("slowest requests (total_us seed_us loop_us flat_us pops scanned max_live spill):")
+for i in slow:
+    print(" ", [round(float(st[i, k] / conv[k]), 1) for k in range(8)])
+print("per-pop loop us: mean %.2f" % (st[:, 2] / 1.965e3 / np.maximum(st[:, 4], 1)).mean())
 print("per-request us: mean %.1f p50 %.1f p90 %.1f p99 %.1f max %.1f" % (c.mean(), *np.percentile(c, [50, 90, 99]), c.max()))
 for n in (4736, 9472, 16384):
     ms = eng.propose_profile(seq, off[:n], ln[:n], 2048)
