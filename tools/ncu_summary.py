@@ -52,7 +52,7 @@ for r in data:
     rec["stalls"] = {k: round(100 * x / tot, 1) for k, x in sorted(st, key=lambda t: -t[1])[:5]}
     out.append(rec)
 
-rows = list(csv.reader(open(launches)))
+rows = list(csv.reader(open(launches))) if launches != "-" else [["Kernel Name", "Metric Value"]]
 hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 h = rows[hi]
 ki, vi = h.index("Kernel Name"), h.index("Metric Value")
@@ -65,7 +65,7 @@ for r in rows[hi + 1:]:
         v *= {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}.get(unit, 1e-6)
         per[r[ki].split("(")[0]].append(v)
 
-md = ["| kernel | launches | mean ms (ncu, cold, serialised) | max ms |", "|---|---|---|---|"]
+md = ["| kernel | launches | mean ms (ncu, cold, serialised) | max ms |", "|---|---|---|---|"] if per else []
 for k, v in per.items():
     md.append(f"| {k} | {len(v)} | {sum(v)/len(v):.4f} | {max(v):.4f} |")
 md.append("")
