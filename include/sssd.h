@@ -87,6 +87,9 @@ typedef struct sssd_cfg {
   int32_t disc_stride;      /* = max depth + 1                                   */
   const double* disc;       /* device [(P+1)][disc_stride]: rank 0 = datastore,
                                rank r = input p=P-r+1 (fusion.py:141-155)        */
+  int32_t fusion;           /* 0 = level-synchronous fusion (needs every disc row
+                               non-increasing in depth, which FusionConfig's
+                               ranges guarantee); 1 = heap-order fusion         */
 } sssd_cfg;
 
 /* Per-element record of a source's sorted element array:

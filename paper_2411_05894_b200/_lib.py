@@ -35,7 +35,7 @@ class Cfg(C.Structure):
         ("input_branch_len", C.c_int32), ("M", C.c_int32), ("T", C.c_int32),
         ("use_datastore", C.c_int32), ("use_input", C.c_int32), ("n_input_trees", C.c_int32),
         ("has_separator", C.c_int32), ("separator", C.c_uint32), ("disc_stride", C.c_int32),
-        ("disc", vp),
+        ("disc", vp), ("fusion", C.c_int32),
     ]
 
 

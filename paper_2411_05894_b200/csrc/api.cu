@@ -65,6 +65,7 @@ static int validate_cfg(const sssd_cfg* c) {
   const int md = c->branch_len > c->input_branch_len ? c->branch_len : c->input_branch_len;
   if (c->disc_stride < md + 1) return fail(SSSD_E_ARG, "disc_stride %d < max depth + 1", c->disc_stride);
   if (!c->disc) return fail(SSSD_E_ARG, "discount table is NULL");
+  if (c->fusion != 0 && c->fusion != 1) return fail(SSSD_E_ARG, "fusion must be 0 or 1, got %d", c->fusion);
   return SSSD_OK;
 }
 
@@ -87,6 +88,7 @@ static KCfg kcfg(const sssd_cfg* c) {
   k.sep = c->separator;
   k.disc_stride = c->disc_stride;
   k.disc = c->disc;
+  k.fusion = c->fusion;
   return k;
 }
 
@@ -245,14 +247,37 @@ __global__ void merge_setup_kernel(Cols cols, const int64_t* el_off, const int32
   }
 }
 
+static int fusion_smem_attr(const KCfg& k) {
+  if (k.fusion == 1)
+    return cuda_check(cudaFuncSetAttribute(draft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           draft_smem_bytes(k.P, k.S)), "draft_kernel smem attribute");
+  return cuda_check(cudaFuncSetAttribute(draft_ls_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         ls_smem_bytes(k.P, k.S)), "draft_ls_kernel smem attribute");
+}
+
+// One fusion + flatten launch over requests [k.b0, k.b0 + nb) (or order[] of them).
+static void launch_fusion(const DraftWs& d, const KCfg& k, int nb, const sssd_draft_out* out,
+                          cudaStream_t st, long long* cyc, const int32_t* order) {
+  if (k.fusion == 1)
+    draft_kernel<<<nb, 32, draft_smem_bytes(k.P, k.S), st>>>(d.desc, d.root, k, d.slabs, kSlabChildren, d.pool,
+                                                             d.cursor, d.pool_cap, d.err, d.gover, d.gover_bytes,
+                                                             *out, cyc, order);
+  else
+  {
+    // the level-synchronous kernel uses the heap form's slabs + pool as one pool
+    uint8_t* lo = reinterpret_cast<uint8_t*>(d.slabs);
+    uint8_t* hi = reinterpret_cast<uint8_t*>(d.pool) + d.pool_cap * kChildBytes;
+    draft_ls_kernel<<<nb, 32, ls_smem_bytes(k.P, k.S), st>>>(d.desc, d.root, k, lo, d.cursor, (uint64_t)(hi - lo),
+                                                             d.err, *out, cyc, order);
+  }
+}
+
 static int launch_draft(const DraftWs& d, const KCfg& k, int B, const sssd_draft_out* out,
                         cudaStream_t st) {
-  const int smem = draft_smem_bytes(k.P, k.S);
-  cudaError_t e = cudaFuncSetAttribute(draft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return cuda_check(e, "draft_kernel smem attribute");
-  draft_kernel<<<B, 32, smem, st>>>(d.desc, d.root, k, d.slabs, kSlabChildren, d.pool, d.cursor,
-                                    d.pool_cap, d.err, d.gover, d.gover_bytes, *out, nullptr, nullptr);
-  return cuda_check(cudaGetLastError(), "draft_kernel launch");
+  int rc = fusion_smem_attr(k);
+  if (rc) return rc;
+  launch_fusion(d, k, B, out, st, nullptr, nullptr);
+  return cuda_check(cudaGetLastError(), "fusion kernel launch");
 }
 
 static int validate_out(const sssd_draft_out* out) {
@@ -362,10 +387,7 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
   sssd_lookup_out lk{};
   if (lookup) lk = *lookup;
   if ((rc = cuda_check(cudaMemsetAsync(w.d.cursor, 0, 16 + 512, st), "memset status"))) return rc;
-  const int smem = draft_smem_bytes(k.P, k.S);
-  if ((rc = cuda_check(cudaFuncSetAttribute(draft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                       "draft_kernel smem attribute")))
-    return rc;
+  if ((rc = fusion_smem_attr(k))) return rc;
 
   auto launch_lookup = [&](cudaStream_t s, int b0, int b1) {
     KCfg kk = k;
@@ -391,9 +413,7 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
                                                                  w.in_n, w.d.desc, w.d.root,
                                                                  lpt ? w.d.bucket : nullptr, w.d.hist);
     if (lpt) lpt_scatter_kernel<<<(B + 255) / 256, 256, 0, s>>>(w.d.bucket, w.d.hist, w.d.hist + 64, B, w.d.order);
-    draft_kernel<<<b1 - b0, 32, smem, s>>>(w.d.desc, w.d.root, kk, w.d.slabs, kSlabChildren, w.d.pool,
-                                           w.d.cursor, w.d.pool_cap, w.d.err, w.d.gover, w.d.gover_bytes, *out,
-                                           g_cycles, lpt ? w.d.order : nullptr);
+    launch_fusion(w.d, kk, b1 - b0, out, s, g_cycles, lpt ? w.d.order : nullptr);
   };
 
   if (ev) {  // profiling: stages back to back on the caller's stream
@@ -411,9 +431,7 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
                                                             w.d.hist);
     if (lpt) lpt_scatter_kernel<<<(B + 255) / 256, 256, 0, st>>>(w.d.bucket, w.d.hist, w.d.hist + 64, B, w.d.order);
     cudaEventRecord(ev[3], st);
-    draft_kernel<<<B, 32, smem, st>>>(w.d.desc, w.d.root, kk, w.d.slabs, kSlabChildren, w.d.pool, w.d.cursor,
-                                      w.d.pool_cap, w.d.err, w.d.gover, w.d.gover_bytes, *out, g_cycles,
-                                      lpt ? w.d.order : nullptr);
+    launch_fusion(w.d, kk, B, out, st, g_cycles, lpt ? w.d.order : nullptr);
     cudaEventRecord(ev[4], st);
     return cuda_check(cudaGetLastError(), "propose launch");
   }

@@ -1,0 +1,654 @@
+// K5, level-synchronous form: fusion + DFS flatten for SSSD drafts (sm_100a).
+// Replaces ref fusion.py:209-261 (merge) and draft.py:67-86 (flatten) with the
+// same output bit for bit; tests/ls_model.py states the algorithm over the
+// oracle's tries and DESIGN.md 3.1 the equivalence argument:
+//
+//  * a source node's key (-priority, depth, rank, ticket) exceeds its parent's
+//    (count ratios <= 1, discount rows non-increasing in depth), so the
+//    reference heap pops all source-trie nodes in global key order;
+//  * tickets of equal (priority, depth, rank) order by the parent's pop order,
+//    then child order, so inside one (depth, rank) class the order is
+//    (-priority, parent's class position, child first-appearance) -- one sort
+//    per level gives each node its class position tb and its global key
+//    G = (~bits(priority), depth, rank, tb);
+//  * the draft is the first dec_len-1 distinct token paths in G order and a
+//    path's parent path precedes it, so only nodes with G <= the current
+//    (dec_len-1)-th best distinct-path key are ever expanded.
+//
+// One warp per request, one trie level per iteration: the children of every
+// expanded node of the level are generated together (element ranges of the
+// sorted source arrays, flattened over the lanes), sorted, given class
+// positions and path ids, and merged into the running top list.  The heap
+// form (fusion.cu) needs ~78 dependent pops per cfg2 request; this form needs
+// <= branch_len levels of lane-parallel work, all in shared memory unless a
+// level outgrows kLsCap nodes (then the request's global pool slice).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "propose.cuh"
+
+namespace sssd {
+
+// One level's nodes, structure of arrays.  k0/k1/ord/tbr/pid are indexed by
+// sorted position, pp/a/z/cnt/tok/ppid by generation index (ord maps).
+struct LsLevel {
+  uint64_t* k0;  // ~bits(priority)
+  uint64_t* k1;  // rank<<56 | parent tb<<32 | first; path key ppid<<32 | tok after the class pass
+  double* pp;    // path probability (ref fusion.py:244,259)
+  uint32_t *a, *z, *cnt, *tok, *ppid, *ord;
+  uint32_t* tbr;  // rank << 22 | class position tb
+  uint32_t* pid;  // path id (0 = the root path)
+};
+static_assert(kLsLevelBytes == 3 * 8 + 8 * 4, "level record");
+
+__device__ __forceinline__ LsLevel level_carve(uint8_t* p, uint32_t cap) {
+  LsLevel l;
+  l.k0 = reinterpret_cast<uint64_t*>(p);
+  l.k1 = l.k0 + cap;
+  l.pp = reinterpret_cast<double*>(l.k1 + cap);
+  uint32_t* u = reinterpret_cast<uint32_t*>(l.pp + cap);
+  l.a = u;
+  l.z = u + cap;
+  l.cnt = u + 2 * cap;
+  l.tok = u + 3 * cap;
+  l.ppid = u + 4 * cap;
+  l.ord = u + 5 * cap;
+  l.tbr = u + 6 * cap;
+  l.pid = u + 7 * cap;
+  return l;
+}
+
+// The expanded prefix of the previous level (the parents of this level).
+struct LsPar {
+  double* pp;
+  uint32_t *a, *z, *cnt, *tbr, *pid, *off;  // off = exclusive scan of the range sizes
+};
+static_assert(kLsParBytes == 8 + 6 * 4, "parent record");
+
+__device__ __forceinline__ LsPar par_carve(uint8_t* p, uint32_t cap) {
+  LsPar q;
+  q.pp = reinterpret_cast<double*>(p);
+  uint32_t* u = reinterpret_cast<uint32_t*>(q.pp + cap);
+  q.a = u;
+  q.z = u + cap;
+  q.cnt = u + 2 * cap;
+  q.tbr = u + 3 * cap;
+  q.pid = u + 4 * cap;
+  q.off = u + 5 * cap;
+  return q;
+}
+
+// Running top list: the best (dec_len-1) distinct paths in G order.
+struct LsTop {
+  uint64_t* g0;
+  uint32_t *g1, *pid, *tok, *ppid;  // g1 = depth << 26 | rank << 22 | tb
+};
+
+__device__ __forceinline__ LsTop top_carve(uint8_t* p, int S) {
+  LsTop t;
+  t.g0 = reinterpret_cast<uint64_t*>(p);
+  t.g1 = reinterpret_cast<uint32_t*>(t.g0 + S);
+  t.pid = t.g1 + S;
+  t.tok = t.pid + S;
+  t.ppid = t.tok + S;
+  return t;
+}
+
+__device__ __forceinline__ bool g_less(uint64_t a0, uint32_t a1, uint64_t b0, uint32_t b1) {
+  return a0 < b0 || (a0 == b0 && a1 < b1);
+}
+__device__ __forceinline__ bool k_less(uint64_t a0, uint64_t a1, uint64_t b0, uint64_t b1) {
+  return a0 < b0 || (a0 == b0 && a1 < b1);
+}
+
+constexpr uint32_t kTbBits = 22;
+constexpr uint32_t kTbMask = (1u << kTbBits) - 1;
+
+__host__ __device__ inline int top_bytes(int S) { return (S * 24 + 15) / 16 * 16; }
+
+int ls_smem_bytes(int P, int S) {
+  return kLsLevelBytes * kLsCap + kLsParBytes * kLsParCap + (P + 1) * (int)sizeof(SrcDesc) +
+         2 * top_bytes(S) + S * 4 + 16 * 4;
+}
+
+// Bump-allocate `bytes` from the fusion pool (warp-uniform); nullptr + status
+// word on exhaustion.
+__device__ __forceinline__ uint8_t* pool_take(uint8_t* pool, unsigned long long* cursor, uint64_t pool_bytes,
+                                              int32_t* err, unsigned long long bytes) {
+  unsigned long long at = 0;
+  if (lane_id() == 0) at = atomicAdd(cursor, bytes);
+  at = __shfl_sync(SSSD_FULL, at, 0);
+  if (at + bytes > pool_bytes) {
+    if (lane_id() == 0) atomicExch(err, SSSD_E_WORKSPACE);
+    return nullptr;
+  }
+  return pool + at;
+}
+
+// Generate the depth-d children of parents [0, np) (element ranges scanned
+// flat over the lanes; runs of equal token inside one parent's range are
+// one child).  Writes nodes with index < cap, returns the total count.
+__device__ __noinline__ uint32_t ls_generate(const LsPar par, int np, uint32_t E, LsLevel L, uint32_t cap,
+                                             const SrcDesc* sd, const double* disc, int disc_stride, int d) {
+  const int lane = lane_id();
+  const uint32_t lt = lanemask_lt();
+  uint32_t n = 0;
+  const double* drow = disc + d;
+  auto emit = [&](bool pred, int j, uint32_t tk, uint32_t cnt, uint32_t first, uint32_t s, uint32_t e) {
+    const bool live = pred && cnt > 0;
+    const uint32_t bal = __ballot_sync(SSSD_FULL, live);
+    if (live) {
+      const uint32_t pos = n + __popc(bal & lt);
+      if (pos < cap) {
+        const uint32_t tr = par.tbr[j], rk = tr >> kTbBits, pc = par.cnt[j];
+        const double ratio = cnt == pc ? 1.0 : __ddiv_rn((double)cnt, (double)pc);  // c/c == 1.0 exactly
+        const double pp = __dmul_rn(par.pp[j], ratio);                            // ref fusion.py:259
+        const double pr = __dmul_rn(pp, drow[rk * disc_stride]);                  // ref fusion.py:246
+        L.k0[pos] = ~(uint64_t)__double_as_longlong(pr);
+        L.k1[pos] = (uint64_t)rk << 56 | (uint64_t)(tr & kTbMask) << 32 | first;
+        L.pp[pos] = pp;
+        L.a[pos] = s;
+        L.z[pos] = e;
+        L.cnt[pos] = cnt;
+        L.tok[pos] = tk;
+        L.ppid[pos] = par.pid[j];
+        L.ord[pos] = pos;
+      }
+    }
+    n += __popc(bal);
+  };
+  bool c_open = false;
+  int c_j = 0;
+  uint32_t c_tok = 0, c_cnt = 0, c_first = 0, c_start = 0, c_end = 0;
+  for (uint32_t base = 0; base < E; base += 32) {
+    const uint32_t x = base + lane;
+    int j = 0;
+    bool has = false, w = false;
+    uint32_t tk = 0, orig = 0xffffffffu, i = 0;
+    if (x < E) {
+      int lo = 0, hi = np;  // last parent whose offset is <= x
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (par.off[mid] <= x) lo = mid;
+        else hi = mid;
+      }
+      j = lo;
+      const SrcDesc& s = sd[par.tbr[j] >> kTbBits];
+      i = par.a[j] + (x - par.off[j]);
+      const uint32_t lm = s.meta[i];
+      if (el_len(lm) >= (uint32_t)d) {
+        has = true;
+        tk = s.tok[(int64_t)(d - 1) * s.stride + i];
+        if ((int)el_m(lm) >= s.thr) {
+          w = true;
+          orig = s.orig[i];
+        }
+      }
+    }
+    const uint32_t hasm = __ballot_sync(SSSD_FULL, has);
+    if (!hasm && !c_open) continue;
+    const unsigned long long key = has ? ((unsigned long long)j << 32 | tk) : (1ull << 63 | (unsigned)lane);
+    const uint32_t gm = __match_any_sync(SSSD_FULL, key);
+    const uint32_t wm = __ballot_sync(SSSD_FULL, w);
+    const int lo_l = __ffs(gm) - 1, hi_l = 31 - __clz(gm);
+    uint32_t fm = orig;  // run minimum of orig (segmented down-scan; runs are lane intervals)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_down_sync(SSSD_FULL, fm, o);
+      if (lane + o <= hi_l) fm = min(fm, y);
+    }
+    fm = __shfl_sync(SSSD_FULL, fm, lo_l);
+    uint32_t cnt = __popc(gm & wm);
+    const unsigned long long key0 = __shfl_sync(SSSD_FULL, key, 0);
+    if (c_open && !((hasm & 1u) && key0 == ((unsigned long long)c_j << 32 | c_tok))) {
+      emit(lane == 0, c_j, c_tok, c_cnt, c_first, c_start, c_end);  // the carried run ended at the edge
+      c_open = false;
+    }
+    uint32_t start = i - (uint32_t)(lane - lo_l);
+    if (c_open && has && lo_l == 0) {  // continuation of the carried run
+      cnt += c_cnt;
+      fm = min(fm, c_first);
+      start = c_start;
+    }
+    const bool to_next = has && hi_l == 31 && base + 32 < E;
+    emit(has && lane == hi_l && !to_next, j, tk, cnt, fm, start, i + 1);
+    if (__ballot_sync(SSSD_FULL, lane == 31 && to_next)) {
+      c_j = __shfl_sync(SSSD_FULL, j, 31);
+      c_tok = __shfl_sync(SSSD_FULL, tk, 31);
+      c_cnt = __shfl_sync(SSSD_FULL, cnt, 31);
+      c_first = __shfl_sync(SSSD_FULL, fm, 31);
+      c_start = __shfl_sync(SSSD_FULL, start, 31);
+      c_end = __shfl_sync(SSSD_FULL, i, 31) + 1;
+      c_open = true;
+    } else {
+      c_open = false;
+    }
+  }
+  if (c_open) emit(lane == 0, c_j, c_tok, c_cnt, c_first, c_start, c_end);
+  __syncwarp();
+  return n;
+}
+
+// Sort positions [0, n) by (k0, k1), carrying ord (n <= 32: ranks in
+// registers; otherwise a bitonic network over the power-of-two padded range,
+// which the level's capacity covers).
+__device__ __noinline__ void ls_sort(LsLevel L, uint32_t n) {
+  const int lane = lane_id();
+  if (n <= 32) {
+    uint64_t m0 = ~0ull, m1 = ~0ull;
+    if (lane < (int)n) {
+      m0 = L.k0[lane];
+      m1 = L.k1[lane];
+    }
+    uint32_t r = 0;
+    for (uint32_t q = 0; q < n; ++q) {
+      const uint64_t q0 = __shfl_sync(SSSD_FULL, m0, q), q1 = __shfl_sync(SSSD_FULL, m1, q);
+      r += k_less(q0, q1, m0, m1) ? 1u : 0u;
+    }
+    __syncwarp();
+    if (lane < (int)n) {
+      L.k0[r] = m0;
+      L.k1[r] = m1;
+      L.ord[r] = (uint32_t)lane;
+    }
+    __syncwarp();
+    return;
+  }
+  uint32_t N2 = 64;
+  while (N2 < n) N2 <<= 1;
+  for (uint32_t q = n + lane; q < N2; q += 32) {
+    L.k0[q] = ~0ull;
+    L.k1[q] = ~0ull;
+    L.ord[q] = 0xffffffffu;
+  }
+  __syncwarp();
+  for (uint32_t kk = 2; kk <= N2; kk <<= 1) {
+    for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
+      for (uint32_t p = lane; p < N2 / 2; p += 32) {
+        const uint32_t lo = 2 * jj * (p / jj) + (p % jj), hi = lo + jj;
+        const bool asc = (lo & kk) == 0;
+        const uint64_t a0 = L.k0[lo], a1 = L.k1[lo], b0 = L.k0[hi], b1 = L.k1[hi];
+        if (k_less(b0, b1, a0, a1) == asc) {
+          const uint32_t oa = L.ord[lo], ob = L.ord[hi];
+          L.k0[lo] = b0;
+          L.k1[lo] = b1;
+          L.ord[lo] = ob;
+          L.k0[hi] = a0;
+          L.k1[hi] = a1;
+          L.ord[hi] = oa;
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+#ifndef SSSD_LS_MINB
+#define SSSD_LS_MINB 16
+#endif
+
+__global__ void __launch_bounds__(32, SSSD_LS_MINB)
+    draft_ls_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, uint8_t* pool,
+                    unsigned long long* cursor, uint64_t pool_bytes, int32_t* err, sssd_draft_out out,
+                    long long* cycles, const int32_t* order) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const long long t_start = clock64();
+  const int b = order ? order[c.b0 + blockIdx.x] : c.b0 + blockIdx.x;
+  const int lane = lane_id();
+  const uint32_t lt = lanemask_lt();
+  const int S = c.S, K = S - 1;
+  const int NR = c.P + 1;
+
+  uint8_t* sp = smem;
+  const LsLevel Ls = level_carve(sp, kLsCap);
+  sp += kLsLevelBytes * kLsCap;
+  LsPar par = par_carve(sp, kLsParCap);
+  sp += kLsParBytes * kLsParCap;
+  SrcDesc* sd = reinterpret_cast<SrcDesc*>(sp);
+  sp += NR * sizeof(SrcDesc);
+  uint8_t* top_base = sp;
+  sp += 2 * top_bytes(S);
+  uint32_t* nl = reinterpret_cast<uint32_t*>(sp);  // sorted positions of the level's new paths
+  sp += S * 4;
+  uint32_t* rcnt = reinterpret_cast<uint32_t*>(sp);  // per-rank class counters
+
+  for (int r = lane; r < NR; r += 32) sd[r] = desc[(size_t)b * NR + r];
+  __syncwarp();
+
+  // level 0: the source roots are the parents of the seeds (path prob 1.0, so
+  // pp * (count / root_count) is the seed's count / root_count exactly)
+  int np = 0;
+  if (K > 0) {
+    for (int rk = 0; rk < NR; ++rk) {
+      if (sd[rk].n <= 0) continue;
+      uint32_t rc = 0;
+      for (int i = lane; i < sd[rk].n; i += 32) rc += (int)el_m(sd[rk].meta[i]) >= sd[rk].thr ? 1u : 0u;
+      rc = __reduce_add_sync(SSSD_FULL, rc);
+      if (rc == 0) continue;
+      if (lane == 0) {
+        par.a[np] = 0;
+        par.z[np] = (uint32_t)sd[rk].n;
+        par.cnt[np] = rc;
+        par.pp[np] = 1.0;
+        par.tbr[np] = (uint32_t)rk << kTbBits;
+        par.pid[np] = 0;
+      }
+      ++np;
+    }
+  }
+  __syncwarp();
+
+  uint8_t* glev = nullptr;  // global level / parent buffers (pool), grown on demand
+  uint32_t glev_cap = 0;
+  uint8_t* gpar = nullptr;
+  uint32_t gpar_cap = 0;
+  int t = 0, cur = 0;
+  uint32_t next_pid = 1;
+  uint32_t gen_total = 0, max_level = 0, gallocs = 0, levels = 0;
+
+  for (int d = 1; np > 0 && d < c.disc_stride; ++d) {
+    // 1. exclusive scan of the parents' element-range sizes
+    uint32_t E = 0;
+    for (int j0 = 0; j0 < np; j0 += 32) {
+      const int j = j0 + lane;
+      uint32_t e = 0;
+      if (j < np && d <= sd[par.tbr[j] >> kTbBits].depth) e = par.z[j] - par.a[j];
+      uint32_t inc = e;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(SSSD_FULL, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (j < np) par.off[j] = E + inc - e;
+      E += __shfl_sync(SSSD_FULL, inc, 31);
+    }
+    __syncwarp();
+    if (E == 0) break;
+    ++levels;
+
+    // 2. generate into shared memory; a level larger than kLsCap is generated
+    //    again into a global buffer of its exact power-of-two size
+    LsLevel L = Ls;
+    uint32_t n = ls_generate(par, np, E, Ls, kLsCap, sd, c.disc, c.disc_stride, d);
+    if (n == 0) break;
+    if (n > (uint32_t)kLsCap) {
+      uint32_t need = 64;
+      while (need < n) need <<= 1;
+      if (glev_cap < need) {
+        glev = pool_take(pool, cursor, pool_bytes, err, (unsigned long long)need * kLsLevelBytes);
+        if (!glev) break;
+        glev_cap = need;
+        ++gallocs;
+      }
+      L = level_carve(glev, glev_cap);
+      ls_generate(par, np, E, L, glev_cap, sd, c.disc, c.disc_stride, d);
+    }
+    gen_total += n;
+    max_level = max(max_level, n);
+    if (n > kTbMask) {  // class positions must fit their field
+      if (lane == 0) atomicExch(err, SSSD_E_LIMIT);
+      break;
+    }
+
+    // 3. sort the level by (k0, k1) = (~priority, rank, parent tb, first)
+    ls_sort(L, n);
+
+    // 4. class positions, path ids (first occurrence in G order wins), new paths
+    if (lane < 16) rcnt[lane] = 0;
+    __syncwarp();
+    uint32_t nnew = 0;
+    for (uint32_t s0 = 0; s0 < n; s0 += 32) {
+      const uint32_t s = s0 + lane;
+      const bool v = s < n;
+      uint32_t rk = 0, tb = 0;
+      unsigned long long pk = 1ull << 63 | (unsigned)lane;
+      if (v) {
+        rk = (uint32_t)(L.k1[s] >> 56);
+        const uint32_t g = L.ord[s];
+        pk = (unsigned long long)L.ppid[g] << 32 | L.tok[g];
+      }
+      const uint32_t rm = __match_any_sync(SSSD_FULL, v ? rk : 64u + lane);
+      if (v) tb = rcnt[rk] + __popc(rm & lt);
+      const uint32_t pm = __match_any_sync(SSSD_FULL, pk);
+      const int rep = __ffs(pm) - 1;
+      int found = -1;
+      if (v && lane == rep && s0 > 0) {  // an earlier chunk holds the path?
+        for (uint32_t q = 0; q < s0; ++q)
+          if (L.k1[q] == pk) {
+            found = (int)q;
+            break;
+          }
+      }
+      const uint32_t newm = __ballot_sync(SSSD_FULL, v && lane == rep && found < 0);
+      uint32_t id = 0;
+      if (v && lane == rep) id = found >= 0 ? L.pid[found] : next_pid + __popc(newm & lt);
+      id = __shfl_sync(SSSD_FULL, id, rep);
+      if ((newm >> lane) & 1u) {
+        const uint32_t at = nnew + __popc(newm & lt);
+        if (at < (uint32_t)K) nl[at] = s;
+      }
+      next_pid += __popc(newm);
+      nnew += __popc(newm);
+      __syncwarp();
+      if (v) {
+        if (lane == 31 - __clz(rm)) rcnt[rk] += __popc(rm);
+        L.tbr[s] = rk << kTbBits | tb;
+        L.pid[s] = id;
+        L.k1[s] = pk;
+      }
+      __syncwarp();
+    }
+
+    // 5. merge the level's new paths (already in G order) into the top list
+    const uint32_t dd = (uint32_t)d << 26;
+    {
+      const uint32_t u = min(nnew, (uint32_t)K);
+      const LsTop tc = top_carve(top_base + cur * top_bytes(S), S);
+      const LsTop tn = top_carve(top_base + (cur ^ 1) * top_bytes(S), S);
+      for (int i = lane; i < t; i += 32) {
+        const uint64_t x0 = tc.g0[i];
+        const uint32_t x1 = tc.g1[i];
+        uint32_t lo = 0, hi = u;  // new paths with G < x
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1, sm = nl[mid];
+          if (g_less(L.k0[sm], dd | L.tbr[sm], x0, x1)) lo = mid + 1;
+          else hi = mid;
+        }
+        const uint32_t pos = (uint32_t)i + lo;
+        if (pos < (uint32_t)K) {
+          tn.g0[pos] = x0;
+          tn.g1[pos] = x1;
+          tn.pid[pos] = tc.pid[i];
+          tn.tok[pos] = tc.tok[i];
+          tn.ppid[pos] = tc.ppid[i];
+        }
+      }
+      for (uint32_t m = lane; m < u; m += 32) {
+        const uint32_t sm = nl[m];
+        const uint64_t x0 = L.k0[sm];
+        const uint32_t x1 = dd | L.tbr[sm];
+        uint32_t lo = 0, hi = (uint32_t)t;  // top entries with G < x
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (g_less(tc.g0[mid], tc.g1[mid], x0, x1)) lo = mid + 1;
+          else hi = mid;
+        }
+        const uint32_t pos = m + lo;
+        if (pos < (uint32_t)K) {
+          const uint32_t g = L.ord[sm];
+          tn.g0[pos] = x0;
+          tn.g1[pos] = x1;
+          tn.pid[pos] = L.pid[sm];
+          tn.tok[pos] = L.tok[g];
+          tn.ppid[pos] = L.ppid[g];
+        }
+      }
+      t = min(K, t + (int)u);
+      cur ^= 1;
+      __syncwarp();
+    }
+
+    // 6. the parents of the next level: the prefix at or below the threshold
+    uint32_t nexp = n;
+    if (t == K) {
+      const LsTop tc = top_carve(top_base + cur * top_bytes(S), S);
+      const uint64_t tau0 = tc.g0[K - 1];
+      const uint32_t tau1 = tc.g1[K - 1];
+      nexp = 0;
+      for (uint32_t s0 = 0; s0 < n; s0 += 32) {
+        const uint32_t s = s0 + lane;
+        const bool ok = s < n && !g_less(tau0, tau1, L.k0[s], dd | L.tbr[s]);
+        const uint32_t okm = __ballot_sync(SSSD_FULL, ok);
+        nexp += __popc(okm);
+        if (okm != SSSD_FULL) break;
+      }
+    }
+    if (nexp > (uint32_t)kLsParCap) {
+      if (gpar_cap < nexp) {
+        uint32_t need = 2 * kLsParCap;
+        while (need < nexp) need <<= 1;
+        gpar = pool_take(pool, cursor, pool_bytes, err, (unsigned long long)need * kLsParBytes);
+        if (!gpar) break;
+        gpar_cap = need;
+        ++gallocs;
+      }
+      par = par_carve(gpar, gpar_cap);
+    } else {
+      par = par_carve(smem + kLsLevelBytes * kLsCap, kLsParCap);
+    }
+    for (uint32_t j = lane; j < nexp; j += 32) {
+      const uint32_t g = L.ord[j];
+      par.pp[j] = L.pp[g];
+      par.a[j] = L.a[g];
+      par.z[j] = L.z[g];
+      par.cnt[j] = L.cnt[g];
+      par.tbr[j] = L.tbr[j];
+      par.pid[j] = L.pid[j];
+    }
+    __syncwarp();
+    np = (int)nexp;
+  }
+  __syncwarp();
+  const long long t_levels = clock64();
+
+  // 7. flatten: node v = 1..t is top entry v-1 (insertion order = G order;
+  //    a parent path precedes its children, siblings insert in index order)
+  const LsTop T = top_carve(top_base + cur * top_bytes(S), S);
+  int* f_par = reinterpret_cast<int*>(smem);  // the level buffer is free now
+  int* f_fc = f_par + S;                      // first child
+  int* f_ns = f_fc + S;                       // next sibling
+  int* f_pos = f_ns + S;                      // pre-order position
+  int* f_dep = f_pos + S;
+  int* pmap = f_dep + S;  // path id -> node (path ids < next_pid)
+  const int size = t + 1;
+  const bool use_map = (int)next_pid <= (kLsLevelBytes * kLsCap) / 4 - 5 * S;
+  if (use_map)
+    for (int v = 1 + lane; v < size; v += 32) pmap[T.pid[v - 1]] = v;
+  __syncwarp();
+  int maxd = 0;
+  for (int v = lane; v < size; v += 32) {
+    int pr = -1, dv = 0;
+    if (v > 0) {
+      const uint32_t pp = T.ppid[v - 1];
+      pr = 0;
+      if (pp != 0) {
+        if (use_map) {
+          pr = pmap[pp];
+        } else {
+          for (int u = 0; u < v - 1; ++u)
+            if (T.pid[u] == pp) {
+              pr = u + 1;
+              break;
+            }
+        }
+      }
+      dv = (int)(T.g1[v - 1] >> 26);
+    }
+    f_par[v] = pr;
+    f_dep[v] = dv;
+    f_fc[v] = -1;
+    maxd = max(maxd, dv);
+  }
+  __syncwarp();
+  // next sibling = the next index with the same parent: inside a chunk by
+  // match_any, across chunks through a first-index-per-parent table built
+  // from the last chunk backwards (f_pos doubles as that table)
+  for (int v = lane; v < size; v += 32) f_pos[v] = -1;
+  __syncwarp();
+  for (int c0 = ((size - 1) >> 5) << 5; c0 >= 0; c0 -= 32) {
+    const int v = c0 + lane;
+    const bool ok = v >= 1 && v < size;
+    const int p = ok ? f_par[v] : -2 - lane;
+    const uint32_t mm = __match_any_sync(SSSD_FULL, p);
+    const uint32_t above = mm & ~((2u << lane) - 1u);
+    int ns = -1;
+    if (ok) ns = above ? c0 + __ffs(above) - 1 : f_pos[p];
+    __syncwarp();
+    if (ok) {
+      f_ns[v] = ns;
+      if (lane == __ffs(mm) - 1) f_pos[p] = v;  // first index with parent p so far
+    }
+    __syncwarp();
+  }
+  for (int v = lane; v < size; v += 32) f_fc[v] = f_pos[v];
+  __syncwarp();
+  uint32_t* o_tok = out.tokens + (size_t)b * S;
+  int32_t* o_par = out.parents + (size_t)b * S;
+  int32_t* o_dep = out.depths + (size_t)b * S;
+  if (lane == 0) {  // DFS walk: first child, else next sibling of the nearest ancestor that has one
+    int v = 0, k = 0;
+    while (true) {
+      f_pos[v] = k;
+      o_tok[k] = v == 0 ? root_tok[b] : T.tok[v - 1];
+      o_par[k] = v == 0 ? -1 : f_pos[f_par[v]];
+      o_dep[k] = f_dep[v];
+      ++k;
+      int nx = f_fc[v];
+      if (nx < 0) {
+        int u = v;
+        while (u > 0 && f_ns[u] < 0) u = f_par[u];
+        if (u <= 0) break;
+        nx = f_ns[u];
+      }
+      v = nx;
+    }
+  }
+  __syncwarp();
+  const int W = (S + 63) >> 6;
+  uint64_t* o_mask = out.mask + (size_t)b * S * W;
+  for (int v = lane; v < size; v += 32) {  // mask row = ancestors-or-self (ref draft.py:80-84)
+    const int k = f_pos[v];
+    for (int w = 0; w < W; ++w) {
+      uint64_t m = 0;
+      for (int x = v; x >= 0; x = f_par[x]) {
+        const int pk = f_pos[x];
+        if ((pk >> 6) == w) m |= 1ull << (pk & 63);
+      }
+      o_mask[(size_t)k * W + w] = m;
+    }
+  }
+  for (int k = size + lane; k < S; k += 32) {
+    o_tok[k] = 0;
+    o_par[k] = -1;
+    o_dep[k] = -1;
+    for (int w = 0; w < W; ++w) o_mask[(size_t)k * W + w] = 0;
+  }
+  if (lane == 0) {
+    out.size[b] = size;
+    if (cycles) {  // per-request profile (optional): see sssd_set_cycle_probe
+      long long* st = cycles + (size_t)b * 8;
+      const long long t_end = clock64();
+      st[0] = t_end - t_start;
+      st[1] = 0;
+      st[2] = t_levels - t_start;
+      st[3] = t_end - t_levels;
+      st[4] = levels;
+      st[5] = gen_total;
+      st[6] = max_level;
+      st[7] = gallocs;
+    }
+  }
+}
+
+}  // namespace sssd

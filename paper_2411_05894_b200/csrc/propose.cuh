@@ -12,6 +12,7 @@ struct KCfg {
   uint32_t sep;
   int disc_stride;
   const double* disc;
+  int fusion;  // 0 = level-synchronous (fusion_ls.cu), 1 = heap order (fusion.cu)
 };
 
 struct Child;
@@ -51,6 +52,17 @@ __device__ __forceinline__ int lpt_bucket(const SrcDesc* d, int P) {
 }
 __global__ void lpt_scatter_kernel(const uint8_t* bucket, const int32_t* hist, int32_t* fill, int B,
                                    int32_t* order);
+
+// level-synchronous fusion: level-node and parent record bytes, and how many
+// of each a warp keeps in shared memory (larger levels use the fusion pool)
+constexpr int kLsLevelBytes = 56;
+constexpr int kLsParBytes = 32;
+constexpr int kLsCap = 128;
+constexpr int kLsParCap = 64;
+int ls_smem_bytes(int P, int S);
+__global__ void draft_ls_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, uint8_t* pool,
+                                unsigned long long* cursor, uint64_t pool_bytes, int32_t* err,
+                                sssd_draft_out out, long long* cycles, const int32_t* order);
 
 constexpr int kChildBytes = 32;
 constexpr int kGroupBytes = 16;  // cold group record

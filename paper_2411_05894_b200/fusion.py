@@ -9,6 +9,7 @@ device, and fused by the same best-first kernel the batched propose uses
 
 from __future__ import annotations
 
+import functools
 import math
 import os
 from dataclasses import dataclass, fields, replace
@@ -150,11 +151,34 @@ def _cfg_struct(P: int, dec_len: int, branch_len: int, input_branch_len: int, M:
                 separator: int | None = None, use_datastore: bool = True, use_input: bool = True,
                 n_input_trees: int | None = None, device=None):
     md = max(branch_len, input_branch_len)
-    disc = _disc_device((P, md, alpha, beta, gamma_ds, gamma_in), device)
+    key = (P, md, alpha, beta, gamma_ds, gamma_in)
+    disc = _disc_device(key, device)
     c = _lib.Cfg(P, dec_len, branch_len, input_branch_len, M, T, int(use_datastore), int(use_input),
                  P if n_input_trees is None else n_input_trees, int(separator is not None),
-                 0 if separator is None else int(separator) & 0xFFFFFFFF, md + 1, ptr(disc))
+                 0 if separator is None else int(separator) & 0xFFFFFFFF, md + 1, ptr(disc),
+                 fusion_mode(key))
     return c, disc
+
+
+@functools.lru_cache(maxsize=64)
+def _disc_monotone(key: tuple) -> bool:
+    tab = discount_table(*key)
+    return bool(np.all(tab[:, 2:] <= tab[:, 1:-1])) if tab.shape[1] > 2 else True
+
+
+def fusion_mode(key: tuple) -> int:
+    """Fusion kernel: 0 = level-synchronous (csrc/fusion_ls.cu), 1 = heap order
+    (csrc/fusion.cu).  The level-synchronous form relies on priorities never
+    growing along a source path, i.e. every discount row non-increasing in
+    depth; FusionConfig's ranges (ref fusion.py:74-79) guarantee it, the check
+    keeps the heap form for anything else.  SSSD_FUSION=heap|ls overrides."""
+    env = os.environ.get("SSSD_FUSION", "").lower()
+    if env == "heap":
+        return 1
+    mono = _disc_monotone(key)
+    if env == "ls" and not mono:
+        raise ValueError("SSSD_FUSION=ls needs non-increasing discount rows")
+    return 0 if mono else 1
 
 
 def cfg_struct(cfg: FusionConfig, separator=None, use_datastore=True, use_input=True,

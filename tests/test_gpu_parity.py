@@ -266,3 +266,64 @@ def test_propose_pinned_equals_resident_propose():
                     assert torch.equal(g[b, :n], v[b, :n]), (chunks, k, b)
     eng.propose_host([c.tolist() for c in ctxs[:3]])  # smaller call through a larger workspace
     eng.check_status()
+
+
+def _engines(monkeypatch, ds, cfg, **kw):
+    monkeypatch.setenv("SSSD_FUSION", "heap")
+    heap = G.DraftEngine(ds, cfg, **kw)
+    monkeypatch.setenv("SSSD_FUSION", "ls")
+    ls = G.DraftEngine(ds, cfg, **kw)
+    assert heap.c.fusion == 1 and ls.c.fusion == 0
+    return heap, ls
+
+
+def _same_batch(a, b):
+    for k in ("size", "tokens", "parents", "depths", "mask"):
+        x, y = getattr(a, k), getattr(b, k)
+        if k != "size":  # rows past size are padding in both forms
+            assert torch.equal(x, y), k
+        else:
+            assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("dec_len,ctx,n_req,alpha", [(64, 2048, 2048, 0.8), (16, 32768, 8, 0.8),
+                                                     (100, 1024, 512, 0.0), (256, 512, 256, 1.0)])
+def test_level_synchronous_fusion_equals_heap_form(monkeypatch, dec_len, ctx, n_req, alpha):
+    """The level-synchronous fusion kernel (fusion_ls.cu, the default) and the
+    heap-order kernel (fusion.cu) produce identical drafts over phrase-model
+    workloads: cfg2 shape, a prompt-heavy 32k context (big levels in the global
+    pool), alpha = 0 (all input priorities tie at 0) and dec_len 256."""
+    corpus = workload.corpus(1_000_000, 32000)
+    ds = G.build(corpus, vocab_size=32000)
+    cfg = G.FusionConfig(dec_len=dec_len, alpha=alpha)
+    heap, ls = _engines(monkeypatch, ds, cfg)
+    ctxs = workload.prompt_heavy_contexts(n_req, ctx, 32000) if ctx > 4096 else workload.contexts(n_req, ctx, 32000)
+    flat = np.concatenate([np.asarray(c, dtype=np.uint32) for c in ctxs])
+    seq = torch.from_numpy(flat.view(np.int32)).cuda()
+    off = torch.arange(n_req, dtype=torch.int64, device="cuda") * ctx
+    ln = torch.full((n_req,), ctx, dtype=torch.int32, device="cuda")
+    a = heap.propose(seq, off, ln, ctx)
+    heap.check_status()
+    b = ls.propose(seq, off, ln, ctx)
+    ls.check_status()
+    torch.cuda.synchronize()
+    _same_batch(a, b)
+
+
+def test_level_synchronous_fusion_small_alphabets(monkeypatch):
+    """Tie-heavy tiny alphabets (many equal counts / priorities, duplicate paths
+    across all P+1 sources) through both fusion kernels."""
+    rng = np.random.default_rng(5)
+    for trial in range(4):
+        V = int(rng.choice([2, 3, 5]))
+        corpus = rng.integers(0, V, 20000).astype(np.uint32)
+        ds = G.build(corpus)
+        cfg = G.FusionConfig(P=int(rng.integers(1, 6)), dec_len=int(rng.choice([5, 33, 64, 200])),
+                             alpha=float(rng.choice([0.0, 0.5, 1.0])), beta=float(rng.choice([0.5, 1.0])),
+                             gamma_ds=float(rng.choice([0.5, 1.0])), gamma_in=float(rng.choice([0.5, 1.0])))
+        heap, ls = _engines(monkeypatch, ds, cfg)
+        ctxs = [rng.integers(0, V, int(rng.integers(1, 4000))).tolist() for _ in range(64)]
+        fa = heap.propose_host(ctxs)
+        fb = ls.propose_host(ctxs)
+        for x, y in zip(fa, fb):
+            assert (x.tokens, x.parents, x.depths) == (y.tokens, y.parents, y.depths), trial
