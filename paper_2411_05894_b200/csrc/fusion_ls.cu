@@ -109,7 +109,7 @@ __host__ __device__ inline int top_bytes(int S) { return (S * 24 + 15) / 16 * 16
 
 int ls_smem_bytes(int P, int S) {
   return kLsLevelBytes * kLsCap + kLsParBytes * kLsParCap + (P + 1) * (int)sizeof(SrcDesc) +
-         2 * top_bytes(S) + S * 4 + 16 * 4;
+         top_bytes(S) + S * 8 + 16 * 4;
 }
 
 // Bump-allocate `bytes` from the fusion pool (warp-uniform); nullptr + status
@@ -161,33 +161,52 @@ __device__ __noinline__ uint32_t ls_generate(const LsPar par, int np, uint32_t E
   bool c_open = false;
   int c_j = 0;
   uint32_t c_tok = 0, c_cnt = 0, c_first = 0, c_start = 0, c_end = 0;
-  for (uint32_t base = 0; base < E; base += 32) {
-    const uint32_t x = base + lane;
-    int j = 0;
-    bool has = false, w = false;
-    uint32_t tk = 0, orig = 0xffffffffu, i = 0;
-    if (x < E) {
-      int lo = 0, hi = np;  // last parent whose offset is <= x
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (par.off[mid] <= x) lo = mid;
-        else hi = mid;
-      }
-      j = lo;
-      const SrcDesc& s = sd[par.tbr[j] >> kTbBits];
-      i = par.a[j] + (x - par.off[j]);
-      const uint32_t lm = s.meta[i];
-      if (el_len(lm) >= (uint32_t)d) {
-        has = true;
-        tk = s.tok[(int64_t)(d - 1) * s.stride + i];
-        if ((int)el_m(lm) >= s.thr) {
-          w = true;
-          orig = s.orig[i];
+  // elements are fetched kGenBatch chunks at a time (independent loads, one
+  // memory round trip per batch), then scanned chunk by chunk
+#ifndef SSSD_GEN_BATCH
+#define SSSD_GEN_BATCH 1
+#endif
+  constexpr int kGenBatch = SSSD_GEN_BATCH;
+  for (uint32_t base0 = 0; base0 < E; base0 += 32 * kGenBatch) {
+    int jv[kGenBatch];
+    uint32_t iv[kGenBatch], lmv[kGenBatch], tkv[kGenBatch], ogv[kGenBatch], thv[kGenBatch];
+#pragma unroll
+    for (int u = 0; u < kGenBatch; ++u) {
+      const uint32_t x = base0 + 32 * u + lane;
+      jv[u] = 0;
+      iv[u] = 0;
+      lmv[u] = 0;
+      tkv[u] = 0;
+      ogv[u] = 0xffffffffu;
+      thv[u] = 0;
+      if (x < E) {
+        int lo = 0, hi = np;  // last parent whose offset is <= x
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (par.off[mid] <= x) lo = mid;
+          else hi = mid;
         }
+        const SrcDesc& s = sd[par.tbr[lo] >> kTbBits];
+        const uint32_t i = par.a[lo] + (x - par.off[lo]);
+        jv[u] = lo;
+        iv[u] = i;
+        thv[u] = (uint32_t)s.thr;
+        lmv[u] = s.meta[i];
+        tkv[u] = s.tok[(int64_t)(d - 1) * s.stride + i];  // column d-1 exists (d <= source depth)
+        ogv[u] = s.orig[i];
       }
     }
+#pragma unroll
+    for (int u = 0; u < kGenBatch; ++u) {
+    const uint32_t base = base0 + 32 * u;
+    if (base >= E) break;
+    const int j = jv[u];
+    const uint32_t i = iv[u], tk = tkv[u];
+    const bool has = base + lane < E && el_len(lmv[u]) >= (uint32_t)d;
+    const bool w = has && el_m(lmv[u]) >= thv[u];
+    const uint32_t orig = w ? ogv[u] : 0xffffffffu;
     const uint32_t hasm = __ballot_sync(SSSD_FULL, has);
-    if (!hasm && !c_open) continue;
+    if (!hasm && !c_open) continue;  // (warp-uniform)
     const unsigned long long key = has ? ((unsigned long long)j << 32 | tk) : (1ull << 63 | (unsigned)lane);
     const uint32_t gm = __match_any_sync(SSSD_FULL, key);
     const uint32_t wm = __ballot_sync(SSSD_FULL, w);
@@ -224,6 +243,7 @@ __device__ __noinline__ uint32_t ls_generate(const LsPar par, int np, uint32_t E
     } else {
       c_open = false;
     }
+    }
   }
   if (c_open) emit(lane == 0, c_j, c_tok, c_cnt, c_first, c_start, c_end);
   __syncwarp();
@@ -231,8 +251,7 @@ __device__ __noinline__ uint32_t ls_generate(const LsPar par, int np, uint32_t E
 }
 
 // Sort positions [0, n) by (k0, k1), carrying ord (n <= 32: ranks in
-// registers; otherwise a bitonic network over the power-of-two padded range,
-// which the level's capacity covers).
+// registers; otherwise a bitonic network).
 __device__ __noinline__ void ls_sort(LsLevel L, uint32_t n) {
   const int lane = lane_id();
   if (n <= 32) {
@@ -255,21 +274,25 @@ __device__ __noinline__ void ls_sort(LsLevel L, uint32_t n) {
     __syncwarp();
     return;
   }
+  // bitonic network in its all-ascending form (each merge starts by
+  // comparing i with the mirror position of its block), so positions >= n act
+  // as +infinity without being stored: a comparator reaching past n is a no-op
   uint32_t N2 = 64;
   while (N2 < n) N2 <<= 1;
-  for (uint32_t q = n + lane; q < N2; q += 32) {
-    L.k0[q] = ~0ull;
-    L.k1[q] = ~0ull;
-    L.ord[q] = 0xffffffffu;
-  }
-  __syncwarp();
   for (uint32_t kk = 2; kk <= N2; kk <<= 1) {
     for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
       for (uint32_t p = lane; p < N2 / 2; p += 32) {
-        const uint32_t lo = 2 * jj * (p / jj) + (p % jj), hi = lo + jj;
-        const bool asc = (lo & kk) == 0;
+        uint32_t lo, hi;
+        if (jj == kk >> 1) {
+          lo = (p / jj) * kk + (p % jj);
+          hi = (p / jj) * kk + kk - 1 - (p % jj);
+        } else {
+          lo = 2 * jj * (p / jj) + (p % jj);
+          hi = lo + jj;
+        }
+        if (hi >= n) continue;
         const uint64_t a0 = L.k0[lo], a1 = L.k1[lo], b0 = L.k0[hi], b1 = L.k1[hi];
-        if (k_less(b0, b1, a0, a1) == asc) {
+        if (k_less(b0, b1, a0, a1)) {
           const uint32_t oa = L.ord[lo], ob = L.ord[hi];
           L.k0[lo] = b0;
           L.k1[lo] = b1;
@@ -285,7 +308,7 @@ __device__ __noinline__ void ls_sort(LsLevel L, uint32_t n) {
 }
 
 #ifndef SSSD_LS_MINB
-#define SSSD_LS_MINB 16
+#define SSSD_LS_MINB 24
 #endif
 
 __global__ void __launch_bounds__(32, SSSD_LS_MINB)
@@ -307,9 +330,11 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
   sp += kLsParBytes * kLsParCap;
   SrcDesc* sd = reinterpret_cast<SrcDesc*>(sp);
   sp += NR * sizeof(SrcDesc);
-  uint8_t* top_base = sp;
-  sp += 2 * top_bytes(S);
+  const LsTop T = top_carve(sp, S);
+  sp += top_bytes(S);
   uint32_t* nl = reinterpret_cast<uint32_t*>(sp);  // sorted positions of the level's new paths
+  sp += S * 4;
+  uint32_t* npos = reinterpret_cast<uint32_t*>(sp);  // their slots in the merged top list
   sp += S * 4;
   uint32_t* rcnt = reinterpret_cast<uint32_t*>(sp);  // per-rank class counters
 
@@ -343,7 +368,7 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
   uint32_t glev_cap = 0;
   uint8_t* gpar = nullptr;
   uint32_t gpar_cap = 0;
-  int t = 0, cur = 0;
+  int t = 0;
   uint32_t next_pid = 1;
   uint32_t gen_total = 0, max_level = 0, gallocs = 0, levels = 0;
 
@@ -440,30 +465,13 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
       __syncwarp();
     }
 
-    // 5. merge the level's new paths (already in G order) into the top list
+    // 5. merge the level's new paths (already in G order) into the top list,
+    //    in place: new paths find their slots against the old list, old
+    //    entries move up chunk by chunk from the end (pos >= i), then the new
+    //    paths land in the gaps
     const uint32_t dd = (uint32_t)d << 26;
     {
       const uint32_t u = min(nnew, (uint32_t)K);
-      const LsTop tc = top_carve(top_base + cur * top_bytes(S), S);
-      const LsTop tn = top_carve(top_base + (cur ^ 1) * top_bytes(S), S);
-      for (int i = lane; i < t; i += 32) {
-        const uint64_t x0 = tc.g0[i];
-        const uint32_t x1 = tc.g1[i];
-        uint32_t lo = 0, hi = u;  // new paths with G < x
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi) >> 1, sm = nl[mid];
-          if (g_less(L.k0[sm], dd | L.tbr[sm], x0, x1)) lo = mid + 1;
-          else hi = mid;
-        }
-        const uint32_t pos = (uint32_t)i + lo;
-        if (pos < (uint32_t)K) {
-          tn.g0[pos] = x0;
-          tn.g1[pos] = x1;
-          tn.pid[pos] = tc.pid[i];
-          tn.tok[pos] = tc.tok[i];
-          tn.ppid[pos] = tc.ppid[i];
-        }
-      }
       for (uint32_t m = lane; m < u; m += 32) {
         const uint32_t sm = nl[m];
         const uint64_t x0 = L.k0[sm];
@@ -471,30 +479,60 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
         uint32_t lo = 0, hi = (uint32_t)t;  // top entries with G < x
         while (lo < hi) {
           const uint32_t mid = (lo + hi) >> 1;
-          if (g_less(tc.g0[mid], tc.g1[mid], x0, x1)) lo = mid + 1;
+          if (g_less(T.g0[mid], T.g1[mid], x0, x1)) lo = mid + 1;
           else hi = mid;
         }
-        const uint32_t pos = m + lo;
+        npos[m] = m + lo;
+      }
+      __syncwarp();
+      for (int c0 = ((t - 1) >> 5) << 5; c0 >= 0 && t > 0; c0 -= 32) {
+        const int i = c0 + lane;
+        uint64_t x0 = 0;
+        uint32_t x1 = 0, xp = 0, xt = 0, xq = 0, pos = 0xffffffffu;
+        if (i < t) {
+          x0 = T.g0[i];
+          x1 = T.g1[i];
+          xp = T.pid[i];
+          xt = T.tok[i];
+          xq = T.ppid[i];
+          uint32_t lo = 0, hi = u;  // new paths with G < x
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1, sm = nl[mid];
+            if (g_less(L.k0[sm], dd | L.tbr[sm], x0, x1)) lo = mid + 1;
+            else hi = mid;
+          }
+          pos = (uint32_t)i + lo;
+        }
+        __syncwarp();
         if (pos < (uint32_t)K) {
-          const uint32_t g = L.ord[sm];
-          tn.g0[pos] = x0;
-          tn.g1[pos] = x1;
-          tn.pid[pos] = L.pid[sm];
-          tn.tok[pos] = L.tok[g];
-          tn.ppid[pos] = L.ppid[g];
+          T.g0[pos] = x0;
+          T.g1[pos] = x1;
+          T.pid[pos] = xp;
+          T.tok[pos] = xt;
+          T.ppid[pos] = xq;
+        }
+        __syncwarp();
+      }
+      for (uint32_t m = lane; m < u; m += 32) {
+        const uint32_t pos = npos[m];
+        if (pos < (uint32_t)K) {
+          const uint32_t sm = nl[m], g = L.ord[sm];
+          T.g0[pos] = L.k0[sm];
+          T.g1[pos] = dd | L.tbr[sm];
+          T.pid[pos] = L.pid[sm];
+          T.tok[pos] = L.tok[g];
+          T.ppid[pos] = L.ppid[g];
         }
       }
       t = min(K, t + (int)u);
-      cur ^= 1;
       __syncwarp();
     }
 
     // 6. the parents of the next level: the prefix at or below the threshold
     uint32_t nexp = n;
     if (t == K) {
-      const LsTop tc = top_carve(top_base + cur * top_bytes(S), S);
-      const uint64_t tau0 = tc.g0[K - 1];
-      const uint32_t tau1 = tc.g1[K - 1];
+      const uint64_t tau0 = T.g0[K - 1];
+      const uint32_t tau1 = T.g1[K - 1];
       nexp = 0;
       for (uint32_t s0 = 0; s0 < n; s0 += 32) {
         const uint32_t s = s0 + lane;
@@ -534,7 +572,6 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
 
   // 7. flatten: node v = 1..t is top entry v-1 (insertion order = G order;
   //    a parent path precedes its children, siblings insert in index order)
-  const LsTop T = top_carve(top_base + cur * top_bytes(S), S);
   int* f_par = reinterpret_cast<int*>(smem);  // the level buffer is free now
   int* f_fc = f_par + S;                      // first child
   int* f_ns = f_fc + S;                       // next sibling
