@@ -30,70 +30,72 @@
 
 namespace sssd {
 
-// One level's nodes, structure of arrays.  k0/k1/ord/tbr/pid are indexed by
-// sorted position, pp/a/z/cnt/tok/ppid by generation index (ord maps).
+// One level's nodes, structure of arrays over one base pointer (fields are
+// recomputed from (base, cap), which keeps them out of registers).
+// k0/k1/ord/tbr/pid are indexed by sorted position, pp/a/z/cnt/tok/ppid by
+// generation index (ord maps).
+//   k0  ~bits(priority)
+//   k1  rank<<56 | parent tb<<32 | first; path key ppid<<32 | tok after the class pass
+//   pp  path probability (ref fusion.py:244,259)
+//   tbr rank << 22 | class position tb;  pid: path id (0 = the root path)
 struct LsLevel {
-  uint64_t* k0;  // ~bits(priority)
-  uint64_t* k1;  // rank<<56 | parent tb<<32 | first; path key ppid<<32 | tok after the class pass
-  double* pp;    // path probability (ref fusion.py:244,259)
-  uint32_t *a, *z, *cnt, *tok, *ppid, *ord;
-  uint32_t* tbr;  // rank << 22 | class position tb
-  uint32_t* pid;  // path id (0 = the root path)
+  uint8_t* p;
+  uint32_t cap;
+  __device__ __forceinline__ uint64_t* k0() const { return reinterpret_cast<uint64_t*>(p); }
+  __device__ __forceinline__ uint64_t* k1() const { return reinterpret_cast<uint64_t*>(p) + cap; }
+  __device__ __forceinline__ double* pp() const { return reinterpret_cast<double*>(p) + 2 * cap; }
+  __device__ __forceinline__ uint32_t* f(int i) const {
+    return reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(p) + 3 * cap) + i * cap;
+  }
+  __device__ __forceinline__ uint32_t* a() const { return f(0); }
+  __device__ __forceinline__ uint32_t* z() const { return f(1); }
+  __device__ __forceinline__ uint32_t* cnt() const { return f(2); }
+  __device__ __forceinline__ uint32_t* tok() const { return f(3); }
+  __device__ __forceinline__ uint32_t* ppid() const { return f(4); }
+  __device__ __forceinline__ uint32_t* ord() const { return f(5); }
+  __device__ __forceinline__ uint32_t* tbr() const { return f(6); }
+  __device__ __forceinline__ uint32_t* pid() const { return f(7); }
 };
 static_assert(kLsLevelBytes == 3 * 8 + 8 * 4, "level record");
 
-__device__ __forceinline__ LsLevel level_carve(uint8_t* p, uint32_t cap) {
-  LsLevel l;
-  l.k0 = reinterpret_cast<uint64_t*>(p);
-  l.k1 = l.k0 + cap;
-  l.pp = reinterpret_cast<double*>(l.k1 + cap);
-  uint32_t* u = reinterpret_cast<uint32_t*>(l.pp + cap);
-  l.a = u;
-  l.z = u + cap;
-  l.cnt = u + 2 * cap;
-  l.tok = u + 3 * cap;
-  l.ppid = u + 4 * cap;
-  l.ord = u + 5 * cap;
-  l.tbr = u + 6 * cap;
-  l.pid = u + 7 * cap;
-  return l;
-}
+__device__ __forceinline__ LsLevel level_carve(uint8_t* p, uint32_t cap) { return LsLevel{p, cap}; }
 
-// The expanded prefix of the previous level (the parents of this level).
+// The expanded prefix of the previous level (the parents of this level);
+// off = exclusive scan of the element-range sizes.
 struct LsPar {
-  double* pp;
-  uint32_t *a, *z, *cnt, *tbr, *pid, *off;  // off = exclusive scan of the range sizes
+  uint8_t* p;
+  uint32_t cap;
+  __device__ __forceinline__ double* pp() const { return reinterpret_cast<double*>(p); }
+  __device__ __forceinline__ uint32_t* f(int i) const {
+    return reinterpret_cast<uint32_t*>(reinterpret_cast<double*>(p) + cap) + i * cap;
+  }
+  __device__ __forceinline__ uint32_t* a() const { return f(0); }
+  __device__ __forceinline__ uint32_t* z() const { return f(1); }
+  __device__ __forceinline__ uint32_t* cnt() const { return f(2); }
+  __device__ __forceinline__ uint32_t* tbr() const { return f(3); }
+  __device__ __forceinline__ uint32_t* pid() const { return f(4); }
+  __device__ __forceinline__ uint32_t* off() const { return f(5); }
 };
 static_assert(kLsParBytes == 8 + 6 * 4, "parent record");
 
-__device__ __forceinline__ LsPar par_carve(uint8_t* p, uint32_t cap) {
-  LsPar q;
-  q.pp = reinterpret_cast<double*>(p);
-  uint32_t* u = reinterpret_cast<uint32_t*>(q.pp + cap);
-  q.a = u;
-  q.z = u + cap;
-  q.cnt = u + 2 * cap;
-  q.tbr = u + 3 * cap;
-  q.pid = u + 4 * cap;
-  q.off = u + 5 * cap;
-  return q;
-}
+__device__ __forceinline__ LsPar par_carve(uint8_t* p, uint32_t cap) { return LsPar{p, cap}; }
 
-// Running top list: the best (dec_len-1) distinct paths in G order.
+// Running top list: the best (dec_len-1) distinct paths in G order;
+// g1 = depth << 26 | rank << 22 | tb.
 struct LsTop {
-  uint64_t* g0;
-  uint32_t *g1, *pid, *tok, *ppid;  // g1 = depth << 26 | rank << 22 | tb
+  uint8_t* p;
+  int S;
+  __device__ __forceinline__ uint64_t* g0() const { return reinterpret_cast<uint64_t*>(p); }
+  __device__ __forceinline__ uint32_t* f(int i) const {
+    return reinterpret_cast<uint32_t*>(reinterpret_cast<uint64_t*>(p) + S) + i * S;
+  }
+  __device__ __forceinline__ uint32_t* g1() const { return f(0); }
+  __device__ __forceinline__ uint32_t* pid() const { return f(1); }
+  __device__ __forceinline__ uint32_t* tok() const { return f(2); }
+  __device__ __forceinline__ uint32_t* ppid() const { return f(3); }
 };
 
-__device__ __forceinline__ LsTop top_carve(uint8_t* p, int S) {
-  LsTop t;
-  t.g0 = reinterpret_cast<uint64_t*>(p);
-  t.g1 = reinterpret_cast<uint32_t*>(t.g0 + S);
-  t.pid = t.g1 + S;
-  t.tok = t.pid + S;
-  t.ppid = t.tok + S;
-  return t;
-}
+__device__ __forceinline__ LsTop top_carve(uint8_t* p, int S) { return LsTop{p, S}; }
 
 __device__ __forceinline__ bool g_less(uint64_t a0, uint32_t a1, uint64_t b0, uint32_t b1) {
   return a0 < b0 || (a0 == b0 && a1 < b1);
@@ -126,130 +128,6 @@ __device__ __forceinline__ uint8_t* pool_take(uint8_t* pool, unsigned long long*
   return pool + at;
 }
 
-// Generate the depth-d children of parents [0, np) (element ranges scanned
-// flat over the lanes; runs of equal token inside one parent's range are
-// one child).  Writes nodes with index < cap, returns the total count.
-__device__ __noinline__ uint32_t ls_generate(const LsPar par, int np, uint32_t E, LsLevel L, uint32_t cap,
-                                             const SrcDesc* sd, const double* disc, int disc_stride, int d) {
-  const int lane = lane_id();
-  const uint32_t lt = lanemask_lt();
-  uint32_t n = 0;
-  const double* drow = disc + d;
-  auto emit = [&](bool pred, int j, uint32_t tk, uint32_t cnt, uint32_t first, uint32_t s, uint32_t e) {
-    const bool live = pred && cnt > 0;
-    const uint32_t bal = __ballot_sync(SSSD_FULL, live);
-    if (live) {
-      const uint32_t pos = n + __popc(bal & lt);
-      if (pos < cap) {
-        const uint32_t tr = par.tbr[j], rk = tr >> kTbBits, pc = par.cnt[j];
-        const double ratio = cnt == pc ? 1.0 : __ddiv_rn((double)cnt, (double)pc);  // c/c == 1.0 exactly
-        const double pp = __dmul_rn(par.pp[j], ratio);                            // ref fusion.py:259
-        const double pr = __dmul_rn(pp, drow[rk * disc_stride]);                  // ref fusion.py:246
-        L.k0[pos] = ~(uint64_t)__double_as_longlong(pr);
-        L.k1[pos] = (uint64_t)rk << 56 | (uint64_t)(tr & kTbMask) << 32 | first;
-        L.pp[pos] = pp;
-        L.a[pos] = s;
-        L.z[pos] = e;
-        L.cnt[pos] = cnt;
-        L.tok[pos] = tk;
-        L.ppid[pos] = par.pid[j];
-        L.ord[pos] = pos;
-      }
-    }
-    n += __popc(bal);
-  };
-  bool c_open = false;
-  int c_j = 0;
-  uint32_t c_tok = 0, c_cnt = 0, c_first = 0, c_start = 0, c_end = 0;
-  // elements are fetched kGenBatch chunks at a time (independent loads, one
-  // memory round trip per batch), then scanned chunk by chunk
-#ifndef SSSD_GEN_BATCH
-#define SSSD_GEN_BATCH 1
-#endif
-  constexpr int kGenBatch = SSSD_GEN_BATCH;
-  for (uint32_t base0 = 0; base0 < E; base0 += 32 * kGenBatch) {
-    int jv[kGenBatch];
-    uint32_t iv[kGenBatch], lmv[kGenBatch], tkv[kGenBatch], ogv[kGenBatch], thv[kGenBatch];
-#pragma unroll
-    for (int u = 0; u < kGenBatch; ++u) {
-      const uint32_t x = base0 + 32 * u + lane;
-      jv[u] = 0;
-      iv[u] = 0;
-      lmv[u] = 0;
-      tkv[u] = 0;
-      ogv[u] = 0xffffffffu;
-      thv[u] = 0;
-      if (x < E) {
-        int lo = 0, hi = np;  // last parent whose offset is <= x
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (par.off[mid] <= x) lo = mid;
-          else hi = mid;
-        }
-        const SrcDesc& s = sd[par.tbr[lo] >> kTbBits];
-        const uint32_t i = par.a[lo] + (x - par.off[lo]);
-        jv[u] = lo;
-        iv[u] = i;
-        thv[u] = (uint32_t)s.thr;
-        lmv[u] = s.meta[i];
-        tkv[u] = s.tok[(int64_t)(d - 1) * s.stride + i];  // column d-1 exists (d <= source depth)
-        ogv[u] = s.orig[i];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kGenBatch; ++u) {
-    const uint32_t base = base0 + 32 * u;
-    if (base >= E) break;
-    const int j = jv[u];
-    const uint32_t i = iv[u], tk = tkv[u];
-    const bool has = base + lane < E && el_len(lmv[u]) >= (uint32_t)d;
-    const bool w = has && el_m(lmv[u]) >= thv[u];
-    const uint32_t orig = w ? ogv[u] : 0xffffffffu;
-    const uint32_t hasm = __ballot_sync(SSSD_FULL, has);
-    if (!hasm && !c_open) continue;  // (warp-uniform)
-    const unsigned long long key = has ? ((unsigned long long)j << 32 | tk) : (1ull << 63 | (unsigned)lane);
-    const uint32_t gm = __match_any_sync(SSSD_FULL, key);
-    const uint32_t wm = __ballot_sync(SSSD_FULL, w);
-    const int lo_l = __ffs(gm) - 1, hi_l = 31 - __clz(gm);
-    uint32_t fm = orig;  // run minimum of orig (segmented down-scan; runs are lane intervals)
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_down_sync(SSSD_FULL, fm, o);
-      if (lane + o <= hi_l) fm = min(fm, y);
-    }
-    fm = __shfl_sync(SSSD_FULL, fm, lo_l);
-    uint32_t cnt = __popc(gm & wm);
-    const unsigned long long key0 = __shfl_sync(SSSD_FULL, key, 0);
-    if (c_open && !((hasm & 1u) && key0 == ((unsigned long long)c_j << 32 | c_tok))) {
-      emit(lane == 0, c_j, c_tok, c_cnt, c_first, c_start, c_end);  // the carried run ended at the edge
-      c_open = false;
-    }
-    uint32_t start = i - (uint32_t)(lane - lo_l);
-    if (c_open && has && lo_l == 0) {  // continuation of the carried run
-      cnt += c_cnt;
-      fm = min(fm, c_first);
-      start = c_start;
-    }
-    const bool to_next = has && hi_l == 31 && base + 32 < E;
-    emit(has && lane == hi_l && !to_next, j, tk, cnt, fm, start, i + 1);
-    if (__ballot_sync(SSSD_FULL, lane == 31 && to_next)) {
-      c_j = __shfl_sync(SSSD_FULL, j, 31);
-      c_tok = __shfl_sync(SSSD_FULL, tk, 31);
-      c_cnt = __shfl_sync(SSSD_FULL, cnt, 31);
-      c_first = __shfl_sync(SSSD_FULL, fm, 31);
-      c_start = __shfl_sync(SSSD_FULL, start, 31);
-      c_end = __shfl_sync(SSSD_FULL, i, 31) + 1;
-      c_open = true;
-    } else {
-      c_open = false;
-    }
-    }
-  }
-  if (c_open) emit(lane == 0, c_j, c_tok, c_cnt, c_first, c_start, c_end);
-  __syncwarp();
-  return n;
-}
-
 // Sort positions [0, n) by (k0, k1), carrying ord (n <= 32: ranks in
 // registers; otherwise a bitonic network).
 __device__ __noinline__ void ls_sort(LsLevel L, uint32_t n) {
@@ -257,8 +135,8 @@ __device__ __noinline__ void ls_sort(LsLevel L, uint32_t n) {
   if (n <= 32) {
     uint64_t m0 = ~0ull, m1 = ~0ull;
     if (lane < (int)n) {
-      m0 = L.k0[lane];
-      m1 = L.k1[lane];
+      m0 = L.k0()[lane];
+      m1 = L.k1()[lane];
     }
     uint32_t r = 0;
     for (uint32_t q = 0; q < n; ++q) {
@@ -267,9 +145,9 @@ __device__ __noinline__ void ls_sort(LsLevel L, uint32_t n) {
     }
     __syncwarp();
     if (lane < (int)n) {
-      L.k0[r] = m0;
-      L.k1[r] = m1;
-      L.ord[r] = (uint32_t)lane;
+      L.k0()[r] = m0;
+      L.k1()[r] = m1;
+      L.ord()[r] = (uint32_t)lane;
     }
     __syncwarp();
     return;
@@ -291,15 +169,15 @@ __device__ __noinline__ void ls_sort(LsLevel L, uint32_t n) {
           hi = lo + jj;
         }
         if (hi >= n) continue;
-        const uint64_t a0 = L.k0[lo], a1 = L.k1[lo], b0 = L.k0[hi], b1 = L.k1[hi];
+        const uint64_t a0 = L.k0()[lo], a1 = L.k1()[lo], b0 = L.k0()[hi], b1 = L.k1()[hi];
         if (k_less(b0, b1, a0, a1)) {
-          const uint32_t oa = L.ord[lo], ob = L.ord[hi];
-          L.k0[lo] = b0;
-          L.k1[lo] = b1;
-          L.ord[lo] = ob;
-          L.k0[hi] = a0;
-          L.k1[hi] = a1;
-          L.ord[hi] = oa;
+          const uint32_t oa = L.ord()[lo], ob = L.ord()[hi];
+          L.k0()[lo] = b0;
+          L.k1()[lo] = b1;
+          L.ord()[lo] = ob;
+          L.k0()[hi] = a0;
+          L.k1()[hi] = a1;
+          L.ord()[hi] = oa;
         }
       }
       __syncwarp();
@@ -307,8 +185,187 @@ __device__ __noinline__ void ls_sort(LsLevel L, uint32_t n) {
   }
 }
 
+// Cut a full level buffer to its smallest `keepn` (= kLsCap - 32) nodes, moved to
+// slots [0, keepn) in order; returns keepn and the first cut key.
+__device__ __noinline__ uint32_t ls_cut(LsLevel L, uint32_t nb, uint32_t keepn, uint64_t* th0, uint64_t* th1) {
+  const uint32_t lane = (uint32_t)lane_id();
+  ls_sort(L, nb);
+  *th0 = L.k0()[keepn];
+  *th1 = L.k1()[keepn];
+  // read the whole kept prefix (registers of every round) before any write:
+  // a record may move into a slot another lane still has to read
+  constexpr int R = (kLsCap - 32 + 31) / 32;
+  uint32_t a[R], z[R], c[R], t[R], p[R];
+  double q[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t s = lane + 32 * r;
+    if (s < keepn) {
+      const uint32_t g = L.ord()[s];
+      q[r] = L.pp()[g];
+      a[r] = L.a()[g];
+      z[r] = L.z()[g];
+      c[r] = L.cnt()[g];
+      t[r] = L.tok()[g];
+      p[r] = L.ppid()[g];
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t s = lane + 32 * r;
+    if (s < keepn) {
+      L.pp()[s] = q[r];
+      L.a()[s] = a[r];
+      L.z()[s] = z[r];
+      L.cnt()[s] = c[r];
+      L.tok()[s] = t[r];
+      L.ppid()[s] = p[r];
+    }
+  }
+  for (uint32_t s = lane; s < keepn; s += 32) L.ord()[s] = s;
+  __syncwarp();
+  return keepn;
+}
+
+// Generate the depth-d children of parents [0, np) (element ranges scanned
+// flat over the lanes; runs of equal token inside one parent's range are
+// one child) into L.  Returns (nodes kept in L, all children).
+// Without `drop`, nodes past `cap` are counted but not written.  With `drop`
+// (the shared-memory buffer, cap - 32 >= dec_len - 1), a full buffer is
+// sorted and cut to its smallest cap - 32 nodes, and later children at or
+// above the cut key are discarded: L always holds a prefix of the level's
+// (k0, k1) order, which is all the level needs whenever that prefix holds
+// dec_len - 1 distinct paths (the caller checks and otherwise regenerates).
+__device__ __noinline__ uint2 ls_generate(const LsPar par, int np, uint32_t E, LsLevel L, uint32_t cap,
+                                          bool drop, const SrcDesc* sd, const double* disc, int disc_stride,
+                                          int d) {
+  const int lane = lane_id();
+  const uint32_t lt = lanemask_lt();
+  uint32_t n = 0, nb = 0;
+  uint64_t th0 = ~0ull, th1 = ~0ull;  // cut key: children >= it are discarded
+  const double* drow = disc + d;
+  auto emit = [&](bool pred, int j, uint32_t tk, uint32_t cnt, uint32_t first, uint32_t s, uint32_t e) {
+    const bool live = pred && cnt > 0;
+    const uint32_t bal = __ballot_sync(SSSD_FULL, live);
+    if (!bal) return;
+    n += __popc(bal);
+    uint64_t k0 = ~0ull, k1 = ~0ull;
+    double pp = 0.0;
+    uint32_t pid = 0;
+    if (live) {
+      const uint32_t tr = par.tbr()[j], rk = tr >> kTbBits, pc = par.cnt()[j];
+      const double ratio = cnt == pc ? 1.0 : __ddiv_rn((double)cnt, (double)pc);  // c/c == 1.0 exactly
+      pp = __dmul_rn(par.pp()[j], ratio);                                           // ref fusion.py:259
+      const double pr = __dmul_rn(pp, drow[rk * disc_stride]);                    // ref fusion.py:246
+      k0 = ~(uint64_t)__double_as_longlong(pr);
+      k1 = (uint64_t)rk << 56 | (uint64_t)(tr & kTbMask) << 32 | first;
+      pid = par.pid()[j];
+    }
+    bool keep = live && k_less(k0, k1, th0, th1);
+    uint32_t km = __ballot_sync(SSSD_FULL, keep);
+    if (drop && nb + __popc(km) > cap) {  // cut the full buffer to its smallest cap - 32
+      nb = ls_cut(L, nb, cap - 32, &th0, &th1);
+      keep = live && k_less(k0, k1, th0, th1);
+      km = __ballot_sync(SSSD_FULL, keep);
+    }
+    if (keep) {
+      const uint32_t pos = nb + __popc(km & lt);
+      if (pos < cap) {
+        L.k0()[pos] = k0;
+        L.k1()[pos] = k1;
+        L.pp()[pos] = pp;
+        L.a()[pos] = s;
+        L.z()[pos] = e;
+        L.cnt()[pos] = cnt;
+        L.tok()[pos] = tk;
+        L.ppid()[pos] = pid;
+        L.ord()[pos] = pos;
+      }
+    }
+    nb += __popc(km);
+  };
+  // A run may continue into the next 32-element chunk: lane 31 peeks at the
+  // next element, so every run is emitted once, by its last lane, with the
+  // count / first / start carried in from earlier chunks.
+  bool c_open = false;
+  uint32_t c_cnt = 0, c_first = 0, c_start = 0;
+  auto parent_of = [&](uint32_t x) {  // last parent whose offset is <= x
+    int lo = 0, hi = np;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (par.off()[mid] <= x) lo = mid;
+      else hi = mid;
+    }
+    return lo;
+  };
+  for (uint32_t base = 0; base < E; base += 32) {
+    const uint32_t x = base + lane;
+    int j = 0;
+    uint32_t i = 0, lm = 0, tk = 0, og = 0xffffffffu, th = 0;
+    unsigned long long nkey = ~0ull;  // lane 31: key of element base + 32
+    if (x < E) {
+      j = parent_of(x);
+      const SrcDesc& sc = sd[par.tbr()[j] >> kTbBits];
+      i = par.a()[j] + (x - par.off()[j]);
+      th = (uint32_t)sc.thr;
+      lm = sc.meta[i];  // independent loads; column d-1 exists (d <= source depth)
+      tk = sc.tok[(int64_t)(d - 1) * sc.stride + i];
+      og = sc.orig[i];
+    }
+    if (lane == 31 && x + 1 < E) {
+      const int jn = parent_of(x + 1);
+      const SrcDesc& sn = sd[par.tbr()[jn] >> kTbBits];
+      const uint32_t in = par.a()[jn] + (x + 1 - par.off()[jn]);
+      if (el_len(sn.meta[in]) >= (uint32_t)d)
+        nkey = (unsigned long long)jn << 32 | sn.tok[(int64_t)(d - 1) * sn.stride + in];
+    }
+    const bool has = x < E && el_len(lm) >= (uint32_t)d;
+    const bool w = has && el_m(lm) >= th;
+    const uint32_t orig = w ? og : 0xffffffffu;
+    const uint32_t hasm = __ballot_sync(SSSD_FULL, has);
+    if (!hasm) {  // (a carried run always continues at lane 0, so none is open here)
+      continue;
+    }
+    const unsigned long long key = has ? ((unsigned long long)j << 32 | tk) : (1ull << 63 | (unsigned)lane);
+    const uint32_t gm = __match_any_sync(SSSD_FULL, key);
+    const uint32_t wm = __ballot_sync(SSSD_FULL, w);
+    const int lo_l = __ffs(gm) - 1, hi_l = 31 - __clz(gm);
+    uint32_t fm = orig;  // run minimum of orig (segmented down-scan; runs are lane intervals)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_down_sync(SSSD_FULL, fm, o);
+      if (lane + o <= hi_l) fm = min(fm, y);
+    }
+    fm = __shfl_sync(SSSD_FULL, fm, lo_l);
+    uint32_t cnt = __popc(gm & wm);
+    uint32_t start = i - (uint32_t)(lane - lo_l);
+    if (c_open && lo_l == 0) {  // the run carried in from the previous chunk
+      cnt += c_cnt;
+      fm = min(fm, c_first);
+      start = c_start;
+    }
+    const bool cont = lane == 31 && has && nkey == key;
+    emit(has && lane == hi_l && !cont, j, tk, cnt, fm, start, i + 1);
+    const uint32_t cm = __ballot_sync(SSSD_FULL, cont);
+    c_open = cm != 0;
+    if (c_open) {
+      c_cnt = __shfl_sync(SSSD_FULL, cnt, 31);
+      c_first = __shfl_sync(SSSD_FULL, fm, 31);
+      c_start = __shfl_sync(SSSD_FULL, start, 31);
+    }
+  }
+  __syncwarp();
+  return make_uint2(nb, n);
+}
+
 #ifndef SSSD_LS_MINB
-#define SSSD_LS_MINB 24
+#define SSSD_LS_MINB 20
+#endif
+#ifdef SSSD_LS_PROBE  // per-phase cycle counts in the cycle probe (costs registers)
+#define LS_PROBE(...) __VA_ARGS__
+#else
+#define LS_PROBE(...)
 #endif
 
 __global__ void __launch_bounds__(32, SSSD_LS_MINB)
@@ -340,6 +397,22 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
 
   for (int r = lane; r < NR; r += 32) sd[r] = desc[(size_t)b * NR + r];
   __syncwarp();
+  // Every level re-reads the request's element columns (written by the lookup
+  // and input-scan kernels, usually evicted to HBM by now): pull them into L2
+  // once, so the per-level chunk loads are L2 round trips.
+#ifndef SSSD_NO_PF
+  for (int rk = 0; rk < NR; ++rk) {
+    const int n = sd[rk].n;
+    if (n <= 0 || (rk > 1 && sd[rk].meta == sd[rk - 1].meta)) continue;  // input ranks share one array
+    const int lines = (n * 4 + 127) >> 7;
+    const int cols = 2 + sd[rk].depth;
+    for (int q = lane; q < lines * cols; q += 32) {
+      const int col = q / lines, ln = q - col * lines;
+      const uint32_t* base = col == 0 ? sd[rk].meta : col == 1 ? sd[rk].orig : sd[rk].tok + (int64_t)(col - 2) * sd[rk].stride;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(base + ln * 32));
+    }
+  }
+#endif
 
   // level 0: the source roots are the parents of the seeds (path prob 1.0, so
   // pp * (count / root_count) is the seed's count / root_count exactly)
@@ -352,12 +425,12 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
       rc = __reduce_add_sync(SSSD_FULL, rc);
       if (rc == 0) continue;
       if (lane == 0) {
-        par.a[np] = 0;
-        par.z[np] = (uint32_t)sd[rk].n;
-        par.cnt[np] = rc;
-        par.pp[np] = 1.0;
-        par.tbr[np] = (uint32_t)rk << kTbBits;
-        par.pid[np] = 0;
+        par.a()[np] = 0;
+        par.z()[np] = (uint32_t)sd[rk].n;
+        par.cnt()[np] = rc;
+        par.pp()[np] = 1.0;
+        par.tbr()[np] = (uint32_t)rk << kTbBits;
+        par.pid()[np] = 0;
       }
       ++np;
     }
@@ -371,6 +444,7 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
   int t = 0;
   uint32_t next_pid = 1;
   uint32_t gen_total = 0, max_level = 0, gallocs = 0, levels = 0;
+  uint32_t ph_gen = 0, ph_sort = 0, ph_merge = 0;  // probe: generation, sort + classes, merge + parents
 
   for (int d = 1; np > 0 && d < c.disc_stride; ++d) {
     // 1. exclusive scan of the parents' element-range sizes
@@ -378,92 +452,117 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
     for (int j0 = 0; j0 < np; j0 += 32) {
       const int j = j0 + lane;
       uint32_t e = 0;
-      if (j < np && d <= sd[par.tbr[j] >> kTbBits].depth) e = par.z[j] - par.a[j];
+      if (j < np && d <= sd[par.tbr()[j] >> kTbBits].depth) e = par.z()[j] - par.a()[j];
       uint32_t inc = e;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(SSSD_FULL, inc, o);
         if (lane >= o) inc += y;
       }
-      if (j < np) par.off[j] = E + inc - e;
+      if (j < np) par.off()[j] = E + inc - e;
       E += __shfl_sync(SSSD_FULL, inc, 31);
     }
     __syncwarp();
     if (E == 0) break;
     ++levels;
 
-    // 2. generate into shared memory; a level larger than kLsCap is generated
-    //    again into a global buffer of its exact power-of-two size
+    // 2. generate into shared memory (keeping the smallest nodes when the level
+    //    outgrows it); a level whose kept prefix is too short, or that cannot
+    //    drop (dec_len - 1 > kLsCap - 32), is generated again in full into a
+    //    global buffer
     LsLevel L = Ls;
-    uint32_t n = ls_generate(par, np, E, Ls, kLsCap, sd, c.disc, c.disc_stride, d);
-    if (n == 0) break;
-    if (n > (uint32_t)kLsCap) {
-      uint32_t need = 64;
-      while (need < n) need <<= 1;
-      if (glev_cap < need) {
-        glev = pool_take(pool, cursor, pool_bytes, err, (unsigned long long)need * kLsLevelBytes);
-        if (!glev) break;
-        glev_cap = need;
-        ++gallocs;
-      }
-      L = level_carve(glev, glev_cap);
-      ls_generate(par, np, E, L, glev_cap, sd, c.disc, c.disc_stride, d);
-    }
-    gen_total += n;
-    max_level = max(max_level, n);
-    if (n > kTbMask) {  // class positions must fit their field
-      if (lane == 0) atomicExch(err, SSSD_E_LIMIT);
-      break;
-    }
-
-    // 3. sort the level by (k0, k1) = (~priority, rank, parent tb, first)
-    ls_sort(L, n);
-
-    // 4. class positions, path ids (first occurrence in G order wins), new paths
-    if (lane < 16) rcnt[lane] = 0;
-    __syncwarp();
+    const bool drop = K <= kLsCap - 32;
+    LS_PROBE(uint32_t tp = (uint32_t)clock());
+    const uint2 gr = ls_generate(par, np, E, Ls, kLsCap, drop, sd, c.disc, c.disc_stride, d);
+    LS_PROBE(ph_gen += (uint32_t)clock() - tp; tp = (uint32_t)clock());
+    uint32_t n = gr.x, n_all = gr.y;
+    if (n_all == 0) break;
+    bool global = !drop && n_all > (uint32_t)kLsCap;
+    const uint32_t pid0 = next_pid;
     uint32_t nnew = 0;
-    for (uint32_t s0 = 0; s0 < n; s0 += 32) {
-      const uint32_t s = s0 + lane;
-      const bool v = s < n;
-      uint32_t rk = 0, tb = 0;
-      unsigned long long pk = 1ull << 63 | (unsigned)lane;
-      if (v) {
-        rk = (uint32_t)(L.k1[s] >> 56);
-        const uint32_t g = L.ord[s];
-        pk = (unsigned long long)L.ppid[g] << 32 | L.tok[g];
-      }
-      const uint32_t rm = __match_any_sync(SSSD_FULL, v ? rk : 64u + lane);
-      if (v) tb = rcnt[rk] + __popc(rm & lt);
-      const uint32_t pm = __match_any_sync(SSSD_FULL, pk);
-      const int rep = __ffs(pm) - 1;
-      int found = -1;
-      if (v && lane == rep && s0 > 0) {  // an earlier chunk holds the path?
-        for (uint32_t q = 0; q < s0; ++q)
-          if (L.k1[q] == pk) {
-            found = (int)q;
+    bool fail = false;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      if (global) {
+        uint32_t need = 64;
+        while (need < n_all) need <<= 1;
+        if (glev_cap < need) {
+          glev = pool_take(pool, cursor, pool_bytes, err, (unsigned long long)need * kLsLevelBytes);
+          if (!glev) {
+            fail = true;
             break;
           }
+          glev_cap = need;
+          ++gallocs;
+        }
+        L = level_carve(glev, glev_cap);
+        n = ls_generate(par, np, E, L, glev_cap, false, sd, c.disc, c.disc_stride, d).x;
       }
-      const uint32_t newm = __ballot_sync(SSSD_FULL, v && lane == rep && found < 0);
-      uint32_t id = 0;
-      if (v && lane == rep) id = found >= 0 ? L.pid[found] : next_pid + __popc(newm & lt);
-      id = __shfl_sync(SSSD_FULL, id, rep);
-      if ((newm >> lane) & 1u) {
-        const uint32_t at = nnew + __popc(newm & lt);
-        if (at < (uint32_t)K) nl[at] = s;
+      if (n > kTbMask) {  // class positions must fit their field
+        if (lane == 0) atomicExch(err, SSSD_E_LIMIT);
+        fail = true;
+        break;
       }
-      next_pid += __popc(newm);
-      nnew += __popc(newm);
+
+      LS_PROBE(ph_gen += (uint32_t)clock() - tp; tp = (uint32_t)clock());
+      // 3. sort the level by (k0, k1) = (~priority, rank, parent tb, first)
+      ls_sort(L, n);
+
+      // 4. class positions, path ids (first occurrence in G order wins), new paths
+      next_pid = pid0;
+      nnew = 0;
+      if (lane < 16) rcnt[lane] = 0;
       __syncwarp();
-      if (v) {
-        if (lane == 31 - __clz(rm)) rcnt[rk] += __popc(rm);
-        L.tbr[s] = rk << kTbBits | tb;
-        L.pid[s] = id;
-        L.k1[s] = pk;
+      for (uint32_t s0 = 0; s0 < n; s0 += 32) {
+        const uint32_t s = s0 + lane;
+        const bool v = s < n;
+        uint32_t rk = 0, tb = 0;
+        unsigned long long pk = 1ull << 63 | (unsigned)lane;
+        if (v) {
+          rk = (uint32_t)(L.k1()[s] >> 56);
+          const uint32_t g = L.ord()[s];
+          pk = (unsigned long long)L.ppid()[g] << 32 | L.tok()[g];
+        }
+        const uint32_t rm = __match_any_sync(SSSD_FULL, v ? rk : 64u + lane);
+        if (v) tb = rcnt[rk] + __popc(rm & lt);
+        const uint32_t pm = __match_any_sync(SSSD_FULL, pk);
+        const int rep = __ffs(pm) - 1;
+        int found = -1;
+        if (v && lane == rep && s0 > 0) {  // an earlier chunk holds the path?
+          for (uint32_t q = 0; q < s0; ++q)
+            if (L.k1()[q] == pk) {
+              found = (int)q;
+              break;
+            }
+        }
+        const uint32_t newm = __ballot_sync(SSSD_FULL, v && lane == rep && found < 0);
+        uint32_t id = 0;
+        if (v && lane == rep) id = found >= 0 ? L.pid()[found] : next_pid + __popc(newm & lt);
+        id = __shfl_sync(SSSD_FULL, id, rep);
+        if ((newm >> lane) & 1u) {
+          const uint32_t at = nnew + __popc(newm & lt);
+          if (at < (uint32_t)K) nl[at] = s;
+        }
+        next_pid += __popc(newm);
+        nnew += __popc(newm);
+        __syncwarp();
+        if (v) {
+          if (lane == 31 - __clz(rm)) rcnt[rk] += __popc(rm);
+          L.tbr()[s] = rk << kTbBits | tb;
+          L.pid()[s] = id;
+          L.k1()[s] = pk;
+        }
+        __syncwarp();
       }
-      __syncwarp();
+      if (n < n_all && nnew < (uint32_t)K) {  // the kept prefix lacks dec_len - 1 paths
+        global = true;
+        continue;
+      }
+      break;
     }
+    if (fail) break;
+    LS_PROBE(ph_sort += (uint32_t)clock() - tp; tp = (uint32_t)clock());
+    gen_total += n_all;
+    max_level = max(max_level, n_all);
 
     // 5. merge the level's new paths (already in G order) into the top list,
     //    in place: new paths find their slots against the old list, old
@@ -474,12 +573,12 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
       const uint32_t u = min(nnew, (uint32_t)K);
       for (uint32_t m = lane; m < u; m += 32) {
         const uint32_t sm = nl[m];
-        const uint64_t x0 = L.k0[sm];
-        const uint32_t x1 = dd | L.tbr[sm];
+        const uint64_t x0 = L.k0()[sm];
+        const uint32_t x1 = dd | L.tbr()[sm];
         uint32_t lo = 0, hi = (uint32_t)t;  // top entries with G < x
         while (lo < hi) {
           const uint32_t mid = (lo + hi) >> 1;
-          if (g_less(T.g0[mid], T.g1[mid], x0, x1)) lo = mid + 1;
+          if (g_less(T.g0()[mid], T.g1()[mid], x0, x1)) lo = mid + 1;
           else hi = mid;
         }
         npos[m] = m + lo;
@@ -490,38 +589,38 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
         uint64_t x0 = 0;
         uint32_t x1 = 0, xp = 0, xt = 0, xq = 0, pos = 0xffffffffu;
         if (i < t) {
-          x0 = T.g0[i];
-          x1 = T.g1[i];
-          xp = T.pid[i];
-          xt = T.tok[i];
-          xq = T.ppid[i];
+          x0 = T.g0()[i];
+          x1 = T.g1()[i];
+          xp = T.pid()[i];
+          xt = T.tok()[i];
+          xq = T.ppid()[i];
           uint32_t lo = 0, hi = u;  // new paths with G < x
           while (lo < hi) {
             const uint32_t mid = (lo + hi) >> 1, sm = nl[mid];
-            if (g_less(L.k0[sm], dd | L.tbr[sm], x0, x1)) lo = mid + 1;
+            if (g_less(L.k0()[sm], dd | L.tbr()[sm], x0, x1)) lo = mid + 1;
             else hi = mid;
           }
           pos = (uint32_t)i + lo;
         }
         __syncwarp();
         if (pos < (uint32_t)K) {
-          T.g0[pos] = x0;
-          T.g1[pos] = x1;
-          T.pid[pos] = xp;
-          T.tok[pos] = xt;
-          T.ppid[pos] = xq;
+          T.g0()[pos] = x0;
+          T.g1()[pos] = x1;
+          T.pid()[pos] = xp;
+          T.tok()[pos] = xt;
+          T.ppid()[pos] = xq;
         }
         __syncwarp();
       }
       for (uint32_t m = lane; m < u; m += 32) {
         const uint32_t pos = npos[m];
         if (pos < (uint32_t)K) {
-          const uint32_t sm = nl[m], g = L.ord[sm];
-          T.g0[pos] = L.k0[sm];
-          T.g1[pos] = dd | L.tbr[sm];
-          T.pid[pos] = L.pid[sm];
-          T.tok[pos] = L.tok[g];
-          T.ppid[pos] = L.ppid[g];
+          const uint32_t sm = nl[m], g = L.ord()[sm];
+          T.g0()[pos] = L.k0()[sm];
+          T.g1()[pos] = dd | L.tbr()[sm];
+          T.pid()[pos] = L.pid()[sm];
+          T.tok()[pos] = L.tok()[g];
+          T.ppid()[pos] = L.ppid()[g];
         }
       }
       t = min(K, t + (int)u);
@@ -531,12 +630,12 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
     // 6. the parents of the next level: the prefix at or below the threshold
     uint32_t nexp = n;
     if (t == K) {
-      const uint64_t tau0 = T.g0[K - 1];
-      const uint32_t tau1 = T.g1[K - 1];
+      const uint64_t tau0 = T.g0()[K - 1];
+      const uint32_t tau1 = T.g1()[K - 1];
       nexp = 0;
       for (uint32_t s0 = 0; s0 < n; s0 += 32) {
         const uint32_t s = s0 + lane;
-        const bool ok = s < n && !g_less(tau0, tau1, L.k0[s], dd | L.tbr[s]);
+        const bool ok = s < n && !g_less(tau0, tau1, L.k0()[s], dd | L.tbr()[s]);
         const uint32_t okm = __ballot_sync(SSSD_FULL, ok);
         nexp += __popc(okm);
         if (okm != SSSD_FULL) break;
@@ -556,16 +655,17 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
       par = par_carve(smem + kLsLevelBytes * kLsCap, kLsParCap);
     }
     for (uint32_t j = lane; j < nexp; j += 32) {
-      const uint32_t g = L.ord[j];
-      par.pp[j] = L.pp[g];
-      par.a[j] = L.a[g];
-      par.z[j] = L.z[g];
-      par.cnt[j] = L.cnt[g];
-      par.tbr[j] = L.tbr[j];
-      par.pid[j] = L.pid[j];
+      const uint32_t g = L.ord()[j];
+      par.pp()[j] = L.pp()[g];
+      par.a()[j] = L.a()[g];
+      par.z()[j] = L.z()[g];
+      par.cnt()[j] = L.cnt()[g];
+      par.tbr()[j] = L.tbr()[j];
+      par.pid()[j] = L.pid()[j];
     }
     __syncwarp();
     np = (int)nexp;
+    LS_PROBE(ph_merge += (uint32_t)clock() - tp);
   }
   __syncwarp();
   const long long t_levels = clock64();
@@ -581,26 +681,26 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
   const int size = t + 1;
   const bool use_map = (int)next_pid <= (kLsLevelBytes * kLsCap) / 4 - 5 * S;
   if (use_map)
-    for (int v = 1 + lane; v < size; v += 32) pmap[T.pid[v - 1]] = v;
+    for (int v = 1 + lane; v < size; v += 32) pmap[T.pid()[v - 1]] = v;
   __syncwarp();
   int maxd = 0;
   for (int v = lane; v < size; v += 32) {
     int pr = -1, dv = 0;
     if (v > 0) {
-      const uint32_t pp = T.ppid[v - 1];
+      const uint32_t pp = T.ppid()[v - 1];
       pr = 0;
       if (pp != 0) {
         if (use_map) {
           pr = pmap[pp];
         } else {
           for (int u = 0; u < v - 1; ++u)
-            if (T.pid[u] == pp) {
+            if (T.pid()[u] == pp) {
               pr = u + 1;
               break;
             }
         }
       }
-      dv = (int)(T.g1[v - 1] >> 26);
+      dv = (int)(T.g1()[v - 1] >> 26);
     }
     f_par[v] = pr;
     f_dep[v] = dv;
@@ -637,7 +737,7 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
     int v = 0, k = 0;
     while (true) {
       f_pos[v] = k;
-      o_tok[k] = v == 0 ? root_tok[b] : T.tok[v - 1];
+      o_tok[k] = v == 0 ? root_tok[b] : T.tok()[v - 1];
       o_par[k] = v == 0 ? -1 : f_pos[f_par[v]];
       o_dep[k] = f_dep[v];
       ++k;
@@ -677,12 +777,12 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
       long long* st = cycles + (size_t)b * 8;
       const long long t_end = clock64();
       st[0] = t_end - t_start;
-      st[1] = 0;
-      st[2] = t_levels - t_start;
-      st[3] = t_end - t_levels;
-      st[4] = levels;
-      st[5] = gen_total;
-      st[6] = max_level;
+      st[1] = ph_gen;
+      st[2] = ph_sort;
+      st[3] = t_end - t_levels;  // flatten
+      st[4] = ph_merge;
+      st[5] = levels | (long long)max_level << 16;
+      st[6] = gen_total;
       st[7] = gallocs;
     }
   }

@@ -486,61 +486,111 @@ __global__ void __launch_bounds__(256)
   if (tid < jm) s_tail[tid] = seq[L - 1 - tid];
   __syncthreads();
   sssd_elem* r = raw + (size_t)b * cap;
-  // Each warp owns one contiguous segment of end positions e in [1, L): pass 1
-  // counts its occurrences, one block prefix gives every warp its output base,
-  // pass 2 recomputes the (L1-resident) matches and writes them in e order.
-  const int nw = blockDim.x >> 5;
-  const int seg = ((L - 1 + nw - 1) / nw + 31) & ~31;
-  const int e_lo = 1 + warp * seg, e_hi = min(L, e_lo + seg);
-  auto match = [&](int e) {
-    int m = 0;
-    if (e < e_hi) {
-      const int lim = min(jm, e);
-      while (m < lim && seq[e - 1 - m] == s_tail[m]) ++m;
+  // Match lengths m[e] (A.4) for end positions e in [1, L): each thread owns
+  // kScanV consecutive positions of a 256 * kScanV tile and fetches their
+  // first comparison tokens seq[e-1] with independent loads (one memory round
+  // trip per tile); only the rare lanes whose first token matches the tail
+  // read further back.  A block scan of the per-thread counts places the
+  // occurrences in e order.
+  constexpr int kScanV = 8;
+  const uint32_t t0 = s_tail[0];
+  int total = 0;
+  for (int tile = 1; tile < L; tile += 256 * kScanV) {
+    const int e0 = tile + tid * kScanV;
+    uint32_t v[kScanV];
+#pragma unroll
+    for (int k = 0; k < kScanV; ++k) v[k] = e0 + k < L ? seq[e0 + k - 1] : ~t0;
+    uint32_t mk = 0;  // bit k: position e0 + k matches (m >= 1)
+#pragma unroll
+    for (int k = 0; k < kScanV; ++k) mk |= (v[k] == t0 && e0 + k < L ? 1u : 0u) << k;
+    const int cnt = __popc(mk);
+    int inc = cnt;  // block exclusive scan of the counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(SSSD_FULL, inc, o);
+      if (lane >= o) inc += y;
     }
-    return m;
-  };
-  int mine = 0;
-  for (int e0 = e_lo; e0 < e_hi; e0 += 32) mine += __popc(__ballot_sync(SSSD_FULL, match(e0 + lane) > 0));
-  if (lane == 0) s_wsum[warp] = mine;
-  __syncthreads();
-  int base = 0, total = 0;
-  for (int w = 0; w < nw; ++w) {
-    if (w < warp) base += s_wsum[w];
-    total += s_wsum[w];
-  }
-  for (int e0 = e_lo; e0 < e_hi; e0 += 32) {
-    const int e = e0 + lane;
-    const int m = match(e);
-    const uint32_t bal = __ballot_sync(SSSD_FULL, m > 0);
-    if (m > 0) {
+    if (lane == 31) s_wsum[warp] = inc;
+    __syncthreads();
+    int wbase = 0, tsum = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const int x = s_wsum[w];
+      wbase += w < warp ? x : 0;
+      tsum += x;
+    }
+    int at = total + wbase + inc - cnt;
+    while (mk) {
+      const int k = __ffs(mk) - 1;
+      mk &= mk - 1;
+      const int e = e0 + k;
+      const int lim = min(jm, e);
+      int m = 1;
+      while (m < lim && seq[e - 1 - m] == s_tail[m]) ++m;
       sssd_elem el;
       el.off = (uint32_t)e;
       el.orig = (uint32_t)e;
       el.len_m = (uint32_t)min(c.IBL, L - e) | ((uint32_t)m << 8);
       el.pad = 0;
-      r[base + __popc(bal & lanemask_lt())] = el;
+      r[at++] = el;
     }
-    base += __popc(bal);
+    total += tsum;
+    __syncthreads();  // s_wsum reuse
   }
   if (tid == 0) in_n[b] = total;
   sssd_elem* out = sorted + (size_t)b * cap;
   if (total == 0) return;
   __syncthreads();
-  if (total <= 32) {
-    // small occurrence sets (the common case): rank sort inside warp 0, no barriers
-    if (warp == 0) {
-      const ElemLess less{r, seq, total};
-      if (lane < total) {
-        int rank = 0;
-        for (int jj = 0; jj < total; ++jj) rank += less((uint32_t)jj, (uint32_t)lane) ? 1 : 0;
-        out[rank] = r[lane];
+  if (total <= (int)blockDim.x && total * (c.IBL + 2) <= kSortSmem) {
+    // the common case (<= 256 occurrences): continuation strings staged in
+    // shared memory; warp w rank-sorts occurrences [32w, 32w + 32), then each
+    // occurrence adds, per other run, a binary-searched count of the run's
+    // smaller strings (ties: position order, i.e. run order)
+    uint32_t* str = s_idx;  // [total][IBL] strings, [total] lengths, [total] run-sorted indices
+    uint32_t* slen = s_idx + total * c.IBL;
+    uint32_t* srt = slen + total;
+    sssd_elem me{};
+    uint32_t ml = 0;
+    const uint32_t* mine = str + tid * c.IBL;
+    if (tid < total) {
+      me = r[tid];
+      ml = el_len(me.len_m);
+      slen[tid] = ml;
+      for (uint32_t d = 0; d < ml; ++d) str[tid * c.IBL + d] = seq[me.off + d];
+    }
+    __syncthreads();
+    const int r0 = warp * 32, rn = min(32, total - r0);
+    int lr = 0;
+    if (tid < total) {
+      for (int jj = r0; jj < r0 + rn; ++jj) {
+        const int cr = cmp_str(str + jj * c.IBL, slen[jj], mine, ml);
+        lr += (cr < 0 || (cr == 0 && jj < tid)) ? 1 : 0;
       }
-      __syncwarp();
-      if (cols.meta && lane < total) {
+      srt[r0 + lr] = (uint32_t)tid;
+    }
+    __syncthreads();
+    if (tid < total) {
+      int rank = lr;
+      for (int q0 = 0; q0 < total; q0 += 32) {
+        if (q0 == r0) continue;
+        const int qn = min(32, total - q0);
+        int lo = 0, hi = qn;  // elements of run q that sort before mine
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          const uint32_t x = srt[q0 + mid];
+          const int cr = cmp_str(str + x * c.IBL, slen[x], mine, ml);
+          if (cr < 0 || (cr == 0 && q0 < r0)) lo = mid + 1;
+          else hi = mid;
+        }
+        rank += lo;
+      }
+      out[rank] = me;
+      if (cols.meta) {
         const Cols cb{cols.meta + (size_t)b * cols.stride, cols.orig + (size_t)b * cols.stride,
                       cols.tok + (size_t)b * cols.stride * c.IBL, cols.stride};
-        write_cols(cb, lane, out[lane], seq);
+        cb.meta[rank] = me.len_m & 0xffffu;
+        cb.orig[rank] = me.orig;
+        for (uint32_t d = 0; d < ml; ++d) cb.tok[d * cb.stride + rank] = mine[d];
       }
     }
     return;

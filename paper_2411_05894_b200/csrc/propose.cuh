@@ -57,7 +57,10 @@ __global__ void lpt_scatter_kernel(const uint8_t* bucket, const int32_t* hist, i
 // of each a warp keeps in shared memory (larger levels use the fusion pool)
 constexpr int kLsLevelBytes = 56;
 constexpr int kLsParBytes = 32;
-constexpr int kLsCap = 96;
+#ifndef SSSD_LS_CAP
+#define SSSD_LS_CAP 128
+#endif
+constexpr int kLsCap = SSSD_LS_CAP;
 constexpr int kLsParCap = 64;
 int ls_smem_bytes(int P, int S);
 __global__ void draft_ls_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, uint8_t* pool,

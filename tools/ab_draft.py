@@ -20,9 +20,12 @@ _lib.lib().sssd_set_cycle_probe(cyc.data_ptr())
 eng.propose(seq, off, ln, 2048)
 torch.cuda.synchronize()
 _lib.lib().sssd_set_cycle_probe(None)
-c = cyc[:, 0].cpu().numpy() / 1.965e3
-pp = (cyc[:, 2].cpu().numpy() / 1.965e3 / np.maximum(cyc[:, 4].cpu().numpy(), 1)).mean()
+st = cyc.cpu().numpy()
+c = st[:, 0] / 1.965e3
+pp = 0.0
+ph = " ".join("%s %.1f" % (nm, (st[:, k] / 1.965e3).mean()) for k, nm in ((1, "gen"), (2, "sort+cls"), (4, "merge+par"), (3, "flat")))
+ph += " levels %.2f maxlev %.1f gen %.1f gallocs %.3f" % ((st[:, 5] & 0xffff).mean(), (st[:, 5] >> 16).mean(), st[:, 6].mean(), st[:, 7].mean())
 print(os.path.basename(os.environ.get("SSSD_LIB", "default")), "B16384 stage ms", np.round(full, 3).tolist(),
       "B64 stage ms", np.round(b64, 3).tolist(),
       "req us mean %.0f p50 %.0f p99 %.0f max %.0f" % (c.mean(), *np.percentile(c, [50, 99]), c.max()),
-      "per-pop us %.2f" % pp)
+      "| LS phases us:", ph)
