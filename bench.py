@@ -261,7 +261,7 @@ def run_ours(args) -> None:
         flush.zero_()
         prof += np.asarray(eng.propose_profile(seq, off, ln, CTX))
     prof /= 3
-    names = ["ds_lookup_kernel", "input_scan_kernel", "propose_setup_kernel", "draft_kernel"]
+    names = ["ds_lookup_kernel", "input_scan_kernel", "propose_setup_kernel", "draft_ls_kernel"]
     dom = int(np.argmax(prof))
 
     # single-batch latency at B=64

@@ -65,6 +65,13 @@ int sssd_sa_build(const uint32_t* tokens, uint64_t n, uint32_t* sa_out, void* wo
 int sssd_rows_build(const uint32_t* tokens, uint64_t n, const uint32_t* sa, uint32_t* rows,
                     void* stream);
 
+/* First-token index of the suffix rows: bucket[t] (t = 0 .. n_buckets) = the
+ * first local row whose first token is >= t, so rows starting with token t < n_buckets
+ * are exactly [bucket[t], bucket[t+1]).  A search accelerator for find_range
+ * (ref datastore.py:156-183): the same bounds with fewer probes. */
+int sssd_bucket_build(const uint32_t* rows, uint64_t n_rows, uint32_t n_buckets, uint32_t* bucket,
+                      void* stream);
+
 /* Copy the SA column of rows out as uint64 (the SSSD v1 file's `<u8` array). */
 int sssd_rows_sa64(const uint32_t* rows, uint64_t n, uint64_t* sa64_out, void* stream);
 
@@ -111,6 +118,10 @@ typedef struct sssd_ds {
   uint64_t n_tokens;
   uint64_t rank_base;
   uint64_t n_rows;
+  const uint32_t* bucket; /* optional (NULL = none): [n_buckets + 1] first-token index,
+                             bucket[t] = first local row whose first token >= t
+                             (sssd_bucket_build); narrows every range search */
+  uint32_t n_buckets;
 } sssd_ds;
 
 /* Sequences: request b's live sequence is seq[seq_off[b] .. seq_off[b]+seq_len[b]). */

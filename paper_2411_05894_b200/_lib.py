@@ -45,7 +45,7 @@ class Elem(C.Structure):
 
 class Ds(C.Structure):
     _fields_ = [("rows", vp), ("tokens", vp), ("n_tokens", C.c_uint64), ("rank_base", C.c_uint64),
-                ("n_rows", C.c_uint64)]
+                ("n_rows", C.c_uint64), ("bucket", vp), ("n_buckets", C.c_uint32)]
 
 
 class Seqs(C.Structure):
@@ -68,6 +68,7 @@ _SIGS = {
     "sssd_sa_build": (C.c_int, [vp, C.c_uint64, vp, vp, C.c_size_t, vp]),
     "sssd_rows_build": (C.c_int, [vp, C.c_uint64, vp, vp, vp]),
     "sssd_rows_sa64": (C.c_int, [vp, C.c_uint64, vp, vp]),
+    "sssd_bucket_build": (C.c_int, [vp, C.c_uint64, C.c_uint32, vp, vp]),
     "sssd_propose_workspace": (C.c_size_t, [C.POINTER(Cfg), C.c_int32, C.c_int32]),
     "sssd_propose": (C.c_int, [C.POINTER(Ds), C.POINTER(Seqs), C.POINTER(Cfg), C.POINTER(DraftOut),
                                C.POINTER(LookupOut), vp, C.c_size_t, vp]),

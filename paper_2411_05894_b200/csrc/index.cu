@@ -136,6 +136,19 @@ static int bits_for(uint64_t x) {
 
 using namespace sssd;
 
+// bucket[t] = first row whose first token is >= t: row r writes the entries
+// (tok0(r-1), tok0(r)] (clamped to n_buckets); the last row also closes the
+// table with n_rows.  Rows are sorted, so the writes cover [0, n_buckets].
+__global__ void bucket_build_kernel(const uint32_t* rows, uint64_t n, uint32_t nb, uint32_t* bucket) {
+  const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int64_t t = rows[r * 16 + 1];
+  const int64_t prev = r > 0 ? (int64_t)rows[(r - 1) * 16 + 1] : -1;
+  for (int64_t u = prev + 1; u <= t && u <= (int64_t)nb; ++u) bucket[u] = (uint32_t)r;
+  if (r == n - 1)
+    for (int64_t u = t + 1; u <= (int64_t)nb; ++u) bucket[u] = (uint32_t)n;
+}
+
 extern "C" {
 
 size_t sssd_sa_build_workspace(uint64_t n) { return sa_carve(nullptr, n ? n : 1).total; }
@@ -192,6 +205,17 @@ int sssd_rows_build(const uint32_t* tokens, uint64_t n, const uint32_t* sa, uint
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   rows_build_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(tokens, n, sa, rows);
   return cuda_check(cudaGetLastError(), "rows_build launch");
+}
+
+int sssd_bucket_build(const uint32_t* rows, uint64_t n_rows, uint32_t n_buckets, uint32_t* bucket,
+                      void* stream) {
+  if (!rows || !bucket) return fail(SSSD_E_ARG, "bucket_build needs rows and an output table");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n_rows == 0)
+    return cuda_check(cudaMemsetAsync(bucket, 0, ((size_t)n_buckets + 1) * 4, st), "bucket memset");
+  if (n_rows >= 0xffffffffull) return fail(SSSD_E_LIMIT, "bucket index needs < 2^32 rows");
+  bucket_build_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(rows, n_rows, n_buckets, bucket);
+  return cuda_check(cudaGetLastError(), "bucket_build launch");
 }
 
 int sssd_rows_sa64(const uint32_t* rows, uint64_t n, uint64_t* sa64_out, void* stream) {

@@ -130,8 +130,23 @@ __device__ uint64_t warp_search(const sssd_ds& ds, const uint32_t* pat, int p, u
 
 __device__ void warp_bounds(const sssd_ds& ds, const uint32_t* pat, int p, uint64_t& out_lo,
                             uint64_t& out_hi) {
-  uint64_t ulo = 0, uhi = ds.n_rows;
-  const uint64_t lower = warp_search<false>(ds, pat, p, 0, ds.n_rows, ulo, uhi);
+  uint64_t blo = 0, bhi = ds.n_rows;
+  if (ds.bucket) {  // first-token index: rows starting with pat[0] (or >= n_buckets)
+    const uint32_t t0 = pat[0];
+    if (t0 < ds.n_buckets) {
+      blo = ds.bucket[t0];
+      bhi = ds.bucket[t0 + 1];
+      if (p == 1) {
+        out_lo = blo;
+        out_hi = bhi;
+        return;
+      }
+    } else {
+      blo = ds.bucket[ds.n_buckets];
+    }
+  }
+  uint64_t ulo = blo, uhi = bhi;
+  const uint64_t lower = warp_search<false>(ds, pat, p, blo, bhi, ulo, uhi);
   ulo = max(ulo, lower);
   uint64_t d0 = 0, d1 = 0;
   const uint64_t upper = warp_search<true>(ds, pat, p, ulo, uhi, d0, d1);

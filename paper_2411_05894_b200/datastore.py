@@ -90,6 +90,7 @@ class Datastore:
         self.vocab_size = vocab_size
         self._np_tokens: np.ndarray | None = None
         self._np_sa: np.ndarray | None = None
+        self._bucket: torch.Tensor | None = None
 
     # -- reference-compatible views -------------------------------------------------
     @property
@@ -117,8 +118,22 @@ class Datastore:
         check(lib().sssd_rows_sa64(ptr(self._rows), self.n_rows, ptr(out), stream_ptr(self.device)))
         return out
 
+    # first-token index over the (local) suffix rows: narrows every range search
+    # to the rows starting with the pattern's first token (same bounds)
+    MAX_BUCKETS = 1 << 22
+
+    def bucket(self) -> torch.Tensor:
+        if self._bucket is None:
+            nb = min(int(self.vocab_size) if self.vocab_size else 65536, self.MAX_BUCKETS)
+            self._bucket = torch.empty(nb + 1, dtype=torch.int32, device=self.device)
+            check(lib().sssd_bucket_build(ptr(self._rows), self.n_rows, nb, ptr(self._bucket),
+                                          stream_ptr(self.device)))
+        return self._bucket
+
     def c_view(self) -> _lib.Ds:
-        return _lib.Ds(ptr(self._rows), ptr(self._tok), self._n_tokens, self.rank_base, self.n_rows)
+        bk = self.bucket() if self.n_rows > 0 else None
+        return _lib.Ds(ptr(self._rows), ptr(self._tok), self._n_tokens, self.rank_base, self.n_rows,
+                       ptr(bk) if bk is not None else None, (bk.numel() - 1) if bk is not None else 0)
 
     @property
     def rows(self) -> torch.Tensor:

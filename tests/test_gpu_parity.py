@@ -327,3 +327,22 @@ def test_level_synchronous_fusion_small_alphabets(monkeypatch):
         fb = ls.propose_host(ctxs)
         for x, y in zip(fa, fb):
             assert (x.tokens, x.parents, x.depths) == (y.tokens, y.parents, y.depths), trial
+
+
+def test_first_token_bucket_index():
+    """bucket[t] = first suffix row whose first token >= t (checked against the
+    sorted suffixes), and range searches with the index equal the oracle's
+    find_range for p = 1..6, including tokens beyond the table."""
+    rng = np.random.default_rng(17)
+    corpus = rng.integers(0, 40, 30000).astype(np.uint32)
+    ds = G.build(corpus, vocab_size=40)
+    sa = O.suffix_array(corpus)
+    first = corpus[sa]
+    bk = ds.bucket().cpu().numpy().astype(np.int64)
+    want = np.searchsorted(first, np.arange(bk.size), side="left")
+    assert np.array_equal(bk, want)
+    pats = [rng.integers(0, 45, int(rng.integers(1, 7))).tolist() for _ in range(300)]
+    pats += [corpus[i:i + k].tolist() for i, k in zip(rng.integers(0, 29990, 200), rng.integers(1, 7, 200))]
+    got = ds.find_ranges(pats)
+    for pt, g in zip(pats, got):
+        assert tuple(g) == O.find_range(corpus, sa, pt), pt
