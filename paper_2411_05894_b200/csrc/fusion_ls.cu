@@ -314,7 +314,8 @@ __device__ __noinline__ uint2 ls_generate(const LsPar par, int np, uint32_t E, L
       og = sc.orig[i];
     }
     if (lane == 31 && x + 1 < E) {
-      const int jn = parent_of(x + 1);
+      int jn = j;  // parent of x + 1: j or a later one (empty parents share offsets)
+      while (jn + 1 < np && par.off()[jn + 1] <= x + 1) ++jn;
       const SrcDesc& sn = sd[par.tbr()[jn] >> kTbBits];
       const uint32_t in = par.a()[jn] + (x + 1 - par.off()[jn]);
       if (el_len(sn.meta[in]) >= (uint32_t)d)
@@ -570,12 +571,25 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
     //    paths land in the gaps
     const uint32_t dd = (uint32_t)d << 26;
     {
-      const uint32_t u = min(nnew, (uint32_t)K);
+      uint32_t u = min(nnew, (uint32_t)K);
+      // top entries below the level's best new path keep their slots: lb of them
+      uint32_t lb = (uint32_t)t;
+      if (u > 0 && t > 0) {
+        const uint64_t f0 = L.k0()[nl[0]];
+        const uint32_t f1 = dd | L.tbr()[nl[0]];
+        uint32_t cntl = 0;
+        for (int i0 = 0; i0 < t; i0 += 32) {
+          const int i = i0 + lane;
+          cntl += __popc(__ballot_sync(SSSD_FULL, i < t && g_less(T.g0()[i], T.g1()[i], f0, f1)));
+        }
+        lb = cntl;
+        if (lb >= (uint32_t)K) u = 0;  // the top list is full of better paths: nothing enters
+      }
       for (uint32_t m = lane; m < u; m += 32) {
         const uint32_t sm = nl[m];
         const uint64_t x0 = L.k0()[sm];
         const uint32_t x1 = dd | L.tbr()[sm];
-        uint32_t lo = 0, hi = (uint32_t)t;  // top entries with G < x
+        uint32_t lo = lb, hi = (uint32_t)t;  // top entries with G < x
         while (lo < hi) {
           const uint32_t mid = (lo + hi) >> 1;
           if (g_less(T.g0()[mid], T.g1()[mid], x0, x1)) lo = mid + 1;
@@ -584,11 +598,11 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
         npos[m] = m + lo;
       }
       __syncwarp();
-      for (int c0 = ((t - 1) >> 5) << 5; c0 >= 0 && t > 0; c0 -= 32) {
+      for (int c0 = ((t - 1) >> 5) << 5; c0 >= (int)(lb & ~31u) && t > 0 && u > 0; c0 -= 32) {
         const int i = c0 + lane;
         uint64_t x0 = 0;
         uint32_t x1 = 0, xp = 0, xt = 0, xq = 0, pos = 0xffffffffu;
-        if (i < t) {
+        if (i < t && i >= (int)lb) {
           x0 = T.g0()[i];
           x1 = T.g1()[i];
           xp = T.pid()[i];
@@ -708,47 +722,73 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
     maxd = max(maxd, dv);
   }
   __syncwarp();
-  // next sibling = the next index with the same parent: inside a chunk by
-  // match_any, across chunks through a first-index-per-parent table built
-  // from the last chunk backwards (f_pos doubles as that table)
-  for (int v = lane; v < size; v += 32) f_pos[v] = -1;
-  __syncwarp();
-  for (int c0 = ((size - 1) >> 5) << 5; c0 >= 0; c0 -= 32) {
-    const int v = c0 + lane;
-    const bool ok = v >= 1 && v < size;
-    const int p = ok ? f_par[v] : -2 - lane;
-    const uint32_t mm = __match_any_sync(SSSD_FULL, p);
-    const uint32_t above = mm & ~((2u << lane) - 1u);
-    int ns = -1;
-    if (ok) ns = above ? c0 + __ffs(above) - 1 : f_pos[p];
-    __syncwarp();
-    if (ok) {
-      f_ns[v] = ns;
-      if (lane == __ffs(mm) - 1) f_pos[p] = v;  // first index with parent p so far
-    }
-    __syncwarp();
-  }
-  for (int v = lane; v < size; v += 32) f_fc[v] = f_pos[v];
-  __syncwarp();
   uint32_t* o_tok = out.tokens + (size_t)b * S;
   int32_t* o_par = out.parents + (size_t)b * S;
   int32_t* o_dep = out.depths + (size_t)b * S;
-  if (lane == 0) {  // DFS walk: first child, else next sibling of the nearest ancestor that has one
-    int v = 0, k = 0;
-    while (true) {
-      f_pos[v] = k;
+  maxd = __reduce_max_sync(SSSD_FULL, maxd);
+  if (maxd <= 8 && size <= 127) {
+    // pre-order position = rank of the node's ancestor-index path (7 bits per
+    // depth, index order = sibling insertion order, a prefix sorts first)
+    uint64_t* kk = reinterpret_cast<uint64_t*>(smem + ((20 * S + 7) & ~7));
+    for (int v = lane; v < size; v += 32) {
+      uint64_t key = 0;
+      for (int u = v; u > 0; u = f_par[u]) key |= (uint64_t)u << (7 * (8 - f_dep[u]));
+      kk[v] = key;
+    }
+    __syncwarp();
+    for (int v = lane; v < size; v += 32) {
+      const uint64_t kv = kk[v];
+      int r = 0;
+      for (int q = 0; q < size; ++q) r += kk[q] < kv ? 1 : 0;
+      f_pos[v] = r;
+    }
+    __syncwarp();
+    for (int v = lane; v < size; v += 32) {
+      const int k = f_pos[v];
       o_tok[k] = v == 0 ? root_tok[b] : T.tok()[v - 1];
       o_par[k] = v == 0 ? -1 : f_pos[f_par[v]];
       o_dep[k] = f_dep[v];
-      ++k;
-      int nx = f_fc[v];
-      if (nx < 0) {
-        int u = v;
-        while (u > 0 && f_ns[u] < 0) u = f_par[u];
-        if (u <= 0) break;
-        nx = f_ns[u];
+    }
+  } else {
+    // next sibling = the next index with the same parent: inside a chunk by
+    // match_any, across chunks through a first-index-per-parent table built
+    // from the last chunk backwards (f_pos doubles as that table)
+    for (int v = lane; v < size; v += 32) f_pos[v] = -1;
+    __syncwarp();
+    for (int c0 = ((size - 1) >> 5) << 5; c0 >= 0; c0 -= 32) {
+      const int v = c0 + lane;
+      const bool ok = v >= 1 && v < size;
+      const int p = ok ? f_par[v] : -2 - lane;
+      const uint32_t mm = __match_any_sync(SSSD_FULL, p);
+      const uint32_t above = mm & ~((2u << lane) - 1u);
+      int ns = -1;
+      if (ok) ns = above ? c0 + __ffs(above) - 1 : f_pos[p];
+      __syncwarp();
+      if (ok) {
+        f_ns[v] = ns;
+        if (lane == __ffs(mm) - 1) f_pos[p] = v;  // first index with parent p so far
       }
-      v = nx;
+      __syncwarp();
+    }
+    for (int v = lane; v < size; v += 32) f_fc[v] = f_pos[v];
+    __syncwarp();
+    if (lane == 0) {  // DFS walk: first child, else next sibling of the nearest ancestor that has one
+      int v = 0, k = 0;
+      while (true) {
+        f_pos[v] = k;
+        o_tok[k] = v == 0 ? root_tok[b] : T.tok()[v - 1];
+        o_par[k] = v == 0 ? -1 : f_pos[f_par[v]];
+        o_dep[k] = f_dep[v];
+        ++k;
+        int nx = f_fc[v];
+        if (nx < 0) {
+          int u = v;
+          while (u > 0 && f_ns[u] < 0) u = f_par[u];
+          if (u <= 0) break;
+          nx = f_ns[u];
+        }
+        v = nx;
+      }
     }
   }
   __syncwarp();
