@@ -157,15 +157,18 @@ __device__ __noinline__ void ls_sort(LsLevel L, uint32_t n) {
   // as +infinity without being stored: a comparator reaching past n is a no-op
   uint32_t N2 = 64;
   while (N2 < n) N2 <<= 1;
-  for (uint32_t kk = 2; kk <= N2; kk <<= 1) {
-    for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
+  for (uint32_t lk = 1; (1u << lk) <= N2; ++lk) {
+    const uint32_t kk = 1u << lk;
+    for (int lj = (int)lk - 1; lj >= 0; --lj) {
+      const uint32_t jj = 1u << lj;
       for (uint32_t p = lane; p < N2 / 2; p += 32) {
+        const uint32_t pb = p >> lj, pr = p & (jj - 1);
         uint32_t lo, hi;
-        if (jj == kk >> 1) {
-          lo = (p / jj) * kk + (p % jj);
-          hi = (p / jj) * kk + kk - 1 - (p % jj);
+        if (lj == (int)lk - 1) {
+          lo = (pb << lk) + pr;
+          hi = (pb << lk) + kk - 1 - pr;
         } else {
-          lo = 2 * jj * (p / jj) + (p % jj);
+          lo = (pb << (lj + 1)) + pr;
           hi = lo + jj;
         }
         if (hi >= n) continue;
@@ -299,13 +302,35 @@ __device__ __noinline__ uint2 ls_generate(const LsPar par, int np, uint32_t E, L
     }
     return lo;
   };
+  // Without empty parents every parent starting inside a chunk owns a distinct
+  // element, so the chunk's parent starts form a 32-bit head mask (one OR
+  // reduction) and an element's parent is the carried parent plus the heads
+  // at or before it; a level with empty (depth-capped) parents binary-searches.
+  bool has_empty = false;
+  for (int j0 = 0; j0 < np; j0 += 32) {
+    const int j = j0 + lane;
+    const bool em = j < np && (j + 1 < np ? par.off()[j + 1] : E) == par.off()[j];
+    has_empty |= __ballot_sync(SSSD_FULL, em) != 0;
+  }
+  int jprev = -1;  // parent of element base - 1
   for (uint32_t base = 0; base < E; base += 32) {
     const uint32_t x = base + lane;
     int j = 0;
     uint32_t i = 0, lm = 0, tk = 0, og = 0xffffffffu, th = 0;
     unsigned long long nkey = ~0ull;  // lane 31: key of element base + 32
+    if (!has_empty) {
+      const int q = jprev + 1 + lane;
+      uint32_t bit = 0;
+      if (q < np) {
+        const uint32_t st = par.off()[q] - base;
+        if (st < 32) bit = 1u << st;
+      }
+      const uint32_t heads = __reduce_or_sync(SSSD_FULL, bit);
+      j = jprev + __popc(heads & (0xffffffffu >> (31 - lane)));
+      jprev = __shfl_sync(SSSD_FULL, j, 31);
+    }
     if (x < E) {
-      j = parent_of(x);
+      if (has_empty) j = parent_of(x);
       const SrcDesc& sc = sd[par.tbr()[j] >> kTbBits];
       i = par.a()[j] + (x - par.off()[j]);
       th = (uint32_t)sc.thr;
