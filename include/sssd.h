@@ -72,6 +72,11 @@ int sssd_rows_build(const uint32_t* tokens, uint64_t n, const uint32_t* sa, uint
 int sssd_bucket_build(const uint32_t* rows, uint64_t n_rows, uint32_t n_buckets, uint32_t* bucket,
                       void* stream);
 
+/* Widen n uint16 token ids to uint32 (device to device): the compact host
+ * format of a propose_pinned batch whose vocabulary fits 16 bits, uploaded at
+ * half the PCIe bytes and widened next to the kernels that read it. */
+int sssd_widen_u16(const uint16_t* src, uint32_t* dst, int64_t n, void* stream);
+
 /* Copy the SA column of rows out as uint64 (the SSSD v1 file's `<u8` array). */
 int sssd_rows_sa64(const uint32_t* rows, uint64_t n, uint64_t* sa64_out, void* stream);
 

@@ -149,6 +149,26 @@ __global__ void bucket_build_kernel(const uint32_t* rows, uint64_t n, uint32_t n
     for (int64_t u = t + 1; u <= (int64_t)nb; ++u) bucket[u] = (uint32_t)n;
 }
 
+// u16 -> u32 token widening: 4 tokens per thread per step (8 B in, 16 B out)
+// when both pointers are suitably aligned, grid-stride, scalar tail.
+__global__ void widen_u16_kernel(const uint16_t* src, uint32_t* dst, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool vec = (reinterpret_cast<uintptr_t>(src) % 8 == 0) && (reinterpret_cast<uintptr_t>(dst) % 16 == 0);
+  int64_t done = 0;
+  if (vec) {
+    const int64_t n4 = n / 4;
+    const uint2* s4 = reinterpret_cast<const uint2*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (int64_t i = t0; i < n4; i += stride) {
+      const uint2 v = s4[i];
+      d4[i] = make_uint4(v.x & 0xffffu, v.x >> 16, v.y & 0xffffu, v.y >> 16);
+    }
+    done = n4 * 4;
+  }
+  for (int64_t i = done + t0; i < n; i += stride) dst[i] = src[i];
+}
+
 extern "C" {
 
 size_t sssd_sa_build_workspace(uint64_t n) { return sa_carve(nullptr, n ? n : 1).total; }
@@ -216,6 +236,15 @@ int sssd_bucket_build(const uint32_t* rows, uint64_t n_rows, uint32_t n_buckets,
   if (n_rows >= 0xffffffffull) return fail(SSSD_E_LIMIT, "bucket index needs < 2^32 rows");
   bucket_build_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(rows, n_rows, n_buckets, bucket);
   return cuda_check(cudaGetLastError(), "bucket_build launch");
+}
+
+int sssd_widen_u16(const uint16_t* src, uint32_t* dst, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!src || !dst))) return fail(SSSD_E_ARG, "widen_u16: bad buffers");
+  if (n == 0) return SSSD_OK;
+  const int64_t n4 = n / 4;
+  const unsigned blocks = (unsigned)min((n4 + 255) / 256 + 1, (int64_t)148 * 16);
+  widen_u16_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, dst, n);
+  return cuda_check(cudaGetLastError(), "widen_u16 launch");
 }
 
 int sssd_rows_sa64(const uint32_t* rows, uint64_t n, uint64_t* sa64_out, void* stream) {

@@ -133,9 +133,11 @@ class DraftEngine:
         return list(ms)
 
     def propose_pinned(self, seq_h: torch.Tensor, off_h: torch.Tensor, len_h: torch.Tensor, max_len: int,
-                       out_h: DraftBatch | None = None, chunks: int = 8) -> DraftBatch:
+                       out_h: DraftBatch | None = None, chunks: int = 6) -> DraftBatch:
         """Host-buffer entry point for a large batch: contexts in pinned host
-        memory (seq_h int32, off_h int64 [B], len_h int32 [B], CPU tensors),
+        memory (seq_h int32 = u32 token ids, or int16 = u16 token ids when the
+        vocabulary fits 16 bits: half the upload bytes, widened on the device by
+        ``sssd_widen_u16``; off_h int64 [B], len_h int32 [B], CPU tensors),
         drafts returned in pinned host tensors (``out_h``, allocated if None —
         pass it back in to reuse the pinned buffers).
 
@@ -167,6 +169,11 @@ class DraftEngine:
         st = getattr(self, "_pin", None)
         if st is None:
             st = self._pin = {"streams": [torch.cuda.Stream(dev) for _ in range(4)], "key": None, "ws_key": None}
+        narrow = seq_h.dtype == torch.int16
+        if not narrow and seq_h.dtype != torch.int32:
+            raise ValueError("seq_h must be int32 (u32 tokens) or int16 (u16 tokens)")
+        if narrow and (st.get("seq16") is None or st["seq16"].numel() < n_tok):
+            st["seq16"] = torch.empty(n_tok, dtype=torch.int16, device=dev)
         if st["key"] != (n_tok, B):
             st["seq"] = torch.empty(n_tok, dtype=torch.int32, device=dev)
             st["off"] = torch.empty(B, dtype=torch.int64, device=dev)
@@ -194,14 +201,22 @@ class DraftEngine:
                 r0, r1 = cuts[c], cuts[c + 1]
                 t0 = int(offs[r0:r1].min())
                 t1 = int((offs[r0:r1] + lens[r0:r1]).max())
-                seq_d[t0:t1].copy_(seq_h[t0:t1], non_blocking=True)
+                if narrow:
+                    st["seq16"][t0:t1].copy_(seq_h[t0:t1], non_blocking=True)
+                else:
+                    seq_d[t0:t1].copy_(seq_h[t0:t1], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(up)
-                uploaded.append(ev)
+                uploaded.append((ev, t0, t1))
         for c in range(chunks):
             r0, r1 = cuts[c], cuts[c + 1]
             cs = comp[c & 1]
-            cs.wait_event(uploaded[c])
+            ev_up, t0, t1 = uploaded[c]
+            cs.wait_event(ev_up)
+            if narrow:
+                s16 = st["seq16"]
+                check(lib().sssd_widen_u16(s16.data_ptr() + 2 * t0, seq_d.data_ptr() + 4 * t0, t1 - t0,
+                                           cs.cuda_stream))
             view = DraftBatch(out.size[r0:r1], out.tokens[r0:r1], out.parents[r0:r1], out.depths[r0:r1],
                               out.mask[r0:r1])
             with torch.cuda.stream(cs):

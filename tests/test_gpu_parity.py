@@ -253,8 +253,9 @@ def test_propose_pinned_equals_resident_propose():
     want = eng.propose(seq_h.cuda(), off_h.cuda(), len_h.cuda(), mx)
     want = {k: getattr(want, k).cpu().clone() for k in ("size", "tokens", "parents", "depths", "mask")}
     eng.check_status()
-    for chunks in (1, 3, 8):
-        got = eng.propose_pinned(seq_h, off_h, len_h, mx, chunks=chunks)
+    seq16_h = torch.from_numpy(seq_h.numpy().astype(np.uint16).view(np.int16)).pin_memory()  # vocab 500 < 2^16
+    for chunks, src in ((1, seq_h), (3, seq_h), (8, seq_h), (3, seq16_h), (8, seq16_h)):
+        got = eng.propose_pinned(src, off_h, len_h, mx, chunks=chunks)
         for k, v in want.items():
             g = getattr(got, k)
             assert not g.is_cuda and g.is_pinned()

@@ -13,7 +13,9 @@ ds = G.build(corpus, vocab_size=V)
 eng = G.DraftEngine(ds, G.FusionConfig(dec_len=64))
 stream = workload.phrase_stream(B * CTX, V, workload.HELDOUT_SEED)
 ctx_h = torch.from_numpy(stream.view(np.int32)).pin_memory()
+ctx16_h = torch.from_numpy(stream.astype(np.uint16).view(np.int16)).pin_memory()
 seq = ctx_h.cuda()
+seq16 = ctx16_h.cuda()
 off_h = torch.arange(B, dtype=torch.int64) * CTX
 len_h = torch.full((B,), CTX, dtype=torch.int32)
 off, ln = off_h.cuda(), len_h.cuda()
@@ -32,18 +34,21 @@ def timed(fn, n=5):
 
 
 print("h2d 134MB", timed(lambda: seq.copy_(ctx_h, non_blocking=True)))
+print("h2d 67MB u16", timed(lambda: seq16.copy_(ctx16_h, non_blocking=True)))
 print("propose resident", timed(lambda: eng.propose(seq, off, ln, CTX)))
 out_h = eng.propose_pinned(ctx_h, off_h, len_h, CTX)  # pinned outputs reused below
 for c in (1, 2, 4, 8, 16, 32):
     print("pinned chunks", c, timed(lambda: eng.propose_pinned(ctx_h, off_h, len_h, CTX, out_h=out_h, chunks=c)))
+for c in (1, 2, 3, 4, 6, 8, 16):
+    print("pinned u16 chunks", c, timed(lambda: eng.propose_pinned(ctx16_h, off_h, len_h, CTX, out_h=out_h, chunks=c)))
 
 # stream timeline of the pipelined call (chrome trace -> gpurun_out/)
 from torch.profiler import ProfilerActivity, profile
 out_h = eng.propose_pinned(ctx_h, off_h, len_h, CTX, chunks=4)
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
-    for c in (8,):
-        eng.propose_pinned(ctx_h, off_h, len_h, CTX, out_h=out_h, chunks=c)
+    for c in (4,):
+        eng.propose_pinned(ctx16_h, off_h, len_h, CTX, out_h=out_h, chunks=c)
         torch.cuda.synchronize()
 os.makedirs("gpurun_out", exist_ok=True)
 prof.export_chrome_trace("gpurun_out/e2e_trace.json")
