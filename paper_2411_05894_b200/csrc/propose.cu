@@ -556,31 +556,58 @@ __global__ void __launch_bounds__(256)
   sssd_elem* out = sorted + (size_t)b * cap;
   if (total == 0) return;
   __syncthreads();
-  if (total <= (int)blockDim.x && total * (c.IBL + 2) <= kSortSmem) {
+  if (total <= (int)blockDim.x && total * (c.IBL + 6) <= kSortSmem) {
     // the common case (<= 256 occurrences): continuation strings staged in
     // shared memory; warp w rank-sorts occurrences [32w, 32w + 32), then each
     // occurrence adds, per other run, a binary-searched count of the run's
-    // smaller strings (ties: position order, i.e. run order)
-    uint32_t* str = s_idx;  // [total][IBL] strings, [total] lengths, [total] run-sorted indices
+    // smaller strings (ties: position order, i.e. run order).  When every
+    // token is < 65535 and IBL <= 8, a string is compared as one 128-bit key
+    // (16 bits of token + 1 per depth; an absent token is 0, so a proper
+    // prefix sorts first, as cmp_str orders them).
+    uint32_t* str = s_idx;  // [total][IBL] strings, [total] lengths, [total] run-sorted indices, keys
     uint32_t* slen = s_idx + total * c.IBL;
     uint32_t* srt = slen + total;
+    uint64_t* kh = reinterpret_cast<uint64_t*>(s_idx + ((total * (c.IBL + 2) + 1) & ~1));
+    uint64_t* kl = kh + total;
     sssd_elem me{};
     uint32_t ml = 0;
     const uint32_t* mine = str + tid * c.IBL;
+    bool wide = false;
     if (tid < total) {
       me = r[tid];
       ml = el_len(me.len_m);
       slen[tid] = ml;
-      for (uint32_t d = 0; d < ml; ++d) str[tid * c.IBL + d] = seq[me.off + d];
+      for (uint32_t d = 0; d < ml; ++d) {
+        const uint32_t tk = seq[me.off + d];
+        str[tid * c.IBL + d] = tk;
+        wide |= tk >= 65535u;
+      }
     }
-    __syncthreads();
+    const bool packed = !__syncthreads_or(wide || c.IBL > 8);
+    uint64_t mh = 0, mlo = 0;
+    if (packed && tid < total) {
+      for (uint32_t d = 0; d < ml; ++d) {
+        const uint64_t v = (uint64_t)(mine[d] + 1);
+        if (d < 4) mh |= v << (16 * (3 - d));
+        else mlo |= v << (16 * (7 - d));
+      }
+      kh[tid] = mh;
+      kl[tid] = mlo;
+    }
+    if (packed) __syncthreads();
+    // does occurrence j sort before mine?  (q_before: j's run precedes mine on ties)
+    auto before = [&](uint32_t j, bool q_before) {
+      if (packed) {
+        const uint64_t h = kh[j], l = kl[j];
+        return h < mh || (h == mh && (l < mlo || (l == mlo && q_before)));
+      }
+      const int cr = cmp_str(str + j * c.IBL, slen[j], mine, ml);
+      return cr < 0 || (cr == 0 && q_before);
+    };
     const int r0 = warp * 32, rn = min(32, total - r0);
     int lr = 0;
     if (tid < total) {
-      for (int jj = r0; jj < r0 + rn; ++jj) {
-        const int cr = cmp_str(str + jj * c.IBL, slen[jj], mine, ml);
-        lr += (cr < 0 || (cr == 0 && jj < tid)) ? 1 : 0;
-      }
+      for (int jj = r0; jj < r0 + rn; ++jj) lr += before((uint32_t)jj, jj < tid) ? 1 : 0;
       srt[r0 + lr] = (uint32_t)tid;
     }
     __syncthreads();
@@ -592,9 +619,7 @@ __global__ void __launch_bounds__(256)
         int lo = 0, hi = qn;  // elements of run q that sort before mine
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;
-          const uint32_t x = srt[q0 + mid];
-          const int cr = cmp_str(str + x * c.IBL, slen[x], mine, ml);
-          if (cr < 0 || (cr == 0 && q0 < r0)) lo = mid + 1;
+          if (before(srt[q0 + mid], q0 < r0)) lo = mid + 1;
           else hi = mid;
         }
         rank += lo;

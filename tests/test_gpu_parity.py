@@ -347,3 +347,21 @@ def test_first_token_bucket_index():
     got = ds.find_ranges(pats)
     for pt, g in zip(pats, got):
         assert tuple(g) == O.find_range(corpus, sa, pt), pt
+
+
+@pytest.mark.parametrize("ibl", [4, 12])
+def test_propose_large_token_ids(ibl):
+    """Token ids >= 65535 (and input_branch_len > 8) take the string-compare
+    path of the input-scan sort instead of packed 16-bit keys; drafts stay
+    bit-exact against the oracle."""
+    rng = np.random.default_rng(23)
+    alphabet = np.array([3, 7, 65534, 65535, 70000, 4_000_000_000], dtype=np.uint32)
+    corpus = alphabet[rng.integers(0, alphabet.size, 30000)]
+    store = O.Store(corpus, O.suffix_array(corpus))
+    cfg = G.FusionConfig(dec_len=40, input_branch_len=ibl)
+    ctxs = [alphabet[rng.integers(0, alphabet.size, int(rng.integers(50, 600)))].tolist() for _ in range(40)]
+    flats = G.DraftEngine(G.build(corpus), cfg).propose_host(ctxs)
+    oc = O.Cfg(dec_len=40, input_branch_len=ibl)
+    for f, ctx in zip(flats, ctxs):
+        d = O.propose(store, ctx, oc)
+        assert (f.tokens, f.parents, f.depths) == (d.tokens, d.parents, d.depths)
