@@ -168,7 +168,7 @@ static PropWs carve_propose(uint8_t* base, const sssd_cfg* c, int B, int max_len
   const bool sep = c->has_separator != 0;
   w.ds_idx_cap = ds_idx_cap(c->P, c->M);
   w.ds_raw = cv.take<sssd_elem>(sep ? (size_t)B * PM : 1);
-  w.ds_idx = cv.take<uint32_t>(sep && w.ds_idx_cap > 4096 ? (size_t)B * w.ds_idx_cap : 1);
+  w.ds_idx = cv.take<uint32_t>(sep && w.ds_idx_cap > ds_lookup_smem_words(c->P, c->M) ? (size_t)B * w.ds_idx_cap : 1);
   w.cap = max_len > 1 ? max_len : 1;
   int64_t p2 = 1;
   while (p2 < w.cap) p2 <<= 1;
@@ -393,7 +393,7 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
     KCfg kk = k;
     kk.b0 = b0;
     kk.b1 = b1;
-    ds_lookup_kernel<<<b1 - b0, 32 * cfg->P, 0, s>>>(*ds, *seqs, kk, w.ds_tab, w.ds_len, w.ds_el, w.ds_n, lk,
+    ds_lookup_kernel<<<b1 - b0, 32 * cfg->P, 4 * ds_lookup_smem_words(cfg->P, cfg->M), s>>>(*ds, *seqs, kk, w.ds_tab, w.ds_len, w.ds_el, w.ds_n, lk,
                                                        w.ds_raw, w.ds_idx, w.ds_idx_cap, w.ds_cols, pre_bounds,
                                                        pre_rows);
   };
@@ -545,7 +545,7 @@ int sssd_ds_lookup(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg
   sssd_elem* raw = static_cast<sssd_elem*>(workspace);
   uint32_t* idx = reinterpret_cast<uint32_t*>(
       align_up(reinterpret_cast<uintptr_t>(raw + (size_t)seqs->B * cfg->P * cfg->M), 256));
-  ds_lookup_kernel<<<seqs->B, 32 * cfg->P, 0, static_cast<cudaStream_t>(stream)>>>(
+  ds_lookup_kernel<<<seqs->B, 32 * cfg->P, 4 * ds_lookup_smem_words(cfg->P, cfg->M), static_cast<cudaStream_t>(stream)>>>(
       *ds, *seqs, kcfg(cfg), tab, lens, el, n_el, lk, raw, idx, ds_idx_cap(cfg->P, cfg->M), Cols{}, nullptr,
       nullptr);
   return cuda_check(cudaGetLastError(), "ds_lookup_kernel launch");

@@ -218,7 +218,6 @@ __device__ void block_sort_elems(const sssd_elem* src, sssd_elem* dst, const uin
 // K2+K3: datastore lookup (ref datastore.py:156-218, A.3 phase-split form)
 // --------------------------------------------------------------------------
 
-constexpr int kRowStride = 16;  // u32 per staged row in smem
 
 // Gather the sampled continuations of prefix length p into this request's
 // string table (non-empty ones compacted, SA order kept).  Returns the count.
@@ -274,7 +273,10 @@ __device__ int gather_p(const sssd_ds& ds, const KCfg& c, int p, uint64_t lo, ui
   return cnt;
 }
 
-__global__ void __launch_bounds__(32 * SSSD_MAX_P)
+#ifndef SSSD_LOOKUP_MINB
+#define SSSD_LOOKUP_MINB 8  // 32 registers: 16 resident 128-thread CTAs per SM (measured best)
+#endif
+__global__ void __launch_bounds__(32 * SSSD_MAX_P, SSSD_LOOKUP_MINB)
     ds_lookup_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, uint32_t* ds_tab, uint8_t* ds_len,
                      sssd_elem* ds_el, int32_t* ds_n, sssd_lookup_out lk, sssd_elem* ds_raw,
                      uint32_t* ds_idx, int64_t idx_cap, Cols cols, const int64_t* pre_bounds,
@@ -284,7 +286,7 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P)
   __shared__ uint32_t s_pat[SSSD_MAX_P];
   __shared__ uint64_t s_lo[SSSD_MAX_P], s_hi[SSSD_MAX_P];
   __shared__ int s_cnt[SSSD_MAX_P];
-  __shared__ __align__(16) uint32_t s_rows[SSSD_MAX_P * 32 * kRowStride];
+  extern __shared__ __align__(16) uint32_t s_rows[];  // ds_lookup_smem_words(P, M) words
 
   const int L = seqs.seq_len[b];
   const uint32_t* seq = seqs.seq + seqs.seq_off[b];
@@ -377,7 +379,9 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P)
     int n = 0;
     for (int q = pcut; q <= pmax; ++q) n += s_cnt[q - 1];
     if (n > 0) {
-      uint32_t* idx = (n <= SSSD_MAX_P * 32 * kRowStride) ? s_rows : ds_idx + (size_t)b * idx_cap;
+      int n2 = 1;
+      while (n2 < n) n2 <<= 1;
+      uint32_t* idx = (n2 <= ds_lookup_smem_words(c.P, c.M)) ? s_rows : ds_idx + (size_t)b * idx_cap;
       sssd_elem* sorted = ds_el + (size_t)b * c.P * c.M;
       block_sort_elems(raw, sorted, tab, n, idx);
       if (cols.meta) {

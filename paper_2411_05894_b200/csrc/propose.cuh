@@ -29,10 +29,18 @@ __global__ void shard_search_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, int64_t*
 __global__ void shard_gather_kernel(sssd_ds ds, KCfg c, int B, const int64_t* gbounds, uint32_t* xrows);
 
 // scratch of the datastore lookup when a separator forces a block sort
-inline int64_t ds_idx_cap(int P, int M) {
+__host__ __device__ inline int64_t ds_idx_cap(int P, int M) {
   int64_t n = (int64_t)P * M, p2 = 1;
   while (p2 < n) p2 <<= 1;
   return p2;
+}
+constexpr int kRowStride = 16;  // u32 per staged suffix row in shared memory
+// dynamic shared memory of ds_lookup_kernel (u32 words): one staged row per
+// thread, and room for the separator sort's index array up to 4096 entries
+__host__ __device__ inline int ds_lookup_smem_words(int P, int M) {
+  const int64_t cap = ds_idx_cap(P, M);
+  const int rows = P * 32 * kRowStride;
+  return rows > (cap < 4096 ? (int)cap : 4096) ? rows : (cap < 4096 ? (int)cap : 4096);
 }
 __global__ void input_scan_kernel(sssd_seqs seqs, KCfg c, sssd_elem* raw, sssd_elem* sorted,
                                   int32_t* in_n, uint32_t* idx_ws, int64_t cap, int64_t cap2,
