@@ -288,8 +288,9 @@ __device__ __noinline__ uint2 ls_generate(const LsPar par, int np, uint32_t E, L
     }
     nb += __popc(km);
   };
-  // A run may continue into the next 32-element chunk: lane 31 peeks at the
-  // next element, so every run is emitted once, by its last lane, with the
+  // Chunks of 32 lanes advance by 31 elements: lane 31 holds the next chunk's
+  // first element as a look-ahead, so a run reaching lane 30 knows whether it
+  // continues; every run is emitted once, by its last owned lane, with the
   // count / first / start carried in from earlier chunks.
   bool c_open = false;
   uint32_t c_cnt = 0, c_first = 0, c_start = 0;
@@ -313,11 +314,12 @@ __device__ __noinline__ uint2 ls_generate(const LsPar par, int np, uint32_t E, L
     has_empty |= __ballot_sync(SSSD_FULL, em) != 0;
   }
   int jprev = -1;  // parent of element base - 1
-  for (uint32_t base = 0; base < E; base += 32) {
+  for (uint32_t base = 0; base < E; base += 31) {
     const uint32_t x = base + lane;
+    const bool last = base + 32 >= E;  // no look-ahead: lane 31 (if any) is the final element
+    const bool owned = x < E && (lane < 31 || last);
     int j = 0;
     uint32_t i = 0, lm = 0, tk = 0, og = 0xffffffffu, th = 0;
-    unsigned long long nkey = ~0ull;  // lane 31: key of element base + 32
     if (!has_empty) {
       const int q = jprev + 1 + lane;
       uint32_t bit = 0;
@@ -327,7 +329,6 @@ __device__ __noinline__ uint2 ls_generate(const LsPar par, int np, uint32_t E, L
       }
       const uint32_t heads = __reduce_or_sync(SSSD_FULL, bit);
       j = jprev + __popc(heads & (0xffffffffu >> (31 - lane)));
-      jprev = __shfl_sync(SSSD_FULL, j, 31);
     }
     if (x < E) {
       if (has_empty) j = parent_of(x);
@@ -338,48 +339,40 @@ __device__ __noinline__ uint2 ls_generate(const LsPar par, int np, uint32_t E, L
       tk = sc.tok[(int64_t)(d - 1) * sc.stride + i];
       og = sc.orig[i];
     }
-    if (lane == 31 && x + 1 < E) {
-      int jn = j;  // parent of x + 1: j or a later one (empty parents share offsets)
-      while (jn + 1 < np && par.off()[jn + 1] <= x + 1) ++jn;
-      const SrcDesc& sn = sd[par.tbr()[jn] >> kTbBits];
-      const uint32_t in = par.a()[jn] + (x + 1 - par.off()[jn]);
-      if (el_len(sn.meta[in]) >= (uint32_t)d)
-        nkey = (unsigned long long)jn << 32 | sn.tok[(int64_t)(d - 1) * sn.stride + in];
-    }
+    jprev = __shfl_sync(SSSD_FULL, j, 30);
     const bool has = x < E && el_len(lm) >= (uint32_t)d;
-    const bool w = has && el_m(lm) >= th;
+    const bool w = owned && has && el_m(lm) >= th;
     const uint32_t orig = w ? og : 0xffffffffu;
     const uint32_t hasm = __ballot_sync(SSSD_FULL, has);
-    if (!hasm) {  // (a carried run always continues at lane 0, so none is open here)
-      continue;
-    }
-    const unsigned long long key = has ? ((unsigned long long)j << 32 | tk) : (1ull << 63 | (unsigned)lane);
-    const uint32_t gm = __match_any_sync(SSSD_FULL, key);
-    const uint32_t wm = __ballot_sync(SSSD_FULL, w);
-    const int lo_l = __ffs(gm) - 1, hi_l = 31 - __clz(gm);
-    uint32_t fm = orig;  // run minimum of orig (segmented down-scan; runs are lane intervals)
+    if (hasm) {  // (a carried run always continues at lane 0, so none is open otherwise)
+      const unsigned long long key = has ? ((unsigned long long)j << 32 | tk) : (1ull << 63 | (unsigned)lane);
+      const uint32_t gm = __match_any_sync(SSSD_FULL, key);
+      const uint32_t wm = __ballot_sync(SSSD_FULL, w);
+      const int lo_l = __ffs(gm) - 1, hi_l = 31 - __clz(gm);
+      uint32_t fm = orig;  // run minimum of orig (segmented down-scan; runs are lane intervals)
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_down_sync(SSSD_FULL, fm, o);
-      if (lane + o <= hi_l) fm = min(fm, y);
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_down_sync(SSSD_FULL, fm, o);
+        if (lane + o <= hi_l) fm = min(fm, y);
+      }
+      fm = __shfl_sync(SSSD_FULL, fm, lo_l);
+      uint32_t cnt = __popc(gm & wm);
+      uint32_t start = i - (uint32_t)(lane - lo_l);
+      if (c_open && lo_l == 0) {  // the run carried in from the previous chunk
+        cnt += c_cnt;
+        fm = min(fm, c_first);
+        start = c_start;
+      }
+      const bool to_next = !last && has && (gm >> 31) != 0;  // my run reaches the look-ahead
+      emit(owned && has && lane == hi_l && !to_next, j, tk, cnt, fm, start, i + 1);
+      c_open = __ballot_sync(SSSD_FULL, lane == 30 && to_next) != 0;
+      if (c_open) {
+        c_cnt = __shfl_sync(SSSD_FULL, cnt, 30);
+        c_first = __shfl_sync(SSSD_FULL, fm, 30);
+        c_start = __shfl_sync(SSSD_FULL, start, 30);
+      }
     }
-    fm = __shfl_sync(SSSD_FULL, fm, lo_l);
-    uint32_t cnt = __popc(gm & wm);
-    uint32_t start = i - (uint32_t)(lane - lo_l);
-    if (c_open && lo_l == 0) {  // the run carried in from the previous chunk
-      cnt += c_cnt;
-      fm = min(fm, c_first);
-      start = c_start;
-    }
-    const bool cont = lane == 31 && has && nkey == key;
-    emit(has && lane == hi_l && !cont, j, tk, cnt, fm, start, i + 1);
-    const uint32_t cm = __ballot_sync(SSSD_FULL, cont);
-    c_open = cm != 0;
-    if (c_open) {
-      c_cnt = __shfl_sync(SSSD_FULL, cnt, 31);
-      c_first = __shfl_sync(SSSD_FULL, fm, 31);
-      c_start = __shfl_sync(SSSD_FULL, start, 31);
-    }
+    if (last) break;
   }
   __syncwarp();
   return make_uint2(nb, n);
