@@ -603,20 +603,34 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
         lb = cntl;
         if (lb >= (uint32_t)K) u = 0;  // the top list is full of better paths: nothing enters
       }
-      for (uint32_t m = lane; m < u; m += 32) {
-        const uint32_t sm = nl[m];
-        const uint64_t x0 = L.k0()[sm];
-        const uint32_t x1 = dd | L.tbr()[sm];
-        uint32_t lo = lb, hi = (uint32_t)t;  // top entries with G < x
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (g_less(T.g0()[mid], T.g1()[mid], x0, x1)) lo = mid + 1;
-          else hi = mid;
+      // slots of the new paths against the old list; they increase with m, so
+      // the paths that land inside the list (slot < K) are a prefix of ue
+      uint32_t ue = 0;
+      for (uint32_t m0 = 0; m0 < u; m0 += 32) {
+        const uint32_t m = m0 + lane;
+        uint32_t slot = 0xffffffffu;
+        if (m < u) {
+          const uint32_t sm = nl[m];
+          const uint64_t x0 = L.k0()[sm];
+          const uint32_t x1 = dd | L.tbr()[sm];
+          uint32_t lo = lb, hi = (uint32_t)t;  // top entries with G < x
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (g_less(T.g0()[mid], T.g1()[mid], x0, x1)) lo = mid + 1;
+            else hi = mid;
+          }
+          slot = m + lo;
+          npos[m] = slot;
         }
-        npos[m] = m + lo;
+        const uint32_t okm = __ballot_sync(SSSD_FULL, slot < (uint32_t)K);
+        ue += __popc(okm);
+        if (okm != SSSD_FULL) break;
       }
       __syncwarp();
-      for (int c0 = ((t - 1) >> 5) << 5; c0 >= (int)(lb & ~31u) && t > 0 && u > 0; c0 -= 32) {
+      // an old entry i moves up by the landing new paths that precede it:
+      // #{m < ue : npos[m] - m <= i} (non-decreasing in m); entries pushed past
+      // K drop out.  Chunks go from the end so no unread entry is overwritten.
+      for (int c0 = ((t - 1) >> 5) << 5; c0 >= (int)(lb & ~31u) && t > 0 && ue > 0; c0 -= 32) {
         const int i = c0 + lane;
         uint64_t x0 = 0;
         uint32_t x1 = 0, xp = 0, xt = 0, xq = 0, pos = 0xffffffffu;
@@ -626,10 +640,10 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
           xp = T.pid()[i];
           xt = T.tok()[i];
           xq = T.ppid()[i];
-          uint32_t lo = 0, hi = u;  // new paths with G < x
+          uint32_t lo = 0, hi = ue;
           while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1, sm = nl[mid];
-            if (g_less(L.k0()[sm], dd | L.tbr()[sm], x0, x1)) lo = mid + 1;
+            const uint32_t mid = (lo + hi) >> 1;
+            if (npos[mid] - mid <= (uint32_t)i) lo = mid + 1;
             else hi = mid;
           }
           pos = (uint32_t)i + lo;
@@ -644,16 +658,13 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
         }
         __syncwarp();
       }
-      for (uint32_t m = lane; m < u; m += 32) {
-        const uint32_t pos = npos[m];
-        if (pos < (uint32_t)K) {
-          const uint32_t sm = nl[m], g = L.ord()[sm];
-          T.g0()[pos] = L.k0()[sm];
-          T.g1()[pos] = dd | L.tbr()[sm];
-          T.pid()[pos] = L.pid()[sm];
-          T.tok()[pos] = L.tok()[g];
-          T.ppid()[pos] = L.ppid()[g];
-        }
+      for (uint32_t m = lane; m < ue; m += 32) {
+        const uint32_t pos = npos[m], sm = nl[m], g = L.ord()[sm];
+        T.g0()[pos] = L.k0()[sm];
+        T.g1()[pos] = dd | L.tbr()[sm];
+        T.pid()[pos] = L.pid()[sm];
+        T.tok()[pos] = L.tok()[g];
+        T.ppid()[pos] = L.ppid()[g];
       }
       t = min(K, t + (int)u);
       __syncwarp();
