@@ -35,7 +35,9 @@ def phrase_stream(n: int, vocab: int, seed: int, n_phrases: int = 20000,
     rng = np.random.default_rng(seed)
     out = np.empty(n, dtype=np.uint32)
     filled = 0
-    block = max(4096, int(n / float(lens.mean()) * 1.05) + 64)
+    # (phrases per block capped so a 1B-token stream stays within a few GB of
+    # host memory; streams up to ~100M tokens are one block, as before)
+    block = min(max(4096, int(n / float(lens.mean()) * 1.05) + 64), 6_000_000)
     while filled < n:
         ids = (rng.zipf(1.1, block) - 1) % n_phrases
         ln = lens[ids]
@@ -49,8 +51,14 @@ def phrase_stream(n: int, vocab: int, seed: int, n_phrases: int = 20000,
         take = min(total, n - filled)
         out[filled:filled + take] = seg[:take]
         filled += take
-    mask = rng.random(n) < noise
-    out[mask] = rng.integers(0, vocab, int(mask.sum())).astype(np.uint32)
+    if n <= 1 << 27:
+        mask = rng.random(n) < noise
+        out[mask] = rng.integers(0, vocab, int(mask.sum())).astype(np.uint32)
+    else:  # chunked noise for very long streams (host memory)
+        for a in range(0, n, 1 << 26):
+            seg = out[a:a + (1 << 26)]
+            mask = rng.random(seg.size) < noise
+            seg[mask] = rng.integers(0, vocab, int(mask.sum())).astype(np.uint32)
     return out
 
 
