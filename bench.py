@@ -337,6 +337,10 @@ def run_ours(args) -> None:
         except Exception as exc:  # report, never hide
             extra["verify_attention"] = {"error": repr(exc)}
         try:
+            extra["lookup_cfg4"] = bench_lookup_cfg4(ds, corpus)
+        except Exception as exc:
+            extra["lookup_cfg4"] = {"error": repr(exc)}
+        try:
             extra["decode_cfg1"] = bench_decode_cfg1()
         except Exception as exc:
             extra["decode_cfg1"] = {"error": repr(exc)}
@@ -421,6 +425,56 @@ def bench_verify(peak: float, peak_tf: float) -> dict:
                      "achieved_TFLOPs": round(fl / ms / 1e9, 1), "tensor_frac": round(fl / ms / 1e9 / peak_tf, 4)}
         del q, k, v
     return out
+
+
+def bench_lookup_cfg4(ds, corpus) -> dict:
+    """cfg4 (BASELINE configs[3]): long-context RAG shape, B=8, ctx 32k,
+    dec_len 16, prompt-heavy contexts (40 spans of 8-64 tokens copied from the
+    first half into the second) against the cfg2 datastore:
+    B=8 propose latency, throughput over 256 such batches, bit-exactness of
+    two requests against the CPU oracle and the oracle's time per lookup."""
+    import torch
+
+    import paper_2411_05894_b200 as G
+    from oracle import sssd_oracle as O
+    from paper_2411_05894_b200 import workload
+
+    Bq, L, R = 8, 32768, 256
+    ctxs = workload.prompt_heavy_contexts(Bq * R, L, VOCAB)
+    flat = np.concatenate(ctxs).astype(np.uint32)
+    seq = torch.from_numpy(flat.view(np.int32)).cuda()
+    off = (torch.arange(Bq * R, dtype=torch.int64) * L).cuda()
+    ln = torch.full((Bq * R,), L, dtype=torch.int32, device="cuda")
+    eng = G.DraftEngine(ds, G.FusionConfig(dec_len=16))
+    for _ in range(3):
+        eng.propose(seq, off, ln, L)
+        eng.propose(seq, off[:Bq], ln[:Bq], L)
+    torch.cuda.synchronize()
+    eng.check_status()
+
+    def timed(fn, n):
+        ts = []
+        for _ in range(n):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return float(np.median(ts))
+
+    lat = timed(lambda: eng.propose(seq, off[:Bq], ln[:Bq], L), 20)
+    thr = timed(lambda: eng.propose(seq, off, ln, L), 5)
+    got = eng.propose_host([c.tolist() for c in ctxs[:2]])
+    store = O.Store(corpus, ds.suffix_index)
+    t0 = time.perf_counter()
+    want = [O.propose(store, c.tolist(), O.Cfg(dec_len=16)) for c in ctxs[:2]]
+    cpu_s = (time.perf_counter() - t0) / 2
+    exact = all((g.tokens, g.parents, g.depths) == (w.tokens, w.parents, w.depths) for g, w in zip(got, want))
+    return {"workload": "cfg4: B=8, ctx 32768 prompt-heavy, dec_len 16, 100M-token datastore",
+            "b8_latency_ms": round(lat, 4), "b8_lookups_per_s": round(Bq / lat * 1e3, 1),
+            "throughput_lookups_per_s": round(Bq * R / thr * 1e3, 1), "throughput_requests": Bq * R,
+            "drafts_bitexact_vs_cpu_oracle": exact, "cpu_oracle_s_per_lookup": round(cpu_s, 3)}
 
 
 def bench_decode_cfg1(budget_s: float = 60.0) -> dict:
