@@ -247,6 +247,11 @@ __global__ void merge_setup_kernel(Cols cols, const int64_t* el_off, const int32
   }
 }
 
+static int input_scan_attr(int ibl) {
+  return cuda_check(cudaFuncSetAttribute(input_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         input_scan_smem_bytes(1024, ibl)), "input_scan_kernel smem attribute");
+}
+
 static int fusion_smem_attr(const KCfg& k) {
   if (k.fusion == 1)
     return cuda_check(cudaFuncSetAttribute(draft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -388,6 +393,7 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
   if (lookup) lk = *lookup;
   if ((rc = cuda_check(cudaMemsetAsync(w.d.cursor, 0, 16 + 512, st), "memset status"))) return rc;
   if ((rc = fusion_smem_attr(k))) return rc;
+  if ((rc = input_scan_attr(cfg->input_branch_len))) return rc;
 
   auto launch_lookup = [&](cudaStream_t s, int b0, int b1) {
     KCfg kk = k;
@@ -401,7 +407,9 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
     KCfg kk = k;
     kk.b0 = b0;
     kk.b1 = b1;
-    input_scan_kernel<<<b1 - b0, 256, 0, s>>>(*seqs, kk, w.in_raw, w.in_el, w.in_n, w.idx, w.cap, w.cap2,
+    const int th = input_scan_threads(seqs->max_len);
+    input_scan_kernel<<<b1 - b0, th, input_scan_smem_bytes(th, cfg->input_branch_len), s>>>(
+        *seqs, kk, w.in_raw, w.in_el, w.in_n, w.idx, w.cap, w.cap2,
                                                w.in_cols);
   };
   auto launch_fuse = [&](cudaStream_t s, int b0, int b1) {
@@ -574,7 +582,10 @@ int sssd_input_scan(const sssd_seqs* seqs, const sssd_cfg* cfg, sssd_elem* el, i
   uint32_t* idx = reinterpret_cast<uint32_t*>(raw + (size_t)seqs->B * cap);
   KCfg k = kcfg(cfg);
   k.use_in = 1;
-  input_scan_kernel<<<seqs->B, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  const int th = input_scan_threads(seqs->max_len);
+  if ((rc = input_scan_attr(cfg->input_branch_len))) return rc;
+  input_scan_kernel<<<seqs->B, th, input_scan_smem_bytes(th, cfg->input_branch_len),
+                      static_cast<cudaStream_t>(stream)>>>(
       *seqs, k, raw, el, n_el, idx, cap, cap > 4096 ? p2 : 0, Cols{});
   return cuda_check(cudaGetLastError(), "input_scan_kernel launch");
 }

@@ -487,14 +487,16 @@ __global__ void shard_gather_kernel(sssd_ds ds, KCfg c, int B, const int64_t* gb
 
 constexpr int kSortSmem = 4096;
 
-__global__ void __launch_bounds__(256)
+// Launched with 256 threads, or 1024 for long contexts (input_scan_threads);
+// dynamic shared memory input_scan_smem_bytes(threads, IBL).
+__global__ void __launch_bounds__(1024)
     input_scan_kernel(sssd_seqs seqs, KCfg c, sssd_elem* raw, sssd_elem* sorted, int32_t* in_n,
                       uint32_t* idx_ws, int64_t cap, int64_t cap2, Cols cols) {
   const int b = c.b0 + blockIdx.x;
-  const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5, nw = blockDim.x >> 5;
   __shared__ uint32_t s_tail[SSSD_MAX_P];
-  __shared__ int s_wsum[8];
-  __shared__ uint32_t s_idx[kSortSmem];
+  __shared__ int s_wsum[32];
+  extern __shared__ __align__(16) uint32_t s_idx[];  // >= kSortSmem words
   const int L = seqs.seq_len[b];
   const uint32_t* seq = seqs.seq + seqs.seq_off[b];
   if (!c.use_in || L < 2) {
@@ -514,7 +516,7 @@ __global__ void __launch_bounds__(256)
   constexpr int kScanV = 8;
   const uint32_t t0 = s_tail[0];
   int total = 0;
-  for (int tile = 1; tile < L; tile += 256 * kScanV) {
+  for (int tile = 1; tile < L; tile += (int)blockDim.x * kScanV) {
     const int e0 = tile + tid * kScanV;
     uint32_t v[kScanV];
 #pragma unroll
@@ -532,8 +534,7 @@ __global__ void __launch_bounds__(256)
     if (lane == 31) s_wsum[warp] = inc;
     __syncthreads();
     int wbase = 0, tsum = 0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) {
+    for (int w = 0; w < nw; ++w) {
       const int x = s_wsum[w];
       wbase += w < warp ? x : 0;
       tsum += x;
@@ -560,8 +561,8 @@ __global__ void __launch_bounds__(256)
   sssd_elem* out = sorted + (size_t)b * cap;
   if (total == 0) return;
   __syncthreads();
-  if (total <= (int)blockDim.x && total * (c.IBL + 6) <= kSortSmem) {
-    // the common case (<= 256 occurrences): continuation strings staged in
+  if (total <= (int)blockDim.x && total * (c.IBL + 6) <= input_scan_smem_bytes(blockDim.x, c.IBL) / 4) {
+    // the common case (<= blockDim occurrences): continuation strings staged in
     // shared memory; warp w rank-sorts occurrences [32w, 32w + 32), then each
     // occurrence adds, per other run, a binary-searched count of the run's
     // smaller strings (ties: position order, i.e. run order).  When every
@@ -639,7 +640,9 @@ __global__ void __launch_bounds__(256)
     }
     return;
   }
-  uint32_t* idx = (total <= kSortSmem) ? s_idx : idx_ws + (size_t)b * cap2;
+  int n2 = 1;
+  while (n2 < total) n2 <<= 1;
+  uint32_t* idx = (n2 <= kSortSmem) ? s_idx : idx_ws + (size_t)b * cap2;
   block_sort_elems(r, out, seq, total, idx);
   if (cols.meta) {
     const Cols cb{cols.meta + (size_t)b * cols.stride, cols.orig + (size_t)b * cols.stride,

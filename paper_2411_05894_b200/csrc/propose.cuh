@@ -42,6 +42,13 @@ __host__ __device__ inline int ds_lookup_smem_words(int P, int M) {
   const int rows = P * 32 * kRowStride;
   return rows > (cap < 4096 ? (int)cap : 4096) ? rows : (cap < 4096 ? (int)cap : 4096);
 }
+// input scan launch shape: 1024 threads once a context spans several
+// 2048-position tiles (fewer sequential tiles, wider occurrence sort)
+inline int input_scan_threads(int max_len) { return max_len > 4096 ? 1024 : 256; }
+__host__ __device__ inline int input_scan_smem_bytes(int threads, int ibl) {
+  const int need = threads * (ibl + 6);
+  return 4 * (need > 4096 ? need : 4096);
+}
 __global__ void input_scan_kernel(sssd_seqs seqs, KCfg c, sssd_elem* raw, sssd_elem* sorted,
                                   int32_t* in_n, uint32_t* idx_ws, int64_t cap, int64_t cap2,
                                   Cols cols);
