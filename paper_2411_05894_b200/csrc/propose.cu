@@ -561,6 +561,71 @@ __global__ void __launch_bounds__(1024)
   sssd_elem* out = sorted + (size_t)b * cap;
   if (total == 0) return;
   __syncthreads();
+  // Packed path (IBL <= 8, every token < 65535): a continuation string is one
+  // 128-bit key (16 bits of token + 1 per depth; an absent token is 0, so a
+  // proper prefix sorts first, as cmp_str orders them).  Runs of 32
+  // consecutive occurrences are rank-sorted, then each occurrence adds the
+  // binary-searched count of smaller keys of every other run (ties: position
+  // order = run order).  Any occurrence count that fits shared memory.
+  if (c.IBL <= 8 && total * 6 <= input_scan_smem_bytes(blockDim.x, c.IBL) / 4) {
+    uint64_t* kh = reinterpret_cast<uint64_t*>(s_idx);
+    uint64_t* kl = kh + total;
+    uint32_t* srt = reinterpret_cast<uint32_t*>(kl + total);
+    uint32_t* lrk = srt + total;
+    bool wide = false;
+    for (int e = tid; e < total; e += blockDim.x) {
+      const sssd_elem el = r[e];
+      const uint32_t len = el_len(el.len_m);
+      uint64_t h = 0, l = 0;
+      for (uint32_t d = 0; d < len; ++d) {
+        const uint32_t tk = seq[el.off + d];
+        wide |= tk >= 65535u;
+        const uint64_t v = (uint64_t)(tk & 0xffffu) + 1;
+        if (d < 4) h |= v << (16 * (3 - d));
+        else l |= v << (16 * (7 - d));
+      }
+      kh[e] = h;
+      kl[e] = l;
+    }
+    if (!__syncthreads_or(wide)) {
+      for (int e = tid; e < total; e += blockDim.x) {
+        const int r0 = e & ~31, rn = min(32, total - r0);
+        const uint64_t h = kh[e], l = kl[e];
+        int lr = 0;
+        for (int j = r0; j < r0 + rn; ++j) {
+          const uint64_t hj = kh[j], lj = kl[j];
+          lr += (hj < h || (hj == h && (lj < l || (lj == l && j < e)))) ? 1 : 0;
+        }
+        srt[r0 + lr] = (uint32_t)e;
+        lrk[e] = (uint32_t)lr;
+      }
+      __syncthreads();
+      const Cols cb{cols.meta ? cols.meta + (size_t)b * cols.stride : nullptr,
+                    cols.orig + (size_t)b * cols.stride, cols.tok + (size_t)b * cols.stride * c.IBL, cols.stride};
+      for (int e = tid; e < total; e += blockDim.x) {
+        const int r0 = e & ~31;
+        const uint64_t h = kh[e], l = kl[e];
+        int rank = (int)lrk[e];
+        for (int q0 = 0; q0 < total; q0 += 32) {
+          if (q0 == r0) continue;
+          int lo = 0, hi = min(32, total - q0);  // elements of run q0 that sort before mine
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            const uint32_t x = srt[q0 + mid];
+            const uint64_t hx = kh[x], lx = kl[x];
+            if (hx < h || (hx == h && (lx < l || (lx == l && q0 < r0)))) lo = mid + 1;
+            else hi = mid;
+          }
+          rank += lo;
+        }
+        const sssd_elem el = r[e];
+        out[rank] = el;
+        if (cb.meta) write_cols(cb, rank, el, seq);
+      }
+      return;
+    }
+    __syncthreads();  // the key area is reused below
+  }
   if (total <= (int)blockDim.x && total * (c.IBL + 6) <= input_scan_smem_bytes(blockDim.x, c.IBL) / 4) {
     // the common case (<= blockDim occurrences): continuation strings staged in
     // shared memory; warp w rank-sorts occurrences [32w, 32w + 32), then each
