@@ -188,7 +188,7 @@ __device__ __noinline__ void ls_sort(LsLevel L, uint32_t n) {
   }
 }
 
-// Cut a full level buffer to its smallest `keepn` (= kLsCap - 32) nodes, moved to
+// Cut a full level buffer to its smallest `keepn` (<= kLsCap - 32) nodes, moved to
 // slots [0, keepn) in order; returns keepn and the first cut key.
 __device__ __noinline__ uint32_t ls_cut(LsLevel L, uint32_t nb, uint32_t keepn, uint64_t* th0, uint64_t* th1) {
   const uint32_t lane = (uint32_t)lane_id();
@@ -234,15 +234,15 @@ __device__ __noinline__ uint32_t ls_cut(LsLevel L, uint32_t nb, uint32_t keepn, 
 // Generate the depth-d children of parents [0, np) (element ranges scanned
 // flat over the lanes; runs of equal token inside one parent's range are
 // one child) into L.  Returns (nodes kept in L, all children).
-// Without `drop`, nodes past `cap` are counted but not written.  With `drop`
-// (the shared-memory buffer, cap - 32 >= dec_len - 1), a full buffer is
-// sorted and cut to its smallest cap - 32 nodes, and later children at or
+// With keepn == 0, nodes past `cap` are counted but not written.  With keepn
+// (the shared-memory buffer, dec_len - 1 <= keepn <= cap - 32), a full buffer
+// is sorted and cut to its smallest keepn nodes, and later children at or
 // above the cut key are discarded: L always holds a prefix of the level's
 // (k0, k1) order, which is all the level needs whenever that prefix holds
 // dec_len - 1 distinct paths (the caller checks and otherwise regenerates).
 __device__ __noinline__ uint2 ls_generate(const LsPar par, int np, uint32_t E, LsLevel L, uint32_t cap,
-                                          bool drop, const SrcDesc* sd, const double* disc, int disc_stride,
-                                          int d) {
+                                          uint32_t keepn, const SrcDesc* sd, const double* disc,
+                                          int disc_stride, int d) {
   const int lane = lane_id();
   const uint32_t lt = lanemask_lt();
   uint32_t n = 0, nb = 0;
@@ -267,8 +267,8 @@ __device__ __noinline__ uint2 ls_generate(const LsPar par, int np, uint32_t E, L
     }
     bool keep = live && k_less(k0, k1, th0, th1);
     uint32_t km = __ballot_sync(SSSD_FULL, keep);
-    if (drop && nb + __popc(km) > cap) {  // cut the full buffer to its smallest cap - 32
-      nb = ls_cut(L, nb, cap - 32, &th0, &th1);
+    if (keepn && nb + __popc(km) > cap) {  // cut the full buffer to its smallest keepn
+      nb = ls_cut(L, nb, keepn, &th0, &th1);
       keep = live && k_less(k0, k1, th0, th1);
       km = __ballot_sync(SSSD_FULL, keep);
     }
@@ -490,9 +490,13 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
     //    drop (dec_len - 1 > kLsCap - 32), is generated again in full into a
     //    global buffer
     LsLevel L = Ls;
-    const bool drop = K <= kLsCap - 32;
+    // a cut keeps cap - 32 nodes: smaller prefixes (fewer cuts for small
+    // drafts) measured worse on prompt-heavy levels, whose duplicate paths
+    // across the P+1 sources then force the full regeneration
+    const uint32_t keepn = K <= kLsCap - 32 ? (uint32_t)(kLsCap - 32) : 0u;
+    const bool drop = keepn != 0;
     LS_PROBE(uint32_t tp = (uint32_t)clock());
-    const uint2 gr = ls_generate(par, np, E, Ls, kLsCap, drop, sd, c.disc, c.disc_stride, d);
+    const uint2 gr = ls_generate(par, np, E, Ls, kLsCap, keepn, sd, c.disc, c.disc_stride, d);
     LS_PROBE(ph_gen += (uint32_t)clock() - tp; tp = (uint32_t)clock());
     uint32_t n = gr.x, n_all = gr.y;
     if (n_all == 0) break;
@@ -514,7 +518,7 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
           ++gallocs;
         }
         L = level_carve(glev, glev_cap);
-        n = ls_generate(par, np, E, L, glev_cap, false, sd, c.disc, c.disc_stride, d).x;
+        n = ls_generate(par, np, E, L, glev_cap, 0u, sd, c.disc, c.disc_stride, d).x;
       }
       if (n > kTbMask) {  // class positions must fit their field
         if (lane == 0) atomicExch(err, SSSD_E_LIMIT);
