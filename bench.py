@@ -618,7 +618,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batches", type=int, default=256, help="independent B=64 batches per step")
-    ap.add_argument("--e2e-chunks", type=int, default=6, help="request chunks pipelined by propose_pinned")
+    ap.add_argument("--e2e-chunks", type=int, default=5, help="request chunks pipelined by propose_pinned")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip verify/decode sub-benchmarks")
     ap.add_argument("--shard", action="store_true", help="N>1: shard the suffix rows by rank range")

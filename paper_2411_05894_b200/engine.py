@@ -133,7 +133,7 @@ class DraftEngine:
         return list(ms)
 
     def propose_pinned(self, seq_h: torch.Tensor, off_h: torch.Tensor, len_h: torch.Tensor, max_len: int,
-                       out_h: DraftBatch | None = None, chunks: int = 6) -> DraftBatch:
+                       out_h: DraftBatch | None = None, chunks: int = 5, taper: float = 1.0) -> DraftBatch:
         """Host-buffer entry point for a large batch: contexts in pinned host
         memory (seq_h int32 = u32 token ids, or int16 = u16 token ids when the
         vocabulary fits 16 bits: half the upload bytes, widened on the device by
@@ -163,7 +163,10 @@ class DraftEngine:
         if (lens < 1).any():
             raise ValueError("empty prompt: the draft root is the last context token")
         chunks = max(1, min(int(chunks), B))
-        cuts = [B * c // chunks for c in range(chunks + 1)]
+        # request ranges shrink geometrically (ratio `taper`): the last range's
+        # drafting + download is the part no upload hides
+        wts = np.power(float(taper), np.arange(chunks))
+        cuts = [0] + [int(round(B * x)) for x in np.cumsum(wts)[:-1] / wts.sum()] + [B]
         bc = max(cuts[c + 1] - cuts[c] for c in range(chunks))
         n_tok = int(seq_h.shape[0])
         st = getattr(self, "_pin", None)
@@ -193,6 +196,14 @@ class DraftEngine:
         out = self.outputs(B)
         for s_ in st["streams"]:
             s_.wait_stream(main)
+        if not (off_h.is_pinned() and len_h.is_pinned()):  # pageable copies would serialise the upload
+            pin = st.get("offlen")
+            if pin is None or pin[0].numel() < B:
+                pin = st["offlen"] = (torch.empty(B, dtype=torch.int64).pin_memory(),
+                                      torch.empty(B, dtype=torch.int32).pin_memory())
+            pin[0][:B].copy_(off_h)
+            pin[1][:B].copy_(len_h)
+            off_h, len_h = pin[0][:B], pin[1][:B]
         with torch.cuda.stream(up):
             off_d.copy_(off_h, non_blocking=True)
             len_d.copy_(len_h, non_blocking=True)

@@ -37,10 +37,11 @@ print("h2d 134MB", timed(lambda: seq.copy_(ctx_h, non_blocking=True)))
 print("h2d 67MB u16", timed(lambda: seq16.copy_(ctx16_h, non_blocking=True)))
 print("propose resident", timed(lambda: eng.propose(seq, off, ln, CTX)))
 out_h = eng.propose_pinned(ctx_h, off_h, len_h, CTX)  # pinned outputs reused below
-for c in (1, 2, 4, 8, 16, 32):
+for c in (6,):
     print("pinned chunks", c, timed(lambda: eng.propose_pinned(ctx_h, off_h, len_h, CTX, out_h=out_h, chunks=c)))
-for c in (1, 2, 3, 4, 6, 8, 16):
-    print("pinned u16 chunks", c, timed(lambda: eng.propose_pinned(ctx16_h, off_h, len_h, CTX, out_h=out_h, chunks=c)))
+for c in (2, 3, 4, 5):
+    for tp in (1.0, 1.25, 1.6, 2.0):
+        print("pinned u16 chunks", c, "taper", tp, timed(lambda: eng.propose_pinned(ctx16_h, off_h, len_h, CTX, out_h=out_h, chunks=c, taper=tp)))
 
 # stream timeline of the pipelined call (chrome trace -> gpurun_out/)
 from torch.profiler import ProfilerActivity, profile
