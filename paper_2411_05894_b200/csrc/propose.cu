@@ -515,12 +515,21 @@ __global__ void __launch_bounds__(1024)
   // occurrences in e order.
   constexpr int kScanV = 8;
   const uint32_t t0 = s_tail[0];
+  const bool aligned = (reinterpret_cast<uintptr_t>(seq) & 15) == 0;
+  static_assert(kScanV == 8, "vector tile loads assume 8 positions per thread");
   int total = 0;
   for (int tile = 1; tile < L; tile += (int)blockDim.x * kScanV) {
     const int e0 = tile + tid * kScanV;
     uint32_t v[kScanV];
+    if (aligned && e0 + kScanV <= L) {  // two 16-byte loads: seq[e0-1 .. e0+7) (e0-1 is a multiple of 8)
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(seq + e0 - 1));
+      const uint4 c2 = __ldg(reinterpret_cast<const uint4*>(seq + e0 + 3));
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+      v[4] = c2.x; v[5] = c2.y; v[6] = c2.z; v[7] = c2.w;
+    } else {
 #pragma unroll
-    for (int k = 0; k < kScanV; ++k) v[k] = e0 + k < L ? seq[e0 + k - 1] : ~t0;
+      for (int k = 0; k < kScanV; ++k) v[k] = e0 + k < L ? seq[e0 + k - 1] : ~t0;
+    }
     uint32_t mk = 0;  // bit k: position e0 + k matches (m >= 1)
 #pragma unroll
     for (int k = 0; k < kScanV; ++k) mk |= (v[k] == t0 && e0 + k < L ? 1u : 0u) << k;
