@@ -22,6 +22,9 @@ want = {
     "launch__grid_size": "grid",
     "smsp__inst_executed.sum": "warp_inst",
     "lts__t_sector_hit_rate.pct": "l2_hit_pct",
+    "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.ratio": "ld_bytes_per_sector",
+    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "tensor_pipe_pct",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tensor_mem_pct",
 }
 out = []
 for r in data:
@@ -69,13 +72,14 @@ md = ["| kernel | launches | mean ms (ncu, cold, serialised) | max ms |", "|---|
 for k, v in per.items():
     md.append(f"| {k} | {len(v)} | {sum(v)/len(v):.4f} | {max(v):.4f} |")
 md.append("")
-md.append("| kernel (full set) | ms | DRAM read MB | DRAM write MB | DRAM % peak | occupancy % | issue active % | regs | warp inst | top stalls (% of samples) |")
-md.append("|---|---|---|---|---|---|---|---|---|---|")
+md.append("| kernel (full set) | ms | DRAM read MB | DRAM write MB | DRAM % peak | global ld B/sector (of 32) | L2 hit % | tensor pipe % | occupancy % | issue active % | regs | warp inst | top stalls (% of samples) |")
+md.append("|---|---|---|---|---|---|---|---|---|---|---|---|---|")
 traffic = {}
 for r in out:
     rd, wr = r.get("dram_read_bytes", 0), r.get("dram_write_bytes", 0)
     traffic[r["kernel"]] = rd + wr
     md.append(f"| {r['kernel']} | {r.get('duration_ms', 0):.3f} | {rd/1e6:.1f} | {wr/1e6:.1f} | {r.get('dram_pct', 0):.1f} | "
+              f"{r.get('ld_bytes_per_sector', 0):.1f} | {r.get('l2_hit_pct', 0):.1f} | {r.get('tensor_pipe_pct', 0):.1f} | "
               f"{r.get('occupancy_pct', 0):.1f} | {r.get('issue_active_pct', 0):.1f} | {int(r.get('regs', 0))} | "
               f"{int(r.get('warp_inst', 0))} | " + ", ".join(f"{k} {v}" for k, v in r["stalls"].items()) + " |")
 open(prefix + "_ncu_summary.md", "w").write("\n".join(md) + "\n")
