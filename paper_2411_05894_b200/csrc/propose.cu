@@ -221,53 +221,70 @@ __device__ void block_sort_elems(const sssd_elem* src, sssd_elem* dst, const uin
 
 // Gather the sampled continuations of prefix length p into this request's
 // string table (non-empty ones compacted, SA order kept).  Returns the count.
+// The warp stages up to `rpl` rows per lane per round in shared memory with
+// cp.async (rpl = 4 when it is the batch's only gathering warp and may use the
+// whole CTA staging area): 128 samples cost one dependent row round trip.
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+
 __device__ int gather_p(const sssd_ds& ds, const KCfg& c, int p, uint64_t lo, uint64_t hi,
-                        uint32_t* tab, uint8_t* lens, int64_t* samples, uint32_t* srows,
+                        uint32_t* tab, uint8_t* lens, int64_t* samples, uint32_t* srows, int rpl,
                         const uint32_t* pre_rows) {
   const int lane = lane_id();
   const uint64_t w = hi - lo;
   const int s = (int)min(w, (uint64_t)c.M);
   uint32_t* ptab = tab + (size_t)(p - 1) * c.M * c.BL;
   uint8_t* plen = lens + (size_t)(p - 1) * c.M;
-  uint32_t* srow = srows + lane * kRowStride;
   int cnt = 0;
-  for (int k0 = 0; k0 < s; k0 += 32) {
-    const int k = k0 + lane;
-    const bool valid = k < s;
-    uint32_t len = 0, pos = 0;
-    if (valid) {
-      const uint64_t r =
-          lo + (w <= (uint64_t)c.M ? (uint64_t)k : ((uint64_t)k * w) / (uint64_t)c.M);
-      // sharded mode: the row was fetched by its owning shard into pre_rows[k]
-      const uint4* row = pre_rows ? reinterpret_cast<const uint4*>(pre_rows) + (uint64_t)k * 4
-                                  : reinterpret_cast<const uint4*>(ds.rows) + (r - ds.rank_base) * 4;
-      uint4* sr = reinterpret_cast<uint4*>(srow);
-      sr[0] = ldg4(row);
-      sr[1] = ldg4(row + 1);
-      sr[2] = ldg4(row + 2);
-      sr[3] = ldg4(row + 3);
-      pos = srow[0];
-      if (samples) samples[k] = (int64_t)pos;
-      const uint64_t start = (uint64_t)pos + p;
-      const uint64_t avail = ds.n_tokens > start ? ds.n_tokens - start : 0;
-      const uint32_t lim = (uint32_t)min((uint64_t)c.BL, avail);
-      for (uint32_t j = 0; j < lim; ++j) {
-        const uint32_t t = (p + j < SSSD_ROW_TOKENS) ? srow[1 + p + j] : __ldg(ds.tokens + start + j);
-        if (c.has_sep && t == c.sep) break;
-        ++len;
+  for (int k00 = 0; k00 < s; k00 += 32 * rpl) {
+    // issue every row fetch of this round first (no register staging)
+    for (int u = 0; u < rpl; ++u) {
+      const int k = k00 + 32 * u + lane;
+      if (k < s) {
+        const uint64_t r =
+            lo + (w <= (uint64_t)c.M ? (uint64_t)k : ((uint64_t)k * w) / (uint64_t)c.M);
+        // sharded mode: the row was fetched by its owning shard into pre_rows[k]
+        const uint4* row = pre_rows ? reinterpret_cast<const uint4*>(pre_rows) + (uint64_t)k * 4
+                                    : reinterpret_cast<const uint4*>(ds.rows) + (r - ds.rank_base) * 4;
+        uint4* sr = reinterpret_cast<uint4*>(srows + (u * 32 + lane) * kRowStride);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) cp_async16(sr + h, row + h);
       }
     }
-    const bool ne = len > 0;
-    const uint32_t bal = __ballot_sync(SSSD_FULL, ne);
-    const int idx = cnt + __popc(bal & lanemask_lt());
-    if (ne) {
-      const uint64_t start = (uint64_t)pos + p;
-      uint32_t* dst = ptab + (size_t)idx * c.BL;
-      for (uint32_t j = 0; j < len; ++j)
-        dst[j] = (p + j < SSSD_ROW_TOKENS) ? srow[1 + p + j] : __ldg(ds.tokens + start + j);
-      plen[idx] = (uint8_t)len;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    for (int u = 0; u < rpl; ++u) {
+      const int k0 = k00 + 32 * u;
+      if (k0 >= s) break;
+      const int k = k0 + lane;
+      const uint32_t* srow = srows + (u * 32 + lane) * kRowStride;
+      uint32_t len = 0, pos = 0;
+      if (k < s) {
+        pos = srow[0];
+        if (samples) samples[k] = (int64_t)pos;
+        const uint64_t start = (uint64_t)pos + p;
+        const uint64_t avail = ds.n_tokens > start ? ds.n_tokens - start : 0;
+        const uint32_t lim = (uint32_t)min((uint64_t)c.BL, avail);
+        for (uint32_t j = 0; j < lim; ++j) {
+          const uint32_t t = (p + j < SSSD_ROW_TOKENS) ? srow[1 + p + j] : __ldg(ds.tokens + start + j);
+          if (c.has_sep && t == c.sep) break;
+          ++len;
+        }
+      }
+      const bool ne = len > 0;
+      const uint32_t bal = __ballot_sync(SSSD_FULL, ne);
+      const int idx = cnt + __popc(bal & lanemask_lt());
+      if (ne) {
+        const uint64_t start = (uint64_t)pos + p;
+        uint32_t* dst = ptab + (size_t)idx * c.BL;
+        for (uint32_t j = 0; j < len; ++j)
+          dst[j] = (p + j < SSSD_ROW_TOKENS) ? srow[1 + p + j] : __ldg(ds.tokens + start + j);
+        plen[idx] = (uint8_t)len;
+      }
+      cnt += __popc(bal);
     }
-    cnt += __popc(bal);
     __syncwarp();
   }
   return cnt;
@@ -333,8 +350,11 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P, SSSD_LOOKUP_MINB)
     }
     const int blo = max(q, 1);
     if (p >= blo && p <= next) {
+      // the batch's only gathering warp stages into the whole CTA area
+      const bool alone = next == blo;
       const int n = gather_p(ds, c, p, s_lo[warp], s_hi[warp], tab, lens,
-                             smp ? smp + (size_t)warp * c.M : nullptr, s_rows + warp * 32 * kRowStride,
+                             smp ? smp + (size_t)warp * c.M : nullptr,
+                             alone ? s_rows : s_rows + warp * 32 * kRowStride, alone ? c.P : 1,
                              pre_rows ? pre_rows + (((size_t)b * c.P + warp) * c.M) * 16 : nullptr);
       if (lane == 0) s_cnt[warp] = n;
     }
