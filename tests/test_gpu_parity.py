@@ -365,3 +365,35 @@ def test_propose_large_token_ids(ibl):
     for f, ctx in zip(flats, ctxs):
         d = O.propose(store, ctx, oc)
         assert (f.tokens, f.parents, f.depths) == (d.tokens, d.parents, d.depths)
+
+
+@pytest.mark.parametrize("dec_len,P,ibl,bl,sep,src", [
+    (1, 4, 8, None, None, "both"), (2, 4, 8, None, None, "both"), (3, 8, 8, None, 3, "both"),
+    (40, 8, 20, 12, 5, "both"), (64, 3, 32, 6, None, "input"), (64, 6, 4, 16, 2, "datastore"),
+    (130, 2, 12, 10, None, "both")])
+def test_fusion_edge_configs(monkeypatch, dec_len, P, ibl, bl, sep, src):
+    """Edge configurations through both fusion kernels and the oracle: tiny
+    budgets (dec_len 1-3), P = 8 (the compiled maximum), deep input trees
+    (input_branch_len 20/32: levels beyond the 8-level key flatten), datastore
+    continuations longer than the 15 inlined row tokens (P + branch_len > 15),
+    separators and single-source sessions, 130-node drafts (3 mask words)."""
+    rng = np.random.default_rng(dec_len * 7 + P)
+    V = 9
+    corpus = rng.integers(0, V, 40000).astype(np.uint32)
+    ds = G.build(corpus)
+    store = O.Store(corpus, O.suffix_array(corpus))
+    cfg = G.FusionConfig(P=P, dec_len=dec_len, input_branch_len=ibl,
+                         **({"branch_len": bl} if bl is not None else {}))
+    use_ds, use_in = src in ("both", "datastore"), src in ("both", "input")
+    monkeypatch.setenv("SSSD_FUSION", "heap")
+    heap = G.DraftEngine(ds, cfg, sep, use_ds, use_in)
+    monkeypatch.setenv("SSSD_FUSION", "ls")
+    ls = G.DraftEngine(ds, cfg, sep, use_ds, use_in)
+    ctxs = [rng.integers(0, V, int(rng.integers(1, 1500))).tolist() for _ in range(24)]
+    fa, fb = heap.propose_host(ctxs), ls.propose_host(ctxs)
+    oc = O.Cfg(P=P, dec_len=dec_len, input_branch_len=ibl, branch_len=cfg.branch_len)
+    for a, b, ctx in zip(fa, fb, ctxs):
+        d = O.propose(store, ctx, oc, separator=sep, use_ds=use_ds, use_in=use_in)
+        assert (b.tokens, b.parents, b.depths) == (d.tokens, d.parents, d.depths)
+        assert (a.tokens, a.parents, a.depths) == (d.tokens, d.parents, d.depths)
+        assert pack_mask(b.mask) == O.pack_mask_rows(d.masks, d.size)
