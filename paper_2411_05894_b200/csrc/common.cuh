@@ -20,6 +20,9 @@ __device__ __forceinline__ uint4 ldg4(const uint4* p) { return __ldg(p); }
 
 __device__ __forceinline__ uint32_t el_len(uint32_t len_m) { return len_m & 0xffu; }
 __device__ __forceinline__ uint32_t el_m(uint32_t len_m) { return (len_m >> 8) & 0xffu; }
+// column meta words carry a multiplicity in bits 16..31 (0 = 1): identical
+// datastore continuations folded into one element (level-synchronous fusion)
+__device__ __forceinline__ uint32_t el_wt(uint32_t meta) { return max(meta >> 16, 1u); }
 
 // Lexicographic compare of two token strings with "shorter sorts first"
 // (a proper prefix precedes its extensions; ref datastore.py:129-141 and the

@@ -343,20 +343,28 @@ __device__ __noinline__ uint2 ls_generate(const LsPar par, int np, uint32_t E, L
     const bool has = x < E && el_len(lm) >= (uint32_t)d;
     const bool w = owned && has && el_m(lm) >= th;
     const uint32_t orig = w ? og : 0xffffffffu;
+    const uint32_t wt = w ? el_wt(lm) : 0u;
     const uint32_t hasm = __ballot_sync(SSSD_FULL, has);
     if (hasm) {  // (a carried run always continues at lane 0, so none is open otherwise)
       const unsigned long long key = has ? ((unsigned long long)j << 32 | tk) : (1ull << 63 | (unsigned)lane);
       const uint32_t gm = __match_any_sync(SSSD_FULL, key);
       const uint32_t wm = __ballot_sync(SSSD_FULL, w);
       const int lo_l = __ffs(gm) - 1, hi_l = 31 - __clz(gm);
-      uint32_t fm = orig;  // run minimum of orig (segmented down-scan; runs are lane intervals)
+      // run minimum of orig and run sum of weights (segmented down-scans;
+      // runs are lane intervals)
+      uint32_t fm = orig, cnt = wt;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_down_sync(SSSD_FULL, fm, o);
-        if (lane + o <= hi_l) fm = min(fm, y);
+        const uint32_t z = __shfl_down_sync(SSSD_FULL, cnt, o);
+        if (lane + o <= hi_l) {
+          fm = min(fm, y);
+          cnt += z;
+        }
       }
       fm = __shfl_sync(SSSD_FULL, fm, lo_l);
-      uint32_t cnt = __popc(gm & wm);
+      cnt = __shfl_sync(SSSD_FULL, cnt, lo_l);
+      (void)wm;
       uint32_t start = i - (uint32_t)(lane - lo_l);
       if (c_open && lo_l == 0) {  // the run carried in from the previous chunk
         cnt += c_cnt;
@@ -440,7 +448,10 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
     for (int rk = 0; rk < NR; ++rk) {
       if (sd[rk].n <= 0) continue;
       uint32_t rc = 0;
-      for (int i = lane; i < sd[rk].n; i += 32) rc += (int)el_m(sd[rk].meta[i]) >= sd[rk].thr ? 1u : 0u;
+      for (int i = lane; i < sd[rk].n; i += 32) {
+        const uint32_t mt = sd[rk].meta[i];
+        rc += (int)el_m(mt) >= sd[rk].thr ? el_wt(mt) : 0u;
+      }
       rc = __reduce_add_sync(SSSD_FULL, rc);
       if (rc == 0) continue;
       if (lane == 0) {

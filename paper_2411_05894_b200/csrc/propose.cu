@@ -383,6 +383,12 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P, SSSD_LOOKUP_MINB)
   int before = 0;  // list position of run p's first element
   for (int q = pmax; q > p; --q)
     if (q >= pcut) before += s_cnt[q - 1];
+  int n_all = 0;
+  for (int q = pcut; q <= pmax; ++q) n_all += s_cnt[q - 1];
+  // the level-synchronous fusion kernel takes the datastore elements with
+  // identical continuation strings folded into one weighted element
+  // (ds_dedupe_kernel, launched next on the same stream, writes the columns)
+  const bool dedupe = cols.meta && ds_dedupe_enabled(c);
   if (c.has_sep) {
     sssd_elem* raw = ds_raw + (size_t)b * c.P * c.M;
     if (p >= pcut && p <= pmax) {
@@ -404,7 +410,7 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P, SSSD_LOOKUP_MINB)
       uint32_t* idx = (n2 <= ds_lookup_smem_words(c.P, c.M)) ? s_rows : ds_idx + (size_t)b * idx_cap;
       sssd_elem* sorted = ds_el + (size_t)b * c.P * c.M;
       block_sort_elems(raw, sorted, tab, n, idx);
-      if (cols.meta) {
+      if (cols.meta && !dedupe) {
         const Cols cb{cols.meta + (size_t)b * cols.stride, cols.orig + (size_t)b * cols.stride,
                       cols.tok + (size_t)b * cols.stride * c.BL, cols.stride};
         for (int i = threadIdx.x; i < n; i += blockDim.x) write_cols(cb, i, sorted[i], tab);
@@ -435,23 +441,68 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P, SSSD_LOOKUP_MINB)
       e.len_m = li | (255u << 8);
       e.pad = 0;
       ds_el[(size_t)b * c.P * c.M + rank] = e;
-      if (cols.meta) {
+      if (cols.meta && !dedupe) {
         const Cols cb{cols.meta + (size_t)b * cols.stride, cols.orig + (size_t)b * cols.stride,
                       cols.tok + (size_t)b * cols.stride * c.BL, cols.stride};
         write_cols(cb, rank, e, tab);
       }
     }
   }
+  const int n_out = n_all;  // ds_dedupe_kernel folds duplicates and writes the columns when dedupe
   if (threadIdx.x == 0) {
-    int n = 0;
-    for (int q = pcut; q <= pmax; ++q) n += s_cnt[q - 1];
-    ds_n[b] = n;
+    ds_n[b] = n_out;
     if (lk.p_cut) lk.p_cut[b] = pmax > 0 ? pcut : 0;
   }
   if (lk.n_conts && threadIdx.x < c.P) {
     const int q = threadIdx.x + 1;
     lk.n_conts[(size_t)b * c.P + threadIdx.x] = (q <= pmax && s_cnt[threadIdx.x] >= 0) ? s_cnt[threadIdx.x] : -1;
   }
+}
+
+// Fold datastore elements with identical continuation strings (adjacent in
+// the sorted array) into one element whose column meta carries the group size
+// as its weight (el_wt); the first element of a group has the smallest list
+// position, which the fusion kernel's first-appearance order needs.  One CTA
+// per request: flags in parallel, compaction by warp 0.
+__global__ void __launch_bounds__(128)
+    ds_dedupe_kernel(KCfg c, const uint32_t* ds_tab, const sssd_elem* ds_el, int32_t* ds_n, Cols cols) {
+  extern __shared__ int gstart[];  // [P*M + 1]
+  const int b = c.b0 + blockIdx.x;
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  const int n_all = ds_n[b];
+  if (n_all <= 0) return;
+  const sssd_elem* sorted = ds_el + (size_t)b * c.P * c.M;
+  const uint32_t* tab = ds_tab + (size_t)b * c.P * c.M * c.BL;
+  for (int r = threadIdx.x; r < n_all; r += blockDim.x) {
+    int st = 1;
+    if (r > 0) {
+      const sssd_elem x = sorted[r - 1], y = sorted[r];
+      st = cmp_str(tab + x.off, el_len(x.len_m), tab + y.off, el_len(y.len_m)) != 0;
+    }
+    gstart[r] = st;
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  int G = 0;
+  for (int r0 = 0; r0 < n_all; r0 += 32) {  // compact the flags into group starts (in place: g <= r)
+    const int r = r0 + lane;
+    const bool st = r < n_all && gstart[r] != 0;
+    const uint32_t sm = __ballot_sync(SSSD_FULL, st);
+    __syncwarp();
+    if (st) gstart[G + __popc(sm & lanemask_lt())] = r;
+    G += __popc(sm);
+    __syncwarp();
+  }
+  if (lane == 0) gstart[G] = n_all;
+  __syncwarp();
+  const Cols cb{cols.meta + (size_t)b * cols.stride, cols.orig + (size_t)b * cols.stride,
+                cols.tok + (size_t)b * cols.stride * c.BL, cols.stride};
+  for (int g = lane; g < G; g += 32) {
+    const sssd_elem e = sorted[gstart[g]];
+    write_cols(cb, g, e, tab);
+    cb.meta[g] = (e.len_m & 0xffffu) | (uint32_t)(gstart[g + 1] - gstart[g]) << 16;
+  }
+  if (lane == 0) ds_n[b] = G;
 }
 
 // --------------------------------------------------------------------------

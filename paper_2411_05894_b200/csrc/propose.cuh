@@ -25,6 +25,9 @@ __global__ void ds_lookup_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, uint32_t* d
                                  sssd_lookup_out lk, sssd_elem* ds_raw, uint32_t* ds_idx,
                                  int64_t idx_cap, Cols cols, const int64_t* pre_bounds,
                                  const uint32_t* pre_rows);
+// datastore element folding for the level-synchronous fusion (weights <= 65535)
+__host__ __device__ inline bool ds_dedupe_enabled(const KCfg& c) { return c.fusion == 0 && c.P * c.M <= 12000; }
+__global__ void ds_dedupe_kernel(KCfg c, const uint32_t* ds_tab, const sssd_elem* ds_el, int32_t* ds_n, Cols cols);
 __global__ void shard_search_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, int64_t* bounds);
 __global__ void shard_gather_kernel(sssd_ds ds, KCfg c, int B, const int64_t* gbounds, uint32_t* xrows);
 
