@@ -242,17 +242,19 @@ __device__ __noinline__ uint32_t ls_cut(LsLevel L, uint32_t nb, uint32_t keepn, 
 // dec_len - 1 distinct paths (the caller checks and otherwise regenerates).
 __device__ __noinline__ uint2 ls_generate(const LsPar par, int np, uint32_t E, LsLevel L, uint32_t cap,
                                           uint32_t keepn, const SrcDesc* sd, const double* disc,
-                                          int disc_stride, int d) {
+                                          int disc_stride, int d, bool has_tau, uint64_t tau0, uint32_t tau_dr) {
   const int lane = lane_id();
   const uint32_t lt = lanemask_lt();
   uint32_t n = 0, nb = 0;
   uint64_t th0 = ~0ull, th1 = ~0ull;  // cut key: children >= it are discarded
   const double* drow = disc + d;
+  // A child whose (~priority, depth, rank) already exceeds the top list's
+  // (dec_len-1)-th key tau (from earlier levels; tau only decreases) can be
+  // neither expanded nor listed, and it sorts after every node that can:
+  // it is not generated at all (a tie on all three keeps the node, tb decides).
   auto emit = [&](bool pred, int j, uint32_t tk, uint32_t cnt, uint32_t first, uint32_t s, uint32_t e) {
-    const bool live = pred && cnt > 0;
-    const uint32_t bal = __ballot_sync(SSSD_FULL, live);
-    if (!bal) return;
-    n += __popc(bal);
+    bool live = pred && cnt > 0;
+    if (!__ballot_sync(SSSD_FULL, live)) return;
     uint64_t k0 = ~0ull, k1 = ~0ull;
     double pp = 0.0;
     uint32_t pid = 0;
@@ -264,7 +266,12 @@ __device__ __noinline__ uint2 ls_generate(const LsPar par, int np, uint32_t E, L
       k0 = ~(uint64_t)__double_as_longlong(pr);
       k1 = (uint64_t)rk << 56 | (uint64_t)(tr & kTbMask) << 32 | first;
       pid = par.pid()[j];
+      const uint32_t dr = (uint32_t)d << 26 | rk << kTbBits;
+      if (has_tau && (k0 > tau0 || (k0 == tau0 && dr > tau_dr))) live = false;
     }
+    const uint32_t bal = __ballot_sync(SSSD_FULL, live);
+    if (!bal) return;
+    n += __popc(bal);
     bool keep = live && k_less(k0, k1, th0, th1);
     uint32_t km = __ballot_sync(SSSD_FULL, keep);
     if (keepn && nb + __popc(km) > cap) {  // cut the full buffer to its smallest keepn
@@ -507,7 +514,10 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
     const uint32_t keepn = K <= kLsCap - 32 ? (uint32_t)(kLsCap - 32) : 0u;
     const bool drop = keepn != 0;
     LS_PROBE(uint32_t tp = (uint32_t)clock());
-    const uint2 gr = ls_generate(par, np, E, Ls, kLsCap, keepn, sd, c.disc, c.disc_stride, d);
+    const bool has_tau = t == K;
+    const uint64_t tau0 = has_tau ? T.g0()[K - 1] : 0ull;
+    const uint32_t tau_dr = has_tau ? T.g1()[K - 1] & ~kTbMask : 0u;
+    const uint2 gr = ls_generate(par, np, E, Ls, kLsCap, keepn, sd, c.disc, c.disc_stride, d, has_tau, tau0, tau_dr);
     LS_PROBE(ph_gen += (uint32_t)clock() - tp; tp = (uint32_t)clock());
     uint32_t n = gr.x, n_all = gr.y;
     if (n_all == 0) break;
@@ -529,7 +539,7 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
           ++gallocs;
         }
         L = level_carve(glev, glev_cap);
-        n = ls_generate(par, np, E, L, glev_cap, 0u, sd, c.disc, c.disc_stride, d).x;
+        n = ls_generate(par, np, E, L, glev_cap, 0u, sd, c.disc, c.disc_stride, d, has_tau, tau0, tau_dr).x;
       }
       if (n > kTbMask) {  // class positions must fit their field
         if (lane == 0) atomicExch(err, SSSD_E_LIMIT);

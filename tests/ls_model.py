@@ -18,7 +18,10 @@ Why it is equivalent:
 * the draft is the first dec_len-1 distinct token paths in that order, and a
   path's parent path always comes first, so a node whose key exceeds the
   current dec_len-1'th best distinct-path key can never contribute: each level
-  only expands nodes at or below that threshold.
+  only expands nodes at or below that threshold, and a child whose
+  (-priority, depth, rank) already exceeds the threshold of the earlier levels
+  is not generated (it sorts after every node that can matter, so class
+  positions and first path occurrences of those are unchanged).
 """
 
 from __future__ import annotations
@@ -42,6 +45,7 @@ def fuse_ls(ds, inputs, P: int, dec_len: int, disc, root_token: int, stats: dict
     top = []  # (global key, path id) of the best distinct paths, key order
     depth = 1
     levels = []
+    tau = None
     while parents and K > 0:
         nodes = []
         for rk, node, pp, tb, pid in parents:
@@ -49,6 +53,8 @@ def fuse_ls(ds, inputs, P: int, dec_len: int, disc, root_token: int, stats: dict
                 dsc = disc[rk][depth]
                 r = c.count / node.count
                 cpp = r if pp is None else pp * r
+                if tau is not None and (-(cpp * dsc), depth, rk) > tau[:3]:
+                    continue  # beyond the threshold of the earlier levels
                 nodes.append(((-(cpp * dsc), rk, tb, i), rk, c, cpp, pid, tok))
         nodes.sort(key=lambda x: x[0])
         cls = {}
