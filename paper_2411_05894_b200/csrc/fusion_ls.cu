@@ -242,7 +242,8 @@ __device__ __noinline__ uint32_t ls_cut(LsLevel L, uint32_t nb, uint32_t keepn, 
 // dec_len - 1 distinct paths (the caller checks and otherwise regenerates).
 __device__ __noinline__ uint2 ls_generate(const LsPar par, int np, uint32_t E, LsLevel L, uint32_t cap,
                                           uint32_t keepn, const SrcDesc* sd, const double* disc,
-                                          int disc_stride, int d, bool has_tau, uint64_t tau0, uint32_t tau_dr) {
+                                          int disc_stride, int d, bool has_empty, bool has_tau, uint64_t tau0,
+                                          uint32_t tau_dr) {
   const int lane = lane_id();
   const uint32_t lt = lanemask_lt();
   uint32_t n = 0, nb = 0;
@@ -314,12 +315,6 @@ __device__ __noinline__ uint2 ls_generate(const LsPar par, int np, uint32_t E, L
   // element, so the chunk's parent starts form a 32-bit head mask (one OR
   // reduction) and an element's parent is the carried parent plus the heads
   // at or before it; a level with empty (depth-capped) parents binary-searches.
-  bool has_empty = false;
-  for (int j0 = 0; j0 < np; j0 += 32) {
-    const int j = j0 + lane;
-    const bool em = j < np && (j + 1 < np ? par.off()[j + 1] : E) == par.off()[j];
-    has_empty |= __ballot_sync(SSSD_FULL, em) != 0;
-  }
   int jprev = -1;  // parent of element base - 1
   for (uint32_t base = 0; base < E; base += 31) {
     const uint32_t x = base + lane;
@@ -431,22 +426,6 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
 
   for (int r = lane; r < NR; r += 32) sd[r] = desc[(size_t)b * NR + r];
   __syncwarp();
-  // Every level re-reads the request's element columns (written by the lookup
-  // and input-scan kernels, usually evicted to HBM by now): pull them into L2
-  // once, so the per-level chunk loads are L2 round trips.
-#ifndef SSSD_NO_PF
-  for (int rk = 0; rk < NR; ++rk) {
-    const int n = sd[rk].n;
-    if (n <= 0 || (rk > 1 && sd[rk].meta == sd[rk - 1].meta)) continue;  // input ranks share one array
-    const int lines = (n * 4 + 127) >> 7;
-    const int cols = 2 + sd[rk].depth;
-    for (int q = lane; q < lines * cols; q += 32) {
-      const int col = q / lines, ln = q - col * lines;
-      const uint32_t* base = col == 0 ? sd[rk].meta : col == 1 ? sd[rk].orig : sd[rk].tok + (int64_t)(col - 2) * sd[rk].stride;
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(base + ln * 32));
-    }
-  }
-#endif
 
   // level 0: the source roots are the parents of the seeds (path prob 1.0, so
   // pp * (count / root_count) is the seed's count / root_count exactly)
@@ -486,10 +465,12 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
   for (int d = 1; np > 0 && d < c.disc_stride; ++d) {
     // 1. exclusive scan of the parents' element-range sizes
     uint32_t E = 0;
+    bool has_empty = false;  // a parent with no element at this depth (shares its offset)
     for (int j0 = 0; j0 < np; j0 += 32) {
       const int j = j0 + lane;
       uint32_t e = 0;
       if (j < np && d <= sd[par.tbr()[j] >> kTbBits].depth) e = par.z()[j] - par.a()[j];
+      has_empty |= __ballot_sync(SSSD_FULL, j < np && e == 0) != 0;
       uint32_t inc = e;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -517,7 +498,8 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
     const bool has_tau = t == K;
     const uint64_t tau0 = has_tau ? T.g0()[K - 1] : 0ull;
     const uint32_t tau_dr = has_tau ? T.g1()[K - 1] & ~kTbMask : 0u;
-    const uint2 gr = ls_generate(par, np, E, Ls, kLsCap, keepn, sd, c.disc, c.disc_stride, d, has_tau, tau0, tau_dr);
+    const uint2 gr = ls_generate(par, np, E, Ls, kLsCap, keepn, sd, c.disc, c.disc_stride, d, has_empty, has_tau, tau0,
+                                 tau_dr);
     LS_PROBE(ph_gen += (uint32_t)clock() - tp; tp = (uint32_t)clock());
     uint32_t n = gr.x, n_all = gr.y;
     if (n_all == 0) break;
@@ -539,7 +521,8 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
           ++gallocs;
         }
         L = level_carve(glev, glev_cap);
-        n = ls_generate(par, np, E, L, glev_cap, 0u, sd, c.disc, c.disc_stride, d, has_tau, tau0, tau_dr).x;
+        n = ls_generate(par, np, E, L, glev_cap, 0u, sd, c.disc, c.disc_stride, d, has_empty, has_tau, tau0,
+                        tau_dr).x;
       }
       if (n > kTbMask) {  // class positions must fit their field
         if (lane == 0) atomicExch(err, SSSD_E_LIMIT);
