@@ -133,7 +133,8 @@ class DraftEngine:
         return list(ms)
 
     def propose_pinned(self, seq_h: torch.Tensor, off_h: torch.Tensor, len_h: torch.Tensor, max_len: int,
-                       out_h: DraftBatch | None = None, chunks: int = 5, taper: float = 1.0) -> DraftBatch:
+                       out_h: DraftBatch | None = None, chunks: int = 5, taper: float = 1.0,
+                       tail: float | None = None) -> DraftBatch:
         """Host-buffer entry point for a large batch: contexts in pinned host
         memory (seq_h int32 = u32 token ids, or int16 = u16 token ids when the
         vocabulary fits 16 bits: half the upload bytes, widened on the device by
@@ -166,6 +167,8 @@ class DraftEngine:
         # request ranges shrink geometrically (ratio `taper`): the last range's
         # drafting + download is the part no upload hides
         wts = np.power(float(taper), np.arange(chunks))
+        if tail is not None and chunks > 1:  # a short last range: less drafting after the last upload
+            wts[-1] = float(tail)
         cuts = [0] + [int(round(B * x)) for x in np.cumsum(wts)[:-1] / wts.sum()] + [B]
         bc = max(cuts[c + 1] - cuts[c] for c in range(chunks))
         n_tok = int(seq_h.shape[0])
@@ -204,18 +207,21 @@ class DraftEngine:
             pin[0][:B].copy_(off_h)
             pin[1][:B].copy_(len_h)
             off_h, len_h = pin[0][:B], pin[1][:B]
+        spans = []  # token span of every request range (computed before any copy is queued)
+        for c in range(chunks):
+            r0, r1 = cuts[c], cuts[c + 1]
+            spans.append((int(offs[r0:r1].min()), int((offs[r0:r1] + lens[r0:r1]).max())))
         with torch.cuda.stream(up):
-            off_d.copy_(off_h, non_blocking=True)
-            len_d.copy_(len_h, non_blocking=True)
             uploaded = []
             for c in range(chunks):  # every upload enqueued up front: the copy engine runs ahead
-                r0, r1 = cuts[c], cuts[c + 1]
-                t0 = int(offs[r0:r1].min())
-                t1 = int((offs[r0:r1] + lens[r0:r1]).max())
+                t0, t1 = spans[c]
                 if narrow:
                     st["seq16"][t0:t1].copy_(seq_h[t0:t1], non_blocking=True)
                 else:
                     seq_d[t0:t1].copy_(seq_h[t0:t1], non_blocking=True)
+                if c == 0:  # offsets / lengths right behind the first range's tokens
+                    off_d.copy_(off_h, non_blocking=True)
+                    len_d.copy_(len_h, non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(up)
                 uploaded.append((ev, t0, t1))

@@ -39,9 +39,9 @@ print("propose resident", timed(lambda: eng.propose(seq, off, ln, CTX)))
 out_h = eng.propose_pinned(ctx_h, off_h, len_h, CTX)  # pinned outputs reused below
 for c in (6,):
     print("pinned chunks", c, timed(lambda: eng.propose_pinned(ctx_h, off_h, len_h, CTX, out_h=out_h, chunks=c)))
-for c in (2, 3, 4, 5):
-    for tp in (1.0, 1.25, 1.6, 2.0):
-        print("pinned u16 chunks", c, "taper", tp, timed(lambda: eng.propose_pinned(ctx16_h, off_h, len_h, CTX, out_h=out_h, chunks=c, taper=tp)))
+for c in (4, 5, 6):
+    for tl in (None, 0.5, 0.3, 0.15):
+        print("pinned u16 chunks", c, "tail", tl, timed(lambda: eng.propose_pinned(ctx16_h, off_h, len_h, CTX, out_h=out_h, chunks=c, tail=tl)))
 
 # stream timeline of the pipelined call (chrome trace -> gpurun_out/)
 from torch.profiler import ProfilerActivity, profile
