@@ -53,7 +53,7 @@ def peaks() -> tuple[float, str]:
 
 
 def algorithmic_bytes(ranges: np.ndarray, p_cut: np.ndarray, sizes: np.ndarray, ctx_lens: np.ndarray,
-                      n: int, P: int, M: int) -> np.ndarray:
+                      n: int, P: int, M: int, parts: bool = False):
     """SURVEY.md 8(d) sector-granular algorithmic bytes per lookup:
     sum over evaluated p of 2*ceil(log2(n+1))*64 B (search probes: SA sector +
     token sector) + s_p * 96 B (SA sector + 2 token sectors per sample)
@@ -61,13 +61,17 @@ def algorithmic_bytes(ranges: np.ndarray, p_cut: np.ndarray, sizes: np.ndarray, 
     probes = 2 * int(np.ceil(np.log2(n + 1))) * 64
     B = ranges.shape[0]
     out = np.zeros(B, dtype=np.float64)
+    look = np.zeros(B, dtype=np.float64)
     pmax = np.minimum(P, ctx_lens)
     for b in range(B):
         tot = 0.0
         for p in range(int(pmax[b]), int(p_cut[b]) - 1, -1):
             lo, hi = ranges[b, p - 1]
             tot += probes + min(M, hi - lo) * 96
+        look[b] = tot
         out[b] = tot + 4 * ctx_lens[b] + 20 * sizes[b]
+    if parts:  # (total, lookup part, input-scan part, output part)
+        return out, look, 4.0 * ctx_lens.astype(np.float64), 20.0 * sizes.astype(np.float64)
     return out
 
 
@@ -228,8 +232,9 @@ def run_ours(args) -> None:
     # correctness spot check + algorithmic bytes (untimed pass with lookup diagnostics)
     out_lk = eng.propose(seq, off, ln, CTX, lookup=True)
     eng.check_status()
-    lk_bytes = algorithmic_bytes(out_lk.ranges.cpu().numpy(), out_lk.p_cut.cpu().numpy(),
-                                 out_lk.size.cpu().numpy(), ln.cpu().numpy(), N_TOKENS, cfg.P, cfg.M)
+    lk_bytes, lk_look, lk_scan, lk_out = algorithmic_bytes(
+        out_lk.ranges.cpu().numpy(), out_lk.p_cut.cpu().numpy(), out_lk.size.cpu().numpy(), ln.cpu().numpy(),
+        N_TOKENS, cfg.P, cfg.M, parts=True)
     bytes_per_step = float(lk_bytes.sum())
     mean_size = float(out_lk.size.float().mean().item())
 
@@ -369,6 +374,15 @@ def run_ours(args) -> None:
                          "scope": "whole propose step (SURVEY 8(d) algorithmic bytes of lookup + tree build)",
                          "algorithmic_bytes_per_lookup": round(bytes_per_step / B, 1), "peak_source": peak_src,
                          "kernel_ms": {n: round(float(x), 4) for n, x in zip(names, prof)},
+                         # per-kernel split of the same algorithmic bytes (search + samples ->
+                         # lookup incl. element folding, 4 B/token -> input scan, 20 B/node -> fusion)
+                         "per_kernel": {
+                             k: {"algorithmic_bytes_per_lookup": round(float(v.sum()) / B, 1),
+                                 "achieved_GBps": round(float(v.sum()) / (float(t) / 1e3) / 1e9, 1),
+                                 "frac": round(float(v.sum()) / (float(t) / 1e3) / 1e9 / peak, 4)}
+                             for k, v, t in (("ds_lookup_kernel", lk_look, prof[0]),
+                                             ("input_scan_kernel", lk_scan, prof[1]),
+                                             ("draft_ls_kernel", lk_out, prof[3]))},
                          "dominant_kernel": names[dom],
                          "dominant_share": round(float(prof[dom] / prof.sum()), 3)},
             "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
