@@ -64,11 +64,17 @@ out["throughput_lookups_per_s"] = round(B * R / thr * 1e3, 1)
 out["throughput_batch"] = f"{R} x {B} requests per launch, ctx {CTX}, dec_len 32"
 recs = workload.records(4096, 512, 256, V)
 t0 = time.perf_counter()
-rep = G.simulate([G.SimRecord(p, q) for p, q in recs], ds, cfg, slots=256)
-dt = time.perf_counter() - t0
+sims = [G.SimRecord(p, q) for p, q in recs]
+rep = G.simulate(sims, ds, cfg, slots=256)
+dt = rep.wall_seconds
+from paper_2411_05894_b200 import harness as H
+graphed = H.simulate.last_graph
+rep2 = G.simulate(sims, ds, cfg, slots=256, use_graph=False)
+assert [r.per_step_tokens for r in rep.records] == [r.per_step_tokens for r in rep2.records]
 out["decode_loop"] = {"records": 4096, "slots": 256, "prompt": 512, "reference": 256,
                       "mean_accepted_per_step": round(rep.mean_accepted_per_step, 4),
-                      "teacher_forced_tokens_per_s": round(4096 * 256 / dt, 1), "wall_s": round(dt, 2)}
+                      "teacher_forced_tokens_per_s": round(4096 * 256 / dt, 1), "wall_s": round(dt, 3),
+                      "cuda_graph": graphed, "eager_wall_s": round(rep2.wall_seconds, 3)}
 line = json.dumps(out)
 print(line)
 os.makedirs("gpurun_out", exist_ok=True)
