@@ -526,6 +526,7 @@ def bench_decode_cfg1(budget_s: float = 60.0) -> dict:
     return {"workload": "cfg1: B=8, 1M-token datastore, TINY decoder (2L h1024 GQA 8/2 d128 V32000, random init), "
                         "prompt 512, 256 new tokens, dec_len 30",
             "spec_tokens_per_s": round(r_spec["tokens_per_s"], 1), "spec_steps": r_spec["steps"],
+            "cuda_graph": bool(r_spec.get("cuda_graph")),
             "spec_accepted_per_step": round(r_spec["accepted_per_step"], 3),
             "autoregressive_tokens_per_s": round(r_ar["tokens_per_s"], 1),
             "sequences_identical_to_autoregressive": f"{same}/8",

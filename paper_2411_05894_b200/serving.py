@@ -57,6 +57,11 @@ class SpecDecoder:
                 torch.ones(B, dtype=torch.int32, device=self.seq.device))
 
     def step(self) -> torch.Tensor:
+        self._step()
+        self.steps += 1
+        return self.emitted
+
+    def _step(self) -> None:
         tokens, parents, depths, mask, size = self._draft()
         ctx = self.seq_len - 1
         pos = ctx.long()[:, None] + depths.clamp(min=0).long()
@@ -67,24 +72,65 @@ class SpecDecoder:
                                 ptr(self.off), ptr(self.seq_len), ptr(self.seq_cap), ptr(self.path),
                                 ptr(self.n_acc), ptr(self.bonus), ptr(self.emitted), stream_ptr(self.seq.device)))
         self.model.compact(ctx, self.path if S == self.S else self.path[:, :S].contiguous(), self.n_acc)
-        self.steps += 1
-        return self.emitted
 
-    def run(self) -> dict:
-        """Decode every slot to its cap; returns tokens, steps and timing."""
+    def run(self, graph_steps: int = 8) -> dict:
+        """Decode every slot to its cap; returns tokens, steps and timing.
+
+        The first step runs eagerly (it creates every lazily allocated buffer);
+        later steps run in groups of ``graph_steps`` replayed from one CUDA
+        graph with the sequence lengths after each step recorded on the device
+        and read back once per group (a finished slot's appends are capped, so
+        steps past the end change nothing).  graph_steps <= 1: eager steps."""
         torch.cuda.synchronize()
         t0 = perf_counter()
         start = self.seq_len.clone()
         per_step = []
-        while bool((self.seq_len < self.seq_cap).any()):
-            before = self.seq_len.clone()
+        cap = self.seq_cap.cpu()
+        lens = self.seq_len.cpu()
+        if bool((lens < cap).any()):
             self.step()
-            per_step.append((self.seq_len - before).cpu())
+            now = self.seq_len.cpu()
+            per_step.append(now - lens)
+            lens = now
+        graph = None
+        if graph_steps > 1 and bool((lens < cap).any()):
+            hist = torch.empty((graph_steps, self.model.B), dtype=torch.int32, device=self.seq.device)
+
+            def group() -> None:
+                for g in range(graph_steps):
+                    self._step()
+                    hist[g].copy_(self.seq_len)
+
+            try:
+                torch.cuda.synchronize()
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, capture_error_mode="thread_local"):
+                    group()
+            except Exception as exc:  # capture not possible here: eager steps (same results)
+                torch.cuda.synchronize()
+                graph = None
+                self.graph_error = repr(exc)
+        while bool((lens < cap).any()):
+            if graph is None:
+                self.step()
+                now = self.seq_len.cpu()
+                per_step.append(now - lens)
+                lens = now
+                continue
+            graph.replay()
+            H = hist.cpu()
+            for g in range(graph_steps):
+                if not bool((lens < cap).any()):
+                    break  # trailing steps after every slot finished are not counted
+                per_step.append(H[g] - lens)
+                lens = H[g]
+                self.steps += 1
         torch.cuda.synchronize()
         dt = perf_counter() - t0
         gen = int((self.seq_len - start).sum())
         return {"tokens": gen, "steps": self.steps, "seconds": dt, "tokens_per_s": gen / dt,
-                "accepted_per_step": float(torch.stack(per_step).float().mean()) if per_step else 0.0}
+                "accepted_per_step": float(torch.stack(per_step).float().mean()) if per_step else 0.0,
+                "cuda_graph": graph is not None}
 
     def sequences(self) -> list[list[int]]:
         s = self.seq.view(self.model.B, self.cap).cpu().numpy().view(np.uint32)
