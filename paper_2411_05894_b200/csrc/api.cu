@@ -399,9 +399,13 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
     KCfg kk = k;
     kk.b0 = b0;
     kk.b1 = b1;
-    ds_lookup_kernel<<<b1 - b0, 32 * cfg->P, 4 * ds_lookup_smem_words(cfg->P, cfg->M), s>>>(*ds, *seqs, kk, w.ds_tab, w.ds_len, w.ds_el, w.ds_n, lk,
-                                                       w.ds_raw, w.ds_idx, w.ds_idx_cap, w.ds_cols, pre_bounds,
-                                                       pre_rows);
+    if (!cfg->has_separator && !pre_bounds)  // one warp per request, lane groups per p
+      ds_lookup_warp_kernel<<<(b1 - b0 + 3) / 4, 128, 0, s>>>(*ds, *seqs, kk, w.ds_tab, w.ds_len, w.ds_el, w.ds_n,
+                                                                lk, w.ds_cols);
+    else
+      ds_lookup_kernel<<<b1 - b0, 32 * cfg->P, 4 * ds_lookup_smem_words(cfg->P, cfg->M), s>>>(
+          *ds, *seqs, kk, w.ds_tab, w.ds_len, w.ds_el, w.ds_n, lk, w.ds_raw, w.ds_idx, w.ds_idx_cap, w.ds_cols,
+          pre_bounds, pre_rows);
     if (ds_dedupe_enabled(kk))
       ds_dedupe_kernel<<<b1 - b0, 128, 4 * (cfg->P * cfg->M + 1), s>>>(kk, w.ds_tab, w.ds_el, w.ds_n, w.ds_cols);
   };
@@ -555,9 +559,16 @@ int sssd_ds_lookup(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg
   sssd_elem* raw = static_cast<sssd_elem*>(workspace);
   uint32_t* idx = reinterpret_cast<uint32_t*>(
       align_up(reinterpret_cast<uintptr_t>(raw + (size_t)seqs->B * cfg->P * cfg->M), 256));
-  ds_lookup_kernel<<<seqs->B, 32 * cfg->P, 4 * ds_lookup_smem_words(cfg->P, cfg->M), static_cast<cudaStream_t>(stream)>>>(
-      *ds, *seqs, kcfg(cfg), tab, lens, el, n_el, lk, raw, idx, ds_idx_cap(cfg->P, cfg->M), Cols{}, nullptr,
-      nullptr);
+  KCfg kk = kcfg(cfg);
+  kk.b0 = 0;
+  kk.b1 = seqs->B;
+  if (!cfg->has_separator)
+    ds_lookup_warp_kernel<<<(seqs->B + 3) / 4, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        *ds, *seqs, kk, tab, lens, el, n_el, lk, Cols{});
+  else
+    ds_lookup_kernel<<<seqs->B, 32 * cfg->P, 4 * ds_lookup_smem_words(cfg->P, cfg->M),
+                       static_cast<cudaStream_t>(stream)>>>(*ds, *seqs, kk, tab, lens, el, n_el, lk, raw, idx,
+                                                            ds_idx_cap(cfg->P, cfg->M), Cols{}, nullptr, nullptr);
   return cuda_check(cudaGetLastError(), "ds_lookup_kernel launch");
 }
 

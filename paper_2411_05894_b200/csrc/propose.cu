@@ -506,6 +506,277 @@ __global__ void __launch_bounds__(128)
 }
 
 // --------------------------------------------------------------------------
+// K2+K3, one warp per request (the default without a separator): every prefix
+// length is searched at the same time by its own group of lanes (a
+// (32/groups + 1)-ary search per p), so no warp waits at a CTA barrier for the
+// other p's and four times as many requests are in flight per SM as with one
+// warp per p.  Same outputs as ds_lookup_kernel (ref datastore.py:156-218).
+// --------------------------------------------------------------------------
+
+constexpr int kLkWarps = 4;     // requests per CTA
+constexpr int kLkStage = 64;    // staged suffix rows per warp and round (2 per lane)
+
+__global__ void __launch_bounds__(32 * kLkWarps)
+    ds_lookup_warp_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, uint32_t* ds_tab, uint8_t* ds_len,
+                          sssd_elem* ds_el, int32_t* ds_n, sssd_lookup_out lk, Cols cols) {
+  __shared__ __align__(16) uint32_t s_stage[kLkWarps][kLkStage * kRowStride];
+  __shared__ uint32_t s_tail[kLkWarps][SSSD_MAX_P];
+  __shared__ uint64_t s_rlo[kLkWarps][SSSD_MAX_P], s_rhi[kLkWarps][SSSD_MAX_P];
+  __shared__ int s_cnt[kLkWarps][SSSD_MAX_P];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int b = c.b0 + blockIdx.x * kLkWarps + warp;
+  if (b >= c.b1) return;  // (warp-uniform)
+  const int L = seqs.seq_len[b];
+  const uint32_t* seq = seqs.seq + seqs.seq_off[b];
+  const int pmax = min(c.P, L);
+  uint32_t* tail = s_tail[warp];
+  if (lane < pmax) tail[lane] = seq[L - pmax + lane];
+  if (lane < SSSD_MAX_P) s_cnt[warp][lane] = -1;
+  __syncwarp();
+
+  // first-token bracket of pattern p (its first token is tail[pmax - p])
+  auto bracket = [&](int p, uint64_t& blo, uint64_t& bhi) {
+    blo = 0;
+    bhi = ds.n_rows;
+    if (ds.bucket && p >= 1) {
+      const uint32_t t0 = tail[pmax - p];
+      if (t0 < ds.n_buckets) {
+        blo = ds.bucket[t0];
+        bhi = ds.bucket[t0 + 1];
+      } else {
+        blo = ds.bucket[ds.n_buckets];
+      }
+    }
+  };
+  // p = 1 needs no probe when its token has a bucket
+  const bool p1_free = pmax >= 1 && ds.bucket && tail[pmax - 1] < ds.n_buckets;
+  const int ng = pmax - (p1_free ? 1 : 0);  // patterns searched: p = pmax, pmax-1, ...
+  if (lane == 0 && p1_free) {
+    uint64_t a, z;
+    bracket(1, a, z);
+    s_rlo[warp][0] = a;
+    s_rhi[warp][0] = z;
+  }
+  if (ng > 0) {
+    const int gs = 32 / ng;
+    const int gid = lane / gs, gl = lane - gid * gs;
+    const bool active = gid < ng;
+    const int myp = active ? pmax - gid : 1;
+    const uint32_t* pat = tail + (pmax - myp);
+    const uint32_t gbits = gs >= 32 ? 0xffffffffu : ((1u << gs) - 1u);
+    const int gbase = active ? gid * gs : 0;
+    uint64_t lo, hi;
+    bracket(myp, lo, hi);
+    uint64_t ulo = lo, uhi = hi;
+    uint64_t q = 0;
+    // my group's first satisfying lane j -> bracket update (all lanes execute the shuffles)
+    auto upd = [&](uint32_t mask, bool apply, uint64_t& l, uint64_t& h) {
+      const uint32_t m = active ? (mask >> gbase) & gbits : 0u;
+      const int j = m ? __ffs(m) - 1 : gs;
+      const uint64_t qb = __shfl_sync(SSSD_FULL, q, gbase + min(j, gs - 1));
+      const uint64_t qa = __shfl_sync(SSSD_FULL, q, gbase + max(j - 1, 0));
+      if (apply) {
+        if (j == gs) {
+          l = max(l, qb + 1);
+        } else {
+          h = min(h, qb);
+          if (j > 0) l = max(l, qa + 1);
+        }
+      }
+    };
+    // lower bound (pred c >= 0), tightening the upper bracket (c > 0) from the same probes
+    while (true) {
+      const bool need = active && hi - lo > (uint64_t)gs;
+      if (!__any_sync(SSSD_FULL, need)) break;
+      int cv = 2;
+      if (need) {
+        q = lo + ((hi - lo) * (uint64_t)(gl + 1)) / (uint64_t)(gs + 1);
+        cv = cmp_rank(ds, q, pat, myp);
+      }
+      const uint32_t ge = __ballot_sync(SSSD_FULL, need && cv >= 0);
+      const uint32_t gt = __ballot_sync(SSSD_FULL, need && cv > 0);
+      upd(ge, need, lo, hi);
+      upd(gt, need, ulo, uhi);
+    }
+    uint64_t lower;
+    {
+      const uint64_t w = hi - lo;
+      const bool v = active && (uint64_t)gl < w;
+      q = lo + gl;
+      const int cv = v ? cmp_rank(ds, q, pat, myp) : 2;
+      const uint32_t ge = (__ballot_sync(SSSD_FULL, v && cv >= 0) >> gbase) & gbits;
+      const uint32_t gt = (__ballot_sync(SSSD_FULL, v && cv > 0) >> gbase) & gbits;
+      lower = lo + (ge ? (uint64_t)(__ffs(ge) - 1) : w);
+      if (gt) {
+        const uint64_t tb = lo + (uint64_t)(__ffs(gt) - 1);
+        uhi = min(uhi, tb);
+        ulo = max(ulo, tb);
+      } else {
+        ulo = max(ulo, lo + w);
+      }
+    }
+    // upper bound (pred c > 0) from the tightened bracket
+    lo = max(ulo, lower);
+    hi = uhi;
+    while (true) {
+      const bool need = active && hi - lo > (uint64_t)gs;
+      if (!__any_sync(SSSD_FULL, need)) break;
+      int cv = 2;
+      if (need) {
+        q = lo + ((hi - lo) * (uint64_t)(gl + 1)) / (uint64_t)(gs + 1);
+        cv = cmp_rank(ds, q, pat, myp);
+      }
+      const uint32_t gt = __ballot_sync(SSSD_FULL, need && cv > 0);
+      upd(gt, need, lo, hi);
+    }
+    uint64_t upper;
+    {
+      const uint64_t w = hi - lo;
+      const bool v = active && (uint64_t)gl < w;
+      q = lo + gl;
+      const int cv = v ? cmp_rank(ds, q, pat, myp) : 2;
+      const uint32_t gt = (__ballot_sync(SSSD_FULL, v && cv > 0) >> gbase) & gbits;
+      upper = lo + (gt ? (uint64_t)(__ffs(gt) - 1) : w);
+    }
+    if (active && gl == 0) {
+      s_rlo[warp][myp - 1] = lower;
+      s_rhi[warp][myp - 1] = upper;
+    }
+  }
+  __syncwarp();
+  if (lk.ranges && lane < c.P) {
+    const bool ok = lane < pmax;
+    lk.ranges[((size_t)b * c.P + lane) * 2] = ok ? (int64_t)(s_rlo[warp][lane] + ds.rank_base) : -1;
+    lk.ranges[((size_t)b * c.P + lane) * 2 + 1] = ok ? (int64_t)(s_rhi[warp][lane] + ds.rank_base) : -1;
+  }
+
+  uint32_t* tab = ds_tab + (size_t)b * c.P * c.M * c.BL;
+  uint8_t* lens = ds_len + (size_t)b * c.P * c.M;
+  int64_t* smp = lk.samples ? lk.samples + (size_t)b * c.P * c.M : nullptr;
+  uint32_t* stage = s_stage[warp];
+
+  // T cut-off (ref datastore.py:216-217): p = pmax, pmax-1, ... in batches sized
+  // by the sample-count upper bound, gathered p by p (rows staged with cp.async,
+  // two per lane per round)
+  int cum = 0, next = pmax, pcut = 1;
+  while (next >= 1) {
+    int ub = 0, qq = next;
+    for (; qq >= 1; --qq) {
+      ub += (int)min(s_rhi[warp][qq - 1] - s_rlo[warp][qq - 1], (uint64_t)c.M);
+      if (cum + ub >= c.T) break;
+    }
+    const int blo = max(qq, 1);
+    bool done = false;
+    for (int p = next; p >= blo; --p) {
+      const uint64_t lo = s_rlo[warp][p - 1], w = s_rhi[warp][p - 1] - lo;
+      const int sc = (int)min(w, (uint64_t)c.M);
+      uint32_t* ptab = tab + (size_t)(p - 1) * c.M * c.BL;
+      uint8_t* plen = lens + (size_t)(p - 1) * c.M;
+      int cnt = 0;
+      for (int k00 = 0; k00 < sc; k00 += kLkStage) {
+        for (int u = 0; u < kLkStage / 32; ++u) {
+          const int k = k00 + 32 * u + lane;
+          if (k < sc) {
+            const uint64_t r = lo + (w <= (uint64_t)c.M ? (uint64_t)k : ((uint64_t)k * w) / (uint64_t)c.M);
+            const uint4* row = reinterpret_cast<const uint4*>(ds.rows) + r * 4;
+            uint4* sr = reinterpret_cast<uint4*>(stage + (u * 32 + lane) * kRowStride);
+#pragma unroll
+            for (int h = 0; h < 4; ++h) cp_async16(sr + h, row + h);
+          }
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        for (int u = 0; u < kLkStage / 32; ++u) {
+          const int k0 = k00 + 32 * u;
+          if (k0 >= sc) break;
+          const int k = k0 + lane;
+          const uint32_t* srow = stage + (u * 32 + lane) * kRowStride;
+          uint32_t len = 0, pos = 0;
+          if (k < sc) {
+            pos = srow[0];
+            if (smp) smp[(size_t)(p - 1) * c.M + k] = (int64_t)pos;
+            const uint64_t start = (uint64_t)pos + p;
+            const uint64_t avail = ds.n_tokens > start ? ds.n_tokens - start : 0;
+            len = (uint32_t)min((uint64_t)c.BL, avail);  // (no separator on this path)
+          }
+          const bool ne = len > 0;
+          const uint32_t bal = __ballot_sync(SSSD_FULL, ne);
+          if (ne) {
+            const int idx = cnt + __popc(bal & lanemask_lt());
+            const uint64_t start = (uint64_t)pos + p;
+            uint32_t* dst = ptab + (size_t)idx * c.BL;
+            for (uint32_t j = 0; j < len; ++j)
+              dst[j] = (p + j < SSSD_ROW_TOKENS) ? srow[1 + p + j] : __ldg(ds.tokens + start + j);
+            plen[idx] = (uint8_t)len;
+          }
+          cnt += __popc(bal);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) s_cnt[warp][p - 1] = cnt;
+      cum += cnt;
+      if (cum >= c.T) {
+        pcut = p;
+        done = true;
+        break;
+      }
+    }
+    __syncwarp();
+    if (done) break;
+    pcut = blo;
+    next = blo - 1;
+  }
+  if (pmax == 0) pcut = 1;
+
+  // merge the included runs (each sorted: SA order = order of the cut
+  // continuations without a separator): rank = index + binary-searched counts
+  // of the other runs (ties: the larger p's run first = list position order)
+  int n_all = 0;
+  for (int q = pcut; q <= pmax; ++q) n_all += s_cnt[warp][q - 1];
+  const bool dedupe = cols.meta && ds_dedupe_enabled(c);
+  const Cols cb{cols.meta ? cols.meta + (size_t)b * cols.stride : nullptr, cols.orig + (size_t)b * cols.stride,
+                cols.tok + (size_t)b * cols.stride * c.BL, cols.stride};
+  int before = 0;
+  for (int p = pmax; p >= pcut; --p) {
+    const int cnt = s_cnt[warp][p - 1];
+    for (int i = lane; i < cnt; i += 32) {
+      const uint32_t* si = tab + ((size_t)(p - 1) * c.M + i) * c.BL;
+      const uint32_t li = lens[(size_t)(p - 1) * c.M + i];
+      int rank = i;
+      for (int q = pcut; q <= pmax; ++q) {
+        if (q == p) continue;
+        int a = 0, z = s_cnt[warp][q - 1];
+        while (a < z) {
+          const int mid = (a + z) >> 1;
+          const int r = cmp_str(tab + ((size_t)(q - 1) * c.M + mid) * c.BL, lens[(size_t)(q - 1) * c.M + mid], si, li);
+          const bool before_i = q > p ? r <= 0 : r < 0;
+          if (before_i) a = mid + 1;
+          else z = mid;
+        }
+        rank += a;
+      }
+      sssd_elem e;
+      e.off = (uint32_t)(((size_t)(p - 1) * c.M + i) * c.BL);
+      e.orig = (uint32_t)(before + i);
+      e.len_m = li | (255u << 8);
+      e.pad = 0;
+      ds_el[(size_t)b * c.P * c.M + rank] = e;
+      if (cb.meta && !dedupe) write_cols(cb, rank, e, tab);
+    }
+    before += cnt;
+  }
+  if (lane == 0) {
+    ds_n[b] = n_all;
+    if (lk.p_cut) lk.p_cut[b] = pmax > 0 ? pcut : 0;
+  }
+  if (lk.n_conts && lane < c.P) {
+    const int q = lane + 1;
+    const int v = (q <= pmax && q >= pcut) ? s_cnt[warp][lane] : -1;
+    lk.n_conts[(size_t)b * c.P + lane] = (q <= pmax && s_cnt[warp][lane] >= 0) ? v : -1;
+  }
+}
+
+// --------------------------------------------------------------------------
 // SA-range sharding: local bounds per shard, then the
 // owning shard copies each sampled suffix row into an exchange buffer
 // --------------------------------------------------------------------------

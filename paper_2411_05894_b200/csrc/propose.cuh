@@ -28,6 +28,8 @@ __global__ void ds_lookup_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, uint32_t* d
 // datastore element folding for the level-synchronous fusion (weights <= 65535)
 __host__ __device__ inline bool ds_dedupe_enabled(const KCfg& c) { return c.fusion == 0 && c.P * c.M <= 12000; }
 __global__ void ds_dedupe_kernel(KCfg c, const uint32_t* ds_tab, const sssd_elem* ds_el, int32_t* ds_n, Cols cols);
+__global__ void ds_lookup_warp_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, uint32_t* ds_tab, uint8_t* ds_len,
+                                      sssd_elem* ds_el, int32_t* ds_n, sssd_lookup_out lk, Cols cols);
 __global__ void shard_search_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, int64_t* bounds);
 __global__ void shard_gather_kernel(sssd_ds ds, KCfg c, int B, const int64_t* gbounds, uint32_t* xrows);
 
