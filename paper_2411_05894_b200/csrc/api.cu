@@ -406,7 +406,7 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
       ds_lookup_kernel<<<b1 - b0, 32 * cfg->P, 4 * ds_lookup_smem_words(cfg->P, cfg->M), s>>>(
           *ds, *seqs, kk, w.ds_tab, w.ds_len, w.ds_el, w.ds_n, lk, w.ds_raw, w.ds_idx, w.ds_idx_cap, w.ds_cols,
           pre_bounds, pre_rows);
-    if (ds_dedupe_enabled(kk))
+    if (ds_dedupe_enabled(kk) && (cfg->has_separator || pre_bounds))  // (the warp kernel folds itself)
       ds_dedupe_kernel<<<b1 - b0, 128, 4 * (cfg->P * cfg->M + 1), s>>>(kk, w.ds_tab, w.ds_el, w.ds_n, w.ds_cols);
   };
   auto launch_scan = [&](cudaStream_t s, int b0, int b1) {

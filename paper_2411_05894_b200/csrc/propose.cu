@@ -733,7 +733,9 @@ __global__ void __launch_bounds__(32 * kLkWarps)
   // of the other runs (ties: the larger p's run first = list position order)
   int n_all = 0;
   for (int q = pcut; q <= pmax; ++q) n_all += s_cnt[warp][q - 1];
-  const bool dedupe = cols.meta && ds_dedupe_enabled(c);
+  // folding of identical continuations (see ds_dedupe_kernel) happens below,
+  // in this warp, when the group starts fit the staging area
+  const bool dedupe = cols.meta && ds_dedupe_enabled(c) && n_all + 1 <= kLkStage * kRowStride;
   const Cols cb{cols.meta ? cols.meta + (size_t)b * cols.stride : nullptr, cols.orig + (size_t)b * cols.stride,
                 cols.tok + (size_t)b * cols.stride * c.BL, cols.stride};
   int before = 0;
@@ -765,8 +767,41 @@ __global__ void __launch_bounds__(32 * kLkWarps)
     }
     before += cnt;
   }
+  int n_out = n_all;
+  if (dedupe) {
+    __syncwarp();  // the sorted elements above are this warp's own global writes
+    int* gst = reinterpret_cast<int*>(stage);
+    const sssd_elem* sorted = ds_el + (size_t)b * c.P * c.M;
+    int G = 0;
+    for (int r0 = 0; r0 < n_all; r0 += 32) {
+      const int r = r0 + lane;
+      bool st = false;
+      if (r < n_all) {
+        if (r == 0) {
+          st = true;
+        } else {
+          const sssd_elem x = sorted[r - 1], y = sorted[r];
+          st = cmp_str(tab + x.off, el_len(x.len_m), tab + y.off, el_len(y.len_m)) != 0;
+        }
+      }
+      const uint32_t sm = __ballot_sync(SSSD_FULL, st);
+      if (st) gst[G + __popc(sm & lanemask_lt())] = r;
+      G += __popc(sm);
+    }
+    if (lane == 0) gst[G] = n_all;
+    __syncwarp();
+    for (int g = lane; g < G; g += 32) {
+      const sssd_elem e = sorted[gst[g]];
+      write_cols(cb, g, e, tab);
+      cb.meta[g] = (e.len_m & 0xffffu) | (uint32_t)(gst[g + 1] - gst[g]) << 16;
+    }
+    n_out = G;
+  } else if (cb.meta && ds_dedupe_enabled(c)) {
+    __syncwarp();  // (too many continuations to fold here: weight 1 each)
+    for (int r = lane; r < n_all; r += 32) write_cols(cb, r, ds_el[(size_t)b * c.P * c.M + r], tab);
+  }
   if (lane == 0) {
-    ds_n[b] = n_all;
+    ds_n[b] = n_out;
     if (lk.p_cut) lk.p_cut[b] = pmax > 0 ? pcut : 0;
   }
   if (lk.n_conts && lane < c.P) {
