@@ -14,7 +14,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-extra --no-cpu-baseline \
   > gpurun_out/launches_bench.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none \
-  -k regex:"ds_lookup|ds_dedupe|input_scan|propose_setup|lpt_scatter|draft_ls_kernel" -c 6 \
+  -k regex:"ds_lookup|input_scan|propose_setup|lpt_scatter|draft_ls_kernel" -c 5 \
   -o gpurun_out/propose_full python tools/profile_propose.py 256 1 > gpurun_out/propose_full.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:tree_attn -c 2 \
   -o gpurun_out/attn_full python tools/profile_attn.py > gpurun_out/attn_full.log 2>&1
