@@ -514,9 +514,15 @@ __global__ void __launch_bounds__(128)
 // --------------------------------------------------------------------------
 
 constexpr int kLkWarps = 4;     // requests per CTA
-constexpr int kLkStage = 64;    // staged suffix rows per warp and round (2 per lane)
+#ifndef SSSD_LK_STAGE
+#define SSSD_LK_STAGE 64
+#endif
+constexpr int kLkStage = SSSD_LK_STAGE;  // staged suffix rows per warp and round (2 per lane)
 
-__global__ void __launch_bounds__(32 * kLkWarps)
+#ifndef SSSD_LKW_MINB
+#define SSSD_LKW_MINB 1
+#endif
+__global__ void __launch_bounds__(32 * kLkWarps, SSSD_LKW_MINB)
     ds_lookup_warp_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, uint32_t* ds_tab, uint8_t* ds_len,
                           sssd_elem* ds_el, int32_t* ds_n, sssd_lookup_out lk, Cols cols) {
   __shared__ __align__(16) uint32_t s_stage[kLkWarps][kLkStage * kRowStride];

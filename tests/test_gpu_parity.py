@@ -370,7 +370,7 @@ def test_propose_large_token_ids(ibl):
 @pytest.mark.parametrize("dec_len,P,ibl,bl,sep,src", [
     (1, 4, 8, None, None, "both"), (2, 4, 8, None, None, "both"), (3, 8, 8, None, 3, "both"),
     (40, 8, 20, 12, 5, "both"), (64, 3, 32, 6, None, "input"), (64, 6, 4, 16, 2, "datastore"),
-    (130, 2, 12, 10, None, "both")])
+    (130, 2, 12, 10, None, "both"), (48, 8, 8, 12, None, "datastore"), (64, 7, 8, 8, None, "both")])
 def test_fusion_edge_configs(monkeypatch, dec_len, P, ibl, bl, sep, src):
     """Edge configurations through both fusion kernels and the oracle: tiny
     budgets (dec_len 1-3), P = 8 (the compiled maximum), deep input trees
