@@ -399,14 +399,16 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
     KCfg kk = k;
     kk.b0 = b0;
     kk.b1 = b1;
-    if (!cfg->has_separator && !pre_bounds)  // one warp per request, lane groups per p
+    // one warp per request (lane groups per p) for throughput; small batches
+    // keep one warp per p (lower latency per request when SMs are idle)
+    if (!cfg->has_separator && !pre_bounds && b1 - b0 >= 2048)
       ds_lookup_warp_kernel<<<(b1 - b0 + 3) / 4, 128, 0, s>>>(*ds, *seqs, kk, w.ds_tab, w.ds_len, w.ds_el, w.ds_n,
                                                                 lk, w.ds_cols);
     else
       ds_lookup_kernel<<<b1 - b0, 32 * cfg->P, 4 * ds_lookup_smem_words(cfg->P, cfg->M), s>>>(
           *ds, *seqs, kk, w.ds_tab, w.ds_len, w.ds_el, w.ds_n, lk, w.ds_raw, w.ds_idx, w.ds_idx_cap, w.ds_cols,
           pre_bounds, pre_rows);
-    if (ds_dedupe_enabled(kk) && (cfg->has_separator || pre_bounds))  // (the warp kernel folds itself)
+    if (ds_dedupe_enabled(kk) && (cfg->has_separator || pre_bounds || b1 - b0 < 2048))  // (the warp kernel folds itself)
       ds_dedupe_kernel<<<b1 - b0, 128, 4 * (cfg->P * cfg->M + 1), s>>>(kk, w.ds_tab, w.ds_el, w.ds_n, w.ds_cols);
   };
   auto launch_scan = [&](cudaStream_t s, int b0, int b1) {
