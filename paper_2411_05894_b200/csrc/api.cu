@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <string>
 
@@ -424,7 +425,8 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
     KCfg kk = k;
     kk.b0 = b0;
     kk.b1 = b1;
-    const bool lpt = b0 == 0 && b1 == B && B >= 2048;  // order only pays with several waves
+    static const bool no_lpt = getenv("SSSD_NO_LPT") != nullptr;  // A/B switch
+    const bool lpt = !no_lpt && b0 == 0 && b1 == B && B >= 2048;  // order only pays with several waves
     propose_setup_kernel<<<(b1 - b0 + 127) / 128, 128, 0, s>>>(*seqs, kk, w.ds_cols, w.ds_n, w.in_cols,
                                                                  w.in_n, w.d.desc, w.d.root,
                                                                  lpt ? w.d.bucket : nullptr, w.d.hist);
@@ -441,7 +443,7 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
     KCfg kk = k;
     kk.b0 = 0;
     kk.b1 = B;
-    const bool lpt = B >= 2048;
+    const bool lpt = getenv("SSSD_NO_LPT") == nullptr && B >= 2048;
     propose_setup_kernel<<<(B + 127) / 128, 128, 0, st>>>(*seqs, kk, w.ds_cols, w.ds_n, w.in_cols, w.in_n,
                                                             w.d.desc, w.d.root, lpt ? w.d.bucket : nullptr,
                                                             w.d.hist);
