@@ -285,6 +285,21 @@ int sssd_tree_attention(const uint16_t* q, const uint16_t* k, const uint16_t* v,
                         uint16_t* o, void* workspace, size_t workspace_bytes, void* stream);
 size_t sssd_tree_attention_workspace(int32_t B, int32_t S, int32_t Hq, int32_t max_pos);
 
+/* ------------------------------------------------------------------------ */
+/* Fused elementwise stages of the verification forward (bf16 tensors;      */
+/* the projections around them are cuBLAS GEMMs)                            */
+/* ------------------------------------------------------------------------ */
+/* y[r] = x[r] * rsqrt(mean(x[r]^2) + eps) * w, h % 8 == 0 */
+int sssd_rmsnorm_bf16(const void* x, const void* w, void* y, int64_t rows, int32_t h, float eps, void* stream);
+/* qkv [b*S][(hq + 2 hkv) d] (fused projection) -> rotary q into q_out [b][S][hq][d]; rotary k and v
+ * into the caches [B][hkv][max_pos][d] at row rows[i] (NULL = i), slot ctx_len[i] + s;
+ * pos [b][S] int64 positions, theta = rope base. */
+int sssd_rope_kv_bf16(const void* qkv, const int64_t* pos, const int32_t* ctx_len, const int64_t* rows,
+                      void* q_out, void* k_cache, void* v_cache, int32_t b, int32_t S, int32_t hq, int32_t hkv,
+                      int32_t d, int32_t max_pos, float theta, void* stream);
+/* a[r][j] = silu(gu[r][j]) * gu[r][m + j] (fused gate|up projection) */
+int sssd_swiglu_bf16(const void* gu, void* a, int64_t rows, int32_t m, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

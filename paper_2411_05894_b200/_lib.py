@@ -70,6 +70,10 @@ _SIGS = {
     "sssd_rows_sa64": (C.c_int, [vp, C.c_uint64, vp, vp]),
     "sssd_bucket_build": (C.c_int, [vp, C.c_uint64, C.c_uint32, vp, vp]),
     "sssd_widen_u16": (C.c_int, [vp, vp, C.c_int64, vp]),
+    "sssd_rmsnorm_bf16": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int32, C.c_float, vp]),
+    "sssd_rope_kv_bf16": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                    C.c_int32, C.c_int32, C.c_float, vp]),
+    "sssd_swiglu_bf16": (C.c_int, [vp, vp, C.c_int64, C.c_int32, vp]),
     "sssd_propose_workspace": (C.c_size_t, [C.POINTER(Cfg), C.c_int32, C.c_int32]),
     "sssd_propose": (C.c_int, [C.POINTER(Ds), C.POINTER(Seqs), C.POINTER(Cfg), C.POINTER(DraftOut),
                                C.POINTER(LookupOut), vp, C.c_size_t, vp]),

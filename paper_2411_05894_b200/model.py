@@ -6,8 +6,9 @@ The reference has no model; its oracle protocol (ref draft.py:29-32
 drafts in ONE forward: the draft tokens are run at positions L-1+depth, their
 K/V rows are written to the cache at [ctx, ctx+S), and attention is the
 tcgen05 tree kernel (prefix + ancestor-or-self mask).  Dense projections use
-cuBLAS through torch (plain library GEMMs); RMSNorm / RoPE / SwiGLU are
-elementwise torch ops.
+cuBLAS through torch (plain library GEMMs; q|k|v and gate|up fused into one
+GEMM each, residual adds folded into addmm); RMSNorm, RoPE + the KV-cache
+write, and SwiGLU are one-pass kernels of csrc/layers.cu.
 
 Specs:
   TINY       2 layers, h=1024, n_q=8, n_kv=2, d=128, SwiGLU 2816, V=32000
@@ -21,6 +22,7 @@ from dataclasses import dataclass
 
 import torch
 
+from ._lib import check, lib, ptr, stream_ptr
 from .verify import kv_compact, tree_attention
 
 
@@ -74,16 +76,26 @@ class Decoder:
         self.embed = w(spec.vocab, h, scale=1.0)
         self.layers = []
         for _ in range(spec.n_layers):
+            wq = w(h, spec.n_q * d, scale=1 / math.sqrt(h))
+            wk = w(h, spec.n_kv * d, scale=1 / math.sqrt(h))
+            wv = w(h, spec.n_kv * d, scale=1 / math.sqrt(h))
+            wo = w(spec.n_q * d, h, scale=1 / math.sqrt(spec.n_q * d))
+            wg = w(h, spec.mlp, scale=1 / math.sqrt(h))
+            wu = w(h, spec.mlp, scale=1 / math.sqrt(h))
+            wd = w(spec.mlp, h, scale=1 / math.sqrt(spec.mlp))
+            # fused projections (one GEMM for q|k|v, one for gate|up); the
+            # per-projection names stay available as column views
+            wqkv = torch.cat([wq, wk, wv], dim=1)
+            wgu = torch.cat([wg, wu], dim=1)
+            del wq, wk, wv, wg, wu
+            nq, nk = spec.n_q * d, spec.n_kv * d
             self.layers.append({
                 "n1": torch.ones(h, dtype=dtype, device=self.device),
-                "wq": w(h, spec.n_q * d, scale=1 / math.sqrt(h)),
-                "wk": w(h, spec.n_kv * d, scale=1 / math.sqrt(h)),
-                "wv": w(h, spec.n_kv * d, scale=1 / math.sqrt(h)),
-                "wo": w(spec.n_q * d, h, scale=1 / math.sqrt(spec.n_q * d)),
+                "wqkv": wqkv, "wq": wqkv[:, :nq], "wk": wqkv[:, nq:nq + nk], "wv": wqkv[:, nq + nk:],
+                "wo": wo,
                 "n2": torch.ones(h, dtype=dtype, device=self.device),
-                "wg": w(h, spec.mlp, scale=1 / math.sqrt(h)),
-                "wu": w(h, spec.mlp, scale=1 / math.sqrt(h)),
-                "wd": w(spec.mlp, h, scale=1 / math.sqrt(spec.mlp)),
+                "wgu": wgu, "wg": wgu[:, :spec.mlp], "wu": wgu[:, spec.mlp:],
+                "wd": wd,
             })
         self.norm = torch.ones(h, dtype=dtype, device=self.device)
         self.lm_head = w(h, spec.vocab, scale=1 / math.sqrt(h))
@@ -96,33 +108,39 @@ class Decoder:
         """Tree forward: tokens / positions [b, S] (rows = cache rows of these b
         requests, default all), mask [b, S, W] int64, ctx_len [b] int32 = committed
         tokens already in the cache.  Writes K/V of the S tokens to cache
-        positions ctx..ctx+S-1 and returns logits [b, S, V] (fp32)."""
+        positions ctx..ctx+S-1 and returns logits [b, S, V] (bf16, the GEMM's
+        fp32 accumulators rounded once; argmax over them equals argmax over
+        their exact fp32 widening)."""
         sp = self.spec
         b, S = tokens.shape
-        rows = torch.arange(self.B, device=self.device) if rows is None else rows
-        d = sp.head_dim
-        x = self.embed[tokens.long()]  # [b, S, h]
-        slot = ctx_len.long()[:, None] + torch.arange(S, device=self.device)[None, :]  # [b, S]
-        bi = rows.long()[:, None].expand(b, S)
+        d, h = sp.head_dim, sp.hidden
+        n = b * S
+        st = stream_ptr(self.device)
+        x = self.embed[tokens.reshape(-1).long()]  # [b*S, h]
+        pos = positions.reshape(-1).long().contiguous()
+        ctx = ctx_len.to(torch.int32).contiguous()
+        rows_l = rows.long().contiguous() if rows is not None else None
+        hN = torch.empty_like(x)
+        q = torch.empty(b, S, sp.n_q, d, dtype=self.dtype, device=self.device)
         for li, L in enumerate(self.layers):
-            hN = _rmsnorm(x, L["n1"], sp.eps)
-            q = (hN @ L["wq"]).view(b, S, sp.n_q, d)
-            k = (hN @ L["wk"]).view(b, S, sp.n_kv, d)
-            v = (hN @ L["wv"]).view(b, S, sp.n_kv, d)
-            q = _rope(q, positions, sp.rope_theta).to(self.dtype).contiguous()
-            k = _rope(k, positions, sp.rope_theta).to(self.dtype)
+            check(lib().sssd_rmsnorm_bf16(ptr(x), ptr(L["n1"]), ptr(hN), n, h, sp.eps, st))
+            qkv = hN @ L["wqkv"]
             kc, vc = self.k_cache[li], self.v_cache[li]
-            kc[bi, :, slot] = k
-            vc[bi, :, slot] = v
-            if rows.numel() == self.B:
-                o = tree_attention(q, kc, vc, mask, ctx_len.to(torch.int32), self.scale)
+            check(lib().sssd_rope_kv_bf16(ptr(qkv), ptr(pos), ptr(ctx), ptr(rows_l) if rows_l is not None else None,
+                                          ptr(q), ptr(kc), ptr(vc), b, S, sp.n_q, sp.n_kv, d, self.max_pos,
+                                          sp.rope_theta, st))
+            if rows is None:
+                o = tree_attention(q, kc, vc, mask, ctx, self.scale)
             else:
-                o = tree_attention(q, kc[rows].contiguous(), vc[rows].contiguous(), mask,
-                                   ctx_len.to(torch.int32), self.scale)
-            x = x + o.view(b, S, sp.n_q * d) @ L["wo"]
-            hN = _rmsnorm(x, L["n2"], sp.eps)
-            x = x + (torch.nn.functional.silu(hN @ L["wg"]) * (hN @ L["wu"])) @ L["wd"]
-        return (_rmsnorm(x, self.norm, sp.eps) @ self.lm_head).float()
+                o = tree_attention(q, kc[rows].contiguous(), vc[rows].contiguous(), mask, ctx, self.scale)
+            x.addmm_(o.view(n, sp.n_q * d), L["wo"])  # residual in place (C == D, no copy)
+            check(lib().sssd_rmsnorm_bf16(ptr(x), ptr(L["n2"]), ptr(hN), n, h, sp.eps, st))
+            gu = hN @ L["wgu"]
+            a = torch.empty(n, sp.mlp, dtype=self.dtype, device=self.device)
+            check(lib().sssd_swiglu_bf16(ptr(gu), ptr(a), n, sp.mlp, st))
+            x.addmm_(a, L["wd"])
+        check(lib().sssd_rmsnorm_bf16(ptr(x), ptr(self.norm), ptr(hN), n, h, sp.eps, st))
+        return (hN @ self.lm_head).view(b, S, -1)
 
     def prefill(self, prompts: list, chunk: int = 256) -> None:
         """Write the cache for prompts[b][:-1] (the last prompt token is the first
