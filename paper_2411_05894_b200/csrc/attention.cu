@@ -192,6 +192,165 @@ __device__ __forceinline__ void wg_bar() {  // both softmax warpgroups (256 thre
   asm volatile("bar.sync 1, %0;" ::"n"(2 * kWgThreads) : "memory");
 }
 
+// One key block of one softmax warpgroup (one thread per query row): the
+// visibility words of the block's 4 x 32 keys (prefix keys visible, tree key t
+// iff ancestor bit t), then P = 2^(S*scale - m) in bf16, written 128B-swizzled
+// over the dead K tile (pbuf), and the running (m, l) with a lazy rescale of O.
+//   * one pass over S (TMEM's read port is the scarce resource): P relative
+//     to the running max, valid whenever the block max does not exceed it by
+//     more than 2^8 — the lazy-rescale rule then keeps m and P unchanged; the
+//     first block of a row and the rare block that raises the max further
+//     take the two-pass form (warp-uniform: tcgen05.ld is warp-collective);
+//   * a warp whose rows are all padding (G*S < 128) skips the block (its P
+//     rows keep whatever the dead K tile held; P V rows are independent);
+//   * fully visible 32-key chunks (every prefix chunk) skip the per-key masks;
+//   * max / sum use 4 independent chains.
+__device__ __forceinline__ void softmax_block(uint64_t* s_full, uint64_t* s_free, uint64_t* pv_done,
+                                              uint64_t* p_ready, uint8_t* pbuf, int rt, bool row_ok,
+                                              const uint64_t* mrow, int S, int ctx, int k0, int kv1, uint32_t tS,
+                                              uint32_t tO, int it, bool has_prev, float sl2, float& m_run,
+                                              float& l_run) {
+  uint32_t visw[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int key0 = k0 + c * 32;
+    uint32_t w = 0;
+    if (row_ok) {
+      const int lim = min(32, kv1 - key0);
+      w = lim >= 32 ? 0xffffffffu : (lim > 0 ? (1u << lim) - 1u : 0u);
+      if (key0 + 32 > ctx) {
+        uint32_t tree = 0;
+#pragma unroll 1
+        for (int jj = max(0, ctx - key0); jj < 32; ++jj) {
+          const int t = key0 + jj - ctx;
+          if (t < S && ((mrow[t >> 6] >> (t & 63)) & 1ull)) tree |= 1u << jj;
+        }
+        const uint32_t pref = ctx - key0 >= 32 ? 0xffffffffu : (ctx > key0 ? (1u << (ctx - key0)) - 1u : 0u);
+        w &= pref | tree;
+      }
+    }
+    visw[c] = w;
+  }
+  mbar_wait(s_full, it & 1);
+  fence_after();
+  const bool live = __any_sync(SSSD_FULL, row_ok);
+  float m_use = m_run, corr = 1.f, psum = 0.f;
+  if (live) {
+    bool two_pass = __any_sync(SSSD_FULL, row_ok && m_run == -INFINITY);
+    if (!two_pass) {
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, ps[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        float sv[32];
+        tmem_ld32(tS + c * 32, sv);
+        const uint32_t w = visw[c];
+        uint32_t pk[16];
+        if (w == 0xffffffffu) {
+#pragma unroll
+          for (int jj = 0; jj < 32; jj += 2) {
+            const int a = (jj >> 1) & 3;
+            mx[a] = fmaxf(mx[a], fmaxf(sv[jj], sv[jj + 1]));
+            const float e0 = fast_exp2(fmaf(sv[jj], sl2, -m_run));
+            const float e1 = fast_exp2(fmaf(sv[jj + 1], sl2, -m_run));
+            ps[a] += e0 + e1;
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
+            pk[jj >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
+          }
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < 32; jj += 2) {
+            const int a = (jj >> 1) & 3;
+            const bool v0 = (w >> jj) & 1u, v1 = (w >> (jj + 1)) & 1u;
+            mx[a] = fmaxf(mx[a], fmaxf(v0 ? sv[jj] : -INFINITY, v1 ? sv[jj + 1] : -INFINITY));
+            const float e0 = v0 ? fast_exp2(fmaf(sv[jj], sl2, -m_run)) : 0.f;
+            const float e1 = v1 ? fast_exp2(fmaf(sv[jj + 1], sl2, -m_run)) : 0.f;
+            ps[a] += e0 + e1;
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
+            pk[jj >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
+          }
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4)
+          *reinterpret_cast<uint4*>(pbuf + sw_off(rt, c * 4 + q4)) =
+              make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+      }
+      psum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
+      const float m4 = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      const float bmax = (m4 == -INFINITY) ? m4 : m4 * sl2;
+      two_pass = __any_sync(SSSD_FULL, bmax > m_run + 8.f);
+    }
+    if (two_pass) {
+      float sv[32];
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        tmem_ld32(tS + c * 32, sv);
+        const uint32_t w = visw[c];
+        if (w == 0xffffffffu) {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) mx[jj & 3] = fmaxf(mx[jj & 3], sv[jj]);
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) mx[jj & 3] = fmaxf(mx[jj & 3], ((w >> jj) & 1u) ? sv[jj] : -INFINITY);
+        }
+      }
+      float bmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      bmax = (bmax == -INFINITY) ? bmax : bmax * sl2;
+      // lazy rescale: keep the running max unless the block max exceeds it by
+      // more than 2^8 (P <= 256 stays exact in bf16 range; O / l is unchanged)
+      if (bmax > m_run + 8.f) {
+        corr = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - bmax);
+        m_use = bmax;
+      }
+      float ps[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        tmem_ld32(tS + c * 32, sv);
+        const uint32_t w = (m_use == -INFINITY) ? 0u : visw[c];
+        uint32_t pk[16];
+#pragma unroll
+        for (int jj = 0; jj < 32; jj += 2) {
+          float e0 = fast_exp2(fmaf(sv[jj], sl2, -m_use));
+          float e1 = fast_exp2(fmaf(sv[jj + 1], sl2, -m_use));
+          e0 = ((w >> jj) & 1u) ? e0 : 0.f;
+          e1 = ((w >> (jj + 1)) & 1u) ? e1 : 0.f;
+          ps[(jj >> 1) & 3] += e0 + e1;
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
+          pk[jj >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4)
+          *reinterpret_cast<uint4*>(pbuf + sw_off(rt, c * 4 + q4)) =
+              make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+      }
+      psum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
+    }
+  }
+  fence_before();
+  mbar_arrive(s_free);  // S[g] fully read
+  l_run = l_run * corr + psum;
+  // O[g] is stable once this warpgroup's previous P V completed
+  if (has_prev && live) {
+    mbar_wait(pv_done, (it - 1) & 1);
+    fence_after();
+    if (__any_sync(SSSD_FULL, corr != 1.f)) {  // warp-collective TMEM ld/st
+      float ov[32];
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        tmem_ld32(tO + c * 32, ov);
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) ov[jj] *= corr;
+        tmem_st32(tO + c * 32, ov);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+  }
+  m_run = m_use;
+  fence_async_smem();
+  fence_before();
+  mbar_arrive(p_ready);
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     tree_attn_kernel(Params p, const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -314,94 +473,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     float m_run = -INFINITY, l_run = 0.f;
     int it = 0;
     for (int j = g; j < nblk; j += 2, ++it) {
-      const int k0 = kv0 + j * kN;
-      // visibility of the 32 keys of chunk c: prefix keys visible, tree key t iff bit t
-      uint32_t visw[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int key0 = k0 + c * 32;
-        uint32_t w = 0;
-        if (row_ok) {
-          const int lim = min(32, kv1 - key0);
-          w = lim >= 32 ? 0xffffffffu : (lim > 0 ? (1u << lim) - 1u : 0u);
-          if (key0 + 32 > ctx) {
-            uint32_t tree = 0;
-#pragma unroll 1
-            for (int jj = max(0, ctx - key0); jj < 32; ++jj) {
-              const int t = key0 + jj - ctx;
-              if (t < p.S && ((mrow[t >> 6] >> (t & 63)) & 1ull)) tree |= 1u << jj;
-            }
-            const uint32_t pref = ctx - key0 >= 32 ? 0xffffffffu : (ctx > key0 ? (1u << (ctx - key0)) - 1u : 0u);
-            w &= pref | tree;
-          }
-        }
-        visw[c] = w;
-      }
-      mbar_wait(&sm.s_full[g], it & 1);
-      fence_after();
-      float sv[32];
-      float bmax = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        tmem_ld32(tS + c * 32, sv);
-        const uint32_t w = visw[c];
-#pragma unroll
-        for (int jj = 0; jj < 32; ++jj) bmax = fmaxf(bmax, ((w >> jj) & 1u) ? sv[jj] : -INFINITY);
-      }
-      bmax = (bmax == -INFINITY) ? bmax : bmax * sl2;
-      // lazy rescale: keep the running max unless the block max exceeds it by
-      // more than 2^8 (P <= 256 stays exact in bf16 range; O / l is unchanged)
-      float m_use = m_run, corr = 1.f;
-      if (bmax > m_run + 8.f) {
-        corr = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - bmax);
-        m_use = bmax;
-      }
       // P_j overwrites K_j (stage j%3), dead since Q K_j^T completed (s_full)
-      uint8_t* pbuf = sm.k[j % kStages];
-      float psum = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        tmem_ld32(tS + c * 32, sv);
-        const uint32_t w = (m_use == -INFINITY) ? 0u : visw[c];
-        uint32_t pk[16];
-#pragma unroll
-        for (int jj = 0; jj < 32; jj += 2) {
-          float e0 = fast_exp2(fmaf(sv[jj], sl2, -m_use));
-          float e1 = fast_exp2(fmaf(sv[jj + 1], sl2, -m_use));
-          e0 = ((w >> jj) & 1u) ? e0 : 0.f;
-          e1 = ((w >> (jj + 1)) & 1u) ? e1 : 0.f;
-          psum += e0 + e1;
-          const __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
-          pk[jj >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
-        }
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4)
-          *reinterpret_cast<uint4*>(pbuf + sw_off(rt, c * 4 + q4)) =
-              make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
-      }
-      fence_before();
-      mbar_arrive(&sm.s_free[g]);  // S[g] fully read
-      l_run = l_run * corr + psum;
-      // O[g] is stable once this warpgroup's previous P V completed
-      if (it > 0) {
-        mbar_wait(&sm.pv_done[g], (it - 1) & 1);
-        fence_after();
-        if (__any_sync(SSSD_FULL, corr != 1.f)) {  // warp-collective TMEM ld/st
-          float ov[32];
-#pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            tmem_ld32(tO + c * 32, ov);
-#pragma unroll
-            for (int jj = 0; jj < 32; ++jj) ov[jj] *= corr;
-            tmem_st32(tO + c * 32, ov);
-          }
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        }
-      }
-      m_run = m_use;
-      fence_async_smem();
-      fence_before();
-      mbar_arrive(&sm.p_ready[g]);
+      softmax_block(&sm.s_full[g], &sm.s_free[g], &sm.pv_done[g], &sm.p_ready[g], sm.k[j % kStages], rt, row_ok,
+                    mrow, p.S, ctx, kv0 + j * kN, kv1, tS, tO, it, it > 0, sl2, m_run, l_run);
     }
     if (it > 0) mbar_wait(&sm.pv_done[g], (it - 1) & 1);
     // ---------------- epilogue: merge the two warpgroups ----------------

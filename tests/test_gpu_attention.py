@@ -104,3 +104,29 @@ def test_tree_attention_growing_max(B, S, Hq, Hkv, ctx_max, max_pos):
     want = ref_tree_attention(q, k, v, mask, ctx, scale)
     err = (got - want).abs().max().item()
     assert err <= 1e-2 * want.abs().max().item(), err
+
+
+@pytest.mark.parametrize("ctxs,S,Hq,Hkv,max_pos", [
+    ([20000, 10, 300], 16, 8, 2, 20100),   # skewed contexts: split-KV with near-empty splits
+    ([3000] * 40, 32, 32, 8, 3100),        # 320 (b, kv head) units
+    ([1, 700, 64, 129], 5, 8, 1, 900),     # G*S = 40 rows (padding warps), block-boundary contexts
+    ([900, 50], 64, 8, 2, 1000),           # two row tiles per (b, kv head)
+])
+def test_tree_attention_ragged_batches(ctxs, S, Hq, Hkv, max_pos):
+    """Ragged context lengths and row-tile shapes against the fp32 reference;
+    two launches in a row give identical outputs (no state kept between calls)."""
+    torch.manual_seed(5)
+    rng = np.random.default_rng(6)
+    B, D = len(ctxs), 128
+    q = torch.randn(B, S, Hq, D, device="cuda").to(torch.bfloat16)
+    k = torch.randn(B, Hkv, max_pos, D, device="cuda").to(torch.bfloat16)
+    v = torch.randn(B, Hkv, max_pos, D, device="cuda").to(torch.bfloat16)
+    ctx = torch.tensor(ctxs, dtype=torch.int32, device="cuda")
+    mask = random_tree_masks(B, S, rng)
+    scale = 1.0 / math.sqrt(D)
+    got1 = tree_attention(q, k, v, mask, ctx, scale).float()
+    got2 = tree_attention(q, k, v, mask, ctx, scale).float()
+    torch.cuda.synchronize()
+    assert torch.equal(got1, got2)
+    want = ref_tree_attention(q, k, v, mask, ctx, scale)
+    assert (got1 - want).abs().max().item() <= 1e-2 * want.abs().max().item()
