@@ -38,7 +38,7 @@ recs = [G.SimRecord(p, q) for p, q in workload.records(64, 512, 256, V)]
 reports = G.sweep(recs, ds, G.FusionConfig(), grid)
 accept = {s: reports[s].mean_accepted_per_step for s in grid}
 
-# 2. measured verify cost: one tree forward (all layers, lm_head) per step
+# 2. measured verify cost: one tree forward (all layers, lm_head) per step, graph-replayed
 b, s_kv = args.b, args.s_kv
 dec = Mo.Decoder(Mo.LLAMA3_8B, b, s_kv + max(grid) + 8, seed=0, init_on_device=True)
 ctx = torch.full((b,), s_kv, dtype=torch.int32, device="cuda")
@@ -56,15 +56,23 @@ for s in grid:
     for _ in range(2):
         dec.forward(toks, pos, mask, ctx)
     torch.cuda.synchronize()
+    # replayed as one CUDA graph (as serving.py runs decode steps): the GPU
+    # time of the forward, not the host's launch rate
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        dec.forward(toks, pos, mask, ctx)
+    graph.replay()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = 5
     e0.record()
     for _ in range(reps):
-        dec.forward(toks, pos, mask, ctx)
+        graph.replay()
     e1.record()
     torch.cuda.synchronize()
     fwd_ms[s] = e0.elapsed_time(e1) / reps
     step_s[s] = fwd_ms[s] / 1e3
+    del graph
 del dec
 torch.cuda.empty_cache()
 
