@@ -512,7 +512,16 @@ def bench_decode_cfg1(budget_s: float = 60.0) -> dict:
     r_spec = spec.run()
     ar = SpecDecoder(None, Mo.Decoder(Mo.TINY, 8, 1024, seed=0), prompts, 256)
     r_ar = ar.run()
-    same = sum(a == b for a, b in zip(spec.sequences(), ar.sequences()))
+    same, tie_only = 0, 0
+    for sa, sb in zip(spec.sequences(), ar.sequences()):
+        if sa == sb:
+            same += 1
+            continue
+        # a divergence is allowed only where the fp32 reference's top-2 margin
+        # is a near-tie (<= 1e-2 |top1|, tests/test_gpu_model.py's rule)
+        j = next(k for k in range(min(len(sa), len(sb))) if sa[k] != sb[k])
+        top2 = torch.topk(ar.model.reference_logits(sb[:j]), 2).values
+        tie_only += int((top2[0] - top2[1]).item() <= 1e-2 * abs(top2[0].item()))
     # teacher-forced acceptance on the GPU decode loop vs the CPU oracle
     t0 = time.perf_counter()
     rep = G.simulate([G.SimRecord(p, r) for p, r in recs], ds, cfg)
@@ -530,6 +539,7 @@ def bench_decode_cfg1(budget_s: float = 60.0) -> dict:
             "spec_accepted_per_step": round(r_spec["accepted_per_step"], 3),
             "autoregressive_tokens_per_s": round(r_ar["tokens_per_s"], 1),
             "sequences_identical_to_autoregressive": f"{same}/8",
+            "divergences_after_reference_near_tie": f"{tie_only}/{8 - same}",
             "teacher_forced": {"mean_accepted_per_step": round(rep.mean_accepted_per_step, 4),
                                "gpu_simulate_s": round(gpu_s, 3),
                                "cpu_oracle_s_per_record": round(cpu_s / 2, 3),

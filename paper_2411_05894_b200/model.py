@@ -108,9 +108,7 @@ class Decoder:
         """Tree forward: tokens / positions [b, S] (rows = cache rows of these b
         requests, default all), mask [b, S, W] int64, ctx_len [b] int32 = committed
         tokens already in the cache.  Writes K/V of the S tokens to cache
-        positions ctx..ctx+S-1 and returns logits [b, S, V] (bf16, the GEMM's
-        fp32 accumulators rounded once; argmax over them equals argmax over
-        their exact fp32 widening)."""
+        positions ctx..ctx+S-1 and returns logits [b, S, V] (fp32)."""
         sp = self.spec
         b, S = tokens.shape
         d, h = sp.head_dim, sp.hidden
@@ -140,7 +138,33 @@ class Decoder:
             check(lib().sssd_swiglu_bf16(ptr(gu), ptr(a), n, sp.mlp, st))
             x.addmm_(a, L["wd"])
         check(lib().sssd_rmsnorm_bf16(ptr(x), ptr(self.norm), ptr(hN), n, h, sp.eps, st))
-        return (hN @ self.lm_head).view(b, S, -1)
+        # fp32 logits straight from the GEMM's fp32 accumulators (no bf16
+        # rounding of the logits: greedy ties stay as rare as in fp32)
+        return torch.mm(hN, self.lm_head, out_dtype=torch.float32).view(b, S, -1)
+
+    def reference_logits(self, seq: list) -> torch.Tensor:
+        """Verification helper (tests, bench): plain fp32 PyTorch causal forward
+        of one whole sequence with this decoder's weights (dense attention,
+        separate projections); logits of the last position [V]."""
+        sp = self.spec
+        d = sp.head_dim
+        f = lambda t: t.float()  # noqa: E731
+        x = f(self.embed)[torch.as_tensor(seq, device=self.device)]
+        n = len(seq)
+        pos = torch.arange(n, device=self.device)
+        G = sp.n_q // sp.n_kv
+        causal = torch.triu(torch.ones(n, n, dtype=torch.bool, device=self.device), 1)
+        for L in self.layers:
+            h = _rmsnorm(x, f(L["n1"]), sp.eps)
+            q = _rope((h @ f(L["wq"])).view(n, sp.n_q, d), pos, sp.rope_theta)
+            k = _rope((h @ f(L["wk"])).view(n, sp.n_kv, d), pos, sp.rope_theta).repeat_interleave(G, dim=1)
+            v = (h @ f(L["wv"])).view(n, sp.n_kv, d).repeat_interleave(G, dim=1)
+            s = torch.einsum("qhd,khd->hqk", q, k) / math.sqrt(d)
+            o = torch.einsum("hqk,khd->qhd", torch.softmax(s.masked_fill(causal, float("-inf")), -1), v)
+            x = x + o.reshape(n, sp.n_q * d) @ f(L["wo"])
+            h = _rmsnorm(x, f(L["n2"]), sp.eps)
+            x = x + (torch.nn.functional.silu(h @ f(L["wg"])) * (h @ f(L["wu"]))) @ f(L["wd"])
+        return (_rmsnorm(x, f(self.norm), sp.eps) @ f(self.lm_head))[-1]
 
     def prefill(self, prompts: list, chunk: int = 256) -> None:
         """Write the cache for prompts[b][:-1] (the last prompt token is the first

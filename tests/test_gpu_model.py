@@ -26,27 +26,7 @@ SMALL = M.ModelSpec(n_layers=2, hidden=512, n_q=8, n_kv=2, mlp=1024, vocab=2000)
 
 def ref_logits(dec: M.Decoder, seq: list[int]) -> torch.Tensor:
     """fp32 causal forward of one full sequence; logits of the last position."""
-    sp = dec.spec
-    d = sp.head_dim
-    f = lambda t: t.float()  # noqa: E731
-    x = f(dec.embed)[torch.tensor(seq, device=dec.device)]
-    n = len(seq)
-    pos = torch.arange(n, device=dec.device)
-    G_ = sp.n_q // sp.n_kv
-    for L in dec.layers:
-        h = M._rmsnorm(x, f(L["n1"]), sp.eps)
-        q = M._rope((h @ f(L["wq"])).view(n, sp.n_q, d), pos, sp.rope_theta)
-        k = M._rope((h @ f(L["wk"])).view(n, sp.n_kv, d), pos, sp.rope_theta)
-        v = (h @ f(L["wv"])).view(n, sp.n_kv, d)
-        k = k.repeat_interleave(G_, dim=1)
-        v = v.repeat_interleave(G_, dim=1)
-        s = torch.einsum("qhd,khd->hqk", q, k) / math.sqrt(d)
-        s = s.masked_fill(torch.triu(torch.ones(n, n, dtype=torch.bool, device=dec.device), 1), float("-inf"))
-        o = torch.einsum("hqk,khd->qhd", torch.softmax(s, -1), v).reshape(n, sp.n_q * d)
-        x = x + o @ f(L["wo"])
-        h = M._rmsnorm(x, f(L["n2"]), sp.eps)
-        x = x + (torch.nn.functional.silu(h @ f(L["wg"])) * (h @ f(L["wu"]))) @ f(L["wd"])
-    return (M._rmsnorm(x, f(dec.norm), sp.eps) @ f(dec.lm_head))[-1]
+    return dec.reference_logits(seq)
 
 
 def test_tree_forward_matches_per_path_fp32():
