@@ -214,7 +214,10 @@ __device__ __forceinline__ void softmax_block(uint64_t* s_full, uint64_t* s_free
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const int key0 = k0 + c * 32;
-    uint32_t w = 0;
+    // padding rows (row_ok false) see every key: their lanes then take the
+    // same mask-free branch as the live rows of a prefix chunk (no divergence
+    // in a partly filled warp); their P rows only feed padding rows of O
+    uint32_t w = 0xffffffffu;
     if (row_ok) {
       const int lim = min(32, kv1 - key0);
       w = lim >= 32 ? 0xffffffffu : (lim > 0 ? (1u << lim) - 1u : 0u);
