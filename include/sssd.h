@@ -167,6 +167,31 @@ int sssd_propose(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
                  const sssd_draft_out* out, const sssd_lookup_out* lookup, void* workspace,
                  size_t workspace_bytes, void* stream);
 
+/* The same propose, stage by stage over request ranges [b0, b1) of one batch
+ * of B requests whose workspace is sssd_propose_workspace(cfg, B, max_len):
+ * SSSD_PHASE_BEGIN once per batch (status reset), then LOOKUP / SCAN / FUSE
+ * for any ranges in dependency order (FUSE of a range after its LOOKUP and
+ * SCAN; FUSE ranges stream-ordered).  LOOKUP reads only the last P tokens of
+ * each request, so `seqs` may then be the tail view of sssd_gather_tails.
+ * Replaces the reference's per-request GenerationSession.propose
+ * (draft.py:183-200) for host-buffer pipelines (DraftEngine.propose_pinned). */
+#define SSSD_PHASE_LOOKUP 1
+#define SSSD_PHASE_SCAN 2
+#define SSSD_PHASE_FUSE 4
+#define SSSD_PHASE_BEGIN 8
+int sssd_propose_phase(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
+                       const sssd_draft_out* out, const sssd_lookup_out* lookup, void* workspace,
+                       size_t workspace_bytes, int32_t phases, int32_t B, int32_t max_len, int32_t b0,
+                       int32_t b1, void* stream);
+
+/* Tail view for the lookup: the last min(P, len[b]) tokens of request b
+ * (seq: u16 if elem_bytes == 2 else u32; device memory or pinned host
+ * memory, read zero-copy) right-aligned in tails[B][P], with
+ * tails_off[b] / tails_len[b] describing them as a sequence batch. */
+int sssd_gather_tails(const void* seq, int32_t elem_bytes, const int64_t* off, const int32_t* len,
+                      int32_t B, int32_t P, uint32_t* tails, int64_t* tails_off, int32_t* tails_len,
+                      void* stream);
+
 /* Stage entry points (the single-request reference API is built on these). */
 
 /* Batched Datastore.find_range (datastore.py:156-183): pattern b =

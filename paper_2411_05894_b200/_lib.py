@@ -20,6 +20,7 @@ SSSD_MAX_DEPTH = 32
 SSSD_MAX_DRAFT = 256
 SSSD_ROW_TOKENS = 15
 SSSD_STATUS_OFFSET = 8  # int32 status word in every propose / merge workspace
+PHASE_LOOKUP, PHASE_SCAN, PHASE_FUSE, PHASE_BEGIN = 1, 2, 4, 8  # sssd_propose_phase bits
 E_WORKSPACE = -4
 
 u32p = C.POINTER(C.c_uint32)
@@ -75,6 +76,10 @@ _SIGS = {
                                     C.c_int32, C.c_int32, C.c_float, vp]),
     "sssd_swiglu_bf16": (C.c_int, [vp, vp, C.c_int64, C.c_int32, vp]),
     "sssd_propose_workspace": (C.c_size_t, [C.POINTER(Cfg), C.c_int32, C.c_int32]),
+    "sssd_propose_phase": (C.c_int, [C.POINTER(Ds), C.POINTER(Seqs), C.POINTER(Cfg), C.POINTER(DraftOut),
+                                     C.POINTER(LookupOut), vp, C.c_size_t, C.c_int32, C.c_int32, C.c_int32,
+                                     C.c_int32, C.c_int32, vp]),
+    "sssd_gather_tails": (C.c_int, [vp, C.c_int32, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp]),
     "sssd_propose": (C.c_int, [C.POINTER(Ds), C.POINTER(Seqs), C.POINTER(Cfg), C.POINTER(DraftOut),
                                C.POINTER(LookupOut), vp, C.c_size_t, vp]),
     "sssd_propose_profile": (C.c_int, [C.POINTER(Ds), C.POINTER(Seqs), C.POINTER(Cfg), C.POINTER(DraftOut),

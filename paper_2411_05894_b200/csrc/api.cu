@@ -368,6 +368,63 @@ int sssd_propose_profile(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cf
   return rc;
 }
 
+// Per-range fusion state: arena cursor and LPT histogram + fill cursors (one
+// launch instead of two memsets; the status word between them is kept).
+__global__ void fuse_reset_kernel(unsigned long long* cursor, int32_t* hist) {
+  if (threadIdx.x == 0) *cursor = 0;
+  hist[threadIdx.x] = 0;  // blockDim = 128: [64] histogram + [64] fill cursors
+}
+
+// The three stages over a request range [b0, b1) of a batch whose workspace
+// was carved for all of it (outputs and stage buffers are indexed by request).
+static void lookup_range(const PropWs& w, const KCfg& k, const sssd_cfg* cfg, const sssd_ds* ds,
+                         const sssd_seqs* seqs, const sssd_lookup_out& lk, const int64_t* pre_bounds,
+                         const uint32_t* pre_rows, cudaStream_t s, int b0, int b1) {
+  KCfg kk = k;
+  kk.b0 = b0;
+  kk.b1 = b1;
+  // one warp per request (lane groups per p) for throughput; small batches
+  // keep one warp per p (lower latency per request when SMs are idle)
+  if (!cfg->has_separator && !pre_bounds && b1 - b0 >= 2048)
+    ds_lookup_warp_kernel<<<(b1 - b0 + 3) / 4, 128, 0, s>>>(*ds, *seqs, kk, w.ds_tab, w.ds_len, w.ds_el, w.ds_n,
+                                                              lk, w.ds_cols);
+  else
+    ds_lookup_kernel<<<b1 - b0, 32 * cfg->P, 4 * ds_lookup_smem_words(cfg->P, cfg->M), s>>>(
+        *ds, *seqs, kk, w.ds_tab, w.ds_len, w.ds_el, w.ds_n, lk, w.ds_raw, w.ds_idx, w.ds_idx_cap, w.ds_cols,
+        pre_bounds, pre_rows);
+  if (ds_dedupe_enabled(kk) && (cfg->has_separator || pre_bounds || b1 - b0 < 2048))  // (the warp kernel folds itself)
+    ds_dedupe_kernel<<<b1 - b0, 128, 4 * (cfg->P * cfg->M + 1), s>>>(kk, w.ds_tab, w.ds_el, w.ds_n, w.ds_cols);
+}
+
+static void scan_range(const PropWs& w, const KCfg& k, const sssd_cfg* cfg, const sssd_seqs* seqs, cudaStream_t s,
+                       int b0, int b1) {
+  KCfg kk = k;
+  kk.b0 = b0;
+  kk.b1 = b1;
+  const int th = input_scan_threads(seqs->max_len);
+  input_scan_kernel<<<b1 - b0, th, input_scan_smem_bytes(th, cfg->input_branch_len), s>>>(
+      *seqs, kk, w.in_raw, w.in_el, w.in_n, w.idx, w.cap, w.cap2, w.in_cols);
+}
+
+// Setup (sources, roots), longest-first order over the range when it spans
+// several waves, fusion.  The LPT histogram is per launch: ranges of one
+// workspace run in stream order (sssd_propose_phase zeroes it per range).
+static void fuse_range(const PropWs& w, const KCfg& k, const sssd_seqs* seqs, const sssd_draft_out* out,
+                       cudaStream_t s, int b0, int b1) {
+  KCfg kk = k;
+  kk.b0 = b0;
+  kk.b1 = b1;
+  static const bool no_lpt = getenv("SSSD_NO_LPT") != nullptr;  // A/B switch
+  const bool lpt = !no_lpt && b1 - b0 >= 2048;                   // order only pays with several waves
+  propose_setup_kernel<<<(b1 - b0 + 127) / 128, 128, 0, s>>>(*seqs, kk, w.ds_cols, w.ds_n, w.in_cols, w.in_n,
+                                                               w.d.desc, w.d.root, lpt ? w.d.bucket : nullptr,
+                                                               w.d.hist);
+  if (lpt)
+    lpt_scatter_kernel<<<(b1 - b0 + 255) / 256, 256, 0, s>>>(w.d.bucket, w.d.hist, w.d.hist + 64, b0, b1,
+                                                               w.d.order);
+  launch_fusion(w.d, kk, b1 - b0, out, s, g_cycles, lpt ? w.d.order : nullptr);
+}
+
 static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
                         const sssd_draft_out* out, const sssd_lookup_out* lookup, void* workspace,
                         size_t workspace_bytes, void* stream, cudaEvent_t* ev, const int64_t* pre_bounds,
@@ -397,42 +454,10 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
   if ((rc = input_scan_attr(cfg->input_branch_len))) return rc;
 
   auto launch_lookup = [&](cudaStream_t s, int b0, int b1) {
-    KCfg kk = k;
-    kk.b0 = b0;
-    kk.b1 = b1;
-    // one warp per request (lane groups per p) for throughput; small batches
-    // keep one warp per p (lower latency per request when SMs are idle)
-    if (!cfg->has_separator && !pre_bounds && b1 - b0 >= 2048)
-      ds_lookup_warp_kernel<<<(b1 - b0 + 3) / 4, 128, 0, s>>>(*ds, *seqs, kk, w.ds_tab, w.ds_len, w.ds_el, w.ds_n,
-                                                                lk, w.ds_cols);
-    else
-      ds_lookup_kernel<<<b1 - b0, 32 * cfg->P, 4 * ds_lookup_smem_words(cfg->P, cfg->M), s>>>(
-          *ds, *seqs, kk, w.ds_tab, w.ds_len, w.ds_el, w.ds_n, lk, w.ds_raw, w.ds_idx, w.ds_idx_cap, w.ds_cols,
-          pre_bounds, pre_rows);
-    if (ds_dedupe_enabled(kk) && (cfg->has_separator || pre_bounds || b1 - b0 < 2048))  // (the warp kernel folds itself)
-      ds_dedupe_kernel<<<b1 - b0, 128, 4 * (cfg->P * cfg->M + 1), s>>>(kk, w.ds_tab, w.ds_el, w.ds_n, w.ds_cols);
+    lookup_range(w, k, cfg, ds, seqs, lk, pre_bounds, pre_rows, s, b0, b1);
   };
-  auto launch_scan = [&](cudaStream_t s, int b0, int b1) {
-    KCfg kk = k;
-    kk.b0 = b0;
-    kk.b1 = b1;
-    const int th = input_scan_threads(seqs->max_len);
-    input_scan_kernel<<<b1 - b0, th, input_scan_smem_bytes(th, cfg->input_branch_len), s>>>(
-        *seqs, kk, w.in_raw, w.in_el, w.in_n, w.idx, w.cap, w.cap2,
-                                               w.in_cols);
-  };
-  auto launch_fuse = [&](cudaStream_t s, int b0, int b1) {
-    KCfg kk = k;
-    kk.b0 = b0;
-    kk.b1 = b1;
-    static const bool no_lpt = getenv("SSSD_NO_LPT") != nullptr;  // A/B switch
-    const bool lpt = !no_lpt && b0 == 0 && b1 == B && B >= 2048;  // order only pays with several waves
-    propose_setup_kernel<<<(b1 - b0 + 127) / 128, 128, 0, s>>>(*seqs, kk, w.ds_cols, w.ds_n, w.in_cols,
-                                                                 w.in_n, w.d.desc, w.d.root,
-                                                                 lpt ? w.d.bucket : nullptr, w.d.hist);
-    if (lpt) lpt_scatter_kernel<<<(B + 255) / 256, 256, 0, s>>>(w.d.bucket, w.d.hist, w.d.hist + 64, B, w.d.order);
-    launch_fusion(w.d, kk, b1 - b0, out, s, g_cycles, lpt ? w.d.order : nullptr);
-  };
+  auto launch_scan = [&](cudaStream_t s, int b0, int b1) { scan_range(w, k, cfg, seqs, s, b0, b1); };
+  auto launch_fuse = [&](cudaStream_t s, int b0, int b1) { fuse_range(w, k, seqs, out, s, b0, b1); };
 
   if (ev) {  // profiling: stages back to back on the caller's stream
     cudaEventRecord(ev[0], st);
@@ -447,7 +472,7 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
     propose_setup_kernel<<<(B + 127) / 128, 128, 0, st>>>(*seqs, kk, w.ds_cols, w.ds_n, w.in_cols, w.in_n,
                                                             w.d.desc, w.d.root, lpt ? w.d.bucket : nullptr,
                                                             w.d.hist);
-    if (lpt) lpt_scatter_kernel<<<(B + 255) / 256, 256, 0, st>>>(w.d.bucket, w.d.hist, w.d.hist + 64, B, w.d.order);
+    if (lpt) lpt_scatter_kernel<<<(B + 255) / 256, 256, 0, st>>>(w.d.bucket, w.d.hist, w.d.hist + 64, 0, B, w.d.order);
     cudaEventRecord(ev[3], st);
     launch_fusion(w.d, kk, B, out, st, g_cycles, lpt ? w.d.order : nullptr);
     cudaEventRecord(ev[4], st);
@@ -650,6 +675,57 @@ int sssd_propose_pre(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* c
   if (cfg && cfg->P + cfg->branch_len > SSSD_ROW_TOKENS)
     return fail(SSSD_E_LIMIT, "sharded lookup needs P + branch_len <= %d", SSSD_ROW_TOKENS);
   return propose_impl(ds, seqs, cfg, out, lookup, workspace, workspace_bytes, stream, nullptr, gbounds, rows);
+}
+
+// Stage-by-stage propose over request ranges of one batch (host-buffer
+// pipelines: the datastore lookup of every request can run from its context
+// tail before the contexts themselves are uploaded; the input scan and the
+// fusion then follow the uploads range by range).  The workspace is carved
+// for (B, max_len) = the whole batch; `seqs` holds B requests (for LOOKUP it
+// may be a tail view, sssd_gather_tails).  FUSE ranges of one workspace must
+// be stream-ordered.
+int sssd_propose_phase(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg, const sssd_draft_out* out,
+                       const sssd_lookup_out* lookup, void* workspace, size_t workspace_bytes, int32_t phases,
+                       int32_t B, int32_t max_len, int32_t b0, int32_t b1, void* stream) {
+  int rc = validate_cfg(cfg);
+  if (rc) return rc;
+  if ((rc = validate_out(out))) return rc;
+  if (!seqs || seqs->B != B || B < 0 || max_len < 0) return fail(SSSD_E_ARG, "bad sequence batch");
+  if (b0 < 0 || b1 < b0 || b1 > B) return fail(SSSD_E_ARG, "bad request range [%d, %d) of %d", b0, b1, B);
+  if (phases & ~(SSSD_PHASE_LOOKUP | SSSD_PHASE_SCAN | SSSD_PHASE_FUSE | SSSD_PHASE_BEGIN))
+    return fail(SSSD_E_ARG, "unknown phase bits 0x%x", phases);
+  if ((phases & SSSD_PHASE_LOOKUP) && cfg->use_datastore) {
+    if (!ds || !ds->rows) return fail(SSSD_E_ARG, "use_datastore requires a datastore");
+    if (ds->n_rows == 0 || ds->n_tokens == 0) return fail(SSSD_E_ARG, "empty corpus");
+    if (ds->n_tokens >= 0xffffffffull) return fail(SSSD_E_LIMIT, "corpus longer than 2^32-1 tokens");
+    if (cfg->P + cfg->branch_len > SSSD_ROW_TOKENS && !ds->tokens)
+      return fail(SSSD_E_ARG, "P + branch_len > %d needs the token array", SSSD_ROW_TOKENS);
+  }
+  if (B == 0) return SSSD_OK;
+  const PropWs w = carve_propose(static_cast<uint8_t*>(workspace), cfg, B, max_len);
+  if (!workspace || workspace_bytes < w.bytes)
+    return fail(SSSD_E_WORKSPACE, "propose needs %zu workspace bytes, got %zu", w.bytes, workspace_bytes);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const KCfg k = kcfg(cfg);
+  sssd_lookup_out lk{};
+  if (lookup) lk = *lookup;
+  if (phases & SSSD_PHASE_BEGIN)  // cursor, status word, LPT histogram
+    if ((rc = cuda_check(cudaMemsetAsync(w.d.cursor, 0, 16 + 512, st), "memset status"))) return rc;
+  if (b1 == b0) return cuda_check(cudaGetLastError(), "propose phase");
+  if ((phases & SSSD_PHASE_LOOKUP) && cfg->use_datastore)
+    lookup_range(w, k, cfg, ds, seqs, lk, nullptr, nullptr, st, b0, b1);
+  if ((phases & SSSD_PHASE_SCAN) && cfg->use_input) {
+    if ((rc = input_scan_attr(cfg->input_branch_len))) return rc;
+    scan_range(w, k, cfg, seqs, st, b0, b1);
+  }
+  if (phases & SSSD_PHASE_FUSE) {
+    if ((rc = fusion_smem_attr(k))) return rc;
+    // a fusion launch's arena slices die with it: the cursor restarts per
+    // range; the status word (offset 8) accumulates
+    fuse_reset_kernel<<<1, 128, 0, st>>>(w.d.cursor, w.d.hist);
+    fuse_range(w, k, seqs, out, st, b0, b1);
+  }
+  return cuda_check(cudaGetLastError(), "propose phase");
 }
 
 // Measurement aid: when set (device pointer, [B] int64), the fusion kernel

@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(32, SSSD_DRAFT_MINB)
 // so long requests start in the first wave instead of forming the tail.
 // Order within a bucket is arbitrary: requests are independent and every
 // output is indexed by request.
-__global__ void lpt_scatter_kernel(const uint8_t* bucket, const int32_t* hist, int32_t* fill, int B,
+__global__ void lpt_scatter_kernel(const uint8_t* bucket, const int32_t* hist, int32_t* fill, int b0, int b1,
                                    int32_t* order) {
   __shared__ int start[64];
   if (threadIdx.x < 64) {
@@ -586,10 +586,10 @@ __global__ void lpt_scatter_kernel(const uint8_t* bucket, const int32_t* hist, i
     start[threadIdx.x] = acc;
   }
   __syncthreads();
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
+  const int b = b0 + blockIdx.x * blockDim.x + threadIdx.x;  // requests [b0, b1): order[b0 ..]
+  if (b >= b1) return;
   const int k = bucket[b];
-  order[start[k] + atomicAdd(&fill[k], 1)] = b;
+  order[b0 + start[k] + atomicAdd(&fill[k], 1)] = b;
 }
 
 }  // namespace sssd

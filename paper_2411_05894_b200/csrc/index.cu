@@ -169,6 +169,27 @@ __global__ void widen_u16_kernel(const uint16_t* src, uint32_t* dst, int64_t n) 
   for (int64_t i = done + t0; i < n; i += stride) dst[i] = src[i];
 }
 
+// Last min(P, len) tokens of every request, right-aligned in a [B][P] u32
+// array, plus the (offset, length) view the datastore lookup reads them
+// through.  `seq` may be pinned host memory (read over PCIe, zero-copy): the
+// lookup needs only these tokens, so it can start before the contexts are
+// uploaded.
+__global__ void gather_tails_kernel(const void* seq, int elem_bytes, const int64_t* off, const int32_t* len, int B,
+                                    int P, uint32_t* tails, int64_t* toff, int32_t* tlen) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int L = len[b];
+  const int pm = L < P ? (L > 0 ? L : 0) : P;
+  const int64_t end = off[b] + L;
+  for (int j = 0; j < pm; ++j) {
+    const int64_t i = end - pm + j;
+    tails[(int64_t)b * P + (P - pm) + j] = elem_bytes == 2 ? (uint32_t)static_cast<const uint16_t*>(seq)[i]
+                                                            : static_cast<const uint32_t*>(seq)[i];
+  }
+  toff[b] = (int64_t)b * P + (P - pm);
+  tlen[b] = pm;
+}
+
 extern "C" {
 
 size_t sssd_sa_build_workspace(uint64_t n) { return sa_carve(nullptr, n ? n : 1).total; }
@@ -245,6 +266,17 @@ int sssd_widen_u16(const uint16_t* src, uint32_t* dst, int64_t n, void* stream) 
   const unsigned blocks = (unsigned)min((n4 + 255) / 256 + 1, (int64_t)148 * 16);
   widen_u16_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, dst, n);
   return cuda_check(cudaGetLastError(), "widen_u16 launch");
+}
+
+int sssd_gather_tails(const void* seq, int32_t elem_bytes, const int64_t* off, const int32_t* len, int32_t B,
+                      int32_t P, uint32_t* tails, int64_t* tails_off, int32_t* tails_len, void* stream) {
+  if (B < 0 || P < 1 || P > SSSD_MAX_P || (elem_bytes != 2 && elem_bytes != 4))
+    return fail(SSSD_E_ARG, "gather_tails: bad arguments");
+  if (B == 0) return SSSD_OK;
+  if (!seq || !off || !len || !tails || !tails_off || !tails_len) return fail(SSSD_E_ARG, "gather_tails: null buffer");
+  gather_tails_kernel<<<(B + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(seq, elem_bytes, off, len, B, P,
+                                                                                        tails, tails_off, tails_len);
+  return cuda_check(cudaGetLastError(), "gather_tails launch");
 }
 
 int sssd_rows_sa64(const uint32_t* rows, uint64_t n, uint64_t* sa64_out, void* stream) {

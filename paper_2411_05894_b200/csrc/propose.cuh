@@ -70,7 +70,7 @@ __device__ __forceinline__ int lpt_bucket(const SrcDesc* d, int P) {
   for (int r = 1; r <= P; ++r) cost += d[r].n;
   return 63 - min(63, 2 * (63 - __clzll(cost + 1)));  // 2 buckets per octave, largest first
 }
-__global__ void lpt_scatter_kernel(const uint8_t* bucket, const int32_t* hist, int32_t* fill, int B,
+__global__ void lpt_scatter_kernel(const uint8_t* bucket, const int32_t* hist, int32_t* fill, int b0, int b1,
                                    int32_t* order);
 
 // level-synchronous fusion: level-node and parent record bytes, and how many

@@ -134,7 +134,7 @@ class DraftEngine:
 
     def propose_pinned(self, seq_h: torch.Tensor, off_h: torch.Tensor, len_h: torch.Tensor, max_len: int,
                        out_h: DraftBatch | None = None, chunks: int = 5, taper: float = 1.0,
-                       tail: float | None = None) -> DraftBatch:
+                       tail: float | None = None, schedule: str = "phased") -> DraftBatch:
         """Host-buffer entry point for a large batch: contexts in pinned host
         memory (seq_h int32 = u32 token ids, or int16 = u16 token ids when the
         vocabulary fits 16 bits: half the upload bytes, widened on the device by
@@ -147,7 +147,16 @@ class DraftEngine:
         workspace each (so the fusion-kernel tail of range c overlaps the lookup
         and drafting of range c+1), downloads run on a D2H copy stream: PCIe
         both ways and the kernels all run concurrently.  Blocks until the drafts
-        are on the host; raises if any range overflowed the fusion arena."""
+        are on the host; raises if any range overflowed the fusion arena.
+
+        ``schedule="phased"`` (default, pinned ``seq_h``): one workspace for the
+        whole batch; the datastore lookup of every request starts at once from
+        its context tail (``sssd_gather_tails`` reads the last P tokens from the
+        pinned host buffer), so only the input scan and the fusion follow the
+        uploads range by range (``sssd_propose_phase``).  ``"ranges"``: every
+        range is an independent propose."""
+        if schedule == "phased" and seq_h.is_pinned() and (self.use_datastore and self.store is not None):
+            return self._propose_pinned_phased(seq_h, off_h, len_h, max_len, out_h, chunks)
         B = int(len_h.shape[0])
         dev = self.device
         S, W = self.S, self.W
@@ -249,6 +258,113 @@ class DraftEngine:
         for s_ in (c0, c1, down):
             main.wait_stream(s_)
         if int(status[:chunks].max().item()) != 0:  # synchronises the current stream
+            raise _lib.SSSDError("device workspace overflow (fusion arena) in propose_pinned")
+        return out_h
+
+    def _propose_pinned_phased(self, seq_h: torch.Tensor, off_h: torch.Tensor, len_h: torch.Tensor, max_len: int,
+                               out_h: DraftBatch | None, chunks: int) -> DraftBatch:
+        B = int(len_h.shape[0])
+        dev = self.device
+        S, W, P = self.S, self.W, int(self.c.P)
+        if out_h is None:
+            out_h = DraftBatch(
+                size=torch.empty(B, dtype=torch.int32).pin_memory(),
+                tokens=torch.empty((B, S), dtype=torch.int32).pin_memory(),
+                parents=torch.empty((B, S), dtype=torch.int32).pin_memory(),
+                depths=torch.empty((B, S), dtype=torch.int32).pin_memory(),
+                mask=torch.empty((B, S, W), dtype=torch.int64).pin_memory())
+        if B == 0:
+            return out_h
+        offs, lens = off_h.numpy(), len_h.numpy()
+        if (lens < 1).any():
+            raise ValueError("empty prompt: the draft root is the last context token")
+        narrow = seq_h.dtype == torch.int16
+        if not narrow and seq_h.dtype != torch.int32:
+            raise ValueError("seq_h must be int32 (u32 tokens) or int16 (u16 tokens)")
+        chunks = max(1, min(int(chunks), B))
+        cuts = [int(round(B * c / chunks)) for c in range(chunks + 1)]
+        n_tok = int(seq_h.shape[0])
+        st = getattr(self, "_pinp", None)
+        if st is None:
+            st = self._pinp = {"streams": [torch.cuda.Stream(dev) for _ in range(5)], "key": None, "ws_key": None}
+        if st["key"] != (n_tok, B, narrow):
+            st["seq"] = torch.empty(n_tok, dtype=torch.int32, device=dev)
+            st["seq16"] = torch.empty(n_tok, dtype=torch.int16, device=dev) if narrow else None
+            st["off"] = torch.empty(B, dtype=torch.int64, device=dev)
+            st["len"] = torch.empty(B, dtype=torch.int32, device=dev)
+            st["tails"] = torch.empty(B * P, dtype=torch.int32, device=dev)
+            st["toff"] = torch.empty(B, dtype=torch.int64, device=dev)
+            st["tlen"] = torch.empty(B, dtype=torch.int32, device=dev)
+            st["key"] = (n_tok, B, narrow)
+        if st["ws_key"] != (B, int(max_len)):
+            st["ws"] = torch.empty(lib().sssd_propose_workspace(self.c, B, int(max_len)), dtype=torch.uint8,
+                                   device=dev)
+            st["ws_key"] = (B, int(max_len))
+        up, lk, sc, fu, down = st["streams"]
+        seq_d, off_d, len_d, ws = st["seq"], st["off"], st["len"], st["ws"]
+        out = self.outputs(B)
+        main = torch.cuda.current_stream(dev)
+        for s_ in st["streams"]:
+            s_.wait_stream(main)
+        if not (off_h.is_pinned() and len_h.is_pinned()):  # pageable copies would serialise the upload
+            pin = st.get("offlen")
+            if pin is None or pin[0].numel() < B:
+                pin = st["offlen"] = (torch.empty(B, dtype=torch.int64).pin_memory(),
+                                      torch.empty(B, dtype=torch.int32).pin_memory())
+            pin[0][:B].copy_(off_h)
+            pin[1][:B].copy_(len_h)
+            off_h, len_h = pin[0][:B], pin[1][:B]
+        spans = [(int(offs[cuts[c]:cuts[c + 1]].min()), int((offs[cuts[c]:cuts[c + 1]] + lens[cuts[c]:cuts[c + 1]]).max()))
+                 for c in range(chunks)]
+        d_out = _lib.DraftOut(ptr(out.size), ptr(out.tokens), ptr(out.parents), ptr(out.depths), ptr(out.mask))
+        ds = self.store.c_view()
+        full = _lib.Seqs(ptr(seq_d), ptr(off_d), ptr(len_d), B, int(max_len))
+        with torch.cuda.stream(up):  # offsets / lengths first, then the token ranges
+            off_d.copy_(off_h, non_blocking=True)
+            len_d.copy_(len_h, non_blocking=True)
+            ev_ol = torch.cuda.Event()
+            ev_ol.record(up)
+            ev_up = []
+            for t0, t1 in spans:
+                (st["seq16"] if narrow else seq_d)[t0:t1].copy_(seq_h[t0:t1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(up)
+                ev_up.append(ev)
+        # every request's datastore lookup, from its last P tokens read zero-copy
+        lk.wait_event(ev_ol)
+        tails = _lib.Seqs(ptr(st["tails"]), ptr(st["toff"]), ptr(st["tlen"]), B, P)
+        check(lib().sssd_gather_tails(seq_h.data_ptr(), 2 if narrow else 4, ptr(off_d), ptr(len_d), B, P,
+                                      ptr(st["tails"]), ptr(st["toff"]), ptr(st["tlen"]), lk.cuda_stream))
+        check(lib().sssd_propose_phase(ds, tails, self.c, d_out, None, ptr(ws), ws.numel(),
+                                       _lib.PHASE_BEGIN | _lib.PHASE_LOOKUP, B, int(max_len), 0, B, lk.cuda_stream))
+        ev_lk = torch.cuda.Event()
+        ev_lk.record(lk)
+        fu.wait_event(ev_lk)
+        for c in range(chunks):
+            r0, r1 = cuts[c], cuts[c + 1]
+            t0, t1 = spans[c]
+            sc.wait_event(ev_up[c])
+            if narrow:
+                check(lib().sssd_widen_u16(st["seq16"].data_ptr() + 2 * t0, seq_d.data_ptr() + 4 * t0, t1 - t0,
+                                           sc.cuda_stream))
+            check(lib().sssd_propose_phase(ds, full, self.c, d_out, None, ptr(ws), ws.numel(), _lib.PHASE_SCAN, B,
+                                           int(max_len), r0, r1, sc.cuda_stream))
+            ev_sc = torch.cuda.Event()
+            ev_sc.record(sc)
+            fu.wait_event(ev_sc)
+            check(lib().sssd_propose_phase(ds, full, self.c, d_out, None, ptr(ws), ws.numel(), _lib.PHASE_FUSE, B,
+                                           int(max_len), r0, r1, fu.cuda_stream))
+            ev_fu = torch.cuda.Event()
+            ev_fu.record(fu)
+            down.wait_event(ev_fu)
+            with torch.cuda.stream(down):
+                for dst, src in ((out_h.size, out.size), (out_h.tokens, out.tokens), (out_h.parents, out.parents),
+                                 (out_h.depths, out.depths), (out_h.mask, out.mask)):
+                    dst[r0:r1].copy_(src[r0:r1], non_blocking=True)
+        for s_ in (fu, down, sc, lk):
+            main.wait_stream(s_)
+        err = ws[_lib.SSSD_STATUS_OFFSET:_lib.SSSD_STATUS_OFFSET + 4].view(torch.int32)
+        if int(err.item()) != 0:  # synchronises the current stream
             raise _lib.SSSDError("device workspace overflow (fusion arena) in propose_pinned")
         return out_h
 

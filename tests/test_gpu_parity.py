@@ -230,8 +230,10 @@ def test_save_load_roundtrip(tmp_path):
 
 
 def test_propose_pinned_equals_resident_propose():
-    """The pipelined host-buffer entry point (chunked H2D / draft / D2H on three
-    streams) returns exactly the drafts of one device-resident propose, for
+    """The pipelined host-buffer entry point (both schedules: phased — lookup of
+    every request from its zero-copy tail, then scan / fusion per uploaded
+    range — and independent ranges) returns exactly the drafts of one
+    device-resident propose, for
     ragged lengths and offsets in shuffled order; the engine's workspace status
     stays readable after calls of different batch sizes."""
     rng = np.random.default_rng(21)
@@ -240,6 +242,7 @@ def test_propose_pinned_equals_resident_propose():
     eng = G.DraftEngine(ds, G.FusionConfig(dec_len=48))
     B = 37
     ctxs = [rng.integers(0, 500, int(rng.integers(1, 900))).astype(np.uint32) for _ in range(B)]
+    ctxs[:3] = [rng.integers(0, 500, n).astype(np.uint32) for n in (1, 2, 3)]  # shorter than P (tail views)
     order = rng.permutation(B)  # request r stored at a shuffled position in the flat buffer
     flat, offs, pos = [], np.zeros(B, np.int64), 0
     for r in order:
@@ -254,17 +257,18 @@ def test_propose_pinned_equals_resident_propose():
     want = {k: getattr(want, k).cpu().clone() for k in ("size", "tokens", "parents", "depths", "mask")}
     eng.check_status()
     seq16_h = torch.from_numpy(seq_h.numpy().astype(np.uint16).view(np.int16)).pin_memory()  # vocab 500 < 2^16
-    for chunks, src in ((1, seq_h), (3, seq_h), (8, seq_h), (3, seq16_h), (8, seq16_h)):
-        got = eng.propose_pinned(src, off_h, len_h, mx, chunks=chunks)
+    for schedule, chunks, src in [(s, c, x) for s in ("phased", "ranges")
+                                  for c, x in ((1, seq_h), (3, seq_h), (8, seq_h), (3, seq16_h), (8, seq16_h))]:
+        got = eng.propose_pinned(src, off_h, len_h, mx, chunks=chunks, schedule=schedule)
         for k, v in want.items():
             g = getattr(got, k)
             assert not g.is_cuda and g.is_pinned()
             if k == "size":
-                assert torch.equal(g, v), (chunks, k)
+                assert torch.equal(g, v), (schedule, chunks, k)
             else:  # entries past size are unspecified
                 for b in range(B):
                     n = int(want["size"][b])
-                    assert torch.equal(g[b, :n], v[b, :n]), (chunks, k, b)
+                    assert torch.equal(g[b, :n], v[b, :n]), (schedule, chunks, k, b)
     eng.propose_host([c.tolist() for c in ctxs[:3]])  # smaller call through a larger workspace
     eng.check_status()
 
