@@ -979,7 +979,50 @@ __global__ void __launch_bounds__(1024)
       kh[e] = h;
       kl[e] = l;
     }
-    if (!__syncthreads_or(wide)) {
+    const bool narrow_keys = !__syncthreads_or(wide);
+    if (narrow_keys && total > 1024) {
+      // many occurrences (prompt-heavy long contexts): a bitonic sort of the
+      // (key, position) triples in shared memory, O(n log^2 n) instead of
+      // the runs' O(n^2 / 32) binary searches; all-ascending form, so
+      // positions >= total act as +infinity without being stored
+      uint32_t* ix = srt;
+      for (int e = tid; e < total; e += blockDim.x) ix[e] = (uint32_t)e;
+      __syncthreads();
+      int n2 = 1;
+      while (n2 < total) n2 <<= 1;
+      for (int lk = 1; (1 << lk) <= n2; ++lk) {
+        for (int lj = lk - 1; lj >= 0; --lj) {
+          for (int q = tid; q < n2 / 2; q += blockDim.x) {
+            const int pb = q >> lj, pr = q & ((1 << lj) - 1);
+            int lo, hi;
+            if (lj == lk - 1) {
+              lo = (pb << lk) + pr;
+              hi = (pb << lk) + (1 << lk) - 1 - pr;
+            } else {
+              lo = (pb << (lj + 1)) + pr;
+              hi = lo + (1 << lj);
+            }
+            if (hi >= total) continue;
+            const uint64_t ha = kh[lo], la = kl[lo], hb = kh[hi], lb = kl[hi];
+            const uint32_t ia = ix[lo], ib = ix[hi];
+            if (hb < ha || (hb == ha && (lb < la || (lb == la && ib < ia)))) {
+              kh[lo] = hb, kl[lo] = lb, ix[lo] = ib;
+              kh[hi] = ha, kl[hi] = la, ix[hi] = ia;
+            }
+          }
+          __syncthreads();
+        }
+      }
+      const Cols cb{cols.meta ? cols.meta + (size_t)b * cols.stride : nullptr,
+                    cols.orig + (size_t)b * cols.stride, cols.tok + (size_t)b * cols.stride * c.IBL, cols.stride};
+      for (int i = tid; i < total; i += blockDim.x) {
+        const sssd_elem el = r[ix[i]];
+        out[i] = el;
+        if (cb.meta) write_cols(cb, i, el, seq);
+      }
+      return;
+    }
+    if (narrow_keys) {
       for (int e = tid; e < total; e += blockDim.x) {
         const int r0 = e & ~31, rn = min(32, total - r0);
         const uint64_t h = kh[e], l = kl[e];

@@ -51,7 +51,10 @@ __host__ __device__ inline int ds_lookup_smem_words(int P, int M) {
 // 2048-position tiles (fewer sequential tiles, wider occurrence sort)
 inline int input_scan_threads(int max_len) { return max_len > 4096 ? 1024 : 256; }
 __host__ __device__ inline int input_scan_smem_bytes(int threads, int ibl) {
-  const int need = threads * (ibl + 6);
+  int need = threads * (ibl + 6);
+  // long contexts (1024 threads, 2 CTAs per SM): room for the packed keys of
+  // up to 4096 occurrences (6 words each), sorted in shared memory
+  if (threads >= 1024 && need < 4096 * 6) need = 4096 * 6;
   return 4 * (need > 4096 ? need : 4096);
 }
 __global__ void input_scan_kernel(sssd_seqs seqs, KCfg c, sssd_elem* raw, sssd_elem* sorted,

@@ -199,6 +199,24 @@ def test_long_context_input_sort_path():
     assert (f.tokens, f.parents, f.depths) == (d.tokens, d.parents, d.depths)
 
 
+@pytest.mark.parametrize("alphabet,dec_len", [(8, 16), (12, 64), (16, 32)])
+def test_long_context_bitonic_input_sort(alphabet, dec_len):
+    """1,024 < occurrences <= 4,096 in a > 4,096-token context: the packed keys
+    are bitonic-sorted in shared memory (ties by position); drafts bit-exact
+    vs the oracle."""
+    rng = np.random.default_rng(alphabet)
+    seqs = [rng.integers(0, alphabet, int(n)).tolist() for n in (20000, 9000, 30000)]
+    corpus = rng.integers(0, alphabet, 50000).astype(np.uint32)
+    store = O.Store(corpus, O.suffix_array(corpus))
+    cfg = G.FusionConfig(dec_len=dec_len)
+    got = G.DraftEngine(G.build(corpus), cfg).propose_host(seqs)
+    for seq, f in zip(seqs, got):
+        occ = sum(1 for t in seq[:-1] if t == seq[-1])
+        assert 1024 < occ <= 4096 or len(seq) < 10000
+        d = O.propose(store, seq, O.Cfg(dec_len=dec_len))
+        assert (f.tokens, f.parents, f.depths) == (d.tokens, d.parents, d.depths)
+
+
 def test_verify_matches_oracle():
     rng = np.random.default_rng(9)
     corpus = workload.corpus(50_000, 50)
