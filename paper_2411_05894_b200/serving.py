@@ -74,7 +74,9 @@ class SpecDecoder:
         self.model.compact(ctx, self.path if S == self.S else self.path[:, :S].contiguous(), self.n_acc)
 
     def run(self, graph_steps: int = 8) -> dict:
-        """Decode every slot to its cap; returns tokens, steps and timing.
+        """Decode every slot to its cap; returns tokens, steps and timing
+        (``tokens_per_s`` over the whole call, ``steady_tokens_per_s`` after
+        the first eager step and the graph capture).
 
         The first step runs eagerly (it creates every lazily allocated buffer);
         later steps run in groups of ``graph_steps`` replayed from one CUDA
@@ -110,6 +112,8 @@ class SpecDecoder:
                 torch.cuda.synchronize()
                 graph = None
                 self.graph_error = repr(exc)
+        torch.cuda.synchronize()
+        t1, lens1 = perf_counter(), lens.clone()  # steady state: after the eager first step and the capture
         while bool((lens < cap).any()):
             if graph is None:
                 self.step()
@@ -126,9 +130,12 @@ class SpecDecoder:
                 lens = H[g]
                 self.steps += 1
         torch.cuda.synchronize()
-        dt = perf_counter() - t0
+        t2 = perf_counter()
+        dt = t2 - t0
         gen = int((self.seq_len - start).sum())
+        steady = int((self.seq_len.cpu() - lens1).sum())
         return {"tokens": gen, "steps": self.steps, "seconds": dt, "tokens_per_s": gen / dt,
+                "steady_tokens_per_s": steady / (t2 - t1) if t2 > t1 and steady else 0.0,
                 "accepted_per_step": float(torch.stack(per_step).float().mean()) if per_step else 0.0,
                 "cuda_graph": graph is not None}
 
