@@ -350,7 +350,6 @@ __device__ __noinline__ uint2 ls_generate(const LsPar par, int np, uint32_t E, L
     if (hasm) {  // (a carried run always continues at lane 0, so none is open otherwise)
       const unsigned long long key = has ? ((unsigned long long)j << 32 | tk) : (1ull << 63 | (unsigned)lane);
       const uint32_t gm = __match_any_sync(SSSD_FULL, key);
-      const uint32_t wm = __ballot_sync(SSSD_FULL, w);
       const int lo_l = __ffs(gm) - 1, hi_l = 31 - __clz(gm);
       // run minimum of orig and run sum of weights (segmented down-scans;
       // runs are lane intervals)
@@ -366,7 +365,6 @@ __device__ __noinline__ uint2 ls_generate(const LsPar par, int np, uint32_t E, L
       }
       fm = __shfl_sync(SSSD_FULL, fm, lo_l);
       cnt = __shfl_sync(SSSD_FULL, cnt, lo_l);
-      (void)wm;
       uint32_t start = i - (uint32_t)(lane - lo_l);
       if (c_open && lo_l == 0) {  // the run carried in from the previous chunk
         cnt += c_cnt;
