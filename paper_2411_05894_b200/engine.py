@@ -156,7 +156,7 @@ class DraftEngine:
         uploads range by range (``sssd_propose_phase``).  ``"ranges"``: every
         range is an independent propose."""
         if schedule == "phased" and seq_h.is_pinned() and (self.use_datastore and self.store is not None):
-            return self._propose_pinned_phased(seq_h, off_h, len_h, max_len, out_h, chunks)
+            return self._propose_pinned_phased(seq_h, off_h, len_h, max_len, out_h, chunks, tail)
         B = int(len_h.shape[0])
         dev = self.device
         S, W = self.S, self.W
@@ -262,7 +262,7 @@ class DraftEngine:
         return out_h
 
     def _propose_pinned_phased(self, seq_h: torch.Tensor, off_h: torch.Tensor, len_h: torch.Tensor, max_len: int,
-                               out_h: DraftBatch | None, chunks: int) -> DraftBatch:
+                               out_h: DraftBatch | None, chunks: int, tail: float | None = None) -> DraftBatch:
         B = int(len_h.shape[0])
         dev = self.device
         S, W, P = self.S, self.W, int(self.c.P)
@@ -282,7 +282,11 @@ class DraftEngine:
         if not narrow and seq_h.dtype != torch.int32:
             raise ValueError("seq_h must be int32 (u32 tokens) or int16 (u16 tokens)")
         chunks = max(1, min(int(chunks), B))
-        cuts = [int(round(B * c / chunks)) for c in range(chunks + 1)]
+        # equal ranges; optionally a shorter last one (its drafting + download is what no upload hides)
+        wts = np.ones(chunks)
+        if tail is not None and chunks > 1:
+            wts[-1] = float(tail)
+        cuts = [0] + [int(round(B * x)) for x in np.cumsum(wts)[:-1] / wts.sum()] + [B]
         n_tok = int(seq_h.shape[0])
         st = getattr(self, "_pinp", None)
         if st is None:

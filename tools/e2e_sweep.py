@@ -32,8 +32,8 @@ def timed(**kw):
     return round(float(np.median(ts)), 3)
 
 
-for kw in [dict(chunks=5), dict(chunks=4), dict(chunks=6), dict(chunks=8),
-           dict(chunks=6, taper=0.8), dict(chunks=8, taper=0.8), dict(chunks=8, taper=0.7),
-           dict(chunks=10, taper=0.75), dict(chunks=6, taper=0.7), dict(chunks=5, tail=0.3),
-           dict(chunks=6, tail=0.25), dict(chunks=8, taper=0.85, tail=0.2)]:
+sweep = [dict(chunks=5), dict(chunks=4), dict(chunks=6), dict(chunks=5, tail=0.6), dict(chunks=5, tail=0.4),
+         dict(chunks=6, tail=0.5), dict(chunks=6, tail=0.3), dict(chunks=4, tail=0.5), dict(chunks=7, tail=0.5),
+         dict(chunks=5, schedule="ranges")]
+for kw in sweep:
     print(kw, timed(**kw), flush=True)
