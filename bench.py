@@ -384,7 +384,8 @@ def run_ours(args) -> None:
                                              ("input_scan_kernel", lk_scan, prof[1]),
                                              ("draft_ls_kernel", lk_out, prof[3]))},
                          "dominant_kernel": names[dom],
-                         "dominant_share": round(float(prof[dom] / prof.sum()), 3)},
+                         "dominant_share": round(float(prof[dom] / prof.sum()), 3),
+                         "issue_roofline": issue_roofline(prof[3], B, clk.summary())},
             "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "input_format": "u16 token ids (vocab 32000), widened on device" if ctx16_h is not None
@@ -489,6 +490,27 @@ def bench_lookup_cfg4(ds, corpus) -> dict:
             "b8_latency_ms": round(lat, 4), "b8_lookups_per_s": round(Bq / lat * 1e3, 1),
             "throughput_lookups_per_s": round(Bq * R / thr * 1e3, 1), "throughput_requests": Bq * R,
             "drafts_bitexact_vs_cpu_oracle": exact, "cpu_oracle_s_per_lookup": round(cpu_s, 3)}
+
+
+def issue_roofline(fusion_ms: float, B: int, clk) -> dict | None:
+    """The fusion kernel is issue-bound, not HBM-bound: its warp instructions
+    per lookup (ncu count of the committed capture, profiles/r1_propose_ncu.json:
+    warp_inst / grid, one warp per request) over this run's kernel time, against
+    148 SMs x 4 schedulers x the SM clock sampled during the timed region."""
+    path = os.path.join(ROOT, "profiles", "r1_propose_ncu.json")
+    if not os.path.exists(path):
+        return None
+    rows = [k for k in json.load(open(path))["kernels"] if k["kernel"] == "draft_ls_kernel"]
+    if not rows:
+        return None
+    per_lookup = rows[0]["warp_inst"] / rows[0]["grid"]
+    mhz = float((clk or {}).get("sm_mhz") or 1965.0)
+    peak = 148 * 4 * mhz * 1e6
+    achieved = per_lookup * B / (float(fusion_ms) / 1e3)
+    return {"kernel": "draft_ls_kernel", "bound": "issue", "unit": "warp instructions/s",
+            "warp_instructions_per_lookup": round(per_lookup, 1), "achieved": round(achieved / 1e9, 1),
+            "peak": round(peak / 1e9, 1), "scale": "1e9", "frac": round(achieved / peak, 4),
+            "source": "profiles/r1_propose_ncu.json (ncu smsp__inst_executed of the same kernel)"}
 
 
 def bench_decode_cfg1(budget_s: float = 60.0) -> dict:
