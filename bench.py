@@ -332,11 +332,44 @@ def run_ours(args) -> None:
         tot = allreduce_max(float(np.sum(ms)), world)
         return B * world * args.steps / (tot / 1e3), src.numel() * src.element_size() + B * 8 + B * 4
 
+    def e2e_stream(src):
+        """Back-to-back steps as a serving loop issues them: two slots in
+        flight (propose_pinned(..., slot, sync=False)), so step i+1's uploads
+        overlap step i's last drafting and downloads; every step still moves
+        its contexts up and its drafts down inside the timed region."""
+        outs = [None, None]
+        for k in range(2):  # pinned output buffers + per-slot device state, outside the timing
+            outs[k] = eng.propose_pinned(src, off_h, len_h, CTX, chunks=args.e2e_chunks, slot=k)
+        torch.cuda.synchronize(dev)
+        best = None
+        for _rep in range(2):
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            pend = [None, None]
+            a.record(st)
+            for i in range(args.steps):
+                k = i & 1
+                if pend[k] is not None:
+                    pend[k].wait()
+                pend[k] = eng.propose_pinned(src, off_h, len_h, CTX, out_h=outs[k], chunks=args.e2e_chunks,
+                                             slot=k, sync=False)
+            for p_ in pend:
+                if p_ is not None:
+                    st.wait_event(p_.done)
+                    p_.wait()
+            b_.record(st)
+            torch.cuda.synchronize(dev)
+            ms = a.elapsed_time(b_)
+            best = ms if best is None else min(best, ms)
+        tot = allreduce_max(best, world)
+        return B * world * args.steps / (tot / 1e3)
+
     e2e_u32, h2d_u32 = e2e_run(ctx_h)
     if ctx16_h is not None:
-        e2e_value, h2d = e2e_run(ctx16_h)
+        e2e_serial, h2d = e2e_run(ctx16_h)
+        e2e_value = e2e_stream(ctx16_h)
     else:
-        e2e_value, h2d = e2e_u32, h2d_u32
+        e2e_serial, h2d = e2e_u32, h2d_u32
+        e2e_value = e2e_stream(ctx_h)
 
     peak, peak_src = peaks()
     achieved = bytes_per_step / (ms_per_step / 1e3) / 1e9
@@ -413,7 +446,9 @@ def run_ours(args) -> None:
                     "d2h_bytes_per_step": int(d2h),
                     "input_format": "u16 token ids (vocab 32000), widened on device" if ctx16_h is not None
                     else "u32 token ids",
-                    "u32_upload": {"value": round(e2e_u32, 1), "h2d_bytes_per_step": int(h2d_u32)}},
+                    "u32_upload": {"value": round(e2e_u32, 1), "h2d_bytes_per_step": int(h2d_u32)},
+                    "schedule": "back-to-back steps, two in flight (propose_pinned slot / sync=False)",
+                    "serial_value": round(e2e_serial, 1)},
             # per propose: ds_lookup, input_scan, propose_setup, (lpt_scatter when B >= 2048), draft_ls
             "gpu_launches": (5 if B >= 2048 else 4) * args.steps,
             "clocks": clk.summary(),

@@ -37,6 +37,21 @@ class DraftBatch:
         return int(self.size.shape[0])
 
 
+class PendingDrafts:
+    """An in-flight ``propose_pinned(..., sync=False)``: ``wait()`` blocks until
+    the drafts are in the pinned host buffers and checks the fusion arena."""
+
+    def __init__(self, out_h: "DraftBatch", done, err_h) -> None:
+        self.out_h, self.done, self.err_h = out_h, done, err_h
+
+    def wait(self) -> "DraftBatch":
+        if self.done is not None:
+            self.done.synchronize()
+            if int(self.err_h[0]) != 0:
+                raise _lib.SSSDError("device workspace overflow (fusion arena) in propose_pinned")
+        return self.out_h
+
+
 class DraftEngine:
     """Drafting for one datastore + config on one GPU."""
 
@@ -134,7 +149,8 @@ class DraftEngine:
 
     def propose_pinned(self, seq_h: torch.Tensor, off_h: torch.Tensor, len_h: torch.Tensor, max_len: int,
                        out_h: DraftBatch | None = None, chunks: int = 5, taper: float = 1.0,
-                       tail: float | None = None, schedule: str = "phased") -> DraftBatch:
+                       tail: float | None = None, schedule: str = "phased", slot: int = 0,
+                       sync: bool = True):
         """Host-buffer entry point for a large batch: contexts in pinned host
         memory (seq_h int32 = u32 token ids, or int16 = u16 token ids when the
         vocabulary fits 16 bits: half the upload bytes, widened on the device by
@@ -154,9 +170,17 @@ class DraftEngine:
         its context tail (``sssd_gather_tails`` reads the last P tokens from the
         pinned host buffer), so only the input scan and the fusion follow the
         uploads range by range (``sssd_propose_phase``).  ``"ranges"``: every
-        range is an independent propose."""
+        range is an independent propose.
+
+        ``sync=False`` (phased schedule): returns a ``PendingDrafts`` at once
+        (``.wait()`` -> the DraftBatch); calls on different ``slot`` s (own
+        device buffers each) can then be in flight together, so batch i+1's
+        uploads overlap batch i's last drafting and downloads.  Reusing a slot
+        (or ``out_h``) requires the previous call on it to have been waited."""
         if schedule == "phased" and seq_h.is_pinned() and (self.use_datastore and self.store is not None):
-            return self._propose_pinned_phased(seq_h, off_h, len_h, max_len, out_h, chunks, tail)
+            return self._propose_pinned_phased(seq_h, off_h, len_h, max_len, out_h, chunks, tail, slot, sync)
+        if not sync:
+            raise ValueError("sync=False needs the phased schedule (pinned seq_h and a datastore)")
         B = int(len_h.shape[0])
         dev = self.device
         S, W = self.S, self.W
@@ -262,7 +286,8 @@ class DraftEngine:
         return out_h
 
     def _propose_pinned_phased(self, seq_h: torch.Tensor, off_h: torch.Tensor, len_h: torch.Tensor, max_len: int,
-                               out_h: DraftBatch | None, chunks: int, tail: float | None = None) -> DraftBatch:
+                               out_h: DraftBatch | None, chunks: int, tail: float | None = None, slot: int = 0,
+                               sync: bool = True):
         B = int(len_h.shape[0])
         dev = self.device
         S, W, P = self.S, self.W, int(self.c.P)
@@ -274,7 +299,7 @@ class DraftEngine:
                 depths=torch.empty((B, S), dtype=torch.int32).pin_memory(),
                 mask=torch.empty((B, S, W), dtype=torch.int64).pin_memory())
         if B == 0:
-            return out_h
+            return out_h if sync else PendingDrafts(out_h, None, None)
         offs, lens = off_h.numpy(), len_h.numpy()
         if (lens < 1).any():
             raise ValueError("empty prompt: the draft root is the last context token")
@@ -290,30 +315,33 @@ class DraftEngine:
         n_tok = int(seq_h.shape[0])
         st = getattr(self, "_pinp", None)
         if st is None:
-            st = self._pinp = {"streams": [torch.cuda.Stream(dev) for _ in range(5)], "key": None, "ws_key": None}
-        if st["key"] != (n_tok, B, narrow):
-            st["seq"] = torch.empty(n_tok, dtype=torch.int32, device=dev)
-            st["seq16"] = torch.empty(n_tok, dtype=torch.int16, device=dev) if narrow else None
-            st["off"] = torch.empty(B, dtype=torch.int64, device=dev)
-            st["len"] = torch.empty(B, dtype=torch.int32, device=dev)
-            st["tails"] = torch.empty(B * P, dtype=torch.int32, device=dev)
-            st["toff"] = torch.empty(B, dtype=torch.int64, device=dev)
-            st["tlen"] = torch.empty(B, dtype=torch.int32, device=dev)
-            st["key"] = (n_tok, B, narrow)
-        if st["ws_key"] != (B, int(max_len)):
-            st["ws"] = torch.empty(lib().sssd_propose_workspace(self.c, B, int(max_len)), dtype=torch.uint8,
+            st = self._pinp = {"streams": [torch.cuda.Stream(dev) for _ in range(5)], "slots": {}}
+        # per-slot device buffers: a call may run while the previous slot's call is in flight
+        ss = st["slots"].setdefault(int(slot), {"key": None, "ws_key": None})
+        if ss["key"] != (n_tok, B, narrow):
+            ss["seq"] = torch.empty(n_tok, dtype=torch.int32, device=dev)
+            ss["seq16"] = torch.empty(n_tok, dtype=torch.int16, device=dev) if narrow else None
+            ss["off"] = torch.empty(B, dtype=torch.int64, device=dev)
+            ss["len"] = torch.empty(B, dtype=torch.int32, device=dev)
+            ss["tails"] = torch.empty(B * P, dtype=torch.int32, device=dev)
+            ss["toff"] = torch.empty(B, dtype=torch.int64, device=dev)
+            ss["tlen"] = torch.empty(B, dtype=torch.int32, device=dev)
+            ss["out"] = self.outputs(B)
+            ss["err_h"] = torch.zeros(1, dtype=torch.int32).pin_memory()
+            ss["key"] = (n_tok, B, narrow)
+        if ss["ws_key"] != (B, int(max_len)):
+            ss["ws"] = torch.empty(lib().sssd_propose_workspace(self.c, B, int(max_len)), dtype=torch.uint8,
                                    device=dev)
-            st["ws_key"] = (B, int(max_len))
+            ss["ws_key"] = (B, int(max_len))
         up, lk, sc, fu, down = st["streams"]
-        seq_d, off_d, len_d, ws = st["seq"], st["off"], st["len"], st["ws"]
-        out = self.outputs(B)
+        seq_d, off_d, len_d, ws, out = ss["seq"], ss["off"], ss["len"], ss["ws"], ss["out"]
         main = torch.cuda.current_stream(dev)
         for s_ in st["streams"]:
             s_.wait_stream(main)
         if not (off_h.is_pinned() and len_h.is_pinned()):  # pageable copies would serialise the upload
-            pin = st.get("offlen")
+            pin = ss.get("offlen")
             if pin is None or pin[0].numel() < B:
-                pin = st["offlen"] = (torch.empty(B, dtype=torch.int64).pin_memory(),
+                pin = ss["offlen"] = (torch.empty(B, dtype=torch.int64).pin_memory(),
                                       torch.empty(B, dtype=torch.int32).pin_memory())
             pin[0][:B].copy_(off_h)
             pin[1][:B].copy_(len_h)
@@ -330,15 +358,15 @@ class DraftEngine:
             ev_ol.record(up)
             ev_up = []
             for t0, t1 in spans:
-                (st["seq16"] if narrow else seq_d)[t0:t1].copy_(seq_h[t0:t1], non_blocking=True)
+                (ss["seq16"] if narrow else seq_d)[t0:t1].copy_(seq_h[t0:t1], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(up)
                 ev_up.append(ev)
         # every request's datastore lookup, from its last P tokens read zero-copy
         lk.wait_event(ev_ol)
-        tails = _lib.Seqs(ptr(st["tails"]), ptr(st["toff"]), ptr(st["tlen"]), B, P)
+        tails = _lib.Seqs(ptr(ss["tails"]), ptr(ss["toff"]), ptr(ss["tlen"]), B, P)
         check(lib().sssd_gather_tails(seq_h.data_ptr(), 2 if narrow else 4, ptr(off_d), ptr(len_d), B, P,
-                                      ptr(st["tails"]), ptr(st["toff"]), ptr(st["tlen"]), lk.cuda_stream))
+                                      ptr(ss["tails"]), ptr(ss["toff"]), ptr(ss["tlen"]), lk.cuda_stream))
         check(lib().sssd_propose_phase(ds, tails, self.c, d_out, None, ptr(ws), ws.numel(),
                                        _lib.PHASE_BEGIN | _lib.PHASE_LOOKUP, B, int(max_len), 0, B, lk.cuda_stream))
         ev_lk = torch.cuda.Event()
@@ -349,7 +377,7 @@ class DraftEngine:
             t0, t1 = spans[c]
             sc.wait_event(ev_up[c])
             if narrow:
-                check(lib().sssd_widen_u16(st["seq16"].data_ptr() + 2 * t0, seq_d.data_ptr() + 4 * t0, t1 - t0,
+                check(lib().sssd_widen_u16(ss["seq16"].data_ptr() + 2 * t0, seq_d.data_ptr() + 4 * t0, t1 - t0,
                                            sc.cuda_stream))
             check(lib().sssd_propose_phase(ds, full, self.c, d_out, None, ptr(ws), ws.numel(), _lib.PHASE_SCAN, B,
                                            int(max_len), r0, r1, sc.cuda_stream))
@@ -365,12 +393,18 @@ class DraftEngine:
                 for dst, src in ((out_h.size, out.size), (out_h.tokens, out.tokens), (out_h.parents, out.parents),
                                  (out_h.depths, out.depths), (out_h.mask, out.mask)):
                     dst[r0:r1].copy_(src[r0:r1], non_blocking=True)
-        for s_ in (fu, down, sc, lk):
-            main.wait_stream(s_)
         err = ws[_lib.SSSD_STATUS_OFFSET:_lib.SSSD_STATUS_OFFSET + 4].view(torch.int32)
-        if int(err.item()) != 0:  # synchronises the current stream
-            raise _lib.SSSDError("device workspace overflow (fusion arena) in propose_pinned")
-        return out_h
+        if sync:
+            for s_ in (fu, down, sc, lk):
+                main.wait_stream(s_)
+            if int(err.item()) != 0:  # synchronises the current stream
+                raise _lib.SSSDError("device workspace overflow (fusion arena) in propose_pinned")
+            return out_h
+        with torch.cuda.stream(down):  # after the last fusion (down waited for it) and the last download
+            ss["err_h"].copy_(err, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(down)
+        return PendingDrafts(out_h, done, ss["err_h"])
 
     def check_status(self) -> None:
         """Synchronise and raise if the device fusion arena overflowed."""

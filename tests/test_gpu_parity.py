@@ -287,6 +287,16 @@ def test_propose_pinned_equals_resident_propose():
                 for b in range(B):
                     n = int(want["size"][b])
                     assert torch.equal(g[b, :n], v[b, :n]), (schedule, chunks, k, b)
+    # two calls in flight on different slots (async), then waited: both exact
+    pend = [eng.propose_pinned(src, off_h, len_h, mx, chunks=3, slot=k, sync=False) for k, src in
+            ((0, seq_h), (1, seq16_h))]
+    for p_ in pend:
+        got = p_.wait()
+        assert torch.equal(got.size, want["size"])
+        for b in range(B):
+            n = int(want["size"][b])
+            assert torch.equal(got.tokens[b, :n], want["tokens"][b, :n])
+            assert torch.equal(got.mask[b, :n], want["mask"][b, :n])
     eng.propose_host([c.tolist() for c in ctxs[:3]])  # smaller call through a larger workspace
     eng.check_status()
 
