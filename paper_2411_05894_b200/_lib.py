@@ -20,7 +20,7 @@ SSSD_MAX_DEPTH = 32
 SSSD_MAX_DRAFT = 256
 SSSD_ROW_TOKENS = 15
 SSSD_STATUS_OFFSET = 8  # int32 status word in every propose / merge workspace
-PHASE_LOOKUP, PHASE_SCAN, PHASE_FUSE, PHASE_BEGIN = 1, 2, 4, 8  # sssd_propose_phase bits
+SSSD_PHASE_LOOKUP, SSSD_PHASE_SCAN, SSSD_PHASE_FUSE, SSSD_PHASE_BEGIN = 1, 2, 4, 8  # sssd_propose_phase bits
 E_WORKSPACE = -4
 
 u32p = C.POINTER(C.c_uint32)

@@ -368,7 +368,7 @@ class DraftEngine:
         check(lib().sssd_gather_tails(seq_h.data_ptr(), 2 if narrow else 4, ptr(off_d), ptr(len_d), B, P,
                                       ptr(ss["tails"]), ptr(ss["toff"]), ptr(ss["tlen"]), lk.cuda_stream))
         check(lib().sssd_propose_phase(ds, tails, self.c, d_out, None, ptr(ws), ws.numel(),
-                                       _lib.PHASE_BEGIN | _lib.PHASE_LOOKUP, B, int(max_len), 0, B, lk.cuda_stream))
+                                       _lib.SSSD_PHASE_BEGIN | _lib.SSSD_PHASE_LOOKUP, B, int(max_len), 0, B, lk.cuda_stream))
         ev_lk = torch.cuda.Event()
         ev_lk.record(lk)
         fu.wait_event(ev_lk)
@@ -379,12 +379,12 @@ class DraftEngine:
             if narrow:
                 check(lib().sssd_widen_u16(ss["seq16"].data_ptr() + 2 * t0, seq_d.data_ptr() + 4 * t0, t1 - t0,
                                            sc.cuda_stream))
-            check(lib().sssd_propose_phase(ds, full, self.c, d_out, None, ptr(ws), ws.numel(), _lib.PHASE_SCAN, B,
+            check(lib().sssd_propose_phase(ds, full, self.c, d_out, None, ptr(ws), ws.numel(), _lib.SSSD_PHASE_SCAN, B,
                                            int(max_len), r0, r1, sc.cuda_stream))
             ev_sc = torch.cuda.Event()
             ev_sc.record(sc)
             fu.wait_event(ev_sc)
-            check(lib().sssd_propose_phase(ds, full, self.c, d_out, None, ptr(ws), ws.numel(), _lib.PHASE_FUSE, B,
+            check(lib().sssd_propose_phase(ds, full, self.c, d_out, None, ptr(ws), ws.numel(), _lib.SSSD_PHASE_FUSE, B,
                                            int(max_len), r0, r1, fu.cuda_stream))
             ev_fu = torch.cuda.Event()
             ev_fu.record(fu)

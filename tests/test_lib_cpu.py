@@ -49,6 +49,24 @@ def test_library_is_sm100a():
     assert "sm_100a" in out
 
 
+def test_phase_entry_points_validate_before_launch():
+    """sssd_propose_phase / sssd_gather_tails reject bad arguments with
+    SSSD_E_ARG before touching the device (no GPU needed)."""
+    import ctypes as C
+
+    from paper_2411_05894_b200 import _lib
+
+    h = _lib.lib()
+    assert h.sssd_propose_phase(None, None, None, None, None, None, 0, _lib.SSSD_PHASE_LOOKUP, 1, 8, 0, 1,
+                                None) == -1
+    buf = C.create_string_buffer(64)
+    for P in (0, _lib.SSSD_MAX_P + 1):
+        assert h.sssd_gather_tails(buf, 2, buf, buf, 1, P, buf, buf, buf, None) == -1
+    assert h.sssd_gather_tails(buf, 3, buf, buf, 1, 4, buf, buf, buf, None) == -1  # elem bytes
+    assert h.sssd_gather_tails(None, 2, buf, buf, 0, 4, buf, buf, buf, None) == 0  # empty batch: no-op
+    assert "gather_tails" in h.sssd_last_error().decode()
+
+
 def test_error_strings():
     from paper_2411_05894_b200 import _lib
 
