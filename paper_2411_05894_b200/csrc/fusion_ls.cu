@@ -30,6 +30,12 @@
 
 namespace sssd {
 
+// the level phases are inlined: as separate calls (__noinline__) the kernel
+// spilled across them and took 0.515 instead of 0.485 ms per cfg2 step
+#ifndef SSSD_LS_CALL
+#define SSSD_LS_CALL __forceinline__
+#endif
+
 // One level's nodes, structure of arrays over one base pointer (fields are
 // recomputed from (base, cap), which keeps them out of registers).
 // k0/k1/ord/tbr/pid are indexed by sorted position, pp/a/z/cnt/tok/ppid by
@@ -130,7 +136,7 @@ __device__ __forceinline__ uint8_t* pool_take(uint8_t* pool, unsigned long long*
 
 // Sort positions [0, n) by (k0, k1), carrying ord (n <= 32: ranks in
 // registers; otherwise a bitonic network).
-__device__ __noinline__ void ls_sort(LsLevel L, uint32_t n) {
+__device__ SSSD_LS_CALL void ls_sort(LsLevel L, uint32_t n) {
   const int lane = lane_id();
   if (n <= 32) {
     uint64_t m0 = ~0ull, m1 = ~0ull;
@@ -190,7 +196,7 @@ __device__ __noinline__ void ls_sort(LsLevel L, uint32_t n) {
 
 // Cut a full level buffer to its smallest `keepn` (<= kLsCap - 32) nodes, moved to
 // slots [0, keepn) in order; returns keepn and the first cut key.
-__device__ __noinline__ uint32_t ls_cut(LsLevel L, uint32_t nb, uint32_t keepn, uint64_t* th0, uint64_t* th1) {
+__device__ SSSD_LS_CALL uint32_t ls_cut(LsLevel L, uint32_t nb, uint32_t keepn, uint64_t* th0, uint64_t* th1) {
   const uint32_t lane = (uint32_t)lane_id();
   ls_sort(L, nb);
   *th0 = L.k0()[keepn];
@@ -240,7 +246,7 @@ __device__ __noinline__ uint32_t ls_cut(LsLevel L, uint32_t nb, uint32_t keepn, 
 // above the cut key are discarded: L always holds a prefix of the level's
 // (k0, k1) order, which is all the level needs whenever that prefix holds
 // dec_len - 1 distinct paths (the caller checks and otherwise regenerates).
-__device__ __noinline__ uint2 ls_generate(const LsPar par, int np, uint32_t E, LsLevel L, uint32_t cap,
+__device__ SSSD_LS_CALL uint2 ls_generate(const LsPar par, int np, uint32_t E, LsLevel L, uint32_t cap,
                                           uint32_t keepn, const SrcDesc* sd, const double* disc,
                                           int disc_stride, int d, bool has_empty, bool has_tau, uint64_t tau0,
                                           uint32_t tau_dr) {
