@@ -393,7 +393,7 @@ __device__ SSSD_LS_CALL uint2 ls_generate(const LsPar par, int np, uint32_t E, L
 }
 
 #ifndef SSSD_LS_MINB
-#define SSSD_LS_MINB 20
+#define SSSD_LS_MINB 24  // 80 registers, no spills (the level phases are inlined)
 #endif
 #ifdef SSSD_LS_PROBE  // per-phase cycle counts in the cycle probe (costs registers)
 #define LS_PROBE(...) __VA_ARGS__
