@@ -11,8 +11,10 @@ a 100M-token phrase-model datastore resident in HBM, dec_len = 64.  `value` is
 whole-job lookups/s with inputs already in HBM (device time, CUDA events,
 max over ranks); `e2e` is the same through the public API with the contexts
 copied H2D from pinned memory and the drafts copied back D2H every step.
-Multi-GPU: every rank drafts its own R*64 requests against a replicated
-datastore (weak scaling, no data-path collective).
+Multi-GPU: every rank drafts its own R*64 requests (weak scaling); the suffix
+rows are sharded by SA-rank range with one NCCL exchange per step (SURVEY
+§8(e)); the replicated datastore (no data-path collective) is timed beside it
+as config.control (--replicated makes it the headline).
 
 `--impl reference` times the reference algorithm on the host cores (the CPU
 oracle port, process-parallel over all cores, one B=64 batch per step).
@@ -140,6 +142,9 @@ def dist_setup(n_gpus: int):
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:  # NCCL's init log (comm nranks / transports) stays on stderr for the record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
@@ -170,23 +175,45 @@ def allreduce_max(x: float, world: int) -> float:
     return float(t.item())
 
 
-def cpu_baseline(tokens: np.ndarray, sa: np.ndarray, ctxs: list, budget_s: float = 12.0) -> dict:
-    """The CPU oracle port, single thread, on a bounded sample of the step's contexts."""
+def cpu_baseline(tokens: np.ndarray, sa: np.ndarray, ctxs: list, budget_s: float = 12.0) -> tuple[dict, list]:
+    """The CPU oracle port, single thread, on a bounded sample of the step's
+    contexts; also returns its drafts (the parity check's expected values)."""
     from oracle import sssd_oracle as O
 
     store = O.Store(tokens, sa)
     cfg = O.Cfg(dec_len=DEC_LEN)
     disc = cfg.disc()
     t0 = time.perf_counter()
-    done = 0
+    drafts = []
     for c in ctxs:
-        O.propose(store, c, cfg, disc=disc)
-        done += 1
+        drafts.append(O.propose(store, c, cfg, disc=disc))
         if time.perf_counter() - t0 > budget_s:
             break
     dt = time.perf_counter() - t0
-    return {"value": done / dt, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{done} cfg2 lookups (oracle/sssd_oracle.py propose, 1 thread) on the same 100M datastore"}
+    return {"value": len(drafts) / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{len(drafts)} cfg2 lookups (oracle/sssd_oracle.py propose, 1 thread) on the same 100M "
+                      "datastore and the first contexts of the timed step"}, drafts
+
+
+def parity_block(gpu_flats: list, oracle_drafts: list) -> dict:
+    """cfg2 drafts of the timed batch (first len(oracle_drafts) requests, the
+    same contexts the reference arm drafts) against the CPU oracle: ordered
+    tokens / parents / depths and the packed ancestor masks, compared through
+    the reference's draft_digest (ref harness.py:316-322) and row by row."""
+    from oracle import sssd_oracle as O
+    from paper_2411_05894_b200 import draft_digest
+
+    n = len(oracle_drafts)
+    g = gpu_flats[:n]
+    rows_equal = sum(int((f.tokens, f.parents, f.depths) == (d.tokens, d.parents, d.depths))
+                     for f, d in zip(g, oracle_drafts))
+    d_gpu, d_cpu = draft_digest(g), O.digest(oracle_drafts)
+    k = min(n, BATCH)
+    return {"cfg2_bitexact": bool(rows_equal == n and d_gpu == d_cpu), "n": n, "rows_equal": rows_equal,
+            "digest": d_gpu, "oracle_digest": d_cpu,
+            "digest_first64": draft_digest(g[:k]), "oracle_digest_first64": O.digest(oracle_drafts[:k]),
+            "checked_against": "oracle/sssd_oracle.py (pinned to reference goldens) on the timed step's first "
+                               f"{n} contexts; digest_first64 = the reference arm's batch"}
 
 
 def run_ours(args) -> None:
@@ -208,12 +235,36 @@ def run_ours(args) -> None:
     stream_all = workload.phrase_stream(B * CTX * world, VOCAB, workload.HELDOUT_SEED)
     mine = stream_all[rank * B * CTX:(rank + 1) * B * CTX]
     cfg = G.FusionConfig(dec_len=DEC_LEN)
-    if args.shard and world > 1:
+    args.shard = world > 1 and not args.replicated
+    control = None
+    if args.shard:
+        # control experiment: the replicated datastore, no
+        # data-path collective, same requests -- timed before the shard split
+        ceng = G.DraftEngine(ds, cfg, device=dev)
+        cseq = torch.from_numpy(mine.view(np.int32)).to(dev)
+        coff = (torch.arange(B, dtype=torch.int64) * CTX).to(dev)
+        cln = torch.full((B,), CTX, dtype=torch.int32, device=dev)
+        for _ in range(args.warmup):
+            ceng.propose(cseq, coff, cln, CTX)
+        barrier(world)
+        torch.cuda.synchronize(dev)
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record()
+        for _ in range(args.steps):
+            ceng.propose(cseq, coff, cln, CTX)
+        b_.record()
+        torch.cuda.synchronize(dev)
+        cms = allreduce_max(a_.elapsed_time(b_), world)
+        control = {"parallelism": f"replicated datastore x{world}, requests partitioned, no data-path collective",
+                   "value": round(B * world * args.steps / (cms / 1e3), 1), "unit": UNIT,
+                   "ms_per_step": round(cms / args.steps, 4)}
+        del ceng, cseq
+    if args.shard:
         # SA-range sharding: keep only this rank's contiguous slice of suffix rows
         from paper_2411_05894_b200.sharded import Collective, ShardedDraftEngine, shard_bounds
 
         a, b_ = shard_bounds(ds.n_rows, world, rank)
-        shard = G.Datastore(ds.token_tensor, ds.rows[a:b_].clone(), b_ - a, VOCAB, rank_base=a,
+        shard = G.Datastore.on_device(ds.token_tensor, ds.rows[a:b_].clone(), b_ - a, VOCAB, rank_base=a,
                             n_tokens=ds.n_tokens)
         del ds
         torch.cuda.empty_cache()
@@ -363,13 +414,14 @@ def run_ours(args) -> None:
         tot = allreduce_max(best, world)
         return B * world * args.steps / (tot / 1e3)
 
-    e2e_u32, h2d_u32 = e2e_run(ctx_h)
+    # headline: the reference's host format (<u4 token ids, ref datastore.py:17);
+    # u16 ids (vocab 32000 fits) reported beside it
+    e2e_serial, h2d = e2e_run(ctx_h)
+    e2e_value = e2e_stream(ctx_h)
+    e2e_u16 = e2e_u16_serial = h2d_u16 = None
     if ctx16_h is not None:
-        e2e_serial, h2d = e2e_run(ctx16_h)
-        e2e_value = e2e_stream(ctx16_h)
-    else:
-        e2e_serial, h2d = e2e_u32, h2d_u32
-        e2e_value = e2e_stream(ctx_h)
+        e2e_u16_serial, h2d_u16 = e2e_run(ctx16_h)
+        e2e_u16 = e2e_stream(ctx16_h)
 
     peak, peak_src = peaks()
     achieved = bytes_per_step / (ms_per_step / 1e3) / 1e9
@@ -381,12 +433,20 @@ def run_ours(args) -> None:
         except Exception:
             traffic = None
 
-    base = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        tokens_h = corpus
-        sa_h = ds.suffix_index
-        ctxs = [mine[i * CTX:(i + 1) * CTX].tolist() for i in range(min(B, 256))]
-        base = cpu_baseline(tokens_h, sa_h, ctxs)
+    base, parity = None, None
+    if rank == 0 and not args.no_cpu_baseline:
+        from paper_2411_05894_b200.draft import _drafts_from_device
+
+        n_par = min(B, 256)
+        sa_h = (ds.suffix_index if not (args.shard and world > 1) else None)
+        if sa_h is not None:
+            ctxs = [mine[i * CTX:(i + 1) * CTX].tolist() for i in range(n_par)]
+            base, want = cpu_baseline(corpus, sa_h, ctxs)
+            got = _drafts_from_device(out_lk.size[:n_par], out_lk.tokens[:n_par], out_lk.parents[:n_par],
+                                      out_lk.depths[:n_par], out_lk.mask[:n_par], n_par, eng.S)
+            parity = parity_block(got, want)
+            if world > 1:
+                base = None  # (the CPU baseline is reported at N=1 only)
 
     extra = {}
     if rank == 0 and world == 1 and not args.no_extra:
@@ -418,9 +478,11 @@ def run_ours(args) -> None:
             "data": "synthetic (seeded phrase-model corpus + held-out contexts, SURVEY App. B)",
             "config": {"workload": WORKLOAD, "batch": BATCH, "batches_per_step": R, "lookups_per_step": B,
                        "n_tokens": N_TOKENS, "vocab": VOCAB, "ctx": CTX, "dec_len": DEC_LEN,
-                       "parallelism": (f"SA-range sharded x{world} (NCCL all-gather + sum all-reduce + "
-                                       f"reduce-scatter per step), requests partitioned") if (args.shard and world > 1)
+                       "parallelism": (f"SA-range sharded x{world} (NCCL all-gather of tails + sum all-reduce of "
+                                       f"bounds + sum reduce-scatter of 4 B sample positions per step), requests "
+                                       f"partitioned") if args.shard
                        else f"replicated datastore x{world}, requests partitioned",
+                       "control": control,
                        "l2": "inputs > L2 (6.4 GB suffix rows, 134 MB contexts) + 256 MB flush between steps",
                        "b64_latency_ms": round(lat_ms, 4), "b64_lookups_per_s": round(BATCH / lat_ms * 1e3, 1),
                        "mean_draft_size": round(mean_size, 2), "gpu_sa_build_s": round(build_s, 2),
@@ -444,9 +506,11 @@ def run_ours(args) -> None:
                          "issue_roofline": issue_roofline(prof[3], B, clk.summary())},
             "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
-                    "input_format": "u16 token ids (vocab 32000), widened on device" if ctx16_h is not None
-                    else "u32 token ids",
-                    "u32_upload": {"value": round(e2e_u32, 1), "h2d_bytes_per_step": int(h2d_u32)},
+                    "input_format": "u32 token ids (the reference's <u4), pinned host buffers",
+                    "u16_upload": None if e2e_u16 is None else {
+                        "value": round(e2e_u16, 1), "serial_value": round(e2e_u16_serial, 1),
+                        "h2d_bytes_per_step": int(h2d_u16),
+                        "format": "u16 token ids (vocab 32000), widened on device (sssd_widen_u16)"},
                     "schedule": "back-to-back steps, two in flight (propose_pinned slot / sync=False)",
                     "serial_value": round(e2e_serial, 1)},
             # per propose: ds_lookup, input_scan, propose_setup, (lpt_scatter when B >= 2048), draft_ls
@@ -455,6 +519,8 @@ def run_ours(args) -> None:
         }
         if base is not None:
             line["cpu_baseline"] = base
+        if parity is not None:
+            line["parity"] = parity
         line.update(extra)
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -676,23 +742,23 @@ def bench_decode_cfg3(steps: int = 5) -> dict:
     return out
 
 
-def _ref_worker(args):
+def _ref_worker(ctxs):
     from oracle import sssd_oracle as O
 
-    ctxs = args
     cfg = O.Cfg(dec_len=DEC_LEN)
     disc = cfg.disc()
-    for c in ctxs:
-        O.propose(_REF_STORE, c, cfg, disc=disc)
-    return len(ctxs)
+    return [O.propose(_REF_STORE, c, cfg, disc=disc) for c in ctxs]
 
 
 _REF_STORE = None
 
 
 def run_reference(args) -> None:
-    """Reference CPU path: the oracle port of the reference algorithm, fork-parallel
-    over all host cores, one B=64 batch per step."""
+    """Reference CPU path: the oracle port of the reference algorithm on every
+    host core.  Each step, every worker process drafts its own B=64 batch (one
+    batch of the GPU arm's step each: worker w takes contexts [64w, 64w+64)),
+    so the pool's dispatch overhead is amortised over whole batches; lookups/s
+    = cores x 64 / step wall time."""
     global _REF_STORE
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -705,28 +771,33 @@ def run_reference(args) -> None:
     corpus = workload.corpus(N_TOKENS, VOCAB)
     sa = O.suffix_array_c(corpus)  # C restatement of the reference's prefix doubling (~40 s at 100M)
     _REF_STORE = O.Store(corpus, sa)
-    stream = workload.phrase_stream(BATCH * CTX, VOCAB, workload.HELDOUT_SEED)
-    ctxs = [stream[i * CTX:(i + 1) * CTX].tolist() for i in range(BATCH)]
     cores = os.cpu_count() or 1
-    chunks = [ctxs[i::cores] for i in range(cores)]
+    stream = workload.phrase_stream(cores * BATCH * CTX, VOCAB, workload.HELDOUT_SEED)
+    chunks = [[stream[(w * BATCH + i) * CTX:(w * BATCH + i + 1) * CTX].tolist() for i in range(BATCH)]
+              for w in range(cores)]
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
+        first = None
         for _ in range(args.warmup):
-            pool.map(_ref_worker, chunks)
+            first = pool.map(_ref_worker, chunks)[0]
         t0 = time.perf_counter()
         for _ in range(args.steps):
             pool.map(_ref_worker, chunks)
         dt = time.perf_counter() - t0
-    value = BATCH * args.steps / dt
+    value = cores * BATCH * args.steps / dt
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 tokens / f64 fusion keys",
             "data": "synthetic (seeded phrase-model corpus + held-out contexts, SURVEY App. B)",
-            "config": {"workload": WORKLOAD, "batch": BATCH, "batches_per_step": 1, "n_tokens": N_TOKENS,
+            "config": {"workload": WORKLOAD, "batch": BATCH, "batches_per_step": cores, "n_tokens": N_TOKENS,
                        "ctx": CTX, "dec_len": DEC_LEN},
             "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"one B=64 batch per step, oracle port fork-parallel over {cores} processes"},
-            "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                             "sample": f"{cores} B=64 batches per step (one per worker process), oracle port "
+                                       f"fork-parallel over {cores} processes"},
+            "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            # the first batch = the GPU arm's first 64 contexts (workload.phrase_stream is prefix-stable)
+            "parity": {"digest_first64": O.digest(first), "n": len(first),
+                       "inputs": "contexts 0-63 of the GPU arm's timed step"}}
     print(json.dumps(line), flush=True)
 
 
@@ -740,7 +811,9 @@ def main() -> None:
     ap.add_argument("--e2e-chunks", type=int, default=5, help="request chunks pipelined by propose_pinned")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip verify/decode sub-benchmarks")
-    ap.add_argument("--shard", action="store_true", help="N>1: shard the suffix rows by rank range")
+    ap.add_argument("--replicated", action="store_true",
+                    help="N>1: replicate the datastore instead of sharding the suffix rows by rank range "
+                         "(the default shards and reports the replicated run as config.control)")
     ap.add_argument("--decode-8b", action="store_true", default=True,
                     help="include the Llama-3-8B-shaped cfg3 decode step (default on)")
     ap.add_argument("--no-decode-8b", dest="decode_8b", action="store_false")

@@ -145,6 +145,15 @@ typedef struct sssd_draft_out {
   int32_t* parents;  /* [B][S]   -1 for the root                */
   int32_t* depths;   /* [B][S]                                  */
   uint64_t* mask;    /* [B][S][W] W = ceil(S/64); bit j of row i = j is i or an ancestor */
+  /* Optional per-node outputs (NULL = not written):                        */
+  double* priority;  /* [B][S] DraftNode.priority (fusion.py:158-198): the path
+                        probability x discount of the node's first insertion;
+                        +inf for the root, 0 for padding                     */
+  int32_t* source;   /* [B][S] DraftNode.source as its merge rank (fusion.py:
+                        245-249): 0 = datastore, r >= 1 = input tree p = P-r+1;
+                        -1 for the root and padding                          */
+  int32_t* pos;      /* [B][S] position id L-1+depth (L = seq_len[b]; depth
+                        alone for sssd_merge); -1 for padding                */
 } sssd_draft_out;
 
 /* Optional lookup diagnostics for parity (any pointer may be NULL). */
@@ -238,6 +247,16 @@ int sssd_shard_search(const sssd_ds* ds, const sssd_seqs* tails, const sssd_cfg*
                       void* stream);
 int sssd_shard_gather(const sssd_ds* ds, const sssd_cfg* cfg, int32_t B, const int64_t* gbounds, uint32_t* xrows,
                       void* stream);
+/* The compact C2 exchange (what sharded.py uses): 4 B per sample instead of
+ * a 64 B row.  sssd_shard_gather_pos writes xpos[b][p-1][k] = corpus position
+ * + 1 of sampled global rank k if this shard owns it, else 0 -> NCCL
+ * reduce-scatter (sum); sssd_rows_from_pos then rebuilds the `count` suffix
+ * rows (64 B each, zero for 0) from the replicated token array for
+ * sssd_propose_pre. */
+int sssd_shard_gather_pos(const sssd_ds* ds, const sssd_cfg* cfg, int32_t B, const int64_t* gbounds, uint32_t* xpos,
+                          void* stream);
+int sssd_rows_from_pos(const uint32_t* tokens, uint64_t n_tokens, const uint32_t* xpos, int64_t count, uint32_t* rows,
+                       void* stream);
 int sssd_propose_pre(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg, const int64_t* gbounds,
                      const uint32_t* rows, const sssd_draft_out* out, const sssd_lookup_out* lookup,
                      void* workspace, size_t workspace_bytes, void* stream);

@@ -54,7 +54,8 @@ class Seqs(C.Structure):
 
 
 class DraftOut(C.Structure):
-    _fields_ = [("size", vp), ("tokens", vp), ("parents", vp), ("depths", vp), ("mask", vp)]
+    _fields_ = [("size", vp), ("tokens", vp), ("parents", vp), ("depths", vp), ("mask", vp),
+                ("priority", vp), ("source", vp), ("pos", vp)]  # (last three optional: NULL = skip)
 
 
 class LookupOut(C.Structure):
@@ -98,6 +99,8 @@ _SIGS = {
                              C.POINTER(DraftOut), vp, C.c_size_t, vp]),
     "sssd_shard_search": (C.c_int, [C.POINTER(Ds), C.POINTER(Seqs), C.POINTER(Cfg), vp, vp]),
     "sssd_shard_gather": (C.c_int, [C.POINTER(Ds), C.POINTER(Cfg), C.c_int32, vp, vp, vp]),
+    "sssd_shard_gather_pos": (C.c_int, [C.POINTER(Ds), C.POINTER(Cfg), C.c_int32, vp, vp, vp]),
+    "sssd_rows_from_pos": (C.c_int, [vp, C.c_uint64, vp, C.c_int64, vp, vp]),
     "sssd_propose_pre": (C.c_int, [C.POINTER(Ds), C.POINTER(Seqs), C.POINTER(Cfg), vp, vp, C.POINTER(DraftOut),
                                    C.POINTER(LookupOut), vp, C.c_size_t, vp]),
     "sssd_teacher_predict": (C.c_int, [vp, vp, C.c_int32, vp, vp, vp, vp, vp, C.c_int32, vp, vp]),

@@ -90,6 +90,7 @@ static KCfg kcfg(const sssd_cfg* c) {
   k.disc_stride = c->disc_stride;
   k.disc = c->disc;
   k.fusion = c->fusion;
+  k.seq_len = nullptr;
   return k;
 }
 
@@ -414,6 +415,7 @@ static void fuse_range(const PropWs& w, const KCfg& k, const sssd_seqs* seqs, co
   KCfg kk = k;
   kk.b0 = b0;
   kk.b1 = b1;
+  kk.seq_len = seqs->seq_len;
   static const bool no_lpt = getenv("SSSD_NO_LPT") != nullptr;  // A/B switch
   const bool lpt = !no_lpt && b1 - b0 >= 2048;                   // order only pays with several waves
   propose_setup_kernel<<<(b1 - b0 + 127) / 128, 128, 0, s>>>(*seqs, kk, w.ds_cols, w.ds_n, w.in_cols, w.in_n,
@@ -468,6 +470,7 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
     KCfg kk = k;
     kk.b0 = 0;
     kk.b1 = B;
+    kk.seq_len = seqs->seq_len;
     const bool lpt = getenv("SSSD_NO_LPT") == nullptr && B >= 2048;
     propose_setup_kernel<<<(B + 127) / 128, 128, 0, st>>>(*seqs, kk, w.ds_cols, w.ds_n, w.in_cols, w.in_n,
                                                             w.d.desc, w.d.root, lpt ? w.d.bucket : nullptr,
@@ -666,6 +669,27 @@ int sssd_shard_gather(const sssd_ds* ds, const sssd_cfg* cfg, int32_t B, const i
   shard_gather_kernel<<<(unsigned)((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       *ds, kcfg(cfg), B, gbounds, xrows);
   return cuda_check(cudaGetLastError(), "shard_gather_kernel launch");
+}
+
+int sssd_shard_gather_pos(const sssd_ds* ds, const sssd_cfg* cfg, int32_t B, const int64_t* gbounds, uint32_t* xpos,
+                          void* stream) {
+  int rc = validate_cfg(cfg);
+  if (rc) return rc;
+  if (!ds || (!ds->rows && ds->n_rows)) return fail(SSSD_E_ARG, "shard has no rows");
+  if (B <= 0) return B == 0 ? SSSD_OK : fail(SSSD_E_ARG, "bad batch");
+  const int64_t total = (int64_t)B * cfg->P * cfg->M;
+  shard_gather_pos_kernel<<<(unsigned)((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      *ds, kcfg(cfg), B, gbounds, xpos);
+  return cuda_check(cudaGetLastError(), "shard_gather_pos_kernel launch");
+}
+
+int sssd_rows_from_pos(const uint32_t* tokens, uint64_t n_tokens, const uint32_t* xpos, int64_t count, uint32_t* rows,
+                       void* stream) {
+  if (!tokens || !xpos || !rows) return fail(SSSD_E_ARG, "rows_from_pos needs tokens, positions and rows");
+  if (count <= 0) return count == 0 ? SSSD_OK : fail(SSSD_E_ARG, "bad count");
+  rows_from_pos_kernel<<<(unsigned)((count * 4 + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      tokens, n_tokens, xpos, count, rows);
+  return cuda_check(cudaGetLastError(), "rows_from_pos_kernel launch");
 }
 
 int sssd_propose_pre(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg, const int64_t* gbounds,

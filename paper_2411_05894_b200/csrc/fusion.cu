@@ -540,6 +540,12 @@ __global__ void __launch_bounds__(32, SSSD_DRAFT_MINB)
       o_tok[k] = d_tok[nid];
       o_par[k] = nid == 0 ? -1 : (int32_t)n2p[d_par[nid]];
       o_dep[k] = d_dep[nid];
+      // (the heap-order cross-check kernel keeps no per-node keys: priority
+      // NaN and source -2 = unknown; position ids are exact)
+      if (out.priority || out.source || out.pos)
+        write_node_extra(out, c, b, k, nid == 0 ? __longlong_as_double(0x7ff0000000000000ll)
+                                                : __longlong_as_double(0x7ff8000000000000ll),
+                         nid == 0 ? -1 : -2, d_dep[nid]);
       uint64_t mw[SSSD_MAX_DRAFT / 64] = {0, 0, 0, 0};
       for (int x = nid; x >= 0; x = d_par[x]) {
         const int pk = n2p[x];
@@ -551,6 +557,7 @@ __global__ void __launch_bounds__(32, SSSD_DRAFT_MINB)
       o_par[k] = -1;
       o_dep[k] = -1;
       for (int w = 0; w < W; ++w) o_mask[(size_t)k * W + w] = 0;
+      if (out.priority || out.source || out.pos) write_node_extra(out, c, b, k, 0.0, -1, -1);
     }
   }
   if (lane == 0) {

@@ -767,6 +767,17 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
   int32_t* o_par = out.parents + (size_t)b * S;
   int32_t* o_dep = out.depths + (size_t)b * S;
   maxd = __reduce_max_sync(SSSD_FULL, maxd);
+  // per-node priority (the top entry's key holds ~bits(priority)) and merge
+  // rank of the node's first insertion (ref fusion.py:185-198), position id
+  const bool extra = out.priority || out.source || out.pos;
+  auto node_extra = [&](int v, int k) {
+    if (v == 0) {
+      write_node_extra(out, c, b, k, __longlong_as_double(0x7ff0000000000000ll), -1, 0);
+    } else {
+      write_node_extra(out, c, b, k, __longlong_as_double((long long)~T.g0()[v - 1]),
+                       (int32_t)((T.g1()[v - 1] >> kTbBits) & 15u), f_dep[v]);
+    }
+  };
   if (maxd <= 8 && size <= 127) {
     // pre-order position = rank of the node's ancestor-index path (7 bits per
     // depth, index order = sibling insertion order, a prefix sorts first)
@@ -789,6 +800,7 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
       o_tok[k] = v == 0 ? root_tok[b] : T.tok()[v - 1];
       o_par[k] = v == 0 ? -1 : f_pos[f_par[v]];
       o_dep[k] = f_dep[v];
+      if (extra) node_extra(v, k);
     }
   } else {
     // next sibling = the next index with the same parent: inside a chunk by
@@ -820,6 +832,7 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
         o_tok[k] = v == 0 ? root_tok[b] : T.tok()[v - 1];
         o_par[k] = v == 0 ? -1 : f_pos[f_par[v]];
         o_dep[k] = f_dep[v];
+        if (extra) node_extra(v, k);
         ++k;
         int nx = f_fc[v];
         if (nx < 0) {
@@ -851,6 +864,7 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
     o_par[k] = -1;
     o_dep[k] = -1;
     for (int w = 0; w < W; ++w) o_mask[(size_t)k * W + w] = 0;
+    if (extra) write_node_extra(out, c, b, k, 0.0, -1, -1);
   }
   if (lane == 0) {
     out.size[b] = size;

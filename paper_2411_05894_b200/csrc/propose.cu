@@ -866,6 +866,45 @@ __global__ void shard_gather_kernel(sssd_ds ds, KCfg c, int B, const int64_t* gb
   reinterpret_cast<uint4*>(xrows)[t] = v;
 }
 
+// Owner-written sample positions (the compact C2 exchange): xpos[b][p-1][k] =
+// corpus position + 1 of sampled global rank k of [lo, hi) if this shard owns
+// it, else 0, so a sum over shards yields every position exactly once.
+__global__ void shard_gather_pos_kernel(sssd_ds ds, KCfg c, int B, const int64_t* gbounds, uint32_t* xpos) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= (int64_t)B * c.P * c.M) return;
+  const int k = (int)(s % c.M);
+  const int64_t bp = s / c.M;
+  const uint64_t lo = (uint64_t)gbounds[bp * 2], hi = (uint64_t)gbounds[bp * 2 + 1];
+  const uint64_t w = hi - lo;
+  uint32_t v = 0;
+  if ((uint64_t)k < min(w, (uint64_t)c.M)) {
+    const uint64_t r = lo + (w <= (uint64_t)c.M ? (uint64_t)k : ((uint64_t)k * w) / (uint64_t)c.M);
+    if (r >= ds.rank_base && r < ds.rank_base + ds.n_rows) v = __ldg(ds.rows + (r - ds.rank_base) * 16) + 1u;
+  }
+  xpos[s] = v;
+}
+
+// Suffix rows of exchanged positions (pos + 1; 0 = none -> zero row) from the
+// replicated token array: the owner rank's requests read their sampled rows
+// locally instead of receiving 64 B per sample over NVLink.
+__global__ void rows_from_pos_kernel(const uint32_t* tokens, uint64_t n, const uint32_t* xpos, int64_t count,
+                                     uint32_t* rows) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 16 B quarter row per thread
+  if (t >= count * 4) return;
+  const int q = (int)(t & 3);
+  const uint32_t pp = xpos[t >> 2];
+  uint32_t v[4] = {0, 0, 0, 0};
+  if (pp) {
+    const uint64_t pos = pp - 1u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = 4 * q + j;  // column 0 = SA position, 1.. = tokens pos + col - 1
+      v[j] = col == 0 ? (uint32_t)pos : (pos + col - 1 < n ? __ldg(tokens + pos + col - 1) : 0u);
+    }
+  }
+  reinterpret_cast<uint4*>(rows)[t] = make_uint4(v[0], v[1], v[2], v[3]);
+}
+
 // --------------------------------------------------------------------------
 // K4: input scan (ref input_cache.py:88-121, stateless form A.4)
 // --------------------------------------------------------------------------

@@ -13,7 +13,18 @@ struct KCfg {
   int disc_stride;
   const double* disc;
   int fusion;  // 0 = level-synchronous (fusion_ls.cu), 1 = heap order (fusion.cu)
+  const int32_t* seq_len;  // [B] live lengths for position ids (nullptr: pos = depth)
 };
+
+// Optional per-node outputs of a flattened draft (priority / source rank /
+// position id, see sssd_draft_out); shared by both fusion kernels.
+__device__ __forceinline__ void write_node_extra(const sssd_draft_out& out, const KCfg& c, int b, int k,
+                                                 double prio, int32_t src, int32_t depth) {
+  const size_t o = (size_t)b * c.S + k;
+  if (out.priority) out.priority[o] = prio;
+  if (out.source) out.source[o] = src;
+  if (out.pos) out.pos[o] = depth < 0 ? -1 : (c.seq_len ? c.seq_len[b] - 1 : 0) + depth;
+}
 
 struct Child;
 
@@ -32,6 +43,9 @@ __global__ void ds_lookup_warp_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, uint32
                                       sssd_elem* ds_el, int32_t* ds_n, sssd_lookup_out lk, Cols cols);
 __global__ void shard_search_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, int64_t* bounds);
 __global__ void shard_gather_kernel(sssd_ds ds, KCfg c, int B, const int64_t* gbounds, uint32_t* xrows);
+__global__ void shard_gather_pos_kernel(sssd_ds ds, KCfg c, int B, const int64_t* gbounds, uint32_t* xpos);
+__global__ void rows_from_pos_kernel(const uint32_t* tokens, uint64_t n, const uint32_t* xpos, int64_t count,
+                                     uint32_t* rows);
 
 // scratch of the datastore lookup when a separator forces a block sort
 __host__ __device__ inline int64_t ds_idx_cap(int P, int M) {

@@ -68,6 +68,24 @@ def sample_range(lo: int, hi: int, cap: int) -> list[int]:
     return [lo + (k * width) // cap for k in range(cap)]
 
 
+def as_u32(tokens, what: str = "token") -> np.ndarray:
+    """Token ids -> <u4, rejecting ids outside [0, 2^32) (they cannot be
+    represented on the device; silently wrapping them would make them match
+    real corpus tokens, which the reference's exact int compare never does)."""
+    a = np.asarray(tokens)
+    if a.size == 0:
+        return np.zeros(0, dtype="<u4")
+    if a.dtype.kind not in "iu":
+        a = np.asarray([int(x) for x in np.ravel(a)], dtype=object).reshape(a.shape)
+        lo, hi = (int(a.min()), int(a.max()))
+    else:
+        lo, hi = int(a.min()), int(a.max())
+    if lo < 0 or hi > 0xFFFFFFFF:
+        bad = lo if lo < 0 else hi
+        raise ValueError(f"{what} id {bad} out of range for uint32")
+    return np.ascontiguousarray(a.astype(np.int64) if a.dtype == object else a, dtype=np.int64).astype("<u4")
+
+
 def _u32_device(arr: np.ndarray, device) -> torch.Tensor:
     a = np.ascontiguousarray(arr, dtype="<u4")
     return torch.from_numpy(a.view(np.int32)).to(device, non_blocking=False)
@@ -78,10 +96,31 @@ def _workspace(nbytes: int, device) -> torch.Tensor:
 
 
 class Datastore:
-    """Token corpus + suffix rows resident on one GPU."""
+    """Token corpus + suffix rows resident on one GPU.
 
-    def __init__(self, tokens_dev: torch.Tensor, rows_dev: torch.Tensor, n: int,
-                 vocab_size: int | None = None, rank_base: int = 0, n_tokens: int | None = None) -> None:
+    ``Datastore(tokens, suffix_index, vocab_size=None)`` is the reference
+    constructor (ref datastore.py:144-154): host arrays, uploaded and indexed
+    into suffix rows on the current GPU.  ``Datastore.on_device`` wraps rows
+    already built on a device (``build``, ``load``, shards)."""
+
+    def __init__(self, tokens, suffix_index, vocab_size: int | None = None, device=None) -> None:
+        dev = torch.device(device) if device is not None else _lib.require_cuda()
+        toks = np.ascontiguousarray(np.asarray(tokens), dtype="<u4")
+        n = int(toks.size)
+        tok = _device_tokens(toks, dev)
+        sa = torch.from_numpy(np.ascontiguousarray(suffix_index, dtype=np.int64).astype(np.int32)).to(dev)
+        self._init(tok, _rows_from_sa(tok, n, sa), n, vocab_size)
+        self._np_tokens = toks
+
+    @classmethod
+    def on_device(cls, tokens_dev: torch.Tensor, rows_dev: torch.Tensor, n: int, vocab_size: int | None = None,
+                  rank_base: int = 0, n_tokens: int | None = None) -> "Datastore":
+        self = cls.__new__(cls)
+        self._init(tokens_dev, rows_dev, n, vocab_size, rank_base, n_tokens)
+        return self
+
+    def _init(self, tokens_dev: torch.Tensor, rows_dev: torch.Tensor, n: int, vocab_size: int | None = None,
+              rank_base: int = 0, n_tokens: int | None = None) -> None:
         self._tok = tokens_dev  # int32 view of <u4 tokens (length n_tokens + 16 pad)
         self._rows = rows_dev  # [n_rows, 16] int32
         self.n_rows = int(n)
@@ -152,7 +191,7 @@ class Datastore:
         if not pats:
             return []
         dev = self.device
-        flat = np.concatenate([np.asarray(p, dtype=np.int64) for p in pats]).astype("<u4")
+        flat = as_u32(np.concatenate([as_u32(p, "prefix token") for p in pats]), "prefix token")
         offs = np.zeros(len(pats), dtype=np.int64)
         np.cumsum([len(p) for p in pats[:-1]], out=offs[1:])
         d_pat = _u32_device(flat, dev)
@@ -264,6 +303,17 @@ def build_device(tok_dev: torch.Tensor, n: int) -> torch.Tensor:
     return sa
 
 
+def build_suffix_array(tokens: np.ndarray, device=None) -> np.ndarray:
+    """Suffix array of a host token array (ref datastore.py:81-109), computed on
+    the GPU by radix-sort prefix doubling; int64 like the reference's."""
+    toks = np.ascontiguousarray(np.asarray(tokens), dtype="<u4")
+    n = int(toks.size)
+    if n == 0:
+        return np.zeros(0, dtype=np.int64)
+    dev = torch.device(device) if device is not None else _lib.require_cuda()
+    return build_device(_device_tokens(toks, dev), n).cpu().numpy().view(np.uint32).astype(np.int64)
+
+
 def build(corpus: Sequence[int] | np.ndarray, vocab_size: int | None = None,
           device: torch.device | str | None = None) -> Datastore:
     """Index ``corpus`` on the GPU (ref datastore.py:229-242): suffix array by
@@ -276,7 +326,7 @@ def build(corpus: Sequence[int] | np.ndarray, vocab_size: int | None = None,
     tok = _device_tokens(tokens, dev)
     sa = build_device(tok, n)
     rows = _rows_from_sa(tok, n, sa)
-    ds = Datastore(tok, rows, n, vocab_size)
+    ds = Datastore.on_device(tok, rows, n, vocab_size)
     ds._np_tokens = tokens
     return ds
 
@@ -284,14 +334,7 @@ def build(corpus: Sequence[int] | np.ndarray, vocab_size: int | None = None,
 def from_arrays(tokens: np.ndarray, suffix_index: np.ndarray, vocab_size: int | None = None,
                 device=None) -> Datastore:
     """Datastore over a precomputed suffix array (e.g. one loaded from disk)."""
-    dev = torch.device(device) if device is not None else _lib.require_cuda()
-    tokens = np.ascontiguousarray(tokens, dtype="<u4")
-    n = int(tokens.size)
-    tok = _device_tokens(tokens, dev)
-    sa = torch.from_numpy(np.ascontiguousarray(suffix_index, dtype=np.int64).astype(np.int32)).to(dev)
-    ds = Datastore(tok, _rows_from_sa(tok, n, sa), n, vocab_size)
-    ds._np_tokens = tokens
-    return ds
+    return Datastore(tokens, suffix_index, vocab_size, device=device)
 
 
 def _read_exact(fh, nbytes: int, field: str) -> bytes:

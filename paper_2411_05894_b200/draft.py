@@ -19,7 +19,7 @@ import torch
 
 from . import _lib
 from ._lib import check, lib, ptr, stream_ptr
-from .datastore import Datastore
+from .datastore import Datastore, as_u32
 from .fusion import DraftTree, FusionConfig
 
 
@@ -128,14 +128,46 @@ def verify_batch(drafts: Sequence[FlattenedDraft], predictions: Sequence[Sequenc
             raise ValueError(f"length mismatch: {len(p)} predictions for {d.s_q} draft nodes")
     if B == 0:
         return []
+    # sssd_accept walks children at indices above their parent (DFS / any
+    # topological numbering).  A caller-built draft numbered otherwise is
+    # renumbered by (depth, index) -- parents first, siblings in index order, so
+    # the first-index-wins rule of ref draft.py:127-128 is unchanged -- and the
+    # accepted path mapped back.
+    perms: list = [None] * B
+    for b, d in enumerate(drafts):
+        if all(0 <= d.parents[i] < i for i in range(1, d.s_q)):
+            continue
+        depth = [0] * d.s_q
+        for i in range(1, d.s_q):
+            j, k = i, 0
+            while j > 0 and k <= d.s_q:
+                j, k = d.parents[j], k + 1
+            depth[i] = k if j == 0 else d.s_q + 1  # unreachable from the root: never accepted
+        perm = sorted(range(d.s_q), key=lambda i: (depth[i], i))
+        new = {old_i: n for n, old_i in enumerate(perm)}
+        par2 = [-1] + [new.get(d.parents[o], -1) if depth[o] <= d.s_q else -1 for o in perm[1:]]
+        drafts = list(drafts)
+        predictions = list(predictions)
+        drafts[b] = FlattenedDraft([d.tokens[o] for o in perm], par2, [depth[o] for o in perm], d.mask)
+        predictions[b] = [predictions[b][o] for o in perm]
+        perms[b] = perm
     S = max(d.s_q for d in drafts)
+    odd: list[dict] = [{} for _ in range(B)]  # out-of-range predictions by node
     tok = np.zeros((B, S), dtype=np.uint32)
     par = np.full((B, S), -1, dtype=np.int32)
     prd = np.zeros((B, S), dtype=np.uint32)
     for b, (d, p) in enumerate(zip(drafts, predictions)):
-        tok[b, : d.s_q] = np.asarray(d.tokens, dtype=np.int64).astype(np.uint32)
+        tok[b, : d.s_q] = as_u32(d.tokens, "draft token")
         par[b, : d.s_q] = d.parents
-        prd[b, : d.s_q] = np.asarray([int(x) for x in p], dtype=np.int64).astype(np.uint32)
+        pv = [int(x) for x in p]
+        if any(x < 0 or x > 0xFFFFFFFF for x in pv):
+            # a prediction no u32 draft token can equal: stand in a value absent
+            # from this draft (the walk stops there, as the reference's exact
+            # compare does); the bonus is restored below
+            free = next(v for v in range(d.s_q + 1) if v not in set(int(t) for t in d.tokens))
+            odd[b] = {i: x for i, x in enumerate(pv) if x < 0 or x > 0xFFFFFFFF}
+            pv = [free if i in odd[b] else x for i, x in enumerate(pv)]
+        prd[b, : d.s_q] = np.asarray(pv, dtype=np.int64).astype(np.uint32)
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).to(dev)  # noqa: E731
     d_tok, d_par, d_prd = t(tok), t(par), t(prd)
     d_size = torch.tensor([d.s_q for d in drafts], dtype=torch.int32, device=dev)
@@ -153,7 +185,13 @@ def verify_batch(drafts: Sequence[FlattenedDraft], predictions: Sequence[Sequenc
     na = n_acc.cpu().tolist()
     ph = path.cpu().tolist()
     bh = bonus.cpu().numpy().view(np.uint32).tolist()
-    return [AcceptResult(ph[b][: na[b]], int(bh[b])) for b in range(B)]
+    res = []
+    for b in range(B):
+        path = ph[b][: na[b]]
+        last = path[-1] if path else 0
+        bonus_b = odd[b].get(last, int(bh[b]))
+        res.append(AcceptResult(path if perms[b] is None else [perms[b][i] for i in path], bonus_b))
+    return res
 
 
 def verify_greedy(draft: FlattenedDraft, node_predictions: Sequence[int]) -> AcceptResult:

@@ -31,6 +31,20 @@ class DraftBatch:
     samples: torch.Tensor | None = None  # [B, P, M] int64
     n_conts: torch.Tensor | None = None  # [B, P] int32
     p_cut: torch.Tensor | None = None    # [B] int32
+    pos: torch.Tensor | None = None       # [B, S] int32 position ids L-1+depth (-1 padding)
+    priority: torch.Tensor | None = None  # [B, S] float64 DraftNode.priority (+inf root)
+    source: torch.Tensor | None = None    # [B, S] int32 merge rank (0 datastore, r: input p=P-r+1; -1 root)
+
+    def c_out(self) -> "_lib.DraftOut":
+        return _lib.DraftOut(ptr(self.size), ptr(self.tokens), ptr(self.parents), ptr(self.depths),
+                             ptr(self.mask), ptr(self.priority), ptr(self.source), ptr(self.pos))
+
+    def rows(self, r0: int, r1: int) -> "DraftBatch":
+        """View of requests [r0, r1)."""
+        sl = lambda t: None if t is None else t[r0:r1]  # noqa: E731
+        return DraftBatch(self.size[r0:r1], self.tokens[r0:r1], self.parents[r0:r1], self.depths[r0:r1],
+                          self.mask[r0:r1], sl(self.ranges), sl(self.samples), sl(self.n_conts), sl(self.p_cut),
+                          sl(self.pos), sl(self.priority), sl(self.source))
 
     @property
     def B(self) -> int:
@@ -92,41 +106,53 @@ class DraftEngine:
             self._ws_key = (B2, L2)
         return self._ws
 
-    def outputs(self, B: int, lookup: bool = False) -> DraftBatch:
-        key = B * 2 + int(lookup)
+    def new_outputs(self, B: int, lookup: bool = False, nodes: bool = False) -> DraftBatch:
+        """Fresh device output buffers for a batch of B (``nodes``: also position
+        ids, per-node priorities and sources)."""
+        dev, S, W, P, M = self.device, self.S, self.W, self.cfg.P, self.cfg.M
+        out = DraftBatch(
+            size=torch.empty(B, dtype=torch.int32, device=dev),
+            tokens=torch.empty((B, S), dtype=torch.int32, device=dev),
+            parents=torch.empty((B, S), dtype=torch.int32, device=dev),
+            depths=torch.empty((B, S), dtype=torch.int32, device=dev),
+            mask=torch.empty((B, S, W), dtype=torch.int64, device=dev),
+        )
+        if lookup:
+            out.ranges = torch.full((B, P, 2), -1, dtype=torch.int64, device=dev)
+            out.samples = torch.full((B, P, M), -1, dtype=torch.int64, device=dev)
+            out.n_conts = torch.full((B, P), -1, dtype=torch.int32, device=dev)
+            out.p_cut = torch.zeros(B, dtype=torch.int32, device=dev)
+        if nodes:
+            out.pos = torch.empty((B, S), dtype=torch.int32, device=dev)
+            out.priority = torch.empty((B, S), dtype=torch.float64, device=dev)
+            out.source = torch.empty((B, S), dtype=torch.int32, device=dev)
+        return out
+
+    def outputs(self, B: int, lookup: bool = False, nodes: bool = False) -> DraftBatch:
+        """The engine's cached output buffers for batch size B (shared by every
+        call with the same (B, lookup, nodes): one propose in flight at a time)."""
+        key = (B, bool(lookup), bool(nodes))
         out = self._out.get(key)
         if out is None:
-            dev, S, W, P, M = self.device, self.S, self.W, self.cfg.P, self.cfg.M
-            out = DraftBatch(
-                size=torch.empty(B, dtype=torch.int32, device=dev),
-                tokens=torch.empty((B, S), dtype=torch.int32, device=dev),
-                parents=torch.empty((B, S), dtype=torch.int32, device=dev),
-                depths=torch.empty((B, S), dtype=torch.int32, device=dev),
-                mask=torch.empty((B, S, W), dtype=torch.int64, device=dev),
-            )
-            if lookup:
-                out.ranges = torch.full((B, P, 2), -1, dtype=torch.int64, device=dev)
-                out.samples = torch.full((B, P, M), -1, dtype=torch.int64, device=dev)
-                out.n_conts = torch.full((B, P), -1, dtype=torch.int32, device=dev)
-                out.p_cut = torch.zeros(B, dtype=torch.int32, device=dev)
-            self._out[key] = out
+            out = self._out[key] = self.new_outputs(B, lookup, nodes)
         return out
 
     def propose(self, seq: torch.Tensor, seq_off: torch.Tensor, seq_len: torch.Tensor, max_len: int,
                 lookup: bool = False, out: DraftBatch | None = None, ws: torch.Tensor | None = None,
-                stream: torch.cuda.Stream | None = None) -> DraftBatch:
+                stream: torch.cuda.Stream | None = None, nodes: bool = False) -> DraftBatch:
         """Draft for B device-resident sequences: seq (int32 view of u32),
         seq_off [B] int64, seq_len [B] int32 (each >= 1).  Runs on ``stream``
         (default: the current stream) with workspace ``ws`` (default: the
-        engine's own; concurrent calls on different streams need their own)."""
+        engine's own; concurrent calls on different streams need their own).
+        ``nodes``: also write position ids, node priorities and sources."""
         B = int(seq_len.shape[0])
-        out = out or self.outputs(B, lookup)
+        out = out or self.outputs(B, lookup, nodes)
         if B == 0:
             return out
         if ws is None:
             ws = self.workspace(B, max_len)
         seqs = _lib.Seqs(ptr(seq), ptr(seq_off), ptr(seq_len), B, int(max_len))
-        d_out = _lib.DraftOut(ptr(out.size), ptr(out.tokens), ptr(out.parents), ptr(out.depths), ptr(out.mask))
+        d_out = out.c_out()
         lk = _lib.LookupOut(ptr(out.ranges), ptr(out.samples), ptr(out.n_conts), ptr(out.p_cut)) if lookup else None
         ds = self.store.c_view() if (self.use_datastore and self.store is not None) else self._null_ds
         sp = stream.cuda_stream if stream is not None else stream_ptr(self.device)
@@ -267,8 +293,7 @@ class DraftEngine:
                 s16 = st["seq16"]
                 check(lib().sssd_widen_u16(s16.data_ptr() + 2 * t0, seq_d.data_ptr() + 4 * t0, t1 - t0,
                                            cs.cuda_stream))
-            view = DraftBatch(out.size[r0:r1], out.tokens[r0:r1], out.parents[r0:r1], out.depths[r0:r1],
-                              out.mask[r0:r1])
+            view = out.rows(r0, r1)
             with torch.cuda.stream(cs):
                 self.propose(seq_d, off_d[r0:r1], len_d[r0:r1], max_len, out=view, ws=st["ws"][c & 1], stream=cs)
                 status[c:c + 1].copy_(err[c & 1])
@@ -326,7 +351,7 @@ class DraftEngine:
             ss["tails"] = torch.empty(B * P, dtype=torch.int32, device=dev)
             ss["toff"] = torch.empty(B, dtype=torch.int64, device=dev)
             ss["tlen"] = torch.empty(B, dtype=torch.int32, device=dev)
-            ss["out"] = self.outputs(B)
+            ss["out"] = self.new_outputs(B)  # own buffers: another slot's drafts may still be downloading
             ss["err_h"] = torch.zeros(1, dtype=torch.int32).pin_memory()
             ss["key"] = (n_tok, B, narrow)
         if ss["ws_key"] != (B, int(max_len)):
@@ -417,7 +442,9 @@ class DraftEngine:
         lens = [len(s) for s in seqs]
         if any(n < 1 for n in lens):
             raise ValueError("empty prompt: the draft root is the last context token")
-        flat = np.concatenate([np.asarray(s, dtype=np.int64) for s in seqs]).astype(np.uint32)
+        from .datastore import as_u32
+
+        flat = np.concatenate([as_u32(s, "context token") for s in seqs])
         offs = np.zeros(len(seqs), dtype=np.int64)
         np.cumsum(lens[:-1], out=offs[1:])
         dev = self.device

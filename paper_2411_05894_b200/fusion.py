@@ -240,8 +240,10 @@ def _serialise_sources(trees_per_request: list[list[ContinuationTree | None]], P
 
 
 def merge_batch(requests: list[tuple[ContinuationTree, Sequence[ContinuationTree], int]],
-                cfg: FusionConfig, device=None) -> list["FlattenedDraft"]:
-    """GPU fusion of B independent (datastore tree, input trees, root) sets."""
+                cfg: FusionConfig, device=None, with_nodes: bool = False):
+    """GPU fusion of B independent (datastore tree, input trees, root) sets.
+    ``with_nodes``: also return, per draft, the per-node (priority, merge rank)
+    lists in DFS order (``sssd_draft_out.priority`` / ``.source``)."""
     from .draft import FlattenedDraft, _drafts_from_device
 
     dev = torch.device(device) if device is not None else _lib.require_cuda()
@@ -278,32 +280,53 @@ def merge_batch(requests: list[tuple[ContinuationTree, Sequence[ContinuationTree
     par = torch.empty(B * S, dtype=torch.int32, device=dev)
     dep = torch.empty(B * S, dtype=torch.int32, device=dev)
     mask = torch.empty(B * S * W, dtype=torch.int64, device=dev)
-    out = _lib.DraftOut(ptr(size), ptr(toks), ptr(par), ptr(dep), ptr(mask))
+    prio = torch.empty(B * S, dtype=torch.float64, device=dev) if with_nodes else None
+    src = torch.empty(B * S, dtype=torch.int32, device=dev) if with_nodes else None
+    out = _lib.DraftOut(ptr(size), ptr(toks), ptr(par), ptr(dep), ptr(mask), ptr(prio), ptr(src), None)
     total = len(elems)
     ws = torch.empty(lib().sssd_merge_workspace(c, B, total), dtype=torch.uint8, device=dev)
     st = stream_ptr(dev)
     check(lib().sssd_merge(ptr(d_tok), ptr(d_el), ptr(d_off), ptr(d_n), total, ptr(roots), B, c, out,
                            ptr(ws), ws.numel(), st))
     check(lib().sssd_workspace_status(c, B, 0, ptr(ws), 1, total, st))
-    return _drafts_from_device(size, toks, par, dep, mask, B, S)
+    flats = _drafts_from_device(size, toks, par, dep, mask, B, S)
+    if not with_nodes:
+        return flats
+    prio_h = prio.reshape(B, S).cpu().numpy()
+    src_h = src.reshape(B, S).cpu().numpy()
+    return flats, [(prio_h[b, :f.s_q].tolist(), src_h[b, :f.s_q].tolist()) for b, f in enumerate(flats)]
 
 
 def merge(datastore_tree: ContinuationTree, input_trees: Sequence[ContinuationTree], cfg: FusionConfig,
           root_token: int) -> DraftTree:
     """Best-first fusion (ref fusion.py:209-261), computed on the GPU.  Returns a
-    ``DraftTree`` whose insertion order is the device's; node priorities and
-    sources are not carried back (the device draft is flattened)."""
+    ``DraftTree`` with the reference's child insertion order and, per node, the
+    priority and ``Source`` of its first insertion (ref fusion.py:185-198),
+    read back from the fusion kernel's per-node outputs."""
     if len(input_trees) > cfg.P:
         raise ValueError(f"got {len(input_trees)} input trees for P={cfg.P}")
-    flat = merge_batch([(datastore_tree, list(input_trees), int(root_token))], cfg)[0]
-    return draft_tree_from_flat(flat)
+    flats, nodes = merge_batch([(datastore_tree, list(input_trees), int(root_token))], cfg, with_nodes=True)
+    prio, ranks = nodes[0]
+    return draft_tree_from_flat(flats[0], prio, [source_of_rank(r, cfg.P) for r in ranks])
 
 
-def draft_tree_from_flat(flat) -> DraftTree:
+def source_of_rank(rank: int, P: int) -> Source | None:
+    """Merge rank -> provenance (ref fusion.py:245-249): 0 = datastore, r >= 1 =
+    the input tree of prefix length P - r + 1; -1 = the root (no source)."""
+    if rank < 0:
+        return None
+    return DATASTORE_SOURCE if rank == 0 else Source(Source.INPUT, P - rank + 1)
+
+
+def draft_tree_from_flat(flat, priorities=None, sources=None) -> DraftTree:
+    """Rebuild a ``DraftTree`` from DFS arrays (children in pre-order = insertion
+    order).  Without per-node data the nodes carry NaN priority and no source."""
     tree = DraftTree(flat.tokens[0])
     nodes = [tree.root]
     for i in range(1, flat.s_q):
-        node, _ = tree.insert(flat.tokens[i], nodes[flat.parents[i]], DATASTORE_SOURCE, float("nan"))
+        pr = float(priorities[i]) if priorities is not None else float("nan")
+        sc = sources[i] if sources is not None else None
+        node, _ = tree.insert(flat.tokens[i], nodes[flat.parents[i]], sc, pr)
         nodes.append(node)
     return tree
 

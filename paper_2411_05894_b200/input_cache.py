@@ -17,6 +17,7 @@ import torch
 
 from . import _lib
 from ._lib import check, lib, ptr, stream_ptr
+from .datastore import as_u32
 from .trees import ContinuationTree
 
 
@@ -77,7 +78,7 @@ def input_trees_batch(seqs: list[list[int]], P: int, ibl: int, device=None) -> l
         raise ValueError(f"input_branch_len {ibl} exceeds the compiled limit {_lib.SSSD_MAX_DEPTH}")
     B = len(seqs)
     lens = [len(s) for s in seqs]
-    flat = np.concatenate([np.asarray(s, dtype=np.int64) for s in seqs]).astype(np.uint32)
+    flat = np.concatenate([as_u32(s, "sequence token") for s in seqs])
     offs = np.zeros(B, dtype=np.int64)
     np.cumsum(lens[:-1], out=offs[1:])
     d_seq = torch.from_numpy(flat.view(np.int32)).to(dev)

@@ -27,38 +27,35 @@ def phrase_dictionary(vocab: int, n_phrases: int = 20000, seed: int = DICT_SEED)
     return toks, offs
 
 
+# phrases drawn per generator block: a fixed block size (and the block's noise
+# drawn right after it) makes every stream PREFIX-STABLE -- phrase_stream(n)
+# is the first n tokens of phrase_stream(m) for any m >= n -- so a B=64 batch
+# is exactly the first 64 contexts of a 16,384-context step (bench.py's two
+# arms draft identical inputs)
+BLOCK_PHRASES = 1 << 16
+
+
 def phrase_stream(n: int, vocab: int, seed: int, n_phrases: int = 20000,
                   noise: float = 0.05, dict_seed: int = DICT_SEED) -> np.ndarray:
-    """``n`` tokens (u32) of phrase-model text."""
+    """``n`` tokens (u32) of phrase-model text; prefix-stable in ``n``."""
     toks, offs = phrase_dictionary(vocab, n_phrases, dict_seed)
     lens = offs[1:] - offs[:-1]
     rng = np.random.default_rng(seed)
     out = np.empty(n, dtype=np.uint32)
     filled = 0
-    # (phrases per block capped so a 1B-token stream stays within a few GB of
-    # host memory; streams up to ~100M tokens are one block, as before)
-    block = min(max(4096, int(n / float(lens.mean()) * 1.05) + 64), 6_000_000)
     while filled < n:
-        ids = (rng.zipf(1.1, block) - 1) % n_phrases
+        ids = (rng.zipf(1.1, BLOCK_PHRASES) - 1) % n_phrases
         ln = lens[ids]
-        starts = offs[ids]
         total = int(ln.sum())
-        # position j of the concatenation -> starts[phrase] + (j - phrase_begin)
+        # position j of the block's concatenation -> offs[phrase] + (j - phrase_begin)
         begin = np.zeros(len(ids), dtype=np.int64)
         np.cumsum(ln[:-1], out=begin[1:])
-        idx = np.repeat(starts - begin, ln) + np.arange(total, dtype=np.int64)
-        seg = toks[idx]
+        seg = toks[np.repeat(offs[ids] - begin, ln) + np.arange(total, dtype=np.int64)]
+        mask = rng.random(total) < noise
+        seg[mask] = rng.integers(0, vocab, int(mask.sum())).astype(np.uint32)
         take = min(total, n - filled)
         out[filled:filled + take] = seg[:take]
         filled += take
-    if n <= 1 << 27:
-        mask = rng.random(n) < noise
-        out[mask] = rng.integers(0, vocab, int(mask.sum())).astype(np.uint32)
-    else:  # chunked noise for very long streams (host memory)
-        for a in range(0, n, 1 << 26):
-            seg = out[a:a + (1 << 26)]
-            mask = rng.random(seg.size) < noise
-            seg[mask] = rng.integers(0, vocab, int(mask.sum())).astype(np.uint32)
     return out
 
 
