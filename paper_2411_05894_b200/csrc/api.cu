@@ -321,6 +321,10 @@ size_t sssd_propose_workspace(const sssd_cfg* cfg, int32_t B, int32_t max_len) {
 
 // Library-internal streams used to fork the independent propose stages off the
 // caller's stream (joined back with events, so the caller sees stream order).
+// One set per (host thread, device): concurrent proposes from several host
+// threads never share fork streams or events (unbounded
+// concurrent readers), and lazy creation needs no lock.  (The set lives as
+// long as its thread; a thread keeps at most one per device.)
 struct Aux {
   cudaStream_t s[2];
   cudaEvent_t fork;
@@ -328,8 +332,8 @@ struct Aux {
 };
 
 static Aux* aux_streams() {
-  static Aux aux[16];
-  static bool ready[16] = {false};
+  thread_local Aux aux[16];
+  thread_local bool ready[16] = {false};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
   if (!ready[dev]) {

@@ -265,6 +265,30 @@ def gen_phrase() -> None:
     dump("phrase.json", out)
 
 
+def gen_files() -> None:
+    """SSSD v1 datastore files written by the reference (ref datastore.py:
+    220-226): sha256 of the exact bytes, which the GPU-built file must equal."""
+    import hashlib
+    import tempfile
+
+    cases = [([5, 6, 7, 5, 6, 8, 5, 6, 7, 9], None), ([1, 1, 1], 4),
+             (workload.corpus(50_000, 1000).tolist(), 1000), (workload.corpus(200_000, 32000).tolist(), None)]
+    out = []
+    with tempfile.TemporaryDirectory() as d:
+        for corpus, vocab in cases:
+            path = os.path.join(d, "ds.bin")
+            rds.build(corpus, vocab_size=vocab).save(path)
+            data = open(path, "rb").read()
+            rec = {"vocab": vocab, "n": len(corpus), "bytes": len(data), "sha256": hashlib.sha256(data).hexdigest()}
+            if len(corpus) <= 16:
+                rec["corpus"] = corpus
+                rec["hex"] = data.hex()
+            else:
+                rec["workload"] = "corpus(%d, %d)" % (len(corpus), 1000 if vocab == 1000 else 32000)
+            out.append(rec)
+    dump("files.json", out)
+
+
 def main() -> None:
     gen_sa(np.random.default_rng(0xC0FFEE))
     gen_lookup(np.random.default_rng(1))
@@ -273,6 +297,7 @@ def main() -> None:
     gen_propose(np.random.default_rng(4))
     gen_simulate(np.random.default_rng(5))
     gen_phrase()
+    gen_files()
 
 
 if __name__ == "__main__":

@@ -59,6 +59,46 @@ def test_tree_forward_matches_per_path_fp32():
     assert checked >= 30
 
 
+# north_star widths: TINY (cfg1) and Llama-3-8B (cfg3), two layers each so the
+# fp32 per-path reference stays cheap; >= 32 draft nodes checked per width
+WIDTHS = {"tiny": M.TINY, "llama3_8b_width": M.ModelSpec(2, 4096, 32, 8, 14336, 128256)}
+
+
+@pytest.mark.parametrize("name", sorted(WIDTHS))
+def test_tree_forward_logits_at_model_widths(name):
+    spec = WIDTHS[name]
+    corpus = workload.corpus(300_000, spec.vocab)
+    ds = G.build(corpus, vocab_size=spec.vocab)
+    B = 2
+    prompts = [c.tolist() for c in workload.contexts(B, 96, spec.vocab)]
+    cfg = G.FusionConfig(dec_len=32)
+    eng = G.DraftEngine(ds, cfg)
+    dec = M.Decoder(spec, batch=B, max_pos=256, seed=3, init_on_device=True)
+    dec.prefill(prompts)
+    seq, off, ln, mx = eng.upload(prompts)
+    out = eng.propose(seq, off, ln, mx, nodes=True)
+    ctx = ln - 1
+    assert torch.equal(out.pos[:, 0].long(), ctx.long())  # the kernel's position ids (L-1+depth)
+    logits = dec.forward(out.tokens, out.pos.clamp(min=0).long(), out.mask, ctx)
+    flats = G.draft._drafts_from_device(out.size, out.tokens, out.parents, out.depths, out.mask, B, cfg.dec_len)
+    checked, worst = 0, 0.0
+    for b, f in enumerate(flats):
+        paths = [[]]
+        for i in range(1, f.s_q):
+            paths.append(paths[f.parents[i]] + [f.tokens[i]])
+        for i in range(f.s_q):
+            want = dec.reference_logits(prompts[b] + paths[i])
+            got = logits[b, i]
+            err = (got - want).abs().max().item() / want.abs().max().item()
+            worst = max(worst, err)
+            assert err <= 1e-2, (name, b, i, err)
+            top2 = torch.topk(want, 2).values
+            if (top2[0] - top2[1]).item() > 1e-2 * abs(top2[0].item()):
+                assert int(got.argmax()) == int(want.argmax()), (name, b, i)
+            checked += 1
+    assert checked >= 32, checked
+
+
 def test_spec_decode_equals_autoregressive():
     corpus = workload.corpus(300_000, SMALL.vocab)
     ds = G.build(corpus)
