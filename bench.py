@@ -469,6 +469,10 @@ def run_ours(args) -> None:
                 extra["decode_cfg3"] = bench_decode_cfg3()
             except Exception as exc:
                 extra["decode_cfg3"] = {"error": repr(exc)}
+        try:
+            extra["decode_b64"] = bench_decode_b64(with_8b=args.decode_8b)
+        except Exception as exc:
+            extra["decode_b64"] = {"error": repr(exc)}
 
     if rank == 0:
         line = {
@@ -694,6 +698,128 @@ def bench_decode_cfg1(budget_s: float = 60.0) -> dict:
                                "gpu_simulate_s": round(gpu_s, 3),
                                "cpu_oracle_s_per_record": round(cpu_s / 2, 3),
                                "per_step_tokens_bitexact_vs_cpu_oracle": bitexact}}
+
+
+def _planned_dec_len(spec, b: int, s_kv: int) -> tuple[int, dict]:
+    """dec_len from the N4 planner (perf_model.plan_dec_len): the teacher-forced
+    acceptance curve measured in round 1 (profiles/r1_cost_curve.json, GPU
+    sweep on the phrase workload) over the roofline cost model of this model
+    at batch b / context s_kv on B200 (MEASURED_PEAKS.json)."""
+    from paper_2411_05894_b200 import perf_model as PM
+
+    curve = {int(k): float(v) for k, v in
+             json.load(open(os.path.join(ROOT, "profiles", "r1_cost_curve.json")))["accept_per_step"].items()}
+    hw = PM.b200_hardware(peaks_path=os.path.join(ROOT, "MEASURED_PEAKS.json")
+                          if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else None)
+    s_q, speedup = PM.plan_dec_len(curve, hw, spec, b, s_kv)
+    return int(s_q), {"planned_dec_len": int(s_q), "planned_speedup": round(float(speedup), 3),
+                      "planner": "perf_model.plan_dec_len(r1 teacher-forced accept curve, roofline cost model, "
+                                 f"b={b}, s_kv={s_kv})"}
+
+
+def bench_decode_b64(with_8b: bool = True) -> dict:
+    """north_star: end-to-end SSSD decode tokens/s at batch 64 over a
+    continuously batched loop (serving.ServeLoop: 64 slots refilled from a
+    request queue, propose -> tree forward -> accept -> KV compaction, CUDA
+    graph per step group), TINY (cfg1 model) and the Llama-3-8B shape, both
+    random-init (so ~1 accepted token per step: the speculation gain with
+    these weights is nil; the acceptance the drafts earn on real text is the
+    teacher-forced one, decode_cfg1.teacher_forced), beside the CPU leg
+    (oracle/cpu_decoder.py: oracle-port drafts + fp32 tree verify on every
+    host core, same weights and requests) and a logits parity check."""
+    import torch
+
+    import paper_2411_05894_b200 as G
+    from oracle import cpu_decoder as CD
+    from oracle import sssd_oracle as O
+    from paper_2411_05894_b200 import model as Mo
+    from paper_2411_05894_b200 import perf_model as PM
+    from paper_2411_05894_b200 import workload
+    from paper_2411_05894_b200.serving import ServeLoop
+
+    out = {}
+    B, plen = 64, 512
+    corpus = workload.corpus(1_000_000, VOCAB)
+    ds = G.build(corpus, vocab_size=VOCAB)
+    dl, plan = _planned_dec_len(PM.TINY, B, plen + 64)
+    cfg = G.FusionConfig(dec_len=dl)
+    n_req, max_new = 256, 64
+    prompts = [p.tolist() for p, _ in workload.records(n_req, plen, 0, VOCAB)]
+    dec = Mo.Decoder(Mo.TINY, B, plen + max_new + dl + 8, seed=0)
+    spec = ServeLoop(G.DraftEngine(ds, cfg), dec, plen, max_new)
+    spec.run(prompts[:B], 8)  # warm-up (graph capture, cuBLAS handles)
+    r = spec.run(prompts, max_new)
+    ar_loop = ServeLoop(None, Mo.Decoder(Mo.TINY, B, plen + max_new + 8, seed=0), plen, max_new)
+    ar_loop.run(prompts[:B], 8)
+    ar = ar_loop.run(prompts, max_new)
+    same = sum(int(a == b) for a, b in zip(r["sequences"], ar["sequences"]))
+    # logits parity: one propose + tree forward for 8 slots (>= 32 nodes) vs the fp32 per-path reference
+    eng = G.DraftEngine(ds, cfg)
+    npar = 8
+    pd = Mo.Decoder(Mo.TINY, npar, plen + dl + 8, seed=0)
+    pd.prefill(prompts[:npar])
+    seq, off, ln, mx = eng.upload(prompts[:npar])
+    o = eng.propose(seq, off, ln, mx, nodes=True)
+    lg = pd.forward(o.tokens, o.pos.clamp(min=0).long(), o.mask, ln - 1)
+    flats = G.draft._drafts_from_device(o.size, o.tokens, o.parents, o.depths, o.mask, npar, dl)
+    worst, checked, arg_ok = 0.0, 0, True
+    for b_, f in enumerate(flats):
+        paths = [[]]
+        for i in range(1, f.s_q):
+            paths.append(paths[f.parents[i]] + [f.tokens[i]])
+        for i in range(f.s_q):
+            want = pd.reference_logits(prompts[b_] + paths[i])
+            worst = max(worst, (lg[b_, i] - want).abs().max().item() / want.abs().max().item())
+            t2 = torch.topk(want, 2).values
+            if (t2[0] - t2[1]).item() > 1e-2 * abs(t2[0].item()):
+                arg_ok &= int(lg[b_, i].argmax()) == int(want.argmax())
+            checked += 1
+    # CPU leg: the same model / requests on the host cores (bounded sample: 8 requests)
+    cores = os.cpu_count() or 1
+    store = O.Store(corpus, ds.suffix_index)
+    cpu = CD.decode(store, prompts[:8], O.Cfg(dec_len=dl), dec, 16, threads=cores, budget_s=25.0)
+    cpu_match = sum(int(c == g[: len(c)]) for c, g in zip(cpu["sequences"], r["sequences"][:8]))
+    out["tiny"] = {
+        "workload": f"TINY (2L h1024 GQA 8/2 d128 V32000, random init), 64 slots continuously refilled from "
+                    f"{n_req} requests (prompt {plen}, {max_new} new tokens each), 1M-token datastore, dec_len {dl}",
+        **plan, "gpu_tokens_per_s": round(r["tokens_per_s"], 1),
+        "gpu_device_tokens_per_s": round(r["device_tokens_per_s"], 1),
+        "accepted_per_step": round(r["accepted_per_step"], 3), "steps_per_request": r["steps_per_request"],
+        "cuda_graph": r["cuda_graph"], "autoregressive_tokens_per_s": round(ar["tokens_per_s"], 1),
+        "autoregressive_device_tokens_per_s": round(ar["device_tokens_per_s"], 1),
+        "sequences_identical_to_autoregressive": f"{same}/{n_req}",
+        "logits_parity": {"nodes": checked, "max_rel_err": round(worst, 5), "tol": 1e-2,
+                          "argmax_equal_beyond_margin": bool(arg_ok)},
+        "cpu": {"tokens_per_s": round(cpu["tokens_per_s"], 2), "cores": cpu["threads"],
+                "accepted_per_step": round(cpu["accepted_per_step"], 3), "tokens": cpu["tokens"],
+                "sample": "8 of the same requests, 16 new tokens each (or 25 s), decode steps timed "
+                          "(oracle/cpu_decoder.py: oracle-port propose + fp32 torch tree verify)",
+                "sequences_equal_gpu_prefix": f"{cpu_match}/8"},
+        "gpu_vs_cpu_tokens_per_s": round(r["device_tokens_per_s"] / max(cpu["tokens_per_s"], 1e-9), 1),
+    }
+    del spec, ar_loop, dec, pd
+    torch.cuda.empty_cache()
+    if with_8b:
+        V8 = 128256
+        corpus8 = workload.corpus(10_000_000, V8)
+        ds8 = G.build(corpus8, vocab_size=V8)
+        dl8, plan8 = _planned_dec_len(PM.LLAMA3_8B, B, plen + 64)
+        n8, new8 = 128, 32
+        prompts8 = [p.tolist() for p, _ in workload.records(n8, plen, 0, V8)]
+        dec8 = Mo.Decoder(Mo.LLAMA3_8B, B, plen + new8 + dl8 + 8, seed=0, init_on_device=True)
+        loop8 = ServeLoop(G.DraftEngine(ds8, G.FusionConfig(dec_len=dl8)), dec8, plen, new8)
+        loop8.run(prompts8[:B], 4)
+        r8 = loop8.run(prompts8, new8)
+        out["llama3_8b"] = {
+            "workload": f"Llama-3-8B shape (32L h4096 GQA 32/8 d128 mlp14336 V128256, random init), 64 slots "
+                        f"continuously refilled from {n8} requests (prompt {plen}, {new8} new tokens), "
+                        f"10M-token datastore, dec_len {dl8}",
+            **plan8, "gpu_tokens_per_s": round(r8["tokens_per_s"], 1),
+            "gpu_device_tokens_per_s": round(r8["device_tokens_per_s"], 1),
+            "accepted_per_step": round(r8["accepted_per_step"], 3), "cuda_graph": r8["cuda_graph"]}
+        del loop8, dec8, ds8
+        torch.cuda.empty_cache()
+    return out
 
 
 def bench_decode_cfg3(steps: int = 5) -> dict:

@@ -193,6 +193,35 @@ class Decoder:
             for b in range(B):
                 done[b] = min(n[b], done[b] + S)
 
+    def prefill_rows(self, rows: list, prompts: list, chunk: int = 256) -> None:
+        """``prefill`` for a subset of cache rows (continuous batching: a freed
+        slot's new request), other rows untouched: the KV rows of prompts[i][:-1]
+        go to cache row rows[i]."""
+        n = [len(p) - 1 for p in prompts]
+        if not rows or max(n) <= 0:
+            return
+        r = torch.tensor(list(rows), dtype=torch.int64, device=self.device)
+        R = len(rows)
+        done = 0
+        while done < max(n):
+            S = min(chunk, max(n) - done)
+            toks = torch.zeros(R, S, dtype=torch.int64)
+            for i, p in enumerate(prompts):
+                seg = p[done: min(n[i], done + S)]
+                if seg:
+                    toks[i, : len(seg)] = torch.tensor([int(t) for t in seg])
+            W = (S + 63) // 64
+            bits = torch.tril(torch.ones(S, S, dtype=torch.bool))
+            mask = torch.zeros(S, W, dtype=torch.int64)
+            for w in range(W):
+                blk = bits[:, 64 * w: 64 * (w + 1)].to(torch.int64)
+                mask[:, w] = (blk << torch.arange(blk.shape[1], dtype=torch.int64)).sum(-1)
+            ctx = torch.full((R,), done, dtype=torch.int32, device=self.device)
+            pos = ctx.long()[:, None] + torch.arange(S, device=self.device)[None, :]
+            self.forward(toks.to(self.device), pos, mask[None].expand(R, S, W).contiguous().to(self.device), ctx,
+                         rows=r)
+            done += S
+
     def compact(self, ctx_len: torch.Tensor, path: torch.Tensor, n_acc: torch.Tensor) -> None:
         """Move the K/V rows of accepted draft nodes (cache slot ctx + node) to
         ctx + 1 + k, all layers, in one launch each for K and V."""

@@ -142,3 +142,149 @@ class SpecDecoder:
     def sequences(self) -> list[list[int]]:
         s = self.seq.view(self.model.B, self.cap).cpu().numpy().view(np.uint32)
         return [s[b, : int(n)].tolist() for b, n in enumerate(self.seq_len.cpu())]
+
+
+class ServeLoop:
+    """Continuous batching of speculative decode over a record queue (the
+    north_star "continuously batched decode loop"; step semantics ref
+    draft.py:202-216, loop semantics ref harness.py:171-237 with a model
+    instead of the teacher-forced oracle).
+
+    ``model.B`` slots each hold one live request: its token buffer (prompt,
+    then the accepted tokens + bonus appended in place by ``sssd_accept``,
+    capped at prompt + max_new) and its rows of the model's KV cache.  Steps
+    run in groups of ``group`` replayed from one CUDA graph (propose -> tree
+    forward -> argmax -> accept -> KV compaction for every slot); between
+    groups, finished slots are refilled with the next queued requests: their
+    prompts are written into the slot buffers and prefilled into their cache
+    rows only (``Decoder.forward(..., rows=...)``).  A slot that finishes
+    inside a group idles (appends capped) until the refill."""
+
+    def __init__(self, engine: DraftEngine | None, model: Decoder, max_prompt: int, max_new: int,
+                 group: int = 4) -> None:
+        self.eng, self.model, self.group = engine, model, max(1, int(group))
+        dev = model.device
+        B = model.B
+        self.S = engine.S if engine is not None else 1
+        self.cap = max_prompt + max_new + 1
+        assert self.cap + self.S <= model.max_pos, "model KV cache too short"
+        self.seq = torch.zeros(B * self.cap, dtype=torch.int32, device=dev)
+        self.off = torch.arange(B, dtype=torch.int64, device=dev) * self.cap
+        self.seq_len = torch.ones(B, dtype=torch.int32, device=dev)
+        self.seq_cap = torch.ones(B, dtype=torch.int32, device=dev)
+        self.path = torch.empty(B, self.S, dtype=torch.int32, device=dev)
+        self.n_acc = torch.empty(B, dtype=torch.int32, device=dev)
+        self.bonus = torch.empty(B, dtype=torch.int32, device=dev)
+        self.emitted = torch.empty(B, dtype=torch.int32, device=dev)
+        self.hist = torch.empty((self.group, B), dtype=torch.int32, device=dev)
+        self._graph = None
+        self._dec = SpecDecoder.__new__(SpecDecoder)  # reuse the step body on this loop's buffers
+        d = self._dec
+        d.eng, d.model, d.S, d.cap = engine, model, self.S, self.cap
+        d.seq, d.off, d.seq_len, d.seq_cap = self.seq, self.off, self.seq_len, self.seq_cap
+        d.path, d.n_acc, d.bonus, d.emitted = self.path, self.n_acc, self.bonus, self.emitted
+
+    def load(self, slots: list[int], prompts: list, max_new: list[int]) -> None:
+        """Start requests in ``slots``: tokens into the slot buffers, KV-cache
+        prefill of prompt[:-1] for those rows only (chunked chain masks)."""
+        from .datastore import as_u32
+
+        dev = self.seq.device
+        for s, p, m in zip(slots, prompts, max_new):
+            t = torch.from_numpy(as_u32(p, "prompt token").view(np.int32)).to(dev)
+            self.seq[s * self.cap: s * self.cap + len(p)] = t
+        meta = torch.tensor([[len(p) for p in prompts], [len(p) + int(m) for p, m in zip(prompts, max_new)]],
+                            dtype=torch.int32, device=dev)
+        idx = torch.tensor(list(slots), dtype=torch.int64, device=dev)
+        self.seq_len.index_copy_(0, idx, meta[0])
+        self.seq_cap.index_copy_(0, idx, meta[1])
+        self.model.prefill_rows(list(slots), [list(p) for p in prompts])
+
+    def _group(self) -> None:
+        for g in range(self.group):
+            self._dec._step()
+            self.hist[g].copy_(self.seq_len)
+
+    def run(self, prompts: list, max_new: int, use_graph: bool = True) -> dict:
+        """Decode every request of ``prompts`` (each to ``max_new`` new tokens)
+        through the slots; returns the generated sequences (request order) and
+        throughput (wall clock over the whole loop incl. refills, and the
+        device time of the step groups alone)."""
+        B = self.model.B
+        n_req = len(prompts)
+        nxt = min(B, n_req)
+        slot_req = np.full(B, -1, dtype=np.int64)
+        slot_req[:nxt] = np.arange(nxt)
+        free = list(range(nxt, B))
+        self.seq_len.fill_(1)
+        self.seq_cap.fill_(1)  # idle slots: capped (nothing appended)
+        self.load(list(range(nxt)), prompts[:nxt], [max_new] * nxt)
+        if free:  # idle slots still need a valid one-token context for the kernels
+            self.load(free, [[int(prompts[0][-1])]] * len(free), [0] * len(free))
+        out: list = [None] * n_req
+        steps_of = np.zeros(n_req, dtype=np.int64)
+        if use_graph and self._graph is None:
+            self._dec._step()  # eager warm-up step creates the lazily allocated buffers (results discarded below)
+            torch.cuda.synchronize()
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                    self._group()
+                self._graph = g
+            except Exception as exc:  # capture not possible here: eager groups (same results)
+                torch.cuda.synchronize()
+                self.graph_error = repr(exc)
+            # restart from clean prompts (the warm-up step appended tokens)
+            self.seq_len.fill_(1)
+            self.seq_cap.fill_(1)
+            self.load(list(range(nxt)), prompts[:nxt], [max_new] * nxt)
+            if free:
+                self.load(free, [[int(prompts[0][-1])]] * len(free), [0] * len(free))
+        lens = self.seq_len.cpu().numpy().astype(np.int64)
+        caps = self.seq_cap.cpu().numpy().astype(np.int64)
+        torch.cuda.synchronize()
+        t0 = perf_counter()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dev_ms, groups, tokens = 0.0, 0, 0
+        accepted = []
+        while (slot_req >= 0).any():
+            ev0.record()
+            if self._graph is not None:
+                self._graph.replay()
+            else:
+                self._group()
+            ev1.record()
+            H = self.hist.cpu().numpy().astype(np.int64)  # the group's one synchronisation
+            dev_ms += ev0.elapsed_time(ev1)
+            groups += 1
+            live = np.nonzero(slot_req >= 0)[0]
+            for g in range(self.group):
+                act = live[lens[live] < caps[live]]
+                if not len(act):
+                    break
+                em = H[g][act] - lens[act]
+                accepted.extend(em.tolist())
+                tokens += int(em.sum())
+                steps_of[slot_req[act]] += 1
+                lens[act] = H[g][act]
+            done = live[lens[live] >= caps[live]]
+            if len(done):
+                s = self.seq.view(B, self.cap)[torch.from_numpy(done).to(self.seq.device)].cpu().numpy()
+                for k, sl in enumerate(done):
+                    out[slot_req[sl]] = s[k, : lens[sl]].view(np.uint32).tolist()
+                n_fill = min(len(done), n_req - nxt)
+                fill = done[:n_fill].tolist()
+                if fill:
+                    self.load(fill, prompts[nxt:nxt + n_fill], [max_new] * n_fill)
+                    slot_req[done[:n_fill]] = np.arange(nxt, nxt + n_fill)
+                    lens[done[:n_fill]] = [len(p) for p in prompts[nxt:nxt + n_fill]]
+                    caps[done[:n_fill]] = lens[done[:n_fill]] + max_new
+                    nxt += n_fill
+                slot_req[done[n_fill:]] = -1
+        torch.cuda.synchronize()
+        wall = perf_counter() - t0
+        return {"sequences": out, "tokens": tokens, "requests": n_req, "slots": B, "seconds": wall,
+                "tokens_per_s": tokens / wall, "device_ms": dev_ms, "step_groups": groups, "group": self.group,
+                "device_tokens_per_s": tokens / (dev_ms / 1e3) if dev_ms else 0.0,
+                "accepted_per_step": float(np.mean(accepted)) if accepted else 0.0,
+                "steps_per_request": float(steps_of.mean()), "cuda_graph": self._graph is not None}
