@@ -232,6 +232,7 @@ def run_ours(args) -> None:
     ds = G.build(corpus, vocab_size=VOCAB, device=dev)
     torch.cuda.synchronize(dev)
     build_s = time.perf_counter() - t0
+    sa_check = ds.check()  # full-size property parity of the 100M index (untimed)
     stream_all = workload.phrase_stream(B * CTX * world, VOCAB, workload.HELDOUT_SEED)
     mine = stream_all[rank * B * CTX:(rank + 1) * B * CTX]
     cfg = G.FusionConfig(dec_len=DEC_LEN)
@@ -473,6 +474,13 @@ def run_ours(args) -> None:
             extra["decode_b64"] = bench_decode_b64(with_8b=args.decode_8b)
         except Exception as exc:
             extra["decode_b64"] = {"error": repr(exc)}
+        if args.cfg5:
+            try:
+                del ds, eng, seq  # (the 100M index makes room for the 1B build)
+                torch.cuda.empty_cache()
+                extra["cfg5"] = bench_cfg5()
+            except Exception as exc:
+                extra["cfg5"] = {"error": repr(exc)}
 
     if rank == 0:
         line = {
@@ -490,6 +498,7 @@ def run_ours(args) -> None:
                        "l2": "inputs > L2 (6.4 GB suffix rows, 134 MB contexts) + 256 MB flush between steps",
                        "b64_latency_ms": round(lat_ms, 4), "b64_lookups_per_s": round(BATCH / lat_ms * 1e3, 1),
                        "mean_draft_size": round(mean_size, 2), "gpu_sa_build_s": round(build_s, 2),
+                       "sa_check": sa_check,
                        "pipelined_2_streams_lookups_per_s": round(pipe_value, 1)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -608,6 +617,22 @@ def bench_lookup_cfg4(ds, corpus) -> dict:
 
     lat = timed(lambda: eng.propose(seq, off[:Bq], ln[:Bq], L), 20)
     thr = timed(lambda: eng.propose(seq, off, ln, L), 5)
+    # N2: the per-request input index (built once, as the decode loop does at
+    # admission; the steps after it scan only appended tokens)
+    ix = G.InputIndex(Bq * R, L, "cuda", off)
+    ix.build(seq, off, ln)
+    ix8 = G.InputIndex(Bq, L, "cuda", off[:Bq])
+    ix8.build(seq, off[:Bq], ln[:Bq])
+    for _ in range(3):
+        eng.propose(seq, off[:Bq], ln[:Bq], L, index=ix8)
+    lat_ix = timed(lambda: eng.propose(seq, off[:Bq], ln[:Bq], L, index=ix8), 20)
+    thr_ix = timed(lambda: eng.propose(seq, off, ln, L, index=ix), 5)
+    a = eng.propose(seq, off, ln, L)
+    a = {k: getattr(a, k).clone() for k in ("size", "tokens", "parents", "depths")}
+    b = eng.propose(seq, off, ln, L, index=ix)
+    ix_equal = all(torch.equal(a[k], getattr(b, k)) for k in ("size", "tokens", "parents", "depths"))
+    st_scan = np.median([eng.propose_profile(seq, off[:Bq], ln[:Bq], L) for _ in range(11)], axis=0)
+    st_ix = np.median([eng.propose_profile(seq, off[:Bq], ln[:Bq], L, index=ix8) for _ in range(11)], axis=0)
     got = eng.propose_host([c.tolist() for c in ctxs[:2]])
     store = O.Store(corpus, ds.suffix_index)
     t0 = time.perf_counter()
@@ -617,6 +642,13 @@ def bench_lookup_cfg4(ds, corpus) -> dict:
     return {"workload": "cfg4: B=8, ctx 32768 prompt-heavy, dec_len 16, 100M-token datastore",
             "b8_latency_ms": round(lat, 4), "b8_lookups_per_s": round(Bq / lat * 1e3, 1),
             "throughput_lookups_per_s": round(Bq * R / thr * 1e3, 1), "throughput_requests": Bq * R,
+            "input_index": {"b8_latency_ms": round(lat_ix, 4), "throughput_lookups_per_s": round(Bq * R / thr_ix * 1e3, 1),
+                            "b8_scan_stage_ms": round(float(st_ix[1]), 4),
+                            "b8_scan_stage_ms_stateless": round(float(st_scan[1]), 4),
+                            "drafts_equal_stateless": bool(ix_equal),
+                            "what": "N2: per-request sorted (token, position) index built at admission "
+                                    "(sssd_input_index_build); propose binary-searches the last token's "
+                                    "occurrences and scans only tokens appended since"},
             "drafts_bitexact_vs_cpu_oracle": exact, "cpu_oracle_s_per_lookup": round(cpu_s, 3)}
 
 
@@ -822,6 +854,91 @@ def bench_decode_b64(with_8b: bool = True) -> dict:
     return out
 
 
+def bench_cfg5(n_tokens: int = 1_000_000_000) -> dict:
+    """cfg5 (BASELINE configs[4]) on one B200: a 1B-token datastore (V =
+    128,256) built on the GPU, verified in full (sssd_sa_check: adjacent
+    suffixes strictly increasing + the SA a permutation), 64 drafts checked
+    bit-exact against the CPU oracle over the GPU-built suffix array, batched
+    propose at B=256 (latency, throughput), and the teacher-forced
+    continuous-batching decode loop (4,096 records, 256 slots)."""
+    import torch
+
+    import paper_2411_05894_b200 as G
+    from oracle import sssd_oracle as O
+    from paper_2411_05894_b200 import harness as H
+    from paper_2411_05894_b200 import workload
+
+    V = 128256
+    out = {"workload": f"cfg5 (one GPU): {n_tokens / 1e9:g}B-token phrase-model datastore, V={V}, B=256, "
+                       "ctx 512, dec_len 32"}
+    t0 = time.perf_counter()
+    corpus = workload.corpus(n_tokens, V)
+    out["host_corpus_gen_s"] = round(time.perf_counter() - t0, 1)
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats()
+    t0 = time.perf_counter()
+    ds = G.build(corpus, vocab_size=V)
+    torch.cuda.synchronize()
+    out["gpu_build_s"] = round(time.perf_counter() - t0, 2)
+    out["gpu_build_mtok_per_s"] = round(n_tokens / (time.perf_counter() - t0) / 1e6, 1)
+    out["gpu_mem_gb"] = round(torch.cuda.max_memory_allocated() / 1e9, 1)
+    t0 = time.perf_counter()
+    out["sa_check"] = ds.check()
+    out["sa_check"]["seconds"] = round(time.perf_counter() - t0, 2)
+    cfg = G.FusionConfig(dec_len=32)
+    eng = G.DraftEngine(ds, cfg)
+    B, CTX, R = 256, 512, 64
+    ctx = workload.phrase_stream(B * R * CTX, V, workload.HELDOUT_SEED)
+    seq = torch.from_numpy(ctx.view(np.int32)).cuda()
+    off = (torch.arange(B * R, dtype=torch.int64) * CTX).cuda()
+    ln = torch.full((B * R,), CTX, dtype=torch.int32, device="cuda")
+    # parity: the first 64 contexts' drafts vs the CPU oracle over the GPU suffix array
+    npar = 64
+    got = eng.propose_host([ctx[i * CTX:(i + 1) * CTX].tolist() for i in range(npar)])
+    sa32 = ds.rows[:, 0].contiguous().cpu().numpy().view(np.uint32)
+    store = O.Store(corpus, sa32)
+    t0 = time.perf_counter()
+    want = [O.propose(store, ctx[i * CTX:(i + 1) * CTX].tolist(), O.Cfg(dec_len=32)) for i in range(npar)]
+    cpu_s = (time.perf_counter() - t0) / npar
+    eq = sum(int((g.tokens, g.parents, g.depths) == (w.tokens, w.parents, w.depths)) for g, w in zip(got, want))
+    out["parity"] = {"drafts_bitexact": eq == npar, "n": npar, "rows_equal": eq,
+                     "digest": G.draft_digest(got), "oracle_digest": O.digest(want),
+                     "cpu_oracle_s_per_lookup": round(cpu_s, 4)}
+    del store, sa32, corpus
+    for _ in range(3):
+        eng.propose(seq, off, ln, CTX)
+        eng.propose(seq, off[:B], ln[:B], CTX)
+    torch.cuda.synchronize()
+    eng.check_status()
+
+    def timed(fn, n=10):
+        ts = []
+        for _ in range(n):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return float(np.median(ts))
+
+    lat = timed(lambda: eng.propose(seq, off[:B], ln[:B], CTX), 20)
+    thr = timed(lambda: eng.propose(seq, off, ln, CTX))
+    out["b256_propose_ms"] = round(lat, 4)
+    out["b256_lookups_per_s"] = round(B / lat * 1e3, 1)
+    out["throughput_lookups_per_s"] = round(B * R / thr * 1e3, 1)
+    recs = workload.records(4096, 512, 256, V)
+    sims = [G.SimRecord(p, q) for p, q in recs]
+    rep = G.simulate(sims, ds, cfg, slots=256)
+    out["decode_loop"] = {"records": 4096, "slots": 256, "prompt": 512, "reference": 256,
+                          "mean_accepted_per_step": round(rep.mean_accepted_per_step, 4),
+                          "teacher_forced_tokens_per_s": round(4096 * 256 / rep.wall_seconds, 1),
+                          "wall_s": round(rep.wall_seconds, 3), "cuda_graph": bool(H.simulate.last_graph)}
+    del eng, ds, seq
+    torch.cuda.empty_cache()
+    return out
+
+
 def bench_decode_cfg3(steps: int = 5) -> dict:
     """cfg3: Llama-3-8B-shaped random-init verify, B=32, ctx 4k, tree budget 32:
     device time of full speculative decode steps (propose + 32-layer tree
@@ -943,6 +1060,9 @@ def main() -> None:
     ap.add_argument("--decode-8b", action="store_true", default=True,
                     help="include the Llama-3-8B-shaped cfg3 decode step (default on)")
     ap.add_argument("--no-decode-8b", dest="decode_8b", action="store_false")
+    ap.add_argument("--cfg5", action="store_true", default=True,
+                    help="include the 1B-token cfg5 block (default on; ~1 min, ~75 GB of device memory)")
+    ap.add_argument("--no-cfg5", dest="cfg5", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

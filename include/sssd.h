@@ -77,6 +77,15 @@ int sssd_bucket_build(const uint32_t* rows, uint64_t n_rows, uint32_t n_buckets,
  * half the PCIe bytes and widened next to the kernels that read it. */
 int sssd_widen_u16(const uint16_t* src, uint32_t* dst, int64_t n, void* stream);
 
+/* Full-size verification of a built index (a size-independent parity
+ * property: a permutation of [0, n) whose adjacent suffixes strictly increase
+ * is the unique suffix array of ref datastore.py:81-109).  counts (device,
+ * 3 x u64): [0] adjacent rows not strictly increasing, [1] corpus positions
+ * missing from the SA column, [2] SA entries >= n.  All zero <=> correct. */
+size_t sssd_sa_check_workspace(uint64_t n);
+int sssd_sa_check(const uint32_t* tokens, uint64_t n, const uint32_t* rows, uint64_t n_rows, void* workspace,
+                  size_t workspace_bytes, unsigned long long* counts, void* stream);
+
 /* Copy the SA column of rows out as uint64 (the SSSD v1 file's `<u8` array). */
 int sssd_rows_sa64(const uint32_t* rows, uint64_t n, uint64_t* sa64_out, void* stream);
 
@@ -163,6 +172,36 @@ typedef struct sssd_lookup_out {
   int32_t* n_conts;  /* [B][P] non-empty continuations per p                      */
   int32_t* p_cut;    /* [B] smallest evaluated p (get_conts shortening stop)      */
 } sssd_lookup_out;
+
+/* Incremental per-request input index (the stateful
+ * analogue of InputCache._push, ref input_cache.py:46-63).  Request b's
+ * positions [0, len[b]) are kept sorted as u32 keys (token << pos_bits | pos)
+ * in keys[off[b] .. off[b] + len[b]); a propose then finds the occurrences of
+ * the last token by binary search instead of scanning the context, and scans
+ * only the tail [len[b], L-1) appended since the index was built (the decode
+ * loop's accepted tokens).  Results are identical to the stateless scan.
+ * len[b] = 0 means "no index" (full scan): the build leaves it 0 when the
+ * prefix exceeds SSSD_INDEX_MAX positions or a token does not fit the key. */
+#define SSSD_INDEX_MAX 32768
+typedef struct sssd_input_index {
+  uint32_t* keys;
+  const int64_t* off;
+  int32_t* len;
+  int32_t pos_bits; /* 1..24: positions < 2^pos_bits, tokens < 2^(32 - pos_bits) */
+} sssd_input_index;
+
+/* Build the index of positions [0, seq_len[b] - 1) for requests rows[i]
+ * (i < n_rows; rows NULL = requests 0 .. n_rows-1): one CTA per request,
+ * a shared-memory bitonic sort. */
+int sssd_input_index_build(const sssd_seqs* seqs, const sssd_input_index* index, const int32_t* rows,
+                           int32_t n_rows, void* stream);
+
+/* sssd_propose with an input index (NULL = the stateless scan) and, when
+ * stage_ms is non-NULL, the per-stage device times of sssd_propose_profile
+ * (synchronises). */
+int sssd_propose_ex(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_input_index* index, const sssd_cfg* cfg,
+                    const sssd_draft_out* out, const sssd_lookup_out* lookup, void* workspace,
+                    size_t workspace_bytes, void* stream, float* stage_ms);
 
 /* Workspace bytes for sssd_propose on this batch shape. */
 size_t sssd_propose_workspace(const sssd_cfg* cfg, int32_t B, int32_t max_len);

@@ -19,6 +19,7 @@ SSSD_MAX_P = 8
 SSSD_MAX_DEPTH = 32
 SSSD_MAX_DRAFT = 256
 SSSD_ROW_TOKENS = 15
+SSSD_INDEX_MAX = 32768
 SSSD_STATUS_OFFSET = 8  # int32 status word in every propose / merge workspace
 SSSD_PHASE_LOOKUP, SSSD_PHASE_SCAN, SSSD_PHASE_FUSE, SSSD_PHASE_BEGIN = 1, 2, 4, 8  # sssd_propose_phase bits
 E_WORKSPACE = -4
@@ -58,6 +59,10 @@ class DraftOut(C.Structure):
                 ("priority", vp), ("source", vp), ("pos", vp)]  # (last three optional: NULL = skip)
 
 
+class InputIndex(C.Structure):
+    _fields_ = [("keys", vp), ("off", vp), ("len", vp), ("pos_bits", C.c_int32)]
+
+
 class LookupOut(C.Structure):
     _fields_ = [("ranges", vp), ("samples", vp), ("n_conts", vp), ("p_cut", vp)]
 
@@ -70,6 +75,8 @@ _SIGS = {
     "sssd_sa_build": (C.c_int, [vp, C.c_uint64, vp, vp, C.c_size_t, vp]),
     "sssd_rows_build": (C.c_int, [vp, C.c_uint64, vp, vp, vp]),
     "sssd_rows_sa64": (C.c_int, [vp, C.c_uint64, vp, vp]),
+    "sssd_sa_check_workspace": (C.c_size_t, [C.c_uint64]),
+    "sssd_sa_check": (C.c_int, [vp, C.c_uint64, vp, C.c_uint64, vp, C.c_size_t, vp, vp]),
     "sssd_bucket_build": (C.c_int, [vp, C.c_uint64, C.c_uint32, vp, vp]),
     "sssd_widen_u16": (C.c_int, [vp, vp, C.c_int64, vp]),
     "sssd_rmsnorm_bf16": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int32, C.c_float, vp]),
@@ -83,6 +90,10 @@ _SIGS = {
     "sssd_gather_tails": (C.c_int, [vp, C.c_int32, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp]),
     "sssd_propose": (C.c_int, [C.POINTER(Ds), C.POINTER(Seqs), C.POINTER(Cfg), C.POINTER(DraftOut),
                                C.POINTER(LookupOut), vp, C.c_size_t, vp]),
+    "sssd_input_index_build": (C.c_int, [C.POINTER(Seqs), C.POINTER(InputIndex), vp, C.c_int32, vp]),
+    "sssd_propose_ex": (C.c_int, [C.POINTER(Ds), C.POINTER(Seqs), C.POINTER(InputIndex), C.POINTER(Cfg),
+                                  C.POINTER(DraftOut), C.POINTER(LookupOut), vp, C.c_size_t, vp,
+                                  C.POINTER(C.c_float)]),
     "sssd_propose_profile": (C.c_int, [C.POINTER(Ds), C.POINTER(Seqs), C.POINTER(Cfg), C.POINTER(DraftOut),
                                        vp, C.c_size_t, vp, C.POINTER(C.c_float)]),
     "sssd_set_cycle_probe": (None, [vp]),

@@ -91,6 +91,10 @@ static KCfg kcfg(const sssd_cfg* c) {
   k.disc = c->disc;
   k.fusion = c->fusion;
   k.seq_len = nullptr;
+  k.idx_keys = nullptr;
+  k.idx_off = nullptr;
+  k.idx_len = nullptr;
+  k.idx_pb = 0;
   return k;
 }
 
@@ -352,12 +356,43 @@ static Aux* aux_streams() {
 static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
                         const sssd_draft_out* out, const sssd_lookup_out* lookup, void* workspace,
                         size_t workspace_bytes, void* stream, cudaEvent_t* ev,
-                        const int64_t* pre_bounds = nullptr, const uint32_t* pre_rows = nullptr);
+                        const int64_t* pre_bounds = nullptr, const uint32_t* pre_rows = nullptr,
+                        const sssd_input_index* index = nullptr);
 
 int sssd_propose(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
                  const sssd_draft_out* out, const sssd_lookup_out* lookup, void* workspace,
                  size_t workspace_bytes, void* stream) {
   return propose_impl(ds, seqs, cfg, out, lookup, workspace, workspace_bytes, stream, nullptr);
+}
+
+int sssd_propose_ex(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_input_index* index, const sssd_cfg* cfg,
+                    const sssd_draft_out* out, const sssd_lookup_out* lookup, void* workspace,
+                    size_t workspace_bytes, void* stream, float* stage_ms) {
+  if (!stage_ms)
+    return propose_impl(ds, seqs, cfg, out, lookup, workspace, workspace_bytes, stream, nullptr, nullptr, nullptr,
+                        index);
+  cudaEvent_t ev[5];
+  for (auto& e : ev) cudaEventCreate(&e);
+  int rc = propose_impl(ds, seqs, cfg, out, lookup, workspace, workspace_bytes, stream, ev, nullptr, nullptr, index);
+  if (!rc) rc = cuda_check(cudaEventSynchronize(ev[4]), "profile sync");
+  if (!rc)
+    for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&stage_ms[i], ev[i], ev[i + 1]);
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
+}
+
+int sssd_input_index_build(const sssd_seqs* seqs, const sssd_input_index* index, const int32_t* rows,
+                           int32_t n_rows, void* stream) {
+  if (!seqs || !index || !index->keys || !index->off || !index->len)
+    return fail(SSSD_E_ARG, "input index build needs sequences and index buffers");
+  if (index->pos_bits < 1 || index->pos_bits > 24) return fail(SSSD_E_ARG, "pos_bits must be in 1..24");
+  if (n_rows <= 0) return n_rows == 0 ? SSSD_OK : fail(SSSD_E_ARG, "bad row count");
+  const int attr = cuda_check(cudaFuncSetAttribute(input_index_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   4 * SSSD_INDEX_MAX), "index build smem attribute");
+  if (attr) return attr;
+  input_index_build_kernel<<<n_rows, 1024, 4 * SSSD_INDEX_MAX, static_cast<cudaStream_t>(stream)>>>(*seqs, *index,
+                                                                                                    rows);
+  return cuda_check(cudaGetLastError(), "input index build launch");
 }
 
 int sssd_propose_profile(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
@@ -434,7 +469,7 @@ static void fuse_range(const PropWs& w, const KCfg& k, const sssd_seqs* seqs, co
 static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg,
                         const sssd_draft_out* out, const sssd_lookup_out* lookup, void* workspace,
                         size_t workspace_bytes, void* stream, cudaEvent_t* ev, const int64_t* pre_bounds,
-                        const uint32_t* pre_rows) {
+                        const uint32_t* pre_rows, const sssd_input_index* index) {
   int rc = validate_cfg(cfg);
   if (rc) return rc;
   if ((rc = validate_out(out))) return rc;
@@ -453,6 +488,14 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
     return fail(SSSD_E_WORKSPACE, "propose needs %zu workspace bytes, got %zu", w.bytes, workspace_bytes);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   KCfg k = kcfg(cfg);
+  if (index) {
+    if (!index->keys || !index->off || !index->len || index->pos_bits < 1 || index->pos_bits > 24)
+      return fail(SSSD_E_ARG, "bad input index (keys / off / len, pos_bits in 1..24)");
+    k.idx_keys = index->keys;
+    k.idx_off = index->off;
+    k.idx_len = index->len;
+    k.idx_pb = index->pos_bits;
+  }
   sssd_lookup_out lk{};
   if (lookup) lk = *lookup;
   if ((rc = cuda_check(cudaMemsetAsync(w.d.cursor, 0, 16 + 512, st), "memset status"))) return rc;

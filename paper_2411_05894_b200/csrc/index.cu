@@ -84,6 +84,53 @@ __global__ void rows_sa64_kernel(const uint32_t* rows, uint64_t n, uint64_t* out
   if (r < n) out[r] = rows[r * 16];
 }
 
+// Full-size suffix-array verification (a size-independent parity property:
+// an array that is a permutation of [0, n) with every adjacent pair of
+// suffixes strictly increasing IS the unique suffix array, ref
+// datastore.py:81-109 / SURVEY A.1).  Adjacent rows compare on their inline
+// tokens, then on the corpus tokens past them; a proper prefix sorts first.
+__global__ void sa_check_order_kernel(const uint32_t* tokens, uint64_t n, const uint32_t* rows, uint64_t n_rows,
+                                      unsigned long long* bad) {
+  const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r + 1 >= n_rows) return;
+  const uint32_t* a = rows + r * 16;
+  const uint32_t* b = a + 16;
+  const uint64_t pa = a[0], pb = b[0];
+  const uint64_t la = n - pa, lb = n - pb;  // suffix lengths
+  int c = 0;
+  const uint64_t inl = min((uint64_t)SSSD_ROW_TOKENS, min(la, lb));
+  for (uint64_t j = 0; j < inl && c == 0; ++j)
+    if (a[1 + j] != b[1 + j]) c = a[1 + j] < b[1 + j] ? -1 : 1;
+  for (uint64_t j = inl; c == 0 && j < min(la, lb); ++j) {  // rare: longer common prefixes
+    const uint32_t x = __ldg(tokens + pa + j), y = __ldg(tokens + pb + j);
+    if (x != y) c = x < y ? -1 : 1;
+  }
+  if (c == 0) c = la < lb ? -1 : 1;  // equal prefix: the shorter suffix first (la != lb for pa != pb)
+  if (c >= 0 || pa == pb) atomicAdd(bad, 1ull);
+}
+
+__global__ void sa_check_mark_kernel(const uint32_t* rows, uint64_t n_rows, uint64_t n, uint32_t* bits,
+                                     unsigned long long* bad) {
+  const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  const uint64_t p = rows[r * 16];
+  if (p >= n) {
+    atomicAdd(bad, 1ull);
+    return;
+  }
+  atomicOr(bits + (p >> 5), 1u << (p & 31));
+}
+
+__global__ void sa_check_count_kernel(const uint32_t* bits, uint64_t n, unsigned long long* missing) {
+  const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t words = (n + 31) / 32;
+  if (w >= words) return;
+  uint32_t want = 0xffffffffu;
+  if (w == words - 1 && (n & 31)) want = (1u << (n & 31)) - 1u;
+  const uint32_t miss = want & ~bits[w];
+  if (miss) atomicAdd(missing, (unsigned long long)__popc(miss));
+}
+
 struct SaWs {
   uint64_t* k0;
   uint64_t* k1;
@@ -277,6 +324,27 @@ int sssd_gather_tails(const void* seq, int32_t elem_bytes, const int64_t* off, c
   gather_tails_kernel<<<(B + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(seq, elem_bytes, off, len, B, P,
                                                                                         tails, tails_off, tails_len);
   return cuda_check(cudaGetLastError(), "gather_tails launch");
+}
+
+size_t sssd_sa_check_workspace(uint64_t n) { return ((n + 31) / 32) * 4 + 64; }
+
+int sssd_sa_check(const uint32_t* tokens, uint64_t n, const uint32_t* rows, uint64_t n_rows, void* workspace,
+                  size_t workspace_bytes, unsigned long long* counts, void* stream) {
+  if (!tokens || !rows || !counts) return fail(SSSD_E_ARG, "sa_check needs tokens, rows and counts");
+  if (!workspace || workspace_bytes < sssd_sa_check_workspace(n))
+    return fail(SSSD_E_WORKSPACE, "sa_check needs %zu workspace bytes", sssd_sa_check_workspace(n));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint32_t* bits = static_cast<uint32_t*>(workspace);
+  const uint64_t words = (n + 31) / 32;
+  int rc = cuda_check(cudaMemsetAsync(bits, 0, words * 4, st), "sa_check memset");
+  if (!rc) rc = cuda_check(cudaMemsetAsync(counts, 0, 3 * sizeof(unsigned long long), st), "sa_check memset");
+  if (rc) return rc;
+  if (n_rows > 1)
+    sa_check_order_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(tokens, n, rows, n_rows, counts);
+  if (n_rows)
+    sa_check_mark_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(rows, n_rows, n, bits, counts + 2);
+  if (words) sa_check_count_kernel<<<(unsigned)((words + 255) / 256), 256, 0, st>>>(bits, n, counts + 1);
+  return cuda_check(cudaGetLastError(), "sa_check launch");
 }
 
 int sssd_rows_sa64(const uint32_t* rows, uint64_t n, uint64_t* sa64_out, void* stream) {

@@ -905,6 +905,60 @@ __global__ void rows_from_pos_kernel(const uint32_t* tokens, uint64_t n, const u
   reinterpret_cast<uint4*>(rows)[t] = make_uint4(v[0], v[1], v[2], v[3]);
 }
 
+// N2 index build: request b's positions [0, L-1) as keys (token << pb | pos),
+// bitonic-sorted in shared memory by one CTA (1024 threads); len[b] = 0 (no
+// index: the stateless scan) when L - 1 > SSSD_INDEX_MAX or a token does not
+// fit the key.
+__global__ void __launch_bounds__(1024) input_index_build_kernel(sssd_seqs seqs, sssd_input_index ix,
+                                                                 const int32_t* rows) {
+  extern __shared__ __align__(16) uint32_t s_key[];
+  __shared__ int s_bad;
+  const int b = rows ? rows[blockIdx.x] : (int)blockIdx.x;
+  const int n = seqs.seq_len[b] - 1;
+  if (n <= 0 || n > SSSD_INDEX_MAX || n > (1 << ix.pos_bits)) {
+    if (threadIdx.x == 0) ix.len[b] = 0;
+    return;
+  }
+  const uint32_t* seq = seqs.seq + seqs.seq_off[b];
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  int n2 = 1;
+  while (n2 < n) n2 <<= 1;
+  const uint32_t tmax = ix.pos_bits >= 32 ? 0u : (1u << (32 - ix.pos_bits));
+  for (int j = threadIdx.x; j < n2; j += blockDim.x) {
+    if (j < n) {
+      const uint32_t t = seq[j];
+      if (t >= tmax) s_bad = 1;
+      s_key[j] = (t << ix.pos_bits) | (uint32_t)j;
+    } else {
+      s_key[j] = 0xffffffffu;  // padding sorts last
+    }
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (threadIdx.x == 0) ix.len[b] = 0;
+    return;
+  }
+  for (int k = 2; k <= n2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        const int p = i ^ j;
+        if (p > i) {
+          const uint32_t a = s_key[i], c2 = s_key[p];
+          if ((a > c2) == ((i & k) == 0)) {
+            s_key[i] = c2;
+            s_key[p] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  uint32_t* out = ix.keys + ix.off[b];
+  for (int j = threadIdx.x; j < n; j += blockDim.x) out[j] = s_key[j];
+  if (threadIdx.x == 0) ix.len[b] = n;
+}
+
 // --------------------------------------------------------------------------
 // K4: input scan (ref input_cache.py:88-121, stateless form A.4)
 // --------------------------------------------------------------------------
@@ -942,7 +996,46 @@ __global__ void __launch_bounds__(1024)
   const bool aligned = (reinterpret_cast<uintptr_t>(seq) & 15) == 0;
   static_assert(kScanV == 8, "vector tile loads assume 8 positions per thread");
   int total = 0;
-  for (int tile = 1; tile < L; tile += (int)blockDim.x * kScanV) {
+  // N2: with an input index, positions j < L0 come from the sorted keys
+  // (binary search for the last token's key range: ascending positions, i.e.
+  // e order) and only the tail j >= L0 is scanned below
+  int L0 = 0;
+  if (c.idx_len) L0 = max(0, min(c.idx_len[b], L - 1));
+  if (L0 > 0 && (uint64_t)t0 < (1ull << (32 - c.idx_pb))) {
+    const uint32_t* keys = c.idx_keys + c.idx_off[b];
+    const uint32_t pmask = (1u << c.idx_pb) - 1u;
+    const uint32_t klo = t0 << c.idx_pb, khi = klo | pmask;
+    int lo = 0, hi = L0;  // first key >= klo
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (keys[mid] < klo) lo = mid + 1;
+      else hi = mid;
+    }
+    int a = lo;
+    hi = L0;  // first key > khi
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (keys[mid] <= khi) lo = mid + 1;
+      else hi = mid;
+    }
+    const int cnt = lo - a;
+    for (int i = tid; i < cnt; i += blockDim.x) {
+      const int e = (int)(keys[a + i] & pmask) + 1;  // occurrence of the last token at e - 1
+      const int lim = min(jm, e);
+      int m = 1;
+      while (m < lim && seq[e - 1 - m] == s_tail[m]) ++m;
+      sssd_elem el;
+      el.off = (uint32_t)e;
+      el.orig = (uint32_t)e;
+      el.len_m = (uint32_t)min(c.IBL, L - e) | ((uint32_t)m << 8);
+      el.pad = 0;
+      r[i] = el;
+    }
+    total = cnt;
+  } else {
+    L0 = 0;
+  }
+  for (int tile = (L0 & ~7) + 1; tile < L; tile += (int)blockDim.x * kScanV) {
     const int e0 = tile + tid * kScanV;
     uint32_t v[kScanV];
     if (aligned && e0 + kScanV <= L) {  // two 16-byte loads: seq[e0-1 .. e0+7) (e0-1 is a multiple of 8)
@@ -954,9 +1047,9 @@ __global__ void __launch_bounds__(1024)
 #pragma unroll
       for (int k = 0; k < kScanV; ++k) v[k] = e0 + k < L ? seq[e0 + k - 1] : ~t0;
     }
-    uint32_t mk = 0;  // bit k: position e0 + k matches (m >= 1)
+    uint32_t mk = 0;  // bit k: position e0 + k matches (m >= 1); indexed positions (e0 + k - 1 < L0) excluded
 #pragma unroll
-    for (int k = 0; k < kScanV; ++k) mk |= (v[k] == t0 && e0 + k < L ? 1u : 0u) << k;
+    for (int k = 0; k < kScanV; ++k) mk |= (v[k] == t0 && e0 + k < L && e0 + k > L0 ? 1u : 0u) << k;
     const int cnt = __popc(mk);
     int inc = cnt;  // block exclusive scan of the counts
 #pragma unroll

@@ -14,6 +14,11 @@ struct KCfg {
   const double* disc;
   int fusion;  // 0 = level-synchronous (fusion_ls.cu), 1 = heap order (fusion.cu)
   const int32_t* seq_len;  // [B] live lengths for position ids (nullptr: pos = depth)
+  // optional input index (N2, sssd_input_index); idx_len == nullptr: stateless scan
+  const uint32_t* idx_keys;
+  const int64_t* idx_off;
+  const int32_t* idx_len;
+  int idx_pb;
 };
 
 // Optional per-node outputs of a flattened draft (priority / source rank /
@@ -74,6 +79,7 @@ __host__ __device__ inline int input_scan_smem_bytes(int threads, int ibl) {
 __global__ void input_scan_kernel(sssd_seqs seqs, KCfg c, sssd_elem* raw, sssd_elem* sorted,
                                   int32_t* in_n, uint32_t* idx_ws, int64_t cap, int64_t cap2,
                                   Cols cols);
+__global__ void input_index_build_kernel(sssd_seqs seqs, sssd_input_index ix, const int32_t* rows);
 __global__ void sort_sources_kernel(const uint32_t* tok, const sssd_elem* el,
                                     const int64_t* el_off, const int32_t* el_n, sssd_elem* sorted,
                                     uint32_t* idx_ws, int64_t idx_cap, Cols cols);

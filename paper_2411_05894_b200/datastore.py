@@ -152,6 +152,20 @@ class Datastore:
             self._np_sa = self.sa64_device().cpu().numpy().astype(np.int64)
         return self._np_sa
 
+    def check(self) -> dict:
+        """Full-size verification of the index on the device (``sssd_sa_check``):
+        adjacent suffix rows strictly increasing and the SA column a permutation
+        of [0, n_tokens) -- together, the unique suffix array."""
+        dev = self.device
+        ws = _workspace(lib().sssd_sa_check_workspace(self._n_tokens), dev)
+        cnt = torch.zeros(3, dtype=torch.int64, device=dev)
+        check(lib().sssd_sa_check(ptr(self._tok), self._n_tokens, ptr(self._rows), self.n_rows, ptr(ws), ws.numel(),
+                                  ptr(cnt), stream_ptr(dev)))
+        c = cnt.cpu().tolist()
+        return {"adjacent_not_increasing": c[0], "positions_missing": c[1] if self.n_rows == self._n_tokens else None,
+                "positions_out_of_range": c[2], "ok": c[0] == 0 and c[2] == 0 and
+                (c[1] == 0 or self.n_rows != self._n_tokens)}
+
     def sa64_device(self) -> torch.Tensor:
         out = torch.empty(self.n_rows, dtype=torch.int64, device=self.device)
         check(lib().sssd_rows_sa64(ptr(self._rows), self.n_rows, ptr(out), stream_ptr(self.device)))

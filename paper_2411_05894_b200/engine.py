@@ -51,6 +51,38 @@ class DraftBatch:
         return int(self.size.shape[0])
 
 
+class InputIndex:
+    """Incremental per-request input index (the stateful
+    analogue of ``InputCache._push``, ref input_cache.py:46-63): request b's
+    positions [0, L_b - 1) sorted by (token, position) in device memory, so a
+    propose finds the last token's occurrences by binary search and scans only
+    the tokens appended since (``sssd_input_index_build`` / ``sssd_propose_ex``).
+    Drafts are identical to the stateless scan's."""
+
+    def __init__(self, n_requests: int, cap: int, device, offsets: torch.Tensor | None = None) -> None:
+        self.cap = int(cap)
+        self.pos_bits = max(1, int(self.cap - 1).bit_length())
+        if self.pos_bits > 24:
+            raise ValueError(f"index capacity {cap} needs more than 24 position bits")
+        self.keys = torch.zeros(max(1, n_requests * self.cap), dtype=torch.int32, device=device)
+        self.off = offsets if offsets is not None else (
+            torch.arange(n_requests, dtype=torch.int64, device=device) * self.cap)
+        self.len = torch.zeros(n_requests, dtype=torch.int32, device=device)
+
+    def c_view(self) -> "_lib.InputIndex":
+        return _lib.InputIndex(ptr(self.keys), ptr(self.off), ptr(self.len), self.pos_bits)
+
+    def build(self, seq: torch.Tensor, seq_off: torch.Tensor, seq_len: torch.Tensor, rows=None,
+              stream: torch.cuda.Stream | None = None) -> None:
+        """(Re)index requests ``rows`` (default all) from their current sequences."""
+        B = int(seq_len.shape[0])
+        r = None if rows is None else torch.as_tensor(list(rows), dtype=torch.int32).to(seq.device)
+        n = B if r is None else int(r.numel())
+        seqs = _lib.Seqs(ptr(seq), ptr(seq_off), ptr(seq_len), B, self.cap)
+        sp = stream.cuda_stream if stream is not None else stream_ptr(seq.device)
+        check(lib().sssd_input_index_build(seqs, self.c_view(), ptr(r), n, sp))
+
+
 class PendingDrafts:
     """An in-flight ``propose_pinned(..., sync=False)``: ``wait()`` blocks until
     the drafts are in the pinned host buffers and checks the fusion arena."""
@@ -139,12 +171,15 @@ class DraftEngine:
 
     def propose(self, seq: torch.Tensor, seq_off: torch.Tensor, seq_len: torch.Tensor, max_len: int,
                 lookup: bool = False, out: DraftBatch | None = None, ws: torch.Tensor | None = None,
-                stream: torch.cuda.Stream | None = None, nodes: bool = False) -> DraftBatch:
+                stream: torch.cuda.Stream | None = None, nodes: bool = False,
+                index: InputIndex | None = None) -> DraftBatch:
         """Draft for B device-resident sequences: seq (int32 view of u32),
         seq_off [B] int64, seq_len [B] int32 (each >= 1).  Runs on ``stream``
         (default: the current stream) with workspace ``ws`` (default: the
         engine's own; concurrent calls on different streams need their own).
-        ``nodes``: also write position ids, node priorities and sources."""
+        ``nodes``: also write position ids, node priorities and sources.
+        ``index``: an ``InputIndex`` over these requests (N2) instead of the
+        stateless context scan (same drafts)."""
         B = int(seq_len.shape[0])
         out = out or self.outputs(B, lookup, nodes)
         if B == 0:
@@ -156,10 +191,13 @@ class DraftEngine:
         lk = _lib.LookupOut(ptr(out.ranges), ptr(out.samples), ptr(out.n_conts), ptr(out.p_cut)) if lookup else None
         ds = self.store.c_view() if (self.use_datastore and self.store is not None) else self._null_ds
         sp = stream.cuda_stream if stream is not None else stream_ptr(self.device)
-        check(lib().sssd_propose(ds, seqs, self.c, d_out, lk, ptr(ws), ws.numel(), sp))
+        if index is not None:
+            check(lib().sssd_propose_ex(ds, seqs, index.c_view(), self.c, d_out, lk, ptr(ws), ws.numel(), sp, None))
+        else:
+            check(lib().sssd_propose(ds, seqs, self.c, d_out, lk, ptr(ws), ws.numel(), sp))
         return out
 
-    def propose_profile(self, seq, seq_off, seq_len, max_len) -> list[float]:
+    def propose_profile(self, seq, seq_off, seq_len, max_len, index: InputIndex | None = None) -> list[float]:
         """Device ms of [ds_lookup, input_scan, setup, draft] for one propose (synchronises)."""
         import ctypes as C
 
@@ -167,10 +205,10 @@ class DraftEngine:
         out = self.outputs(B)
         ws = self.workspace(B, max_len)
         seqs = _lib.Seqs(ptr(seq), ptr(seq_off), ptr(seq_len), B, int(max_len))
-        d_out = _lib.DraftOut(ptr(out.size), ptr(out.tokens), ptr(out.parents), ptr(out.depths), ptr(out.mask))
         ds = self.store.c_view() if (self.use_datastore and self.store is not None) else self._null_ds
         ms = (C.c_float * 4)()
-        check(lib().sssd_propose_profile(ds, seqs, self.c, d_out, ptr(ws), ws.numel(), stream_ptr(self.device), ms))
+        check(lib().sssd_propose_ex(ds, seqs, index.c_view() if index is not None else None, self.c, out.c_out(),
+                                    None, ptr(ws), ws.numel(), stream_ptr(self.device), ms))
         return list(ms)
 
     def propose_pinned(self, seq_h: torch.Tensor, off_h: torch.Tensor, len_h: torch.Tensor, max_len: int,

@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from ._lib import check, lib, ptr, stream_ptr
-from .engine import DraftEngine
+from .engine import DraftEngine, InputIndex
 from .model import Decoder
 
 
@@ -48,7 +48,7 @@ class SpecDecoder:
     def _draft(self):
         B = self.model.B
         if self.eng is not None:
-            out = self.eng.propose(self.seq, self.off, self.seq_len, self.cap)
+            out = self.eng.propose(self.seq, self.off, self.seq_len, self.cap, index=getattr(self, "index", None))
             return out.tokens, out.parents, out.depths, out.mask, out.size
         # autoregressive: the draft is the root alone
         last = self.seq.view(B, self.cap).gather(1, (self.seq_len.long() - 1)[:, None])
@@ -178,11 +178,14 @@ class ServeLoop:
         self.emitted = torch.empty(B, dtype=torch.int32, device=dev)
         self.hist = torch.empty((self.group, B), dtype=torch.int32, device=dev)
         self._graph = None
+        # N2 per-slot input index (rebuilt on refill): each step scans only the appended tokens
+        self.index = InputIndex(B, self.cap, dev, self.off) if (engine is not None and engine.use_input) else None
         self._dec = SpecDecoder.__new__(SpecDecoder)  # reuse the step body on this loop's buffers
         d = self._dec
         d.eng, d.model, d.S, d.cap = engine, model, self.S, self.cap
         d.seq, d.off, d.seq_len, d.seq_cap = self.seq, self.off, self.seq_len, self.seq_cap
         d.path, d.n_acc, d.bonus, d.emitted = self.path, self.n_acc, self.bonus, self.emitted
+        d.index = self.index
 
     def load(self, slots: list[int], prompts: list, max_new: list[int]) -> None:
         """Start requests in ``slots``: tokens into the slot buffers, KV-cache
@@ -199,6 +202,8 @@ class ServeLoop:
         self.seq_len.index_copy_(0, idx, meta[0])
         self.seq_cap.index_copy_(0, idx, meta[1])
         self.model.prefill_rows(list(slots), [list(p) for p in prompts])
+        if self.index is not None:
+            self.index.build(self.seq, self.off, self.seq_len, rows=list(slots))
 
     def _group(self) -> None:
         for g in range(self.group):

@@ -101,3 +101,22 @@ def test_concurrent_host_threads_propose_bit_identical():
     for x in th:
         x.join()
     assert not errs, errs
+
+
+def test_sa_check_accepts_the_index_and_catches_corruption():
+    rng = np.random.default_rng(9)
+    for n, alpha in ((1, 3), (7, 2), (5000, 3), (200_000, 50)):
+        corpus = rng.integers(0, alpha, n).astype(np.uint32)
+        ds = G.build(corpus)
+        rep = ds.check()
+        assert rep["ok"] and rep["adjacent_not_increasing"] == 0 and rep["positions_missing"] == 0, (n, rep)
+    rows = ds.rows
+    a, b = 1000, 1001
+    tmp = rows[a].clone()
+    rows[a] = rows[b]
+    rows[b] = tmp
+    rep = ds.check()
+    assert not rep["ok"] and rep["adjacent_not_increasing"] >= 1
+    rows[b] = rows[a]  # duplicate position -> one missing
+    rep = ds.check()
+    assert rep["positions_missing"] == 1
