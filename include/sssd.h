@@ -53,10 +53,16 @@ int sssd_version(void);
 /* Bytes of scratch for sssd_sa_build on n tokens. */
 size_t sssd_sa_build_workspace(uint64_t n);
 
-/* Suffix array of tokens[0..n) by radix-sort prefix doubling.
+/* Suffix array of tokens[0..n) by radix-sort prefix doubling (own LSD radix
+ * sort; each round re-sorts only the positions of not-yet-singleton groups).
  * sa_out: uint32[n] (n < 2^32).  Bit-identical to the reference SA (unique). */
 int sssd_sa_build(const uint32_t* tokens, uint64_t n, uint32_t* sa_out, void* workspace,
                   size_t workspace_bytes, void* stream);
+
+/* sssd_sa_build reporting the number of prefix-doubling rounds (host int,
+ * the reference loop's iteration count for this corpus). */
+int sssd_sa_build_ex(const uint32_t* tokens, uint64_t n, uint32_t* sa_out, void* workspace, size_t workspace_bytes,
+                     void* stream, int32_t* rounds);
 
 /* Suffix rows: row r = {sa[r], tokens[sa[r] .. sa[r]+15)} as 16 x uint32 (64 B,
  * tokens past the corpus end are 0; validity is n - pos).  `rows` must be

@@ -73,6 +73,7 @@ _SIGS = {
     "sssd_version": (C.c_int, []),
     "sssd_sa_build_workspace": (C.c_size_t, [C.c_uint64]),
     "sssd_sa_build": (C.c_int, [vp, C.c_uint64, vp, vp, C.c_size_t, vp]),
+    "sssd_sa_build_ex": (C.c_int, [vp, C.c_uint64, vp, vp, C.c_size_t, vp, C.POINTER(C.c_int32)]),
     "sssd_rows_build": (C.c_int, [vp, C.c_uint64, vp, vp, vp]),
     "sssd_rows_sa64": (C.c_int, [vp, C.c_uint64, vp, vp]),
     "sssd_sa_check_workspace": (C.c_size_t, [C.c_uint64]),

@@ -1,23 +1,14 @@
 // Datastore index construction on the GPU (replaces ref datastore.py:81-109
 // build_suffix_array and the in-memory layout of datastore.py:144-154).
 //
-// Suffix array by prefix doubling: every round sorts all positions by the
-// 64-bit key (rank[i], rank[i+k] + 1 | 0 past the end) and re-ranks each
-// position to the start index of its equal-key group (inclusive max-scan of
-// head indices).  It stops once every key is distinct, exactly like the
-// reference loop (datastore.py:93-109).  The SA of a sequence is unique, so the
-// result is bit-identical to the reference.
-//
-// The per-round key generation, head marking, re-rank scatter and the
-// termination test are our kernels; the 64-bit key/value radix sort and the
-// max-scan use CUB (header-only CCCL inside this library).
+// Suffix array: prefix doubling with group refinement on our own radix sort
+// (csrc/sa_build.cu); the SA of a sequence is unique, so the result is
+// bit-identical to the reference.
 //
 // Suffix rows: the lookup layout.  Row r (64 B, one aligned 2-sector line) =
 // {pos = SA[r], tokens[pos .. pos+15)} so a search probe or a sampled
 // continuation is ONE independent 64 B access instead of an SA load followed
 // by a dependent token load.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -26,42 +17,6 @@
 namespace sssd {
 int fail(int code, const char* fmt, ...);
 int cuda_check(cudaError_t e, const char* what);
-
-__global__ void sa_init_kernel(const uint32_t* tokens, uint64_t n, uint64_t* key, uint32_t* val) {
-  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  key[i] = tokens[i];
-  val[i] = (uint32_t)i;
-}
-
-// head index of each sorted slot: j if its key differs from slot j-1, else 0;
-// counts the non-head slots (ties still pending) into *pending.
-__global__ void sa_heads_kernel(const uint64_t* key, uint64_t n, uint32_t* head,
-                                unsigned long long* pending) {
-  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  bool tie = false;
-  if (j < n) {
-    tie = j > 0 && key[j] == key[j - 1];
-    head[j] = tie ? 0u : (uint32_t)j;
-  }
-  const uint32_t bal = __ballot_sync(SSSD_FULL, tie);
-  if ((threadIdx.x & 31) == 0 && bal) atomicAdd(pending, (unsigned long long)__popc(bal));
-}
-
-__global__ void sa_scatter_rank_kernel(const uint32_t* val, const uint32_t* grp, uint64_t n,
-                                       uint32_t* rank) {
-  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < n) rank[val[j]] = grp[j];
-}
-
-__global__ void sa_keys_kernel(const uint32_t* rank, uint64_t n, uint64_t k, uint64_t* key,
-                               uint32_t* val) {
-  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint64_t second = i + k < n ? (uint64_t)rank[i + k] + 1 : 0;
-  key[i] = ((uint64_t)rank[i] << 32) | second;
-  val[i] = (uint32_t)i;
-}
 
 __global__ void rows_build_kernel(const uint32_t* tokens, uint64_t n, const uint32_t* sa,
                                   uint32_t* rows) {
@@ -131,53 +86,9 @@ __global__ void sa_check_count_kernel(const uint32_t* bits, uint64_t n, unsigned
   if (miss) atomicAdd(missing, (unsigned long long)__popc(miss));
 }
 
-struct SaWs {
-  uint64_t* k0;
-  uint64_t* k1;
-  uint32_t* v0;
-  uint32_t* v1;
-  uint32_t* rank;
-  uint32_t* grp;
-  unsigned long long* pending;
-  void* tmp;
-  size_t tmp_bytes;
-  size_t total;
-};
-
-static size_t al(size_t x) { return (x + 255) / 256 * 256; }
-
-static SaWs sa_carve(uint8_t* base, uint64_t n) {
-  SaWs w{};
-  size_t sort_tmp = 0, scan_tmp = 0;
-  cub::DoubleBuffer<uint64_t> kb(nullptr, nullptr);
-  cub::DoubleBuffer<uint32_t> vb(nullptr, nullptr);
-  cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, kb, vb, (int64_t)n, 0, 64);
-  cub::DeviceScan::InclusiveScan(nullptr, scan_tmp, (uint32_t*)nullptr, (uint32_t*)nullptr,
-                                 cub::Max(), (int64_t)n);
-  size_t off = 0;
-  auto take = [&](size_t bytes) {
-    uint8_t* p = base ? base + off : nullptr;
-    off += al(bytes);
-    return p;
-  };
-  w.k0 = reinterpret_cast<uint64_t*>(take(8 * n));
-  w.k1 = reinterpret_cast<uint64_t*>(take(8 * n));
-  w.v0 = reinterpret_cast<uint32_t*>(take(4 * n));
-  w.v1 = reinterpret_cast<uint32_t*>(take(4 * n));
-  w.rank = reinterpret_cast<uint32_t*>(take(4 * n));
-  w.grp = reinterpret_cast<uint32_t*>(take(4 * n));
-  w.pending = reinterpret_cast<unsigned long long*>(take(8));
-  w.tmp_bytes = sort_tmp > scan_tmp ? sort_tmp : scan_tmp;
-  w.tmp = take(w.tmp_bytes);
-  w.total = off;
-  return w;
-}
-
-static int bits_for(uint64_t x) {
-  int b = 0;
-  while (b < 64 && (x >> b)) ++b;
-  return b;
-}
+size_t sa_build_workspace2(uint64_t n);
+int sa_build2(const uint32_t* tokens, uint64_t n, uint32_t* sa_out, void* workspace, size_t workspace_bytes,
+              cudaStream_t st, int* rounds_out);
 
 }  // namespace sssd
 
@@ -239,51 +150,25 @@ __global__ void gather_tails_kernel(const void* seq, int elem_bytes, const int64
 
 extern "C" {
 
-size_t sssd_sa_build_workspace(uint64_t n) { return sa_carve(nullptr, n ? n : 1).total; }
+size_t sssd_sa_build_workspace(uint64_t n) { return sa_build_workspace2(n ? n : 1); }
 
 int sssd_sa_build(const uint32_t* tokens, uint64_t n, uint32_t* sa_out, void* workspace,
                   size_t workspace_bytes, void* stream) {
   if (n == 0) return fail(SSSD_E_ARG, "empty corpus");
   if (n >= 0xffffffffull) return fail(SSSD_E_LIMIT, "corpus longer than 2^32-1 tokens");
   if (!tokens || !sa_out) return fail(SSSD_E_ARG, "NULL buffer");
-  SaWs w = sa_carve(static_cast<uint8_t*>(workspace), n);
-  if (!workspace || workspace_bytes < w.total)
-    return fail(SSSD_E_WORKSPACE, "sa_build needs %zu workspace bytes, got %zu", w.total, workspace_bytes);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int T = 256;
-  const unsigned grid = (unsigned)((n + T - 1) / T);
-  int rc;
-  if (n == 1) return cuda_check(cudaMemsetAsync(sa_out, 0, 4, st), "sa memset");
-  sa_init_kernel<<<grid, T, 0, st>>>(tokens, n, w.k0, w.v0);
-  int end_bit = 32;
-  const int rank_bits = bits_for(n);
-  for (uint64_t k = 1;; k *= 2) {
-    cub::DoubleBuffer<uint64_t> kb(w.k0, w.k1);
-    cub::DoubleBuffer<uint32_t> vb(w.v0, w.v1);
-    size_t tb = w.tmp_bytes;
-    if ((rc = cuda_check(cub::DeviceRadixSort::SortPairs(w.tmp, tb, kb, vb, (int64_t)n, 0, end_bit, st),
-                         "radix sort")))
-      return rc;
-    uint64_t* ks = kb.Current();
-    uint32_t* vs = vb.Current();
-    if ((rc = cuda_check(cudaMemsetAsync(w.pending, 0, 8, st), "memset"))) return rc;
-    sa_heads_kernel<<<grid, T, 0, st>>>(ks, n, w.grp, w.pending);
-    tb = w.tmp_bytes;
-    if ((rc = cuda_check(cub::DeviceScan::InclusiveScan(w.tmp, tb, w.grp, w.grp, cub::Max(), (int64_t)n, st),
-                         "max scan")))
-      return rc;
-    sa_scatter_rank_kernel<<<grid, T, 0, st>>>(vs, w.grp, n, w.rank);
-    unsigned long long pending = 0;
-    if ((rc = cuda_check(cudaMemcpyAsync(&pending, w.pending, 8, cudaMemcpyDeviceToHost, st), "copy")))
-      return rc;
-    if ((rc = cuda_check(cudaStreamSynchronize(st), "sync"))) return rc;
-    if (pending == 0) {
-      return cuda_check(cudaMemcpyAsync(sa_out, vs, 4 * n, cudaMemcpyDeviceToDevice, st), "sa copy");
-    }
-    if (k >= n) return fail(SSSD_E_ARG, "suffix doubling did not converge");
-    sa_keys_kernel<<<grid, T, 0, st>>>(w.rank, n, k, w.k0, w.v0);
-    end_bit = 32 + rank_bits;
-  }
+  return sa_build2(tokens, n, sa_out, workspace, workspace_bytes, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int sssd_sa_build_ex(const uint32_t* tokens, uint64_t n, uint32_t* sa_out, void* workspace, size_t workspace_bytes,
+                     void* stream, int32_t* rounds) {
+  if (n == 0) return fail(SSSD_E_ARG, "empty corpus");
+  if (n >= 0xffffffffull) return fail(SSSD_E_LIMIT, "corpus longer than 2^32-1 tokens");
+  if (!tokens || !sa_out) return fail(SSSD_E_ARG, "NULL buffer");
+  int r = 1;
+  const int rc = sa_build2(tokens, n, sa_out, workspace, workspace_bytes, static_cast<cudaStream_t>(stream), &r);
+  if (rounds) *rounds = r;
+  return rc;
 }
 
 int sssd_rows_build(const uint32_t* tokens, uint64_t n, const uint32_t* sa, uint32_t* rows,
