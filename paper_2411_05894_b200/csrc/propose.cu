@@ -1005,20 +1005,43 @@ __global__ void __launch_bounds__(1024)
     const uint32_t* keys = c.idx_keys + c.idx_off[b];
     const uint32_t pmask = (1u << c.idx_pb) - 1u;
     const uint32_t klo = t0 << c.idx_pb, khi = klo | pmask;
-    int lo = 0, hi = L0;  // first key >= klo
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (keys[mid] < klo) lo = mid + 1;
-      else hi = mid;
+    // the key range of the last token by two 17-ary searches in warp 0 (lanes
+    // 0-15: first key >= klo, lanes 16-31: first key > khi): ~3 dependent
+    // rounds for 2k keys instead of 2 x 11 binary-search steps
+    if (warp == 0) {
+      const int half = lane >> 4, hl = lane & 15;
+      const uint32_t hmask = 0xffffu << (16 * half);
+      int lo = 0, hi = L0;
+      while (__any_sync(SSSD_FULL, lo < hi)) {
+        const int n = hi - lo;
+        int p = -1;
+        if (n > 0) p = n <= 16 ? (hl < n ? lo + hl : -1) : lo + (int)(((long long)(hl + 1) * n) / 17);
+        bool pr = false;
+        if (p >= 0) {
+          const uint32_t k = keys[p];
+          pr = half == 0 ? k < klo : k <= khi;
+        }
+        const uint32_t bal = (__ballot_sync(SSSD_FULL, pr) & hmask) >> (16 * half);
+        const int cnt = __popc(bal);  // predicate is monotone along the probes
+        const int plast = __shfl_sync(SSSD_FULL, p, (16 * half) + max(cnt - 1, 0));
+        const int pnext = __shfl_sync(SSSD_FULL, p, (16 * half) + min(cnt, 15));
+        if (n > 0) {
+          if (n <= 16) {
+            lo = lo + cnt;
+            hi = lo;
+          } else {
+            if (cnt > 0) lo = plast + 1;
+            if (cnt < 16) hi = pnext;
+          }
+        }
+      }
+      if (lane == 0) s_wsum[0] = lo;
+      if (lane == 16) s_wsum[1] = lo;
     }
-    int a = lo;
-    hi = L0;  // first key > khi
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (keys[mid] <= khi) lo = mid + 1;
-      else hi = mid;
-    }
-    const int cnt = lo - a;
+    __syncthreads();
+    const int a = s_wsum[0];
+    const int cnt = s_wsum[1] - a;
+    __syncthreads();  // (s_wsum is reused by the tail scan)
     for (int i = tid; i < cnt; i += blockDim.x) {
       const int e = (int)(keys[a + i] & pmask) + 1;  // occurrence of the last token at e - 1
       const int lim = min(jm, e);

@@ -161,7 +161,7 @@ class ServeLoop:
     inside a group idles (appends capped) until the refill."""
 
     def __init__(self, engine: DraftEngine | None, model: Decoder, max_prompt: int, max_new: int,
-                 group: int = 4) -> None:
+                 group: int = 4, use_index: bool | None = None) -> None:
         self.eng, self.model, self.group = engine, model, max(1, int(group))
         dev = model.device
         B = model.B
@@ -179,7 +179,10 @@ class ServeLoop:
         self.hist = torch.empty((self.group, B), dtype=torch.int32, device=dev)
         self._graph = None
         # N2 per-slot input index (rebuilt on refill): each step scans only the appended tokens
-        self.index = InputIndex(B, self.cap, dev, self.off) if (engine is not None and engine.use_input) else None
+        if use_index is None:  # (see DecodeLoop: the index pays past one 8k-position scan pass)
+            use_index = self.cap > 8192
+        self.index = (InputIndex(B, self.cap, dev, self.off)
+                      if (use_index and engine is not None and engine.use_input) else None)
         self._dec = SpecDecoder.__new__(SpecDecoder)  # reuse the step body on this loop's buffers
         d = self._dec
         d.eng, d.model, d.S, d.cap = engine, model, self.S, self.cap

@@ -38,7 +38,7 @@ def test_serve_loop_refills_and_is_lossless(slots, group):
     prompts[3] = prompts[3][:20]  # ragged prompt lengths
     max_new = 24
     spec = ServeLoop(G.DraftEngine(ds, G.FusionConfig(dec_len=12)), M.Decoder(SMALL, slots, 160, seed=2),
-                     60, max_new, group=group)
+                     60, max_new, group=group, use_index=(slots == 4))
     r = spec.run(prompts, max_new)
     ar = ServeLoop(None, M.Decoder(SMALL, slots, 160, seed=2), 60, max_new, group=group).run(prompts, max_new)
     assert r["tokens"] == ar["tokens"] == 11 * max_new
