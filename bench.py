@@ -193,6 +193,44 @@ def pcie_h2d_gbps(src, dev) -> float:
     return best
 
 
+def bench_decode_loop_ranks(ds, world: int, rank: int, dev, corpus) -> dict:
+    """Teacher-forced continuous-batching decode loop (harness.DecodeLoop via
+    simulate) with the request pool partitioned over the ranks: 1,024 records
+    per rank (prompt 512, reference 256), 256 slots per GPU, dec_len 32, the
+    cfg2 datastore (replicated; with a sharded index every rank rebuilds a
+    full replica would be needed, so the sharded run reports the replicated
+    control).  Device time is the max over ranks; tokens/s = all ranks' tokens
+    over it."""
+    import torch
+
+    import paper_2411_05894_b200 as G
+    from paper_2411_05894_b200 import workload
+
+    if ds is None:
+        return {"skipped": "sharded run: the decode-loop replicas need a full index per GPU"}
+    per = 1024
+    recs = workload.records(per * world, 512, 256, VOCAB)[rank * per:(rank + 1) * per]
+    sims = [G.SimRecord(p, q) for p, q in recs]
+    cfg = G.FusionConfig(dec_len=32)
+    G.simulate(sims[:64], ds, cfg, slots=64)  # warm (graph capture path)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    rep = G.simulate(sims, ds, cfg, slots=256)
+    wall = allreduce_max(rep.wall_seconds, world)
+    toks = sum(r.tokens_emitted for r in rep.records)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([toks], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        toks = int(t.item())
+    return {"records_per_rank": per, "slots_per_rank": 256, "ranks": world, "tokens": toks,
+            "tokens_per_s": round(toks / wall, 1), "wall_s_max_over_ranks": round(wall, 3),
+            "mean_accepted_per_step": round(rep.mean_accepted_per_step, 4),
+            "workload": "teacher-forced records (prompt 512, reference 256) on the cfg2 datastore, dec_len 32, "
+                        "requests partitioned over ranks, one decode loop per GPU"}
+
+
 def bench_sa_build(ds, dev) -> dict:
     """K1 alone (sssd_sa_build_ex on the resident corpus, CUDA events, best of
     3): Mtok/s and the roofline of SURVEY §8(d) -- 48 B per token per
@@ -530,6 +568,17 @@ def run_ours(args) -> None:
                 base = None  # (the CPU baseline is reported at N=1 only)
 
     extra = {}
+    if not args.no_extra:
+        # the continuously batched decode loop partitioned over the ranks (one
+        # replica per GPU, its own slots and records):
+        # teacher-forced cfg5-shaped records against this rank's datastore view
+        try:
+            dl = bench_decode_loop_ranks(ds if not args.shard else None, world, rank, dev, corpus)
+            if rank == 0:
+                extra["decode_loop_ranks"] = dl
+        except Exception as exc:
+            if rank == 0:
+                extra["decode_loop_ranks"] = {"error": repr(exc)}
     if rank == 0 and world == 1 and not args.no_extra:
         pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
             os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0}
