@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(kT) rs_upsweep(const uint64_t* keys, uint64_t 
   if (h[threadIdx.x]) atomicAdd(totals + threadIdx.x, h[threadIdx.x]);
 }
 
+
 // One CTA per digit: exclusive scan of hist[d][0..nb) plus the digit's base
 // (the counts of all smaller digits).
 __global__ void __launch_bounds__(kT) rs_scan(const uint32_t* hist, unsigned nb, const uint32_t* totals,
@@ -160,6 +161,7 @@ __global__ void __launch_bounds__(kT) rs_scatter(const uint64_t* kin, const uint
     }
   }
 }
+
 
 // ---- scans --------------------------------------------------------------------
 
@@ -431,6 +433,7 @@ int sa_build2(const uint32_t* tokens, uint64_t n, uint32_t* sa_out, void* worksp
     return fail(SSSD_E_WORKSPACE, "sa_build needs %zu workspace bytes, got %zu", w.total, workspace_bytes);
   if (n == 1) return cuda_check(cudaMemsetAsync(sa_out, 0, 4, st), "sa memset");
   int rc = 0;
+
   const int T = 256;
   auto grid = [](uint64_t m) { return (unsigned)((m + 255) / 256); };
   // round 1: sort by token (only the token bits: a max-reduce first)

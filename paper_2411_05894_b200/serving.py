@@ -22,6 +22,35 @@ from .engine import DraftEngine, InputIndex
 from .model import Decoder
 
 
+def spec_step(st, tokens, parents, depths, mask, size) -> None:
+    """One verification step over every slot of ``st`` (a SpecDecoder or
+    ServeLoop: model, seq / off / seq_len / seq_cap, path / n_acc / bonus /
+    emitted, S): tree forward at positions L-1+depth, argmax, greedy accept +
+    in-place append, KV compaction of the accepted nodes."""
+    ctx = st.seq_len - 1
+    pos = ctx.long()[:, None] + depths.clamp(min=0).long()
+    logits = st.model.forward(tokens, pos, mask, ctx)
+    pred = logits.argmax(-1).to(torch.int32).contiguous()
+    B, S = tokens.shape
+    check(lib().sssd_accept(ptr(tokens), ptr(parents), ptr(size), S, ptr(pred), B, ptr(st.seq), ptr(st.off),
+                            ptr(st.seq_len), ptr(st.seq_cap), ptr(st.path), ptr(st.n_acc), ptr(st.bonus),
+                            ptr(st.emitted), stream_ptr(st.seq.device)))
+    st.model.compact(ctx, st.path if S == st.S else st.path[:, :S].contiguous(), st.n_acc)
+
+
+def draft_all(st):
+    """Drafts of every slot of ``st`` (DraftEngine.propose, with its input index
+    if any), or the root alone when ``st.eng`` is None (autoregressive)."""
+    B = st.model.B
+    if st.eng is not None:
+        out = st.eng.propose(st.seq, st.off, st.seq_len, st.cap, index=getattr(st, "index", None))
+        return out.tokens, out.parents, out.depths, out.mask, out.size
+    last = st.seq.view(B, st.cap).gather(1, (st.seq_len.long() - 1)[:, None])
+    z = torch.zeros(B, 1, dtype=torch.int32, device=st.seq.device)
+    return (last.to(torch.int32), z - 1, z, torch.ones(B, 1, 1, dtype=torch.int64, device=st.seq.device),
+            torch.ones(B, dtype=torch.int32, device=st.seq.device))
+
+
 class SpecDecoder:
     def __init__(self, engine: DraftEngine | None, model: Decoder, prompts: list, max_new: int) -> None:
         self.eng, self.model = engine, model
@@ -46,15 +75,7 @@ class SpecDecoder:
         self.steps = 0
 
     def _draft(self):
-        B = self.model.B
-        if self.eng is not None:
-            out = self.eng.propose(self.seq, self.off, self.seq_len, self.cap, index=getattr(self, "index", None))
-            return out.tokens, out.parents, out.depths, out.mask, out.size
-        # autoregressive: the draft is the root alone
-        last = self.seq.view(B, self.cap).gather(1, (self.seq_len.long() - 1)[:, None])
-        z = torch.zeros(B, 1, dtype=torch.int32, device=self.seq.device)
-        return (last.to(torch.int32), z - 1, z, torch.ones(B, 1, 1, dtype=torch.int64, device=self.seq.device),
-                torch.ones(B, dtype=torch.int32, device=self.seq.device))
+        return draft_all(self)
 
     def step(self) -> torch.Tensor:
         self._step()
@@ -62,16 +83,7 @@ class SpecDecoder:
         return self.emitted
 
     def _step(self) -> None:
-        tokens, parents, depths, mask, size = self._draft()
-        ctx = self.seq_len - 1
-        pos = ctx.long()[:, None] + depths.clamp(min=0).long()
-        logits = self.model.forward(tokens, pos, mask, ctx)
-        pred = logits.argmax(-1).to(torch.int32).contiguous()
-        B, S = tokens.shape
-        check(lib().sssd_accept(ptr(tokens), ptr(parents), ptr(size), S, ptr(pred), B, ptr(self.seq),
-                                ptr(self.off), ptr(self.seq_len), ptr(self.seq_cap), ptr(self.path),
-                                ptr(self.n_acc), ptr(self.bonus), ptr(self.emitted), stream_ptr(self.seq.device)))
-        self.model.compact(ctx, self.path if S == self.S else self.path[:, :S].contiguous(), self.n_acc)
+        spec_step(self, *self._draft())
 
     def run(self, graph_steps: int = 8) -> dict:
         """Decode every slot to its cap; returns tokens, steps and timing
@@ -183,12 +195,9 @@ class ServeLoop:
             use_index = self.cap > 8192
         self.index = (InputIndex(B, self.cap, dev, self.off)
                       if (use_index and engine is not None and engine.use_input) else None)
-        self._dec = SpecDecoder.__new__(SpecDecoder)  # reuse the step body on this loop's buffers
-        d = self._dec
-        d.eng, d.model, d.S, d.cap = engine, model, self.S, self.cap
-        d.seq, d.off, d.seq_len, d.seq_cap = self.seq, self.off, self.seq_len, self.seq_cap
-        d.path, d.n_acc, d.bonus, d.emitted = self.path, self.n_acc, self.bonus, self.emitted
-        d.index = self.index
+
+    def _step(self) -> None:
+        spec_step(self, *draft_all(self))
 
     def load(self, slots: list[int], prompts: list, max_new: list[int]) -> None:
         """Start requests in ``slots``: tokens into the slot buffers, KV-cache
@@ -210,7 +219,7 @@ class ServeLoop:
 
     def _group(self) -> None:
         for g in range(self.group):
-            self._dec._step()
+            self._step()
             self.hist[g].copy_(self.seq_len)
 
     def run(self, prompts: list, max_new: int, use_graph: bool = True) -> dict:
@@ -232,7 +241,7 @@ class ServeLoop:
         out: list = [None] * n_req
         steps_of = np.zeros(n_req, dtype=np.int64)
         if use_graph and self._graph is None:
-            self._dec._step()  # eager warm-up step creates the lazily allocated buffers (results discarded below)
+            self._step()  # eager warm-up step creates the lazily allocated buffers (results discarded below)
             torch.cuda.synchronize()
             try:
                 g = torch.cuda.CUDAGraph()
