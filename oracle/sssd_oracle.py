@@ -32,6 +32,7 @@ and against the reference tests' hand-written known answers.
 from __future__ import annotations
 
 import hashlib
+import heapq
 import json
 import struct
 from dataclasses import dataclass, field
@@ -327,18 +328,30 @@ def fuse(ds: Trie | None, inputs: list, P: int, dec_len: int, disc, root_token: 
         if t is not None and t.count > 0:
             new_group(t, P - (i + 1) + 1, 1, None, 0)
 
+    # group heads in a binary heap (the minimum over heads, as the reference's
+    # heapq pop over individual candidates, ref fusion.py:252)
+    heap: list = []
+    pushed = 0
+
+    def push_head(g) -> None:
+        if g["next"] < len(g["cand"]):
+            heapq.heappush(heap, (head(g)[0], g["seq"]))
+
+    for g in groups:
+        push_head(g)
+    pushed = len(groups)
     size = 1
     while size < dec_len:
-        best = None
-        for g in groups:
-            if g["next"] < len(g["cand"]):
-                h = head(g)
-                if best is None or h[0] < best[0][0]:
-                    best = (h, g)
-        if best is None:
+        while pushed < len(groups):  # groups created by the previous pop
+            push_head(groups[pushed])
+            pushed += 1
+        if not heap:
             break
-        (key, tok, c, pp), g = best
+        _, gs = heapq.heappop(heap)
+        g = groups[gs]
+        key, tok, c, pp = head(g)
         g["next"] += 1
+        push_head(g)
         par = g["dparent"]
         nid = d_kids[par].get(tok)
         if nid is None:
@@ -445,8 +458,17 @@ class Store:
     sa: np.ndarray
 
 
+def session_inputs(seq, cfg: Cfg, use_in=True) -> list:
+    """The input tries of a context (what the reference's GenerationSession.start
+    builds once per session into its InputCache, ref draft.py:156-181), so that
+    ``propose(..., inputs=...)`` times only the per-step work, like the
+    reference's bench_retrieval over pre-started sessions (harness.py:325-370)."""
+    seq = [int(x) for x in seq]
+    return [trie_of(s) for s in input_strings(seq, cfg.P, cfg.input_branch_len)] if use_in else []
+
+
 def propose(store: Store | None, seq, cfg: Cfg, separator=None, use_ds=True, use_in=True,
-            disc=None) -> Draft:
+            disc=None, inputs=None) -> Draft:
     seq = [int(x) for x in seq]
     if disc is None:
         disc = cfg.disc()
@@ -456,7 +478,10 @@ def propose(store: Store | None, seq, cfg: Cfg, separator=None, use_ds=True, use
         look = ds_lookup(store.tokens, store.sa, prefix, cfg.P, cfg.M, cfg.T, cfg.branch_len,
                          separator)
         ds = trie_of(look.strings)
-    ins = [trie_of(s) for s in input_strings(seq, cfg.P, cfg.input_branch_len)] if use_in else []
+    if inputs is not None:
+        ins = inputs
+    else:
+        ins = [trie_of(s) for s in input_strings(seq, cfg.P, cfg.input_branch_len)] if use_in else []
     return flatten(*fuse(ds, ins, cfg.P, cfg.dec_len, disc, seq[-1]))
 
 
