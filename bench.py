@@ -150,8 +150,15 @@ def dist_setup(n_gpus: int):
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # SSSD_BENCH_ONE_GPU=1 (code-path test of N > 1 on a one-GPU box): every
+        # rank on cuda:0 with gloo collectives; never a measurement
+        if os.environ.get("SSSD_BENCH_ONE_GPU") == "1":
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     return world, rank, local
@@ -170,7 +177,7 @@ def allreduce_max(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if dist.get_backend() == "gloo" else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -221,7 +228,7 @@ def bench_decode_loop_ranks(ds, world: int, rank: int, dev, corpus) -> dict:
     if world > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([toks], dtype=torch.int64, device=dev)
+        t = torch.tensor([toks], dtype=torch.int64, device="cpu" if dist.get_backend() == "gloo" else dev)
         dist.all_reduce(t)
         toks = int(t.item())
     return {"records_per_rank": per, "slots_per_rank": 256, "ranks": world, "tokens": toks,
@@ -440,24 +447,26 @@ def run_ours(args) -> None:
     # back-to-back steps on two alternating streams (own workspace / outputs
     # each; inputs > L2, no flush): step i+1's lookup and scan fill the SMs the
     # fusion tail of step i releases.  Reported beside the serial value.
-    pipe_ws = [eng.workspace(B, CTX).clone() for _ in range(2)]
-    pipe_out = [eng.outputs(B) for _ in range(2)]
-    pipe_st = [torch.cuda.Stream(dev) for _ in range(2)]
-    pipe_ms = []
-    for _ in range(2):
-        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(st)
-        for s_ in pipe_st:
-            s_.wait_event(a)
-        for i in range(args.steps):
-            eng.propose(seq, off, ln, CTX, out=pipe_out[i & 1], ws=pipe_ws[i & 1], stream=pipe_st[i & 1])
-        for s_ in pipe_st:
-            st.wait_stream(s_)
-        b_.record(st)
-        torch.cuda.synchronize(dev)
-        pipe_ms.append(a.elapsed_time(b_) / args.steps)
-    pipe_value = B / (min(pipe_ms) / 1e3)
-    del pipe_ws, pipe_out
+    pipe_value = None
+    if not args.shard:  # (the sharded propose is a collective on the caller's stream)
+        pipe_ws = [eng.workspace(B, CTX).clone() for _ in range(2)]
+        pipe_out = [eng.new_outputs(B) for _ in range(2)]
+        pipe_st = [torch.cuda.Stream(dev) for _ in range(2)]
+        pipe_ms = []
+        for _ in range(2):
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            for s_ in pipe_st:
+                s_.wait_event(a)
+            for i in range(args.steps):
+                eng.propose(seq, off, ln, CTX, out=pipe_out[i & 1], ws=pipe_ws[i & 1], stream=pipe_st[i & 1])
+            for s_ in pipe_st:
+                st.wait_stream(s_)
+            b_.record(st)
+            torch.cuda.synchronize(dev)
+            pipe_ms.append(a.elapsed_time(b_) / args.steps)
+        pipe_value = B / (min(pipe_ms) / 1e3)
+        del pipe_ws, pipe_out
 
     # single-batch latency at B=64
     seq64, off64, ln64 = seq, off[:BATCH], ln[:BATCH]
@@ -629,7 +638,7 @@ def run_ours(args) -> None:
                        "b64_latency_ms": round(lat_ms, 4), "b64_lookups_per_s": round(BATCH / lat_ms * 1e3, 1),
                        "mean_draft_size": round(mean_size, 2), "gpu_sa_build_s": round(build_s, 2),
                        "sa_check": sa_check, "sa_build": sa_build, "input_index": ix_block,
-                       "pipelined_2_streams_lookups_per_s": round(pipe_value, 1)},
+                       "pipelined_2_streams_lookups_per_s": round(pipe_value, 1) if pipe_value else None},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "scope": "whole propose step (SURVEY 8(d) algorithmic bytes of lookup + tree build)",
@@ -656,8 +665,9 @@ def run_ours(args) -> None:
                         "format": "u16 token ids (vocab 32000), widened on device (sssd_widen_u16)"},
                     "schedule": "back-to-back steps, two in flight (propose_pinned slot / sync=False)",
                     "roofline": {"bound": "pcie_h2d", "unit": "GB/s",
-                                 "achieved": round(h2d * e2e_value / B / 1e9, 2), "peak": round(h2d_peak, 2),
-                                 "frac": round(h2d * e2e_value / B / 1e9 / h2d_peak, 4),
+                                 "achieved": round(h2d * e2e_value / (B * world) / 1e9, 2), "peak": round(h2d_peak, 2),
+                                 "frac": round(h2d * e2e_value / (B * world) / 1e9 / h2d_peak, 4),
+                                 "per": "GPU (each rank uploads its own contexts)",
                                  "peak_source": "measured: 134 MB pinned -> device copy, best of 5 (this box)"},
                     "serial_value": round(e2e_serial, 1)},
             # per propose: ds_lookup, input_scan, propose_setup, (lpt_scatter when B >= 2048), draft_ls
@@ -1178,8 +1188,8 @@ def run_reference(args) -> None:
             "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": f"{cores} B=64 batches per step (one per worker process), oracle port "
                                        f"fork-parallel over {cores} processes; sessions pre-started (input "
-                                       "tries built in warm-up, as the reference's bench_retrieval times "
-                                       "propose() of started sessions)"},
+                                       "tries built before the pool forks, as the reference's bench_retrieval "
+                                       "times propose() of started sessions)"},
             "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             # the first batch = the GPU arm's first 64 contexts (workload.phrase_stream is prefix-stable)
             "parity": {"digest_first64": O.digest(first), "n": len(first),

@@ -58,18 +58,25 @@ class Collective:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
 
+        self.gloo = dist.get_backend(group) == "gloo"
+
     def all_gather(self, x: torch.Tensor) -> torch.Tensor:
+        if self.gloo and x.is_cuda:  # (gloo collectives run on host copies)
+            return self.all_gather(x.cpu()).to(x.device)
         out = torch.empty((self.world * x.shape[0],) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
         self.dist.all_gather_into_tensor(out, x.contiguous(), group=self.group)
         return out
 
     def all_reduce_sum(self, x: torch.Tensor) -> torch.Tensor:
+        if self.gloo and x.is_cuda:
+            x.copy_(self.all_reduce_sum(x.cpu()))
+            return x
         self.dist.all_reduce(x, op=self.dist.ReduceOp.SUM, group=self.group)
         return x
 
     def reduce_scatter_sum(self, x: torch.Tensor) -> torch.Tensor:
         n = x.shape[0] // self.world
-        if self.dist.get_backend(self.group) == "gloo":  # gloo has no reduce_scatter
+        if self.gloo:  # gloo has no reduce_scatter
             self.all_reduce_sum(x)
             return x[self.rank * n:(self.rank + 1) * n].clone()
         out = torch.empty((n,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
