@@ -198,6 +198,7 @@ __device__ SSSD_LS_CALL void ls_sort(LsLevel L, uint32_t n) {
 // slots [0, keepn) in order; returns keepn and the first cut key.
 __device__ SSSD_LS_CALL uint32_t ls_cut(LsLevel L, uint32_t nb, uint32_t keepn, uint64_t* th0, uint64_t* th1) {
   const uint32_t lane = (uint32_t)lane_id();
+  __syncwarp();  // order the level records this warp emitted before the sort reads them (racecheck)
   ls_sort(L, nb);
   *th0 = L.k0()[keepn];
   *th1 = L.k1()[keepn];
