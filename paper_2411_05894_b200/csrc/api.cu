@@ -534,7 +534,10 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
   // chunk i (caller's stream) overlap the lookup / scan of chunk i+1.
   Aux* ax = aux_streams();
   if (!ax) return fail(SSSD_E_CUDA, "could not create auxiliary streams");
-  const int chunks = 1;  // chunked pipelining measured slower: each chunk pays a fusion-kernel tail
+  // chunked pipelining measured slower (each chunk pays a fusion-kernel tail);
+  // SSSD_PROPOSE_CHUNKS (A/B switch, <= 8) re-measures it
+  static const int env_chunks = getenv("SSSD_PROPOSE_CHUNKS") ? atoi(getenv("SSSD_PROPOSE_CHUNKS")) : 1;
+  const int chunks = B >= 4096 ? max(1, min(8, env_chunks)) : 1;
   const int per = (B + chunks - 1) / chunks;
   cudaEventRecord(ax->fork, st);
   cudaStreamWaitEvent(ax->s[0], ax->fork, 0);
@@ -548,6 +551,7 @@ static int propose_impl(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg
     cudaEventRecord(ax->done[1][ci], ax->s[1]);
     cudaStreamWaitEvent(st, ax->done[0][ci], 0);
     cudaStreamWaitEvent(st, ax->done[1][ci], 0);
+    if (ci > 0) fuse_reset_kernel<<<1, 128, 0, st>>>(w.d.cursor, w.d.hist);  // per-range arena + LPT histogram
     launch_fuse(st, b0, b1);
   }
   return cuda_check(cudaGetLastError(), "propose launch");
