@@ -798,7 +798,7 @@ def bench_lookup_cfg4(ds, corpus) -> dict:
 
 def issue_roofline(fusion_ms: float, B: int, clk) -> dict | None:
     """The fusion kernel is issue-bound, not HBM-bound: its warp instructions
-    per lookup (ncu count of the committed capture, profiles/r1_propose_ncu.json:
+    per lookup (ncu count of the committed capture, profiles/r2_propose_ncu.json:
     warp_inst / grid, one warp per request) over this run's kernel time, against
     148 SMs x 4 schedulers x the SM clock sampled during the timed region."""
     path = os.path.join(ROOT, "profiles", "r1_propose_ncu.json")
@@ -814,7 +814,7 @@ def issue_roofline(fusion_ms: float, B: int, clk) -> dict | None:
     return {"kernel": "draft_ls_kernel", "bound": "issue", "unit": "warp instructions/s",
             "warp_instructions_per_lookup": round(per_lookup, 1), "achieved": round(achieved / 1e9, 1),
             "peak": round(peak / 1e9, 1), "scale": "1e9", "frac": round(achieved / peak, 4),
-            "source": "profiles/r1_propose_ncu.json (ncu smsp__inst_executed of the same kernel)"}
+            "source": "profiles/r2_propose_ncu.json (ncu smsp__inst_executed of the same kernel)"}
 
 
 def bench_decode_cfg1(budget_s: float = 60.0) -> dict:
