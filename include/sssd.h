@@ -313,6 +313,13 @@ int sssd_propose_pre(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* c
  * memory}; NULL disables. */
 void sssd_set_cycle_probe(long long* cycles);
 
+/* Fusion form of the level-synchronous path (cfg fusion = 0): -1 = automatic
+ * (by launch size), 0 = level-synchronous only, 1 = all-nodes kernel first
+ * (requests outgrowing its shared-memory tables fall back to the
+ * level-synchronous kernel).  Identical drafts either way; a process-wide
+ * tuning switch, initialised from SSSD_FUSION_ANE. */
+void sssd_set_fusion_form(int form);
+
 /* Fusion of caller-provided source trees (merge fusion.py:209-261 + flatten).
  * Each tree is given as its multiset of root-to-end paths in DFS order (first
  * appearance order = the tree's child order): paths of request b / source s

@@ -98,6 +98,7 @@ _SIGS = {
     "sssd_propose_profile": (C.c_int, [C.POINTER(Ds), C.POINTER(Seqs), C.POINTER(Cfg), C.POINTER(DraftOut),
                                        vp, C.c_size_t, vp, C.POINTER(C.c_float)]),
     "sssd_set_cycle_probe": (None, [vp]),
+    "sssd_set_fusion_form": (None, [C.c_int]),
     "sssd_workspace_status": (C.c_int, [C.POINTER(Cfg), C.c_int32, C.c_int32, vp, C.c_int32,
                                         C.c_int64, vp]),
     "sssd_find_ranges": (C.c_int, [C.POINTER(Ds), vp, vp, vp, C.c_int32, vp, vp]),

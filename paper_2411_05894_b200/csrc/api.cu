@@ -102,6 +102,7 @@ constexpr uint32_t kSlabChildren = 2048;
 
 struct DraftWs {
   int32_t* order;
+  int32_t* fb;  // all-nodes fusion fallback list: [0] = count, [1..] = requests
   uint8_t* bucket;
   int32_t* hist;  // [64] histogram + [64] fill cursors (zeroed with the status words)
   uint8_t* gover;
@@ -129,6 +130,7 @@ static unsigned long long* carve_status(Carver& cv) { return cv.take<unsigned lo
 static DraftWs carve_draft(Carver& cv, unsigned long long* status, int P, int S, int B, int64_t max_len = 0) {
   DraftWs d;
   d.order = cv.take<int32_t>((size_t)B);
+  d.fb = cv.take<int32_t>((size_t)B + 1);
   d.bucket = cv.take<uint8_t>((size_t)B);
   d.gover_bytes = draft_group_overflow_bytes(P, S);
   d.gover = cv.take<uint8_t>((size_t)B * (d.gover_bytes ? d.gover_bytes : 1));
@@ -262,8 +264,22 @@ static int fusion_smem_attr(const KCfg& k) {
   if (k.fusion == 1)
     return cuda_check(cudaFuncSetAttribute(draft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            draft_smem_bytes(k.P, k.S)), "draft_kernel smem attribute");
+  if (int rc = cuda_check(cudaFuncSetAttribute(draft_ane_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               ane_smem_bytes()), "draft_ane_kernel smem attribute"))
+    return rc;
   return cuda_check(cudaFuncSetAttribute(draft_ls_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          ls_smem_bytes(k.P, k.S)), "draft_ls_kernel smem attribute");
+}
+
+// All-nodes fusion (fusion_ane.cu) for launches of at most this many
+// requests; SSSD_FUSION_ANE=0/1 forces it off/on (A/B switch).
+static int g_fusion_form = [] {
+  const char* e = getenv("SSSD_FUSION_ANE");
+  return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
+}();
+static bool ane_enabled(int nb) {
+  if (g_fusion_form >= 0) return g_fusion_form == 1;
+  return false;
 }
 
 // One fusion + flatten launch over requests [k.b0, k.b0 + nb) (or order[] of them).
@@ -278,6 +294,15 @@ static void launch_fusion(const DraftWs& d, const KCfg& k, int nb, const sssd_dr
     // the level-synchronous kernel uses the heap form's slabs + pool as one pool
     uint8_t* lo = reinterpret_cast<uint8_t*>(d.slabs);
     uint8_t* hi = reinterpret_cast<uint8_t*>(d.pool) + d.pool_cap * kChildBytes;
+    if (ane_enabled(nb)) {
+      // all-nodes fusion; the requests it lists in d.fb go to the level-synchronous kernel
+      cudaMemsetAsync(d.fb, 0, sizeof(int32_t), st);
+      draft_ane_kernel<<<nb, 32, ane_smem_bytes(), st>>>(d.desc, d.root, k, *out, d.fb);
+      draft_ls_kernel<<<nb, 32, ls_smem_bytes(k.P, k.S), st>>>(d.desc, d.root, k, lo, d.cursor,
+                                                               (uint64_t)(hi - lo), d.err, *out, cyc,
+                                                               d.fb + 1 - k.b0, d.fb);
+      return;
+    }
     draft_ls_kernel<<<nb, 32, ls_smem_bytes(k.P, k.S), st>>>(d.desc, d.root, k, lo, d.cursor, (uint64_t)(hi - lo),
                                                              d.err, *out, cyc, order);
   }
@@ -806,5 +831,6 @@ int sssd_propose_phase(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg*
 // Measurement aid: when set (device pointer, [B] int64), the fusion kernel
 // records clock64 cycles per request; NULL disables.
 void sssd_set_cycle_probe(long long* cycles) { g_cycles = cycles; }
+void sssd_set_fusion_form(int form) { g_fusion_form = form < 0 ? -1 : (form > 0 ? 1 : 0); }
 
 }  // extern "C"

@@ -405,9 +405,10 @@ __device__ SSSD_LS_CALL uint2 ls_generate(const LsPar par, int np, uint32_t E, L
 __global__ void __launch_bounds__(32, SSSD_LS_MINB)
     draft_ls_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, uint8_t* pool,
                     unsigned long long* cursor, uint64_t pool_bytes, int32_t* err, sssd_draft_out out,
-                    long long* cycles, const int32_t* order) {
+                    long long* cycles, const int32_t* order, const int32_t* order_count) {
   extern __shared__ __align__(16) uint8_t smem[];
   const long long t_start = clock64();
+  if (order_count && (int)blockIdx.x >= *order_count) return;  // a list filled on the device
   const int b = order ? order[c.b0 + blockIdx.x] : c.b0 + blockIdx.x;
   const int lane = lane_id();
   const uint32_t lt = lanemask_lt();

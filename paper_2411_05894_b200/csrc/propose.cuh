@@ -111,7 +111,19 @@ constexpr int kLsParCap = 64;
 int ls_smem_bytes(int P, int S);
 __global__ void draft_ls_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, uint8_t* pool,
                                 unsigned long long* cursor, uint64_t pool_bytes, int32_t* err,
-                                sssd_draft_out out, long long* cycles, const int32_t* order);
+                                sssd_draft_out out, long long* cycles, const int32_t* order,
+                                const int32_t* order_count = nullptr);
+
+// all-nodes fusion (fusion_ane.cu): every live source node of a request in
+// shared memory, threshold + sort instead of level-by-level expansion; the
+// requests that outgrow these tables go to draft_ls_kernel through fb
+// (fb[0] = count, fb[1..] = requests)
+constexpr int kAneNodes = 2048;
+constexpr int kAneElems = 1024;
+constexpr int kAneCands = 256;
+int ane_smem_bytes();
+__global__ void draft_ane_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, sssd_draft_out out,
+                                 int32_t* fb);
 
 constexpr int kChildBytes = 32;
 constexpr int kGroupBytes = 16;  // cold group record
