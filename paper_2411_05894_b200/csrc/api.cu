@@ -201,34 +201,42 @@ static PropWs carve_propose(uint8_t* base, const sssd_cfg* c, int B, int max_len
 __global__ void propose_setup_kernel(sssd_seqs seqs, KCfg c, Cols dsc, const int32_t* ds_n,
                                      Cols inc, const int32_t* in_n, SrcDesc* desc, uint32_t* root,
                                      uint8_t* bucket, int32_t* hist) {
+  __shared__ int sh[64];  // block histogram of LPT buckets (one global atomic per bucket and block)
+  if (bucket && threadIdx.x < 64) sh[threadIdx.x] = 0;
+  if (bucket) __syncthreads();
   const int b = c.b0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= c.b1) return;
-  const int L = seqs.seq_len[b];
-  root[b] = seqs.seq[seqs.seq_off[b] + L - 1];
-  SrcDesc* d = desc + (size_t)b * (c.P + 1);
-  d[0].meta = dsc.meta + (size_t)b * dsc.stride;
-  d[0].orig = dsc.orig + (size_t)b * dsc.stride;
-  d[0].tok = dsc.tok + (size_t)b * dsc.stride * c.BL;
-  d[0].stride = dsc.stride;
-  d[0].n = c.use_ds ? ds_n[b] : 0;
-  d[0].thr = 0;
-  d[0].depth = c.BL;
-  d[0].pad = 0;
-  for (int rk = 1; rk <= c.P; ++rk) {
-    const int p = c.P - rk + 1;
-    d[rk].meta = inc.meta + (size_t)b * inc.stride;
-    d[rk].orig = inc.orig + (size_t)b * inc.stride;
-    d[rk].tok = inc.tok + (size_t)b * inc.stride * c.IBL;
-    d[rk].stride = inc.stride;
-    d[rk].n = (c.use_in && p <= c.n_trees) ? in_n[b] : 0;
-    d[rk].thr = p;
-    d[rk].depth = c.IBL;
-    d[rk].pad = 0;
+  if (b < c.b1) {
+    const int L = seqs.seq_len[b];
+    root[b] = seqs.seq[seqs.seq_off[b] + L - 1];
+    SrcDesc* d = desc + (size_t)b * (c.P + 1);
+    d[0].meta = dsc.meta + (size_t)b * dsc.stride;
+    d[0].orig = dsc.orig + (size_t)b * dsc.stride;
+    d[0].tok = dsc.tok + (size_t)b * dsc.stride * c.BL;
+    d[0].stride = dsc.stride;
+    d[0].n = c.use_ds ? ds_n[b] : 0;
+    d[0].thr = 0;
+    d[0].depth = c.BL;
+    d[0].pad = 0;
+    for (int rk = 1; rk <= c.P; ++rk) {
+      const int p = c.P - rk + 1;
+      d[rk].meta = inc.meta + (size_t)b * inc.stride;
+      d[rk].orig = inc.orig + (size_t)b * inc.stride;
+      d[rk].tok = inc.tok + (size_t)b * inc.stride * c.IBL;
+      d[rk].stride = inc.stride;
+      d[rk].n = (c.use_in && p <= c.n_trees) ? in_n[b] : 0;
+      d[rk].thr = p;
+      d[rk].depth = c.IBL;
+      d[rk].pad = 0;
+    }
+    if (bucket) {
+      const int k = lpt_bucket(d, c.P);
+      bucket[b] = (uint8_t)k;
+      atomicAdd(&sh[k], 1);
+    }
   }
   if (bucket) {
-    const int k = lpt_bucket(d, c.P);
-    bucket[b] = (uint8_t)k;
-    atomicAdd(&hist[k], 1);
+    __syncthreads();
+    if (threadIdx.x < 64 && sh[threadIdx.x]) atomicAdd(&hist[threadIdx.x], sh[threadIdx.x]);
   }
 }
 

@@ -586,17 +586,23 @@ __global__ void __launch_bounds__(32, SSSD_DRAFT_MINB)
 // output is indexed by request.
 __global__ void lpt_scatter_kernel(const uint8_t* bucket, const int32_t* hist, int32_t* fill, int b0, int b1,
                                    int32_t* order) {
-  __shared__ int start[64];
+  // requests [b0, b1) -> order[b0 ..] by bucket; positions inside a bucket are
+  // reserved per block (one global atomic per bucket and block)
+  __shared__ int start[64], cnt[64], base[64];
   if (threadIdx.x < 64) {
     int acc = 0;
     for (int i = 0; i < (int)threadIdx.x; ++i) acc += hist[i];
     start[threadIdx.x] = acc;
+    cnt[threadIdx.x] = 0;
   }
   __syncthreads();
-  const int b = b0 + blockIdx.x * blockDim.x + threadIdx.x;  // requests [b0, b1): order[b0 ..]
-  if (b >= b1) return;
-  const int k = bucket[b];
-  order[b0 + start[k] + atomicAdd(&fill[k], 1)] = b;
+  const int b = b0 + blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = b < b1 ? bucket[b] : 0;
+  const int local = b < b1 ? atomicAdd(&cnt[k], 1) : 0;
+  __syncthreads();
+  if (threadIdx.x < 64 && cnt[threadIdx.x]) base[threadIdx.x] = atomicAdd(&fill[threadIdx.x], cnt[threadIdx.x]);
+  __syncthreads();
+  if (b < b1) order[b0 + start[k] + base[k] + local] = b;
 }
 
 }  // namespace sssd
