@@ -838,6 +838,9 @@ int sssd_propose_phase(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg*
 
 // Measurement aid: when set (device pointer, [B] int64), the fusion kernel
 // records clock64 cycles per request; NULL disables.
+#ifdef SSSD_LK_PROBE
+void sssd_set_lookup_probe(long long* cycles) { sssd::lk_probe_set(cycles); }
+#endif
 void sssd_set_cycle_probe(long long* cycles) { g_cycles = cycles; }
 void sssd_set_fusion_form(int form) { g_fusion_form = form < 0 ? -1 : (form > 0 ? 1 : 0); }
 

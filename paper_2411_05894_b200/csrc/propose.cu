@@ -524,6 +524,14 @@ constexpr int kLkStage = SSSD_LK_STAGE;  // staged suffix rows per warp and roun
 #ifndef SSSD_LKW_MINB
 #define SSSD_LKW_MINB 1
 #endif
+#ifdef SSSD_LK_PROBE  // per-phase cycle stamps of the lookup warp (measurement builds only)
+__device__ long long* g_lk_cyc;
+void lk_probe_set(long long* p) { cudaMemcpyToSymbol(g_lk_cyc, &p, sizeof(p)); }
+#define LK_STAMP(i) \
+  if (g_lk_cyc && lane == 0) g_lk_cyc[(size_t)b * 8 + (i)] = clock64() - lk_t0;
+#else
+#define LK_STAMP(i)
+#endif
 __global__ void __launch_bounds__(32 * kLkWarps, SSSD_LKW_MINB)
     ds_lookup_warp_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, uint32_t* ds_tab, uint8_t* ds_len,
                           sssd_elem* ds_el, int32_t* ds_n, sssd_lookup_out lk, Cols cols) {
@@ -534,6 +542,9 @@ __global__ void __launch_bounds__(32 * kLkWarps, SSSD_LKW_MINB)
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int b = c.b0 + blockIdx.x * kLkWarps + warp;
   if (b >= c.b1) return;  // (warp-uniform)
+#ifdef SSSD_LK_PROBE
+  const long long lk_t0 = clock64();
+#endif
   const int L = seqs.seq_len[b];
   const uint32_t* seq = seqs.seq + seqs.seq_off[b];
   const int pmax = min(c.P, L);
@@ -652,6 +663,7 @@ __global__ void __launch_bounds__(32 * kLkWarps, SSSD_LKW_MINB)
     }
   }
   __syncwarp();
+  LK_STAMP(0)
   if (lk.ranges && lane < c.P) {
     const bool ok = lane < pmax;
     lk.ranges[((size_t)b * c.P + lane) * 2] = ok ? (int64_t)(s_rlo[warp][lane] + ds.rank_base) : -1;
@@ -735,6 +747,7 @@ __global__ void __launch_bounds__(32 * kLkWarps, SSSD_LKW_MINB)
     next = blo - 1;
   }
   if (pmax == 0) pcut = 1;
+  LK_STAMP(1)
 
   // merge the included runs (each sorted: SA order = order of the cut
   // continuations without a separator): rank = index + binary-searched counts
@@ -776,6 +789,7 @@ __global__ void __launch_bounds__(32 * kLkWarps, SSSD_LKW_MINB)
     before += cnt;
   }
   int n_out = n_all;
+  LK_STAMP(2)
   if (dedupe) {
     __syncwarp();  // the sorted elements above are this warp's own global writes
     int* gst = reinterpret_cast<int*>(stage);
@@ -808,6 +822,14 @@ __global__ void __launch_bounds__(32 * kLkWarps, SSSD_LKW_MINB)
     __syncwarp();  // (too many continuations to fold here: weight 1 each)
     for (int r = lane; r < n_all; r += 32) write_cols(cb, r, ds_el[(size_t)b * c.P * c.M + r], tab);
   }
+  LK_STAMP(3)
+#ifdef SSSD_LK_PROBE
+  if (g_lk_cyc && lane == 0) {
+    g_lk_cyc[(size_t)b * 8 + 4] = n_all;
+    g_lk_cyc[(size_t)b * 8 + 5] = pmax - pcut + 1;
+    g_lk_cyc[(size_t)b * 8 + 6] = n_out;
+  }
+#endif
   if (lane == 0) {
     ds_n[b] = n_out;
     if (lk.p_cut) lk.p_cut[b] = pmax > 0 ? pcut : 0;

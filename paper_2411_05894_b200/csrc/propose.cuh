@@ -32,6 +32,9 @@ __device__ __forceinline__ void write_node_extra(const sssd_draft_out& out, cons
 }
 
 struct Child;
+#ifdef SSSD_LK_PROBE
+void lk_probe_set(long long* p);  // measurement builds: per-phase cycles of ds_lookup_warp_kernel
+#endif
 
 __global__ void find_ranges_kernel(sssd_ds ds, const uint32_t* pat, const int64_t* pat_off,
                                    const int32_t* pat_len, int32_t B, int64_t* lo_hi);
