@@ -275,6 +275,9 @@ static int fusion_smem_attr(const KCfg& k) {
   if (int rc = cuda_check(cudaFuncSetAttribute(draft_ane_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                ane_smem_bytes()), "draft_ane_kernel smem attribute"))
     return rc;
+  if (int rc = cuda_check(cudaFuncSetAttribute(draft_ls_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               ls_smem_bytes(k.P, k.S)), "draft_ls_small_kernel smem attribute"))
+    return rc;
   return cuda_check(cudaFuncSetAttribute(draft_ls_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          ls_smem_bytes(k.P, k.S)), "draft_ls_kernel smem attribute");
 }
@@ -288,6 +291,13 @@ static int g_fusion_form = [] {
 static bool ane_enabled(int nb) {
   if (g_fusion_form >= 0) return g_fusion_form == 1;
   return false;
+}
+
+// Launches of at most this many requests use draft_ls_small_kernel (few warps
+// per SM: load latency, not issue slots, bounds them); SSSD_LS_SMALL overrides.
+static int ls_small_max() {
+  static const int v = getenv("SSSD_LS_SMALL") ? atoi(getenv("SSSD_LS_SMALL")) : 1024;
+  return v;
 }
 
 // One fusion + flatten launch over requests [k.b0, k.b0 + nb) (or order[] of them).
@@ -311,8 +321,12 @@ static void launch_fusion(const DraftWs& d, const KCfg& k, int nb, const sssd_dr
                                                                d.fb + 1 - k.b0, d.fb);
       return;
     }
-    draft_ls_kernel<<<nb, 32, ls_smem_bytes(k.P, k.S), st>>>(d.desc, d.root, k, lo, d.cursor, (uint64_t)(hi - lo),
-                                                             d.err, *out, cyc, order);
+    if (nb <= ls_small_max())
+      draft_ls_small_kernel<<<nb, 32, ls_smem_bytes(k.P, k.S), st>>>(d.desc, d.root, k, lo, d.cursor,
+                                                                     (uint64_t)(hi - lo), d.err, *out, cyc, order);
+    else
+      draft_ls_kernel<<<nb, 32, ls_smem_bytes(k.P, k.S), st>>>(d.desc, d.root, k, lo, d.cursor,
+                                                               (uint64_t)(hi - lo), d.err, *out, cyc, order);
   }
 }
 

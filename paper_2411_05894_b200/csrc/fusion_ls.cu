@@ -247,6 +247,7 @@ __device__ SSSD_LS_CALL uint32_t ls_cut(LsLevel L, uint32_t nb, uint32_t keepn, 
 // above the cut key are discarded: L always holds a prefix of the level's
 // (k0, k1) order, which is all the level needs whenever that prefix holds
 // dec_len - 1 distinct paths (the caller checks and otherwise regenerates).
+template <bool kPF>
 __device__ SSSD_LS_CALL uint2 ls_generate(const LsPar par, int np, uint32_t E, LsLevel L, uint32_t cap,
                                           uint32_t keepn, const SrcDesc* sd, const double* disc,
                                           int disc_stride, int d, bool has_empty, bool has_tau, uint64_t tau0,
@@ -322,13 +323,15 @@ __device__ SSSD_LS_CALL uint2 ls_generate(const LsPar par, int np, uint32_t E, L
   // element, so the chunk's parent starts form a 32-bit head mask (one OR
   // reduction) and an element's parent is the carried parent plus the heads
   // at or before it; a level with empty (depth-capped) parents binary-searches.
-  int jprev = -1;  // parent of element base - 1
-  for (uint32_t base = 0; base < E; base += 31) {
+  // one chunk's parents and element loads (kPF: issued one chunk ahead, so a
+  // lone warp overlaps the global-load latency with the previous chunk's work)
+  struct Ld {
+    int j;
+    uint32_t i, lm, tk, og, th;
+  };
+  auto load_chunk = [&](uint32_t base, int jprev) {
+    Ld r{0, 0, 0, 0, 0xffffffffu, 0};
     const uint32_t x = base + lane;
-    const bool last = base + 32 >= E;  // no look-ahead: lane 31 (if any) is the final element
-    const bool owned = x < E && (lane < 31 || last);
-    int j = 0;
-    uint32_t i = 0, lm = 0, tk = 0, og = 0xffffffffu, th = 0;
     if (!has_empty) {
       const int q = jprev + 1 + lane;
       uint32_t bit = 0;
@@ -337,18 +340,29 @@ __device__ SSSD_LS_CALL uint2 ls_generate(const LsPar par, int np, uint32_t E, L
         if (st < 32) bit = 1u << st;
       }
       const uint32_t heads = __reduce_or_sync(SSSD_FULL, bit);
-      j = jprev + __popc(heads & (0xffffffffu >> (31 - lane)));
+      r.j = jprev + __popc(heads & (0xffffffffu >> (31 - lane)));
     }
     if (x < E) {
-      if (has_empty) j = parent_of(x);
-      const SrcDesc& sc = sd[par.tbr()[j] >> kTbBits];
-      i = par.a()[j] + (x - par.off()[j]);
-      th = (uint32_t)sc.thr;
-      lm = sc.meta[i];  // independent loads; column d-1 exists (d <= source depth)
-      tk = sc.tok[(int64_t)(d - 1) * sc.stride + i];
-      og = sc.orig[i];
+      if (has_empty) r.j = parent_of(x);
+      const SrcDesc& sc = sd[par.tbr()[r.j] >> kTbBits];
+      r.i = par.a()[r.j] + (x - par.off()[r.j]);
+      r.th = (uint32_t)sc.thr;
+      r.lm = sc.meta[r.i];  // independent loads; column d-1 exists (d <= source depth)
+      r.tk = sc.tok[(int64_t)(d - 1) * sc.stride + r.i];
+      r.og = sc.orig[r.i];
     }
-    jprev = __shfl_sync(SSSD_FULL, j, 30);
+    return r;
+  };
+  Ld cur = load_chunk(0, -1);
+  for (uint32_t base = 0; base < E; base += 31) {
+    const uint32_t x = base + lane;
+    const bool last = base + 32 >= E;  // no look-ahead: lane 31 (if any) is the final element
+    const bool owned = x < E && (lane < 31 || last);
+    const int jprev = __shfl_sync(SSSD_FULL, cur.j, 30);  // parent of the next chunk's element base + 30
+    Ld nxt{};
+    if (kPF && !last) nxt = load_chunk(base + 31, jprev);
+    const int j = cur.j;
+    const uint32_t i = cur.i, lm = cur.lm, tk = cur.tk, og = cur.og, th = cur.th;
     const bool has = x < E && el_len(lm) >= (uint32_t)d;
     const bool w = owned && has && el_m(lm) >= th;
     const uint32_t orig = w ? og : 0xffffffffu;
@@ -388,6 +402,7 @@ __device__ SSSD_LS_CALL uint2 ls_generate(const LsPar par, int np, uint32_t E, L
       }
     }
     if (last) break;
+    cur = kPF ? nxt : load_chunk(base + 31, jprev);
   }
   __syncwarp();
   return make_uint2(nb, n);
@@ -402,10 +417,11 @@ __device__ SSSD_LS_CALL uint2 ls_generate(const LsPar par, int np, uint32_t E, L
 #define LS_PROBE(...)
 #endif
 
-__global__ void __launch_bounds__(32, SSSD_LS_MINB)
-    draft_ls_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, uint8_t* pool,
-                    unsigned long long* cursor, uint64_t pool_bytes, int32_t* err, sssd_draft_out out,
-                    long long* cycles, const int32_t* order, const int32_t* order_count) {
+template <bool kPF>
+__device__ __forceinline__ void draft_ls_body(const SrcDesc* desc, const uint32_t* root_tok, const KCfg& c,
+                                              uint8_t* pool, unsigned long long* cursor, uint64_t pool_bytes,
+                                              int32_t* err, const sssd_draft_out& out, long long* cycles,
+                                              const int32_t* order, const int32_t* order_count) {
   extern __shared__ __align__(16) uint8_t smem[];
   const long long t_start = clock64();
   if (order_count && (int)blockIdx.x >= *order_count) return;  // a list filled on the device
@@ -504,7 +520,7 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
     const bool has_tau = t == K;
     const uint64_t tau0 = has_tau ? T.g0()[K - 1] : 0ull;
     const uint32_t tau_dr = has_tau ? T.g1()[K - 1] & ~kTbMask : 0u;
-    const uint2 gr = ls_generate(par, np, E, Ls, kLsCap, keepn, sd, c.disc, c.disc_stride, d, has_empty, has_tau, tau0,
+    const uint2 gr = ls_generate<kPF>(par, np, E, Ls, kLsCap, keepn, sd, c.disc, c.disc_stride, d, has_empty, has_tau, tau0,
                                  tau_dr);
     LS_PROBE(ph_gen += (uint32_t)clock() - tp; tp = (uint32_t)clock());
     uint32_t n = gr.x, n_all = gr.y;
@@ -527,7 +543,7 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
           ++gallocs;
         }
         L = level_carve(glev, glev_cap);
-        n = ls_generate(par, np, E, L, glev_cap, 0u, sd, c.disc, c.disc_stride, d, has_empty, has_tau, tau0,
+        n = ls_generate<kPF>(par, np, E, L, glev_cap, 0u, sd, c.disc, c.disc_stride, d, has_empty, has_tau, tau0,
                         tau_dr).x;
       }
       if (n > kTbMask) {  // class positions must fit their field
@@ -883,6 +899,22 @@ __global__ void __launch_bounds__(32, SSSD_LS_MINB)
       st[7] = gallocs;
     }
   }
+}
+
+__global__ void __launch_bounds__(32, SSSD_LS_MINB)
+    draft_ls_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, uint8_t* pool,
+                    unsigned long long* cursor, uint64_t pool_bytes, int32_t* err, sssd_draft_out out,
+                    long long* cycles, const int32_t* order, const int32_t* order_count) {
+  draft_ls_body<false>(desc, root_tok, c, pool, cursor, pool_bytes, err, out, cycles, order, order_count);
+}
+
+// Small launches (a warp alone on its SM sub-partition: latency, not issue
+// slots, bounds it): element loads one chunk ahead, no register cap.
+__global__ void __launch_bounds__(32, 1)
+    draft_ls_small_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, uint8_t* pool,
+                          unsigned long long* cursor, uint64_t pool_bytes, int32_t* err, sssd_draft_out out,
+                          long long* cycles, const int32_t* order, const int32_t* order_count) {
+  draft_ls_body<true>(desc, root_tok, c, pool, cursor, pool_bytes, err, out, cycles, order, order_count);
 }
 
 }  // namespace sssd

@@ -116,6 +116,11 @@ __global__ void draft_ls_kernel(const SrcDesc* desc, const uint32_t* root_tok, K
                                 unsigned long long* cursor, uint64_t pool_bytes, int32_t* err,
                                 sssd_draft_out out, long long* cycles, const int32_t* order,
                                 const int32_t* order_count = nullptr);
+// the same kernel for small launches: element loads issued one chunk ahead
+__global__ void draft_ls_small_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, uint8_t* pool,
+                                      unsigned long long* cursor, uint64_t pool_bytes, int32_t* err,
+                                      sssd_draft_out out, long long* cycles, const int32_t* order,
+                                      const int32_t* order_count = nullptr);
 
 // all-nodes fusion (fusion_ane.cu): every live source node of a request in
 // shared memory, threshold + sort instead of level-by-level expansion; the
