@@ -314,10 +314,12 @@ int sssd_propose_pre(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* c
 void sssd_set_cycle_probe(long long* cycles);
 
 /* Fusion form of the level-synchronous path (cfg fusion = 0): -1 = automatic
- * (by launch size), 0 = level-synchronous only, 1 = all-nodes kernel first
- * (requests outgrowing its shared-memory tables fall back to the
- * level-synchronous kernel).  Identical drafts either way; a process-wide
- * tuning switch, initialised from SSSD_FUSION_ANE. */
+ * (one CTA per request for launches of <= SSSD_CTA_MAX requests, default 512;
+ * one warp per request above), 0 = one warp per request only, 1 = all-nodes
+ * kernel first (requests outgrowing its shared-memory tables fall back to the
+ * level-synchronous kernel), 2 = one CTA per request for every launch.
+ * Identical drafts in every form; a process-wide tuning switch, initialised
+ * from SSSD_FUSION_FORM. */
 void sssd_set_fusion_form(int form);
 
 /* Fusion of caller-provided source trees (merge fusion.py:209-261 + flatten).

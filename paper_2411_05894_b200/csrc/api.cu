@@ -278,20 +278,24 @@ static int fusion_smem_attr(const KCfg& k) {
   if (int rc = cuda_check(cudaFuncSetAttribute(draft_ls_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                ls_smem_bytes(k.P, k.S)), "draft_ls_small_kernel smem attribute"))
     return rc;
+  if (int rc = cuda_check(cudaFuncSetAttribute(draft_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               cta_smem_bytes(k.P, k.S)), "draft_cta_kernel smem attribute"))
+    return rc;
   return cuda_check(cudaFuncSetAttribute(draft_ls_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          ls_smem_bytes(k.P, k.S)), "draft_ls_kernel smem attribute");
 }
 
-// All-nodes fusion (fusion_ane.cu) for launches of at most this many
-// requests; SSSD_FUSION_ANE=0/1 forces it off/on (A/B switch).
+// Fusion form switch (A/B and cross-checks; identical drafts in every form):
+// -1 = automatic (CTA-per-request form for launches of <= cta_max() requests,
+// one warp per request above), 0 = one warp per request only, 1 = all-nodes
+// kernel first (fusion_ane.cu), 2 = CTA-per-request form for every launch.
+// SSSD_FUSION_FORM (or the older SSSD_FUSION_ANE=0/1) sets the start value.
 static int g_fusion_form = [] {
-  const char* e = getenv("SSSD_FUSION_ANE");
-  return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
+  const char* e = getenv("SSSD_FUSION_FORM");
+  if (!e) e = getenv("SSSD_FUSION_ANE");
+  return e && e[0] >= '0' && e[0] <= '2' ? e[0] - '0' : -1;
 }();
-static bool ane_enabled(int nb) {
-  if (g_fusion_form >= 0) return g_fusion_form == 1;
-  return false;
-}
+static bool ane_enabled(int) { return g_fusion_form == 1; }
 
 // Launches of at most this many requests use draft_ls_small_kernel (few warps
 // per SM: load latency, not issue slots, bounds them); SSSD_LS_SMALL overrides.
@@ -299,6 +303,15 @@ static int ls_small_max() {
   static const int v = getenv("SSSD_LS_SMALL") ? atoi(getenv("SSSD_LS_SMALL")) : 1024;
   return v;
 }
+
+// Launches of at most this many requests use draft_cta_kernel (one CTA of
+// cta_threads() per request: the latency of a small batch is its slowest
+// request's dependency chain, which the CTA form shortens).
+static int cta_max() {
+  static const int v = getenv("SSSD_CTA_MAX") ? atoi(getenv("SSSD_CTA_MAX")) : 512;
+  return v;
+}
+static bool cta_enabled(int nb) { return g_fusion_form == 2 || (g_fusion_form < 0 && nb <= cta_max()); }
 
 // One fusion + flatten launch over requests [k.b0, k.b0 + nb) (or order[] of them).
 static void launch_fusion(const DraftWs& d, const KCfg& k, int nb, const sssd_draft_out* out,
@@ -321,7 +334,11 @@ static void launch_fusion(const DraftWs& d, const KCfg& k, int nb, const sssd_dr
                                                                d.fb + 1 - k.b0, d.fb);
       return;
     }
-    if (nb <= ls_small_max())
+    if (cta_enabled(nb))
+      draft_cta_kernel<<<nb, cta_threads(), cta_smem_bytes(k.P, k.S), st>>>(d.desc, d.root, k, lo, d.cursor,
+                                                                           (uint64_t)(hi - lo), d.err, *out, cyc,
+                                                                           order);
+    else if (nb <= ls_small_max())
       draft_ls_small_kernel<<<nb, 32, ls_smem_bytes(k.P, k.S), st>>>(d.desc, d.root, k, lo, d.cursor,
                                                                      (uint64_t)(hi - lo), d.err, *out, cyc, order);
     else
@@ -856,6 +873,6 @@ int sssd_propose_phase(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg*
 void sssd_set_lookup_probe(long long* cycles) { sssd::lk_probe_set(cycles); }
 #endif
 void sssd_set_cycle_probe(long long* cycles) { g_cycles = cycles; }
-void sssd_set_fusion_form(int form) { g_fusion_form = form < 0 ? -1 : (form > 0 ? 1 : 0); }
+void sssd_set_fusion_form(int form) { g_fusion_form = form < 0 ? -1 : (form > 2 ? 2 : form); }
 
 }  // extern "C"

@@ -122,6 +122,14 @@ __global__ void draft_ls_small_kernel(const SrcDesc* desc, const uint32_t* root_
                                       sssd_draft_out out, long long* cycles, const int32_t* order,
                                       const int32_t* order_count = nullptr);
 
+// CTA-per-request form (fusion_cta.cu): the same level-synchronous fusion with
+// a level's generation and sort spread over the warps of one CTA (small launches)
+int cta_smem_bytes(int P, int S);
+int cta_threads();
+__global__ void draft_cta_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, uint8_t* pool,
+                                 unsigned long long* cursor, uint64_t pool_bytes, int32_t* err, sssd_draft_out out,
+                                 long long* cycles, const int32_t* order);
+
 // all-nodes fusion (fusion_ane.cu): every live source node of a request in
 // shared memory, threshold + sort instead of level-by-level expansion; the
 // requests that outgrow these tables go to draft_ls_kernel through fb

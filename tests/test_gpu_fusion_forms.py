@@ -1,5 +1,7 @@
 """The all-nodes fusion kernel (csrc/fusion_ane.cu, sssd_set_fusion_form(1))
-against the level-synchronous default: identical drafts -- tokens, parents,
+and the CTA-per-request kernel (csrc/fusion_cta.cu, form 2, the default for
+small launches) against the one-warp level-synchronous kernel (form 0):
+identical drafts -- tokens, parents,
 depths, masks, per-node priority / source / position -- over the cfg2 shape,
 a prompt-heavy 32k context (its requests outgrow the shared-memory tables and
 take the fallback), tie-heavy tiny alphabets, and the reference's golden
@@ -48,9 +50,11 @@ def _equal(a, b):
             assert torch.equal(x, y), k
 
 
+@pytest.mark.parametrize("other", [1, 2])
 @pytest.mark.parametrize("dec_len,ctx,n_req,alpha", [(64, 2048, 2048, 0.8), (16, 32768, 8, 0.8),
-                                                     (100, 1024, 512, 0.0), (256, 512, 256, 1.0)])
-def test_all_nodes_fusion_equals_level_synchronous(form, dec_len, ctx, n_req, alpha):
+                                                     (100, 1024, 512, 0.0), (256, 512, 256, 1.0),
+                                                     (64, 2048, 64, 0.8), (16, 32768, 64, 0.5)])
+def test_fusion_forms_equal_level_synchronous(form, other, dec_len, ctx, n_req, alpha):
     ds = G.build(workload.corpus(1_000_000, 32000), vocab_size=32000)
     eng = G.DraftEngine(ds, G.FusionConfig(dec_len=dec_len, alpha=alpha))
     ctxs = workload.prompt_heavy_contexts(n_req, ctx, 32000) if ctx > 4096 else workload.contexts(n_req, ctx, 32000)
@@ -60,12 +64,13 @@ def test_all_nodes_fusion_equals_level_synchronous(form, dec_len, ctx, n_req, al
     ln = torch.full((n_req,), ctx, dtype=torch.int32, device="cuda")
     form(0)
     a = _batch(eng, seq, off, ln, ctx)
-    form(1)
+    form(other)
     b = _batch(eng, seq, off, ln, ctx)
     _equal(a, b)
 
 
-def test_all_nodes_fusion_small_alphabets(form):
+@pytest.mark.parametrize("other", [1, 2])
+def test_fusion_forms_small_alphabets(form, other):
     rng = np.random.default_rng(9)
     for trial in range(4):
         V = int(rng.choice([2, 3, 5]))
@@ -77,14 +82,15 @@ def test_all_nodes_fusion_small_alphabets(form):
         ctxs = [rng.integers(0, V, int(rng.integers(1, 4000))).tolist() for _ in range(64)]
         form(0)
         fa = eng.propose_host(ctxs)
-        form(1)
+        form(other)
         fb = eng.propose_host(ctxs)
         for x, y in zip(fa, fb):
             assert (x.tokens, x.parents, x.depths) == (y.tokens, y.parents, y.depths), trial
 
 
-def test_all_nodes_fusion_golden_merges(form, golden):
-    form(1)
+@pytest.mark.parametrize("other", [1, 2])
+def test_fusion_forms_golden_merges(form, golden, other):
+    form(other)
     by_cfg: dict = {}
     for case in golden("merge.json"):
         by_cfg.setdefault(tuple(sorted(case["cfg"].items())), []).append(case)
