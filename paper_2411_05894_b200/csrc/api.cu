@@ -209,25 +209,8 @@ __global__ void propose_setup_kernel(sssd_seqs seqs, KCfg c, Cols dsc, const int
     const int L = seqs.seq_len[b];
     root[b] = seqs.seq[seqs.seq_off[b] + L - 1];
     SrcDesc* d = desc + (size_t)b * (c.P + 1);
-    d[0].meta = dsc.meta + (size_t)b * dsc.stride;
-    d[0].orig = dsc.orig + (size_t)b * dsc.stride;
-    d[0].tok = dsc.tok + (size_t)b * dsc.stride * c.BL;
-    d[0].stride = dsc.stride;
-    d[0].n = c.use_ds ? ds_n[b] : 0;
-    d[0].thr = 0;
-    d[0].depth = c.BL;
-    d[0].pad = 0;
-    for (int rk = 1; rk <= c.P; ++rk) {
-      const int p = c.P - rk + 1;
-      d[rk].meta = inc.meta + (size_t)b * inc.stride;
-      d[rk].orig = inc.orig + (size_t)b * inc.stride;
-      d[rk].tok = inc.tok + (size_t)b * inc.stride * c.IBL;
-      d[rk].stride = inc.stride;
-      d[rk].n = (c.use_in && p <= c.n_trees) ? in_n[b] : 0;
-      d[rk].thr = p;
-      d[rk].depth = c.IBL;
-      d[rk].pad = 0;
-    }
+    const SetupSrc u{seqs, dsc, inc, ds_n, in_n};
+    for (int rk = 0; rk <= c.P; ++rk) d[rk] = make_src_desc(u, c, b, rk);
     if (bucket) {
       const int k = lpt_bucket(d, c.P);
       bucket[b] = (uint8_t)k;
@@ -311,11 +294,15 @@ static int cta_max() {
   static const int v = getenv("SSSD_CTA_MAX") ? atoi(getenv("SSSD_CTA_MAX")) : 512;
   return v;
 }
+static bool getenv_cached_no_inline_setup() {  // A/B switch: SSSD_NO_INLINE_SETUP keeps the setup kernel
+  static const bool v = getenv("SSSD_NO_INLINE_SETUP") != nullptr;
+  return v;
+}
 static bool cta_enabled(int nb) { return g_fusion_form == 2 || (g_fusion_form < 0 && nb <= cta_max()); }
 
 // One fusion + flatten launch over requests [k.b0, k.b0 + nb) (or order[] of them).
 static void launch_fusion(const DraftWs& d, const KCfg& k, int nb, const sssd_draft_out* out,
-                          cudaStream_t st, long long* cyc, const int32_t* order) {
+                          cudaStream_t st, long long* cyc, const int32_t* order, const SetupSrc* su = nullptr) {
   if (k.fusion == 1)
     draft_kernel<<<nb, 32, draft_smem_bytes(k.P, k.S), st>>>(d.desc, d.root, k, d.slabs, kSlabChildren, d.pool,
                                                              d.cursor, d.pool_cap, d.err, d.gover, d.gover_bytes,
@@ -337,7 +324,8 @@ static void launch_fusion(const DraftWs& d, const KCfg& k, int nb, const sssd_dr
     if (cta_enabled(nb))
       draft_cta_kernel<<<nb, cta_threads(), cta_smem_bytes(k.P, k.S), st>>>(d.desc, d.root, k, lo, d.cursor,
                                                                            (uint64_t)(hi - lo), d.err, *out, cyc,
-                                                                           order);
+                                                                           order, su ? *su : SetupSrc{},
+                                                                           su != nullptr);
     else if (nb <= ls_small_max())
       draft_ls_small_kernel<<<nb, 32, ls_smem_bytes(k.P, k.S), st>>>(d.desc, d.root, k, lo, d.cursor,
                                                                      (uint64_t)(hi - lo), d.err, *out, cyc, order);
@@ -496,7 +484,8 @@ static void lookup_range(const PropWs& w, const KCfg& k, const sssd_cfg* cfg, co
     ds_lookup_kernel<<<b1 - b0, 32 * cfg->P, 4 * ds_lookup_smem_words(cfg->P, cfg->M), s>>>(
         *ds, *seqs, kk, w.ds_tab, w.ds_len, w.ds_el, w.ds_n, lk, w.ds_raw, w.ds_idx, w.ds_idx_cap, w.ds_cols,
         pre_bounds, pre_rows);
-  if (ds_dedupe_enabled(kk) && (cfg->has_separator || pre_bounds || b1 - b0 < 2048))  // (the warp kernel folds itself)
+  if (ds_dedupe_enabled(kk) && (cfg->has_separator || pre_bounds || b1 - b0 < 2048) &&
+      !ds_dedupe_in_lookup(cfg->P, cfg->M))  // (the warp kernel and, below 4096 samples, ds_lookup_kernel fold themselves)
     ds_dedupe_kernel<<<b1 - b0, 128, 4 * (cfg->P * cfg->M + 1), s>>>(kk, w.ds_tab, w.ds_el, w.ds_n, w.ds_cols);
 }
 
@@ -521,6 +510,13 @@ static void fuse_range(const PropWs& w, const KCfg& k, const sssd_seqs* seqs, co
   kk.seq_len = seqs->seq_len;
   static const bool no_lpt = getenv("SSSD_NO_LPT") != nullptr;  // A/B switch
   const bool lpt = !no_lpt && b1 - b0 >= 2048;                   // order only pays with several waves
+  if (!lpt && kk.fusion == 0 && cta_enabled(b1 - b0) && !getenv_cached_no_inline_setup()) {
+    // the CTA fusion kernel builds its source descriptors itself: one launch
+    // fewer between the lookup / scan join and the fusion (latency path)
+    const SetupSrc su{*seqs, w.ds_cols, w.in_cols, w.ds_n, w.in_n};
+    launch_fusion(w.d, kk, b1 - b0, out, s, g_cycles, nullptr, &su);
+    return;
+  }
   propose_setup_kernel<<<(b1 - b0 + 127) / 128, 128, 0, s>>>(*seqs, kk, w.ds_cols, w.ds_n, w.in_cols, w.in_n,
                                                                w.d.desc, w.d.root, lpt ? w.d.bucket : nullptr,
                                                                w.d.hist);

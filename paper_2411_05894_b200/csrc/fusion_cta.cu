@@ -253,7 +253,7 @@ __device__ __forceinline__ void cta_generate_all(const LsPar par, int np, LsLeve
 __global__ void __launch_bounds__(kCtaThreads, 1)
     draft_cta_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, uint8_t* pool,
                      unsigned long long* cursor, uint64_t pool_bytes, int32_t* err, sssd_draft_out out,
-                     long long* cycles, const int32_t* order) {
+                     long long* cycles, const int32_t* order, SetupSrc su, int use_su) {
   extern __shared__ __align__(16) uint8_t smem[];
   const long long t_start = clock64();
   const int b = order ? order[c.b0 + blockIdx.x] : c.b0 + blockIdx.x;
@@ -280,7 +280,14 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
   sp += 16 * 4;
   CtaShared* sh = reinterpret_cast<CtaShared*>(sp);
 
-  for (int r = tid; r < NR; r += kCtaThreads) sd[r] = desc[(size_t)b * NR + r];
+  __shared__ uint32_t s_root;
+  if (use_su) {
+    for (int r = tid; r < NR; r += kCtaThreads) sd[r] = make_src_desc(su, c, b, r);
+    if (tid == 0) s_root = su.seqs.seq[su.seqs.seq_off[b] + su.seqs.seq_len[b] - 1];
+  } else {
+    for (int r = tid; r < NR; r += kCtaThreads) sd[r] = desc[(size_t)b * NR + r];
+    if (tid == 0) s_root = root_tok[b];
+  }
   if (tid == 0) {
     sh->glev = nullptr;
     sh->gpar = nullptr;
@@ -683,7 +690,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     __syncthreads();
     for (int v = tid; v < size; v += kCtaThreads) {
       const int k = f_pos[v];
-      o_tok[k] = v == 0 ? root_tok[b] : T.tok()[v - 1];
+      o_tok[k] = v == 0 ? s_root : T.tok()[v - 1];
       o_par[k] = v == 0 ? -1 : f_pos[f_par[v]];
       o_dep[k] = f_dep[v];
       if (extra) node_extra(v, k);
@@ -712,7 +719,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
       int v = 0, k = 0;
       while (true) {
         f_pos[v] = k;
-        o_tok[k] = v == 0 ? root_tok[b] : T.tok()[v - 1];
+        o_tok[k] = v == 0 ? s_root : T.tok()[v - 1];
         o_par[k] = v == 0 ? -1 : f_pos[f_par[v]];
         o_dep[k] = f_dep[v];
         if (extra) node_extra(v, k);

@@ -290,6 +290,9 @@ __device__ int gather_p(const sssd_ds& ds, const KCfg& c, int p, uint64_t lo, ui
   return cnt;
 }
 
+__device__ __forceinline__ void dedupe_request(const KCfg& c, int b, int n_all, const uint32_t* ds_tab,
+                                               const sssd_elem* ds_el, int32_t* ds_n, const Cols& cols, int* gstart);
+
 #ifndef SSSD_LOOKUP_MINB
 // 4: up to 128 registers, no spills — this kernel serves small batches (B < 2048: B = 64 lookup
 // stage 0.037 -> 0.033 ms against the former 8 / 32-register cap) and the separator / sharded paths
@@ -450,7 +453,7 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P, SSSD_LOOKUP_MINB)
       }
     }
   }
-  const int n_out = n_all;  // ds_dedupe_kernel folds duplicates and writes the columns when dedupe
+  const int n_out = n_all;  // folded below (or by ds_dedupe_kernel) when dedupe
   if (threadIdx.x == 0) {
     ds_n[b] = n_out;
     if (lk.p_cut) lk.p_cut[b] = pmax > 0 ? pcut : 0;
@@ -459,19 +462,24 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P, SSSD_LOOKUP_MINB)
     const int q = threadIdx.x + 1;
     lk.n_conts[(size_t)b * c.P + threadIdx.x] = (q <= pmax && s_cnt[threadIdx.x] >= 0) ? s_cnt[threadIdx.x] : -1;
   }
+  if (dedupe && ds_dedupe_in_lookup(c.P, c.M)) {
+    // fold in place: the sorted elements are in ds_el (visible to the CTA
+    // after the barrier); the staged rows are dead, their shared memory holds
+    // the group starts (P*M + 1 <= ds_lookup_smem_words)
+    __syncthreads();
+    dedupe_request(c, b, n_all, ds_tab, ds_el, ds_n, cols, reinterpret_cast<int*>(s_rows));
+  }
 }
 
 // Fold datastore elements with identical continuation strings (adjacent in
 // the sorted array) into one element whose column meta carries the group size
 // as its weight (el_wt); the first element of a group has the smallest list
 // position, which the fusion kernel's first-appearance order needs.  One CTA
-// per request: flags in parallel, compaction by warp 0.
-__global__ void __launch_bounds__(128)
-    ds_dedupe_kernel(KCfg c, const uint32_t* ds_tab, const sssd_elem* ds_el, int32_t* ds_n, Cols cols) {
-  extern __shared__ int gstart[];  // [P*M + 1]
-  const int b = c.b0 + blockIdx.x;
+// per request: flags in parallel, compaction by warp 0.  gstart: n_all + 1 ints
+// of shared memory.
+__device__ __forceinline__ void dedupe_request(const KCfg& c, int b, int n_all, const uint32_t* ds_tab,
+                                               const sssd_elem* ds_el, int32_t* ds_n, const Cols& cols, int* gstart) {
   const int lane = lane_id(), warp = threadIdx.x >> 5;
-  const int n_all = ds_n[b];
   if (n_all <= 0) return;
   const sssd_elem* sorted = ds_el + (size_t)b * c.P * c.M;
   const uint32_t* tab = ds_tab + (size_t)b * c.P * c.M * c.BL;
@@ -505,6 +513,13 @@ __global__ void __launch_bounds__(128)
     cb.meta[g] = (e.len_m & 0xffffu) | (uint32_t)(gstart[g + 1] - gstart[g]) << 16;
   }
   if (lane == 0) ds_n[b] = G;
+}
+
+__global__ void __launch_bounds__(128)
+    ds_dedupe_kernel(KCfg c, const uint32_t* ds_tab, const sssd_elem* ds_el, int32_t* ds_n, Cols cols) {
+  extern __shared__ int gstart[];  // [P*M + 1]
+  const int b = c.b0 + blockIdx.x;
+  dedupe_request(c, b, ds_n[b], ds_tab, ds_el, ds_n, cols, gstart);
 }
 
 // --------------------------------------------------------------------------

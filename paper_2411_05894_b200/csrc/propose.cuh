@@ -31,6 +31,40 @@ __device__ __forceinline__ void write_node_extra(const sssd_draft_out& out, cons
   if (out.pos) out.pos[o] = depth < 0 ? -1 : (c.seq_len ? c.seq_len[b] - 1 : 0) + depth;
 }
 
+// Source descriptors of request b (rank 0 = datastore, rank r >= 1 = input
+// tree p = P - r + 1), written by propose_setup_kernel -- or built in place by
+// the CTA fusion kernel for small launches (one launch fewer on the latency
+// path).
+struct SetupSrc {
+  sssd_seqs seqs;
+  Cols dsc, inc;
+  const int32_t* ds_n;
+  const int32_t* in_n;
+};
+__device__ __forceinline__ SrcDesc make_src_desc(const SetupSrc& u, const KCfg& c, int b, int rk) {
+  SrcDesc d;
+  if (rk == 0) {
+    d.meta = u.dsc.meta + (size_t)b * u.dsc.stride;
+    d.orig = u.dsc.orig + (size_t)b * u.dsc.stride;
+    d.tok = u.dsc.tok + (size_t)b * u.dsc.stride * c.BL;
+    d.stride = u.dsc.stride;
+    d.n = c.use_ds ? u.ds_n[b] : 0;
+    d.thr = 0;
+    d.depth = c.BL;
+  } else {
+    const int p = c.P - rk + 1;
+    d.meta = u.inc.meta + (size_t)b * u.inc.stride;
+    d.orig = u.inc.orig + (size_t)b * u.inc.stride;
+    d.tok = u.inc.tok + (size_t)b * u.inc.stride * c.IBL;
+    d.stride = u.inc.stride;
+    d.n = (c.use_in && p <= c.n_trees) ? u.in_n[b] : 0;
+    d.thr = p;
+    d.depth = c.IBL;
+  }
+  d.pad = 0;
+  return d;
+}
+
 struct Child;
 #ifdef SSSD_LK_PROBE
 void lk_probe_set(long long* p);  // measurement builds: per-phase cycles of ds_lookup_warp_kernel
@@ -46,6 +80,7 @@ __global__ void ds_lookup_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, uint32_t* d
                                  const uint32_t* pre_rows);
 // datastore element folding for the level-synchronous fusion (weights <= 65535)
 __host__ __device__ inline bool ds_dedupe_enabled(const KCfg& c) { return c.fusion == 0 && c.P * c.M <= 12000; }
+
 __global__ void ds_dedupe_kernel(KCfg c, const uint32_t* ds_tab, const sssd_elem* ds_el, int32_t* ds_n, Cols cols);
 __global__ void ds_lookup_warp_kernel(sssd_ds ds, sssd_seqs seqs, KCfg c, uint32_t* ds_tab, uint8_t* ds_len,
                                       sssd_elem* ds_el, int32_t* ds_n, sssd_lookup_out lk, Cols cols);
@@ -69,6 +104,9 @@ __host__ __device__ inline int ds_lookup_smem_words(int P, int M) {
   const int rows = P * 32 * kRowStride;
   return rows > (cap < 4096 ? (int)cap : 4096) ? rows : (cap < 4096 ? (int)cap : 4096);
 }
+// ds_lookup_kernel folds in place (its dynamic shared memory holds the group
+// starts) instead of leaving it to a separate ds_dedupe_kernel launch
+__host__ __device__ inline bool ds_dedupe_in_lookup(int P, int M) { return P * M + 1 <= ds_lookup_smem_words(P, M); }
 // input scan launch shape: 1024 threads once a context spans several
 // 2048-position tiles (fewer sequential tiles, wider occurrence sort)
 inline int input_scan_threads(int max_len) { return max_len > 4096 ? 1024 : 256; }
@@ -126,9 +164,11 @@ __global__ void draft_ls_small_kernel(const SrcDesc* desc, const uint32_t* root_
 // a level's generation and sort spread over the warps of one CTA (small launches)
 int cta_smem_bytes(int P, int S);
 int cta_threads();
+// use_su: build the source descriptors and root tokens from su in the kernel
+// (desc / root_tok unused)
 __global__ void draft_cta_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, uint8_t* pool,
                                  unsigned long long* cursor, uint64_t pool_bytes, int32_t* err, sssd_draft_out out,
-                                 long long* cycles, const int32_t* order);
+                                 long long* cycles, const int32_t* order, SetupSrc su, int use_su);
 
 // all-nodes fusion (fusion_ane.cu): every live source node of a request in
 // shared memory, threshold + sort instead of level-by-level expansion; the
