@@ -268,6 +268,18 @@ __global__ void sa_first_keys(const uint32_t* tokens, uint64_t n, uint64_t* key,
   val[i] = (uint32_t)i;
 }
 
+// round 1 with m-gram keys: key[i] = (t[i]+1, .., t[i+m-1]+1) packed tb bits
+// each, 0 past the corpus end (a shorter suffix sorts first, as in the
+// reference's rank[i+k] + 1 / 0 keys, datastore.py:94-95)
+__global__ void sa_mgram_keys(const uint32_t* tokens, uint64_t n, int m, int tb, uint64_t* key, uint32_t* val) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t k = 0;
+  for (int j = 0; j < m; ++j) k = (k << tb) | (i + j < n ? (uint64_t)tokens[i + j] + 1 : 0ull);
+  key[i] = k;
+  val[i] = (uint32_t)i;
+}
+
 // keys of the active elements (slot order): (group head slot, rank[pos + k] + 1
 // or 0 past the end) -- one random gather per element (the head and the
 // position travel with the active list)
@@ -440,9 +452,22 @@ int sa_build2(const uint32_t* tokens, uint64_t n, uint32_t* sa_out, void* worksp
   uint32_t maxtok = 0;
   scan<1, true>(w, tokens, n, nullptr, st);
   if ((rc = read_grand(w, st, &maxtok))) return rc;
-  sa_first_keys<<<grid(n), T, 0, st>>>(tokens, n, w.k0, w.v0);
-  radix_sort(w, n, bits_of(maxtok) > 0 ? bits_of(maxtok) : 1, st);
-  const bool table = w.table && (uint64_t)maxtok < kTableTokens;
+  // Round 1 sorts by the first m tokens at once when m >= 2 of them fit a
+  // 64-bit key (V = 32,000: 15 bits, m = 4): that replaces the reference's
+  // k = 1 and k = 2 doubling rounds (which re-sort 90 % and 75 % of the
+  // phrase corpus with 54-bit keys) by one 60-bit sort; the rounds below
+  // continue at k = m.  Otherwise: by token, ranks from a token table.
+  const int tb = bits_of((uint64_t)maxtok + 1);
+  int m = 1;
+  while (m < 4 && (m * 2) * tb <= 64) m *= 2;  // m in {1, 2, 4}: the doubling schedule stays k = m, 2m, ...
+  const bool table = m == 1 && w.table && (uint64_t)maxtok < kTableTokens;
+  if (m > 1) {
+    sa_mgram_keys<<<grid(n), T, 0, st>>>(tokens, n, m, tb, w.k0, w.v0);
+    radix_sort(w, n, m * tb, st);
+  } else {
+    sa_first_keys<<<grid(n), T, 0, st>>>(tokens, n, w.k0, w.v0);
+    radix_sort(w, n, bits_of(maxtok) > 0 ? bits_of(maxtok) : 1, st);
+  }
   sa_round_heads<<<grid(n), T, 0, st>>>(w.k0, w.v0, n, nullptr, sa_out, w.tmp, table ? w.table : nullptr);
   scan<1, true>(w, w.tmp, n, w.tmp2, st);
   if (table) sa_rank_from_table<<<grid(n), T, 0, st>>>(tokens, n, w.table, w.rank);
@@ -453,8 +478,12 @@ int sa_build2(const uint32_t* tokens, uint64_t n, uint32_t* sa_out, void* worksp
   if ((rc = read_grand(w, st, &A32))) return rc;
   uint64_t A = A32;
   const int rb = bits_of(n);  // heads < n and rank + 1 <= n
+  // rounds reported as the reference's doubling rounds (datastore.py:93-109:
+  // the initial token rank plus one per k = 1, 2, 4, ... up to the last k
+  // this build processed), so the algorithmic-byte count does not depend on m
   int rounds = 1;
-  for (uint64_t k = 1; A > 0; k *= 2) {
+  for (int mm = m; mm > 1; mm >>= 1) ++rounds;
+  for (uint64_t k = (uint64_t)m; A > 0; k *= 2) {
     if (k >= n) return fail(SSSD_E_ARG, "suffix doubling did not converge");
     ++rounds;
     sa_round_keys<<<grid(A), T, 0, st>>>(w.apos, w.agrp, A, w.rank, n, k, rb, w.k0, w.v0);
