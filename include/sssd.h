@@ -78,6 +78,19 @@ int sssd_rows_build(const uint32_t* tokens, uint64_t n, const uint32_t* sa, uint
 int sssd_bucket_build(const uint32_t* rows, uint64_t n_rows, uint32_t n_buckets, uint32_t* bucket,
                       void* stream);
 
+/* k-gram range index over sorted suffix rows (a find_range accelerator,
+ * ref datastore.py:156-183): every k-gram g (2 <= k <= kmax <= 7) that starts
+ * a suffix gets one open-addressing slot {64-bit hash of (k, g), lo, hi} with
+ * [lo, hi) = the local rows whose suffix starts with g.  sssd_kix_count
+ * writes the number of such k-grams to *count (device u64, synchronise
+ * before reading); sssd_kix_build fills a zeroed table of cap = 2^j >=
+ * 2 * count slots (16 B each).  Lookups verify the tokens of row lo, so a
+ * hash collision costs a search, never a wrong range. */
+int sssd_kix_count(const uint32_t* rows, uint64_t n_rows, uint64_t n_tokens, uint32_t kmax, uint64_t* count,
+                   void* stream);
+int sssd_kix_build(const uint32_t* rows, uint64_t n_rows, uint64_t n_tokens, uint32_t kmax, uint32_t* table,
+                   uint64_t cap, void* stream);
+
 /* Widen n uint16 token ids to uint32 (device to device): the compact host
  * format of a propose_pinned batch whose vocabulary fits 16 bits, uploaded at
  * half the PCIe bytes and widened next to the kernels that read it. */
@@ -142,6 +155,13 @@ typedef struct sssd_ds {
                              bucket[t] = first local row whose first token >= t
                              (sssd_bucket_build); narrows every range search */
   uint32_t n_buckets;
+  const uint32_t* kix;    /* optional (NULL = none): k-gram range table (sssd_kix_build),
+                             [kix_mask + 1] slots of 4 u32 {hash lo, hash hi, lo, hi}:
+                             the local row range of every k-gram (2 <= k <= kix_kmax)
+                             that starts a suffix; a pattern of <= kix_kmax tokens
+                             found there needs no search */
+  uint64_t kix_mask;
+  uint32_t kix_kmax;
 } sssd_ds;
 
 /* Sequences: request b's live sequence is seq[seq_off[b] .. seq_off[b]+seq_len[b]). */

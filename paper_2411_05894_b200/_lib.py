@@ -47,7 +47,8 @@ class Elem(C.Structure):
 
 class Ds(C.Structure):
     _fields_ = [("rows", vp), ("tokens", vp), ("n_tokens", C.c_uint64), ("rank_base", C.c_uint64),
-                ("n_rows", C.c_uint64), ("bucket", vp), ("n_buckets", C.c_uint32)]
+                ("n_rows", C.c_uint64), ("bucket", vp), ("n_buckets", C.c_uint32),
+                ("kix", vp), ("kix_mask", C.c_uint64), ("kix_kmax", C.c_uint32)]
 
 
 class Seqs(C.Structure):
@@ -79,6 +80,8 @@ _SIGS = {
     "sssd_sa_check_workspace": (C.c_size_t, [C.c_uint64]),
     "sssd_sa_check": (C.c_int, [vp, C.c_uint64, vp, C.c_uint64, vp, C.c_size_t, vp, vp]),
     "sssd_bucket_build": (C.c_int, [vp, C.c_uint64, C.c_uint32, vp, vp]),
+    "sssd_kix_count": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.c_uint32, vp, vp]),
+    "sssd_kix_build": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.c_uint32, vp, C.c_uint64, vp]),
     "sssd_widen_u16": (C.c_int, [vp, vp, C.c_int64, vp]),
     "sssd_rmsnorm_bf16": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int32, C.c_float, vp]),
     "sssd_rope_kv_bf16": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32,

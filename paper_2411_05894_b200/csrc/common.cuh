@@ -70,4 +70,42 @@ struct SrcDesc {
   int32_t pad;
 };
 
+// k-gram range index (sssd_kix_build): 64-bit hash of (k, t[0..k)), never 0
+// (0 marks an empty slot).
+__host__ __device__ __forceinline__ uint64_t kix_hash(const uint32_t* t, int k) {
+  uint64_t h = 0x9E3779B97F4A7C15ull * (uint64_t)(k + 1);
+  for (int j = 0; j < k; ++j) {
+    h ^= t[j];
+    h *= 0xff51afd7ed558ccdull;
+    h ^= h >> 32;
+  }
+  h ^= h >> 29;
+  h *= 0xc4ceb9fe1a85ec53ull;
+  h ^= h >> 32;
+  return h | 1ull;
+}
+
+// Rows [lo, hi) whose suffix starts with pat[0..k) (2 <= k <= ds.kix_kmax):
+// returns 1 (found, lo / hi set), 0 (no suffix starts with the k-gram: the
+// range is empty, its insertion point unknown) or -1 (the slot of this hash
+// belongs to another k-gram -- a 64-bit collision: search instead).
+__device__ __forceinline__ int kix_find(const sssd_ds& ds, const uint32_t* pat, int k, uint64_t& lo, uint64_t& hi) {
+  const uint64_t h = kix_hash(pat, k);
+  const uint4* tab = reinterpret_cast<const uint4*>(ds.kix);
+  for (uint64_t s = h & ds.kix_mask;; s = (s + 1) & ds.kix_mask) {
+    const uint4 e = __ldg(tab + s);
+    const uint64_t key = (uint64_t)e.y << 32 | e.x;
+    if (key == 0) return 0;
+    if (key == h) {
+      const uint32_t* row = ds.rows + (uint64_t)e.z * 16;  // verify: row lo starts with the k-gram
+      if (ds.n_tokens - row[0] < (uint64_t)k) return -1;
+      for (int j = 0; j < k; ++j)
+        if (row[1 + j] != pat[j]) return -1;
+      lo = e.z;
+      hi = e.w;
+      return 1;
+    }
+  }
+}
+
 }  // namespace sssd

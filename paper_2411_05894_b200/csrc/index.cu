@@ -107,6 +107,80 @@ __global__ void bucket_build_kernel(const uint32_t* rows, uint64_t n, uint32_t n
     for (int64_t u = t + 1; u <= (int64_t)nb; ++u) bucket[u] = (uint32_t)n;
 }
 
+// ---- k-gram range index (sssd_kix_*) -------------------------------------------
+// Row r starts a k-group when its suffix has >= k tokens and row r-1's first k
+// tokens differ (or row r-1's suffix is shorter than k); the group runs to the
+// next row that is not in it.  Rows hold their first 15 tokens inline, so every
+// test reads the first 32 B sector of two adjacent rows (coalesced).
+__device__ __forceinline__ bool kix_starts(const uint32_t* rows, uint64_t r, uint64_t n_tokens, int k) {
+  const uint32_t* a = rows + r * 16;
+  if (n_tokens - a[0] < (uint64_t)k) return false;
+  if (r == 0) return true;
+  const uint32_t* b = a - 16;
+  if (n_tokens - b[0] < (uint64_t)k) return true;
+  for (int j = 1; j <= k; ++j)
+    if (a[j] != b[j]) return true;
+  return false;
+}
+
+__global__ void kix_count_kernel(const uint32_t* rows, uint64_t n, uint64_t n_tokens, int kmax,
+                                 unsigned long long* count) {
+  const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t c = 0;
+  if (r < n)
+    for (int k = 2; k <= kmax; ++k) c += kix_starts(rows, r, n_tokens, k) ? 1u : 0u;
+  c = __reduce_add_sync(SSSD_FULL, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, (unsigned long long)c);
+}
+
+__global__ void kix_insert_kernel(const uint32_t* rows, uint64_t n, uint64_t n_tokens, int kmax, uint4* tab,
+                                  uint64_t mask) {
+  const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  for (int k = 2; k <= kmax; ++k) {
+    if (!kix_starts(rows, r, n_tokens, k)) continue;
+    const uint64_t h = kix_hash(rows + r * 16 + 1, k);
+    for (uint64_t s = h & mask;; s = (s + 1) & mask) {
+      unsigned long long* key = reinterpret_cast<unsigned long long*>(tab + s);
+      const unsigned long long old = atomicCAS(key, 0ull, (unsigned long long)h);
+      if (old == 0ull) {
+        tab[s].z = (uint32_t)r;
+        break;
+      }
+      if (old == h) break;  // a colliding k-gram holds the slot: its lookups verify and search
+    }
+  }
+}
+
+// hi of the group that row r-1 belongs to, written by the first row after it
+// (or by the last row): the slot is found by the hash and checked to be that
+// group's (its lo row has the same k tokens) before hi is written.
+__global__ void kix_ends_kernel(const uint32_t* rows, uint64_t n, uint64_t n_tokens, int kmax, uint4* tab,
+                                uint64_t mask) {
+  const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > n || r == 0) return;
+  const uint32_t* p = rows + (r - 1) * 16;
+  for (int k = 2; k <= kmax; ++k) {
+    if (n_tokens - p[0] < (uint64_t)k) continue;               // row r-1 is in no k-group
+    if (r < n && !kix_starts(rows, r, n_tokens, k)) {          // row r continues the group...
+      if (n_tokens - rows[r * 16] >= (uint64_t)k) continue;   // ...unless it is shorter than k
+    }
+    const uint64_t h = kix_hash(p + 1, k);
+    for (uint64_t s = h & mask;; s = (s + 1) & mask) {
+      const uint4 e = tab[s];
+      const uint64_t key = (uint64_t)e.y << 32 | e.x;
+      if (key == 0) break;
+      if (key == h) {
+        const uint32_t* lr = rows + (uint64_t)e.z * 16;
+        bool same = n_tokens - lr[0] >= (uint64_t)k;
+        for (int j = 1; j <= k && same; ++j) same = lr[j] == p[j];
+        if (same) tab[s].w = (uint32_t)r;
+        break;
+      }
+    }
+  }
+}
+
 // u16 -> u32 token widening: 4 tokens per thread per step (8 B in, 16 B out)
 // when both pointers are suitably aligned, grid-stride, scalar tail.
 __global__ void widen_u16_kernel(const uint16_t* src, uint32_t* dst, int64_t n) {
@@ -189,6 +263,33 @@ int sssd_bucket_build(const uint32_t* rows, uint64_t n_rows, uint32_t n_buckets,
   if (n_rows >= 0xffffffffull) return fail(SSSD_E_LIMIT, "bucket index needs < 2^32 rows");
   bucket_build_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(rows, n_rows, n_buckets, bucket);
   return cuda_check(cudaGetLastError(), "bucket_build launch");
+}
+
+int sssd_kix_count(const uint32_t* rows, uint64_t n_rows, uint64_t n_tokens, uint32_t kmax, uint64_t* count,
+                   void* stream) {
+  if (!rows || !count) return fail(SSSD_E_ARG, "kix_count needs rows and a count word");
+  if (kmax < 2 || kmax > 7) return fail(SSSD_E_ARG, "kix kmax must be in 2..7");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = cuda_check(cudaMemsetAsync(count, 0, 8, st), "kix count memset");
+  if (rc || n_rows == 0) return rc;
+  kix_count_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(
+      rows, n_rows, n_tokens, (int)kmax, reinterpret_cast<unsigned long long*>(count));
+  return cuda_check(cudaGetLastError(), "kix_count launch");
+}
+
+int sssd_kix_build(const uint32_t* rows, uint64_t n_rows, uint64_t n_tokens, uint32_t kmax, uint32_t* table,
+                   uint64_t cap, void* stream) {
+  if (!rows || !table) return fail(SSSD_E_ARG, "kix_build needs rows and a table");
+  if (kmax < 2 || kmax > 7) return fail(SSSD_E_ARG, "kix kmax must be in 2..7");
+  if (cap == 0 || (cap & (cap - 1))) return fail(SSSD_E_ARG, "kix capacity must be a power of two");
+  if (n_rows >= 0xffffffffull) return fail(SSSD_E_LIMIT, "kix needs < 2^32 rows");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = cuda_check(cudaMemsetAsync(table, 0, cap * 16, st), "kix memset");
+  if (rc || n_rows == 0) return rc;
+  uint4* tab = reinterpret_cast<uint4*>(table);
+  kix_insert_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(rows, n_rows, n_tokens, (int)kmax, tab, cap - 1);
+  kix_ends_kernel<<<(unsigned)((n_rows + 256) / 256), 256, 0, st>>>(rows, n_rows, n_tokens, (int)kmax, tab, cap - 1);
+  return cuda_check(cudaGetLastError(), "kix_build launch");
 }
 
 int sssd_widen_u16(const uint16_t* src, uint32_t* dst, int64_t n, void* stream) {

@@ -130,6 +130,7 @@ __device__ uint64_t warp_search(const sssd_ds& ds, const uint32_t* pat, int p, u
 
 __device__ void warp_bounds(const sssd_ds& ds, const uint32_t* pat, int p, uint64_t& out_lo,
                             uint64_t& out_hi) {
+  if (ds.kix && p >= 2 && p <= (int)ds.kix_kmax && kix_find(ds, pat, p, out_lo, out_hi) == 1) return;
   uint64_t blo = 0, bhi = ds.n_rows;
   if (ds.bucket) {  // first-token index: rows starting with pat[0] (or >= n_buckets)
     const uint32_t t0 = pat[0];
@@ -323,7 +324,12 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P, SSSD_LOOKUP_MINB)
       lo = (uint64_t)pre_bounds[((size_t)b * c.P + warp) * 2] - ds.rank_base;
       hi = (uint64_t)pre_bounds[((size_t)b * c.P + warp) * 2 + 1] - ds.rank_base;
     } else {
-      warp_bounds(ds, s_pat + (pmax - p), p, lo, hi);
+      int kf = -1;
+      if (ds.kix && !lk.ranges && p >= 2 && p <= (int)ds.kix_kmax) {
+        kf = kix_find(ds, s_pat + (pmax - p), p, lo, hi);
+        if (kf == 0) lo = hi = 0;  // absent: empty range (its insertion point is not reported)
+      }
+      if (kf < 0) warp_bounds(ds, s_pat + (pmax - p), p, lo, hi);
     }
     if (lane == 0) {
       s_lo[warp] = lo + ds.rank_base;
@@ -584,18 +590,43 @@ __global__ void __launch_bounds__(32 * kLkWarps, SSSD_LKW_MINB)
   };
   // p = 1 needs no probe when its token has a bucket
   const bool p1_free = pmax >= 1 && ds.bucket && tail[pmax - 1] < ds.n_buckets;
-  const int ng = pmax - (p1_free ? 1 : 0);  // patterns searched: p = pmax, pmax-1, ...
   if (lane == 0 && p1_free) {
     uint64_t a, z;
     bracket(1, a, z);
     s_rlo[warp][0] = a;
     s_rhi[warp][0] = z;
   }
+  // p = 2 .. kix_kmax: the k-gram index holds the exact range (one slot read
+  // + the verification of row lo, which the gather reads next anyway); an
+  // absent k-gram is an empty range unless its insertion point is reported
+  uint32_t known = p1_free ? 1u : 0u;  // bit p-1: range already known
+  if (ds.kix) {
+    const int p = lane + 1;
+    int kf = -1;
+    uint64_t klo = 0, khi = 0;
+    if (p >= 2 && p <= pmax && p <= (int)ds.kix_kmax) {
+      kf = kix_find(ds, tail + (pmax - p), p, klo, khi);
+      if (kf == 0 && lk.ranges) kf = -1;
+    }
+    if (kf >= 0) {
+      s_rlo[warp][p - 1] = kf == 1 ? klo : 0;
+      s_rhi[warp][p - 1] = kf == 1 ? khi : 0;
+    }
+    known |= __ballot_sync(SSSD_FULL, kf >= 0);
+  }
+  const uint32_t todo = ((pmax >= 32 ? 0u : (1u << pmax)) - 1u) & ~known;  // patterns still searched
+  const int ng = __popc(todo);
   if (ng > 0) {
     const int gs = 32 / ng;
     const int gid = lane / gs, gl = lane - gid * gs;
     const bool active = gid < ng;
-    const int myp = active ? pmax - gid : 1;
+    int myp = 1;  // group gid searches the gid-th longest pattern still to do
+    for (int p = pmax, g = 0; p >= 1; --p)
+      if ((todo >> (p - 1)) & 1u) {
+        if (g == gid) myp = p;
+        ++g;
+      }
+    if (!active) myp = 1;
     const uint32_t* pat = tail + (pmax - myp);
     const uint32_t gbits = gs >= 32 ? 0xffffffffu : ((1u << gs) - 1u);
     const int gbase = active ? gid * gs : 0;

@@ -130,6 +130,14 @@ class Datastore:
         self._np_tokens: np.ndarray | None = None
         self._np_sa: np.ndarray | None = None
         self._bucket: torch.Tensor | None = None
+        self._kix: torch.Tensor | None = None
+        self._kix_done = False
+        # the index tables are built here, not on first use: a first use can sit
+        # inside a CUDA-graph capture (the decode loops), where the k-gram count
+        # readback would capture instead of run
+        if self.n_rows > 0:
+            self.bucket()
+            self.kix()
 
     # -- reference-compatible views -------------------------------------------------
     @property
@@ -183,10 +191,37 @@ class Datastore:
                                           stream_ptr(self.device)))
         return self._bucket
 
+    # k-gram range index (sssd_kix_build): the exact row range of every 2..4-gram
+    # that starts a suffix, so lookups of patterns up to 4 tokens need no
+    # search.  Built for a whole datastore (a shard's absent patterns need their
+    # local insertion points for the summed bounds, so shards keep searching);
+    # SSSD_NO_KIX=1 disables it (A/B switch).
+    KIX_KMAX = 4
+
+    def kix(self) -> torch.Tensor | None:
+        if not self._kix_done:
+            self._kix_done = True
+            if (self.n_rows > 0 and self.rank_base == 0 and self.n_rows == self._n_tokens
+                    and os.environ.get("SSSD_NO_KIX", "0") in ("", "0")):
+                dev = self.device
+                cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+                check(lib().sssd_kix_count(ptr(self._rows), self.n_rows, self._n_tokens, self.KIX_KMAX, ptr(cnt),
+                                           stream_ptr(dev)))
+                cap = 1024
+                while cap < 2 * int(cnt.item()):
+                    cap <<= 1
+                self._kix = torch.empty(cap * 4, dtype=torch.int32, device=dev)
+                check(lib().sssd_kix_build(ptr(self._rows), self.n_rows, self._n_tokens, self.KIX_KMAX,
+                                           ptr(self._kix), cap, stream_ptr(dev)))
+        return self._kix
+
     def c_view(self) -> _lib.Ds:
         bk = self.bucket() if self.n_rows > 0 else None
+        kx = self.kix()
         return _lib.Ds(ptr(self._rows), ptr(self._tok), self._n_tokens, self.rank_base, self.n_rows,
-                       ptr(bk) if bk is not None else None, (bk.numel() - 1) if bk is not None else 0)
+                       ptr(bk) if bk is not None else None, (bk.numel() - 1) if bk is not None else 0,
+                       ptr(kx) if kx is not None else None, (kx.numel() // 4 - 1) if kx is not None else 0,
+                       self.KIX_KMAX if kx is not None else 0)
 
     @property
     def rows(self) -> torch.Tensor:

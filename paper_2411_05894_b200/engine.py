@@ -120,7 +120,7 @@ class DraftEngine:
         self._ws: torch.Tensor | None = None
         self._ws_key = (0, 0)
         self._out: dict[int, DraftBatch] = {}
-        self._null_ds = _lib.Ds(None, None, 0, 0, 0, None, 0)
+        self._null_ds = _lib.Ds(None, None, 0, 0, 0, None, 0, None, 0, 0)
 
     @property
     def S(self) -> int:

@@ -87,3 +87,48 @@ def test_simulate_with_and_without_index(golden):
         a = G.simulate(rec, ds, cfg, use_index=True).records[0].per_step_tokens
         b = G.simulate(rec, ds, cfg, use_index=False).records[0].per_step_tokens
         assert a == b == case["per_step"]
+
+
+# ---------------------------------------------------------------------------
+# k-gram range index (sssd_kix_build, the find_range accelerator)
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("vocab", [7, 500, 32000])
+def test_kgram_index_ranges_and_drafts(monkeypatch, vocab):
+    """Patterns of 1..6 tokens (present and absent) get the oracle's exact
+    (lo, hi) through the k-gram table, and drafts with the table equal drafts
+    without it (SSSD_NO_KIX=1) -- including the lookup kernels' 'absent
+    k-gram = empty range' shortcut."""
+    from oracle import sssd_oracle as O
+
+    corpus = workload.corpus(200_000, vocab)
+    ds = G.build(corpus, vocab_size=vocab)
+    assert ds.kix() is not None
+    monkeypatch.setenv("SSSD_NO_KIX", "1")
+    ds0 = G.Datastore.on_device(ds.token_tensor, ds.rows, ds.n_rows, vocab)
+    monkeypatch.delenv("SSSD_NO_KIX")
+    assert ds0.kix() is None
+    sa = ds.suffix_index
+    tok = np.asarray(corpus)
+    rng = np.random.default_rng(5)
+    pats = []
+    for _ in range(300):
+        k = int(rng.integers(1, 7))
+        s = int(rng.integers(0, len(corpus) - k))
+        p = [int(x) for x in corpus[s:s + k]]
+        if rng.random() < 0.3:  # perturb: mostly absent k-grams
+            p[-1] = int(rng.integers(0, vocab))
+        pats.append(p)
+    pats.append([int(x) for x in corpus[-2:]])  # suffixes at the corpus end
+    pats.append([int(x) for x in corpus[-4:]])
+    got = ds.find_ranges(pats)
+    for p, g in zip(pats, got):
+        assert tuple(g) == O.find_range(tok, sa, p), p
+    for B, L in ((64, 2048), (2048, 512)):
+        ctxs = workload.contexts(B, L, vocab)
+        cfg = G.FusionConfig(dec_len=32)
+        a = G.DraftEngine(ds, cfg).propose_host(ctxs)
+        b = G.DraftEngine(ds0, cfg).propose_host(ctxs)
+        for x, y in zip(a, b):
+            assert (x.tokens, x.parents, x.depths) == (y.tokens, y.parents, y.depths)
