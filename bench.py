@@ -117,7 +117,13 @@ class ClockSampler:
                 self.gpu = int(phys[self.gpu]) if self.gpu < len(phys) else self.gpu
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
-            time.sleep(0.01)
+            # the sampler's first NVML calls can take tens of ms: wait until it
+            # is polling, so the samples cover the (short) timed region
+            t0 = time.time()
+            while not self.samples and time.time() - t0 < 1.0:
+                time.sleep(0.001)
+            self.pre = list(self.samples)
+            self.samples.clear()
         except Exception:
             self._t = None
         return self
@@ -127,10 +133,20 @@ class ClockSampler:
         if self._t is not None:
             self._t.join(timeout=2)
 
+    pre: list = []
+
     def summary(self) -> dict:
         sm = [s for s, _, _ in self.samples]
+        if not sm and self.pre:  # region shorter than one poll: the sample taken right before it
+            s = self.summary_of(self.pre[-1:])
+            s["source"] = "nvml, 2 ms polling (no poll inside the region: the last one before it)"
+            return s
+        return self.summary_of(self.samples)
+
+    def summary_of(self, samples) -> dict:
+        sm = [s for s, _, _ in samples]
         reasons = set()
-        for _, rs, _ in self.samples:
+        for _, rs, _ in samples:
             for name, bit in self.REASONS.items():
                 if rs & bit:
                     reasons.add(name)
