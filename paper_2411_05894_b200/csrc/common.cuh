@@ -85,6 +85,10 @@ __host__ __device__ __forceinline__ uint64_t kix_hash(const uint32_t* t, int k) 
   return h | 1ull;
 }
 
+// The table covers the whole corpus (not an SA-range shard, whose absent
+// patterns still need their local insertion points for the summed bounds).
+__device__ __forceinline__ bool kix_whole(const sssd_ds& ds) { return ds.rank_base == 0 && ds.n_rows == ds.n_tokens; }
+
 // Rows [lo, hi) whose suffix starts with pat[0..k) (2 <= k <= ds.kix_kmax):
 // returns 1 (found, lo / hi set), 0 (no suffix starts with the k-gram: the
 // range is empty, its insertion point unknown) or -1 (the slot of this hash

@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P, SSSD_LOOKUP_MINB)
       hi = (uint64_t)pre_bounds[((size_t)b * c.P + warp) * 2 + 1] - ds.rank_base;
     } else {
       int kf = -1;
-      if (ds.kix && !lk.ranges && p >= 2 && p <= (int)ds.kix_kmax) {
+      if (ds.kix && !lk.ranges && kix_whole(ds) && p >= 2 && p <= (int)ds.kix_kmax) {
         kf = kix_find(ds, s_pat + (pmax - p), p, lo, hi);
         if (kf == 0) lo = hi = 0;  // absent: empty range (its insertion point is not reported)
       }
@@ -606,7 +606,7 @@ __global__ void __launch_bounds__(32 * kLkWarps, SSSD_LKW_MINB)
     uint64_t klo = 0, khi = 0;
     if (p >= 2 && p <= pmax && p <= (int)ds.kix_kmax) {
       kf = kix_find(ds, tail + (pmax - p), p, klo, khi);
-      if (kf == 0 && lk.ranges) kf = -1;
+      if (kf == 0 && (lk.ranges || !kix_whole(ds))) kf = -1;
     }
     if (kf >= 0) {
       s_rlo[warp][p - 1] = kf == 1 ? klo : 0;

@@ -191,18 +191,17 @@ class Datastore:
                                           stream_ptr(self.device)))
         return self._bucket
 
-    # k-gram range index (sssd_kix_build): the exact row range of every 2..4-gram
-    # that starts a suffix, so lookups of patterns up to 4 tokens need no
-    # search.  Built for a whole datastore (a shard's absent patterns need their
-    # local insertion points for the summed bounds, so shards keep searching);
-    # SSSD_NO_KIX=1 disables it (A/B switch).
+    # k-gram range index (sssd_kix_build): the exact (local) row range of every
+    # 2..4-gram that starts a suffix, so lookups of patterns up to 4 tokens need
+    # no search.  A shard's table gives exact local ranges of the k-grams it
+    # holds; its absent patterns are still searched (the summed bounds need
+    # their local insertion points).  SSSD_NO_KIX=1 disables it (A/B switch).
     KIX_KMAX = 4
 
     def kix(self) -> torch.Tensor | None:
         if not self._kix_done:
             self._kix_done = True
-            if (self.n_rows > 0 and self.rank_base == 0 and self.n_rows == self._n_tokens
-                    and os.environ.get("SSSD_NO_KIX", "0") in ("", "0")):
+            if self.n_rows > 0 and os.environ.get("SSSD_NO_KIX", "0") in ("", "0"):
                 dev = self.device
                 cnt = torch.zeros(1, dtype=torch.int64, device=dev)
                 check(lib().sssd_kix_count(ptr(self._rows), self.n_rows, self._n_tokens, self.KIX_KMAX, ptr(cnt),
