@@ -1138,9 +1138,15 @@ __global__ void __launch_bounds__(1024)
 #pragma unroll
       for (int k = 0; k < kScanV; ++k) v[k] = e0 + k < L ? seq[e0 + k - 1] : ~t0;
     }
-    uint32_t mk = 0;  // bit k: position e0 + k matches (m >= 1); indexed positions (e0 + k - 1 < L0) excluded
+    // bit k: position e0 + k matches (m >= 1); positions past the end (e0 + k >= L)
+    // and indexed ones (e0 + k <= L0) are masked out
+    uint32_t valid = 0xffu;
+    if (e0 + kScanV > L) valid = L > e0 ? (1u << (L - e0)) - 1u : 0u;
+    if (e0 <= L0) valid &= L0 - e0 + 1 >= kScanV ? 0u : ~((1u << (L0 - e0 + 1)) - 1u);
+    uint32_t mk = 0;
 #pragma unroll
-    for (int k = 0; k < kScanV; ++k) mk |= (v[k] == t0 && e0 + k < L && e0 + k > L0 ? 1u : 0u) << k;
+    for (int k = 0; k < kScanV; ++k) mk |= (v[k] == t0 ? 1u : 0u) << k;
+    mk &= valid;
     const int cnt = __popc(mk);
     int inc = cnt;  // block exclusive scan of the counts
 #pragma unroll
@@ -1150,12 +1156,15 @@ __global__ void __launch_bounds__(1024)
     }
     if (lane == 31) s_wsum[warp] = inc;
     __syncthreads();
-    int wbase = 0, tsum = 0;
-    for (int w = 0; w < nw; ++w) {
-      const int x = s_wsum[w];
-      wbase += w < warp ? x : 0;
-      tsum += x;
+    // warp totals scanned with shuffles (nw <= 32): my warp's base and the tile total
+    int wx = lane < nw ? s_wsum[lane] : 0, wi = wx;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(SSSD_FULL, wi, o);
+      if (lane >= o) wi += y;
     }
+    const int wbase = __shfl_sync(SSSD_FULL, wi - wx, warp);
+    const int tsum = __shfl_sync(SSSD_FULL, wi, nw - 1);
     int at = total + wbase + inc - cnt;
     while (mk) {
       const int k = __ffs(mk) - 1;
