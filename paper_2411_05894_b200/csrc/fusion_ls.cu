@@ -33,7 +33,7 @@ namespace sssd {
 
 int ls_smem_bytes(int P, int S) {
   return kLsLevelBytes * kLsCap + kLsParBytes * kLsParCap + (P + 1) * (int)sizeof(SrcDesc) +
-         top_bytes(S) + S * 8 + 16 * 4;
+         top_bytes(S) + S * 8 + kLsRankWords * 4;
 }
 
 
@@ -267,6 +267,10 @@ __device__ __forceinline__ void draft_ls_body(const SrcDesc* desc, const uint32_
                                               const int32_t* order, const int32_t* order_count) {
   extern __shared__ __align__(16) uint8_t smem[];
   const long long t_start = clock64();
+#ifdef SSSD_LS_TIMELINE  // measurement builds: global start / end stamps per request (cycle probe slots 6, 7)
+  unsigned long long g_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
+#endif
   if (order_count && (int)blockIdx.x >= *order_count) return;  // a list filled on the device
   const int b = order ? order[c.b0 + blockIdx.x] : c.b0 + blockIdx.x;
   const int lane = lane_id();
@@ -402,7 +406,7 @@ __device__ __forceinline__ void draft_ls_body(const SrcDesc* desc, const uint32_
       // 4. class positions, path ids (first occurrence in G order wins), new paths
       next_pid = pid0;
       nnew = 0;
-      if (lane < 16) rcnt[lane] = 0;
+      if (lane < kLsRankWords) rcnt[lane] = 0;
       __syncwarp();
       for (uint32_t s0 = 0; s0 < n; s0 += 32) {
         const uint32_t s = s0 + lane;
@@ -738,8 +742,15 @@ __device__ __forceinline__ void draft_ls_body(const SrcDesc* desc, const uint32_
       st[3] = t_end - t_levels;  // flatten
       st[4] = ph_merge;
       st[5] = levels | (long long)max_level << 16;
+#ifdef SSSD_LS_TIMELINE
+      unsigned long long g_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+      st[6] = (long long)g_start;
+      st[7] = (long long)g_end;
+#else
       st[6] = gen_total;
       st[7] = gallocs;
+#endif
     }
   }
 }

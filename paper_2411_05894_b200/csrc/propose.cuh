@@ -148,7 +148,11 @@ constexpr int kLsParBytes = 32;
 #define SSSD_LS_CAP 96
 #endif
 constexpr int kLsCap = SSSD_LS_CAP;
-constexpr int kLsParCap = 64;
+#ifndef SSSD_LS_PARCAP
+#define SSSD_LS_PARCAP 32  // 8.7 KB per warp: 24 warps per SM (64 parents: 21; cfg2 fusion 0.479 -> 0.469 ms)
+#endif
+constexpr int kLsParCap = SSSD_LS_PARCAP;
+constexpr int kLsRankWords = SSSD_MAX_P + 1;  // per-rank class counters (ranks 0..P)
 int ls_smem_bytes(int P, int S);
 __global__ void draft_ls_kernel(const SrcDesc* desc, const uint32_t* root_tok, KCfg c, uint8_t* pool,
                                 unsigned long long* cursor, uint64_t pool_bytes, int32_t* err,
