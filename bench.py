@@ -285,10 +285,43 @@ def bench_sa_build(ds, dev) -> dict:
     alg = 48.0 * n * rounds.value
     del ws, sa
     torch.cuda.empty_cache()
-    return {"gpu_ms": round(ms, 2), "mtok_per_s": round(n / ms / 1e3, 1), "rounds": rounds.value,
-            "algorithmic_bytes": alg, "achieved_GBps": round(alg / ms / 1e6, 1),
-            "frac": round(alg / ms / 1e6 / peak, 4), "equals_index_sa": same,
-            "kernels": "own LSD radix sort (8-bit digits) + group-refinement rounds (csrc/sa_build.cu); no library"}
+    out = {"gpu_ms": round(ms, 2), "mtok_per_s": round(n / ms / 1e3, 1), "rounds": rounds.value,
+           "algorithmic_bytes": alg, "achieved_GBps": round(alg / ms / 1e6, 1),
+           "frac": round(alg / ms / 1e6 / peak, 4), "equals_index_sa": same,
+           "kernels": "own LSD radix sort (8-bit digits) + group-refinement rounds (csrc/sa_build.cu); no library"}
+    # BASELINE.md §2 "SA build" CPU leg: the reference's NumPy prefix doubling
+    # (restated in oracle.sssd_oracle.suffix_array: same argsort / cumsum
+    # rounds) on a 1M-token prefix of the same corpus, one core, beside the
+    # GPU build of that prefix; both arrays must be equal
+    try:
+        from oracle import sssd_oracle as O
+
+        n1 = min(n, 1_000_000)
+        toks = ds.token_tensor[:n1].cpu().numpy().view(np.uint32).copy()
+        t0 = time.time()
+        sa_cpu = O.suffix_array(toks)
+        cpu_s = time.time() - t0
+        tok1 = ds.token_tensor[:n1].contiguous()
+        ws1 = torch.empty(lib().sssd_sa_build_workspace(n1), dtype=torch.uint8, device=dev)
+        sa1 = torch.empty(n1, dtype=torch.int32, device=dev)
+        ts1 = []
+        for _ in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            check(lib().sssd_sa_build(ptr(tok1), n1, ptr(sa1), ptr(ws1), ws1.numel(), stream_ptr(dev)))
+            b.record()
+            torch.cuda.synchronize(dev)
+            ts1.append(a.elapsed_time(b))
+        gpu1 = min(ts1)
+        out["cpu"] = {"n": n1, "cpu_s": round(cpu_s, 3), "cpu_mtok_per_s": round(n1 / cpu_s / 1e6, 3), "cores": 1,
+                      "kind": "port (oracle.sssd_oracle.suffix_array, the reference's NumPy prefix doubling)",
+                      "gpu_ms_same_n": round(gpu1, 3), "gpu_vs_cpu": round(cpu_s * 1e3 / gpu1, 1),
+                      "arrays_equal": bool(np.array_equal(sa1.cpu().numpy().view(np.uint32).astype(np.int64), sa_cpu)),
+                      "reference_100m_s_survey": 375.7}
+        del ws1, sa1
+    except Exception as exc:  # pragma: no cover - reported, not fatal
+        out["cpu"] = {"error": repr(exc)}
+    return out
 
 
 def cpu_baseline(tokens: np.ndarray, sa: np.ndarray, ctxs: list, budget_s: float = 12.0) -> tuple[dict, list]:

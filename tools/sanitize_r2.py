@@ -1,7 +1,9 @@
-"""Round-2 kernels under compute-sanitizer: the own-radix SA build (incl. the
-token-table round 1 at >= 2^20 tokens) + sssd_sa_check, per-node draft outputs
-(priority / source / pos), the N2 index build + indexed propose, the compact
-sharded exchange (in-process shards), and the continuous-batching model loop."""
+"""Round-2 kernels under compute-sanitizer: the own-radix SA build (its 4-gram
+first round) + sssd_sa_check, the k-gram index build and its lookups
+(find_ranges + propose), per-node draft outputs (priority / source / pos) from
+both fusion forms (one warp / one CTA per request), the N2 index build +
+indexed propose, the compact sharded exchange (in-process shards), and the
+continuous-batching model loop."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -19,7 +21,12 @@ assert small.check()["ok"]
 eng = G.DraftEngine(ds, G.FusionConfig(dec_len=32))
 ctxs = [c.tolist() for c in workload.contexts(24, 300, 500)]
 seq, off, ln, mx = eng.upload(ctxs)
-eng.propose(seq, off, ln, mx, nodes=True)
+from paper_2411_05894_b200._lib import lib
+for form in (0, 2):  # one warp per request, one CTA per request
+    lib().sssd_set_fusion_form(form)
+    eng.propose(seq, off, ln, mx, nodes=True)
+lib().sssd_set_fusion_form(-1)
+ds.find_ranges([c[-k:] for c in ctxs[:8] for k in (1, 2, 3, 4, 6)])
 ix = G.InputIndex(24, mx + 8, "cuda", off)
 ix.build(seq, off, ln)
 eng.propose(seq, off, ln, mx, index=ix)
