@@ -39,3 +39,17 @@ res = {"kernel_us": round(float(T), 1), "max_active": int(cap),
                           "max": round(float((e - s).max()), 1)},
        "active_profile": act[::20].tolist()}
 print(json.dumps(res))
+
+# how well does the LPT cost (datastore + 4 x input elements) predict the time?
+out = eng.propose(seq, off, ln, 2048, lookup=True)
+torch.cuda.synchronize()
+nds = out.n_conts.clamp(min=0).sum(1).cpu().numpy().astype(np.float64)  # raw datastore strings
+tl = ctx.reshape(B, 2048)
+nin = (tl[:, :-1] == tl[:, -1:]).sum(1).astype(np.float64)
+dur = e - s
+for name, x in (("n_ds", nds), ("n_in", nin), ("n_ds+4n_in", nds + 4 * nin), ("n_ds+2n_in", nds + 2 * nin),
+                ("n_ds+n_in", nds + nin), ("sqrt(n_ds)+n_in", np.sqrt(nds) + nin)):
+    print("corr(time, %s) = %.3f" % (name, np.corrcoef(x, dur)[0, 1]))
+# the requests that start last (LPT's cheapest) and their durations
+late = np.argsort(-s)[:200]
+print("last 200 starters: mean dur %.1f us, max %.1f us; overall mean %.1f" % (dur[late].mean(), dur[late].max(), dur.mean()))
