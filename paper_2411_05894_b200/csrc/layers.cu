@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(128) rope_kv_kernel(const __nv_bfloat16* qkv, 
   const int half = d >> 1, hp = half >> 1;
   const int width = (hq + 2 * hkv) * d;
   const __nv_bfloat16* src = qkv + (int64_t)bs * width;
-  const int64_t row = rows ? rows[bi] : bi;
+  const int64_t row = rows ? rows[bi] : bi;  // row < 0: rotate q only, write no K/V (a padding request)
   const int64_t slot = (int64_t)ctx_len[bi] + s;
   if (threadIdx.x < half) {
     // torch: inv = 1 / theta ** (arange(0, d, 2) / d); ang = pos * inv  (float32)
@@ -88,11 +88,13 @@ __global__ void __launch_bounds__(128) rope_kv_kernel(const __nv_bfloat16* qkv, 
     const float c0 = s_cos[i], c1 = s_cos[i + 1], n0 = s_sin[i], n1 = s_sin[i + 1];
     const __nv_bfloat162 y1 = __floats2bfloat162_rn(x1.x * c0 - x2.x * n0, x1.y * c1 - x2.y * n1);
     const __nv_bfloat162 y2 = __floats2bfloat162_rn(x1.x * n0 + x2.x * c0, x1.y * n1 + x2.y * c1);
+    if (hh >= hq && row < 0) continue;
     __nv_bfloat16* dst = hh < hq ? q_out + ((int64_t)bs * hq + hh) * d
                                  : k_cache + ((row * hkv + (hh - hq)) * max_pos + slot) * d;
     *reinterpret_cast<__nv_bfloat162*>(dst + i) = y1;
     *reinterpret_cast<__nv_bfloat162*>(dst + i + half) = y2;
   }
+  if (row < 0) return;
   const int d8 = d >> 3;
   for (int t = threadIdx.x; t < hkv * d8; t += blockDim.x) {
     const int hh = t / d8, i = (t - hh * d8) * 8;

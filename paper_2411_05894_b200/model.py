@@ -20,6 +20,7 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from ._lib import check, lib, ptr, stream_ptr
@@ -57,6 +58,25 @@ def _rope(x: torch.Tensor, pos: torch.Tensor, theta: float) -> torch.Tensor:
 def _rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
     xf = x.float()
     return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps) * w.float()).to(x.dtype)
+
+
+_CHAIN_MASKS: dict = {}
+
+
+def _chain_mask(S: int, device) -> torch.Tensor:
+    """[S, ceil(S/64)] int64 ancestor rows of a causal chain (row i: bits 0..i),
+    cached per (S, device)."""
+    key = (S, str(device))
+    m = _CHAIN_MASKS.get(key)
+    if m is None:
+        W = (S + 63) // 64
+        bits = torch.tril(torch.ones(S, S, dtype=torch.bool))
+        m = torch.zeros(S, W, dtype=torch.int64)
+        for w in range(W):
+            blk = bits[:, 64 * w: 64 * (w + 1)].to(torch.int64)
+            m[:, w] = (blk << torch.arange(blk.shape[1], dtype=torch.int64)).sum(-1)
+        m = _CHAIN_MASKS[key] = m.to(device)
+    return m
 
 
 class Decoder:
@@ -104,11 +124,16 @@ class Decoder:
         self.scale = 1.0 / math.sqrt(d)
 
     def forward(self, tokens: torch.Tensor, positions: torch.Tensor, mask: torch.Tensor,
-                ctx_len: torch.Tensor, rows: torch.Tensor | None = None) -> torch.Tensor:
+                ctx_len: torch.Tensor, rows: torch.Tensor | None = None, logits: bool = True,
+                kv_rows: torch.Tensor | None = None) -> torch.Tensor | None:
         """Tree forward: tokens / positions [b, S] (rows = cache rows of these b
         requests, default all), mask [b, S, W] int64, ctx_len [b] int32 = committed
         tokens already in the cache.  Writes K/V of the S tokens to cache
-        positions ctx..ctx+S-1 and returns logits [b, S, V] (fp32)."""
+        positions ctx..ctx+S-1 and returns logits [b, S, V] (fp32); with
+        logits=False (prefill) only the K/V writes happen: the last layer stops
+        after its K/V and no lm_head is computed.  kv_rows [B] (with b = B, all
+        rows in order): the K/V of request b go to cache row kv_rows[b], -1 =
+        not written (a padding request of a fixed-shape prefill)."""
         sp = self.spec
         b, S = tokens.shape
         d, h = sp.head_dim, sp.hidden
@@ -118,6 +143,9 @@ class Decoder:
         pos = positions.reshape(-1).long().contiguous()
         ctx = ctx_len.to(torch.int32).contiguous()
         rows_l = rows.long().contiguous() if rows is not None else None
+        if kv_rows is not None:
+            assert rows is None and b == self.B
+            rows_l = kv_rows.long().contiguous()
         hN = torch.empty_like(x)
         q = torch.empty(b, S, sp.n_q, d, dtype=self.dtype, device=self.device)
         for li, L in enumerate(self.layers):
@@ -127,6 +155,8 @@ class Decoder:
             check(lib().sssd_rope_kv_bf16(ptr(qkv), ptr(pos), ptr(ctx), ptr(rows_l) if rows_l is not None else None,
                                           ptr(q), ptr(kc), ptr(vc), b, S, sp.n_q, sp.n_kv, d, self.max_pos,
                                           sp.rope_theta, st))
+            if not logits and li == len(self.layers) - 1:
+                return None  # (prefill: this layer's K/V are written; nothing reads its output)
             if rows is None:
                 o = tree_attention(q, kc, vc, mask, ctx, self.scale)
             else:
@@ -176,20 +206,15 @@ class Decoder:
         while any(done[b] < n[b] for b in range(B)):
             S = min(chunk, max(n[b] - done[b] for b in range(B)))
             S = max(S, 1)
-            toks = torch.zeros(B, S, dtype=torch.int64)
+            toks = np.zeros((B, S), dtype=np.int64)
             for b in range(B):
                 seg = prompts[b][done[b]: min(n[b], done[b] + S)]
-                toks[b, : len(seg)] = torch.tensor([int(t) for t in seg])
-            W = (S + 63) // 64
-            bits = torch.tril(torch.ones(S, S, dtype=torch.bool))
-            mask = torch.zeros(S, W, dtype=torch.int64)
-            for w in range(W):
-                blk = bits[:, 64 * w: 64 * (w + 1)].to(torch.int64)
-                sh = torch.arange(blk.shape[1], dtype=torch.int64)
-                mask[:, w] = (blk << sh).sum(-1)
+                toks[b, : len(seg)] = np.asarray(seg, dtype=np.int64)
+            mask = _chain_mask(S, self.device)
             ctx = torch.tensor(done, dtype=torch.int32, device=self.device)
             pos = ctx.long()[:, None] + torch.arange(S, device=self.device)[None, :]
-            self.forward(toks.to(self.device), pos, mask[None].expand(B, S, W).contiguous().to(self.device), ctx)
+            self.forward(torch.from_numpy(toks).to(self.device), pos, mask[None].expand(B, S, -1).contiguous(), ctx,
+                         logits=False)
             for b in range(B):
                 done[b] = min(n[b], done[b] + S)
 
@@ -200,26 +225,27 @@ class Decoder:
         n = [len(p) - 1 for p in prompts]
         if not rows or max(n) <= 0:
             return
-        r = torch.tensor(list(rows), dtype=torch.int64, device=self.device)
-        R = len(rows)
+        # Fixed shape: every prefill runs all B rows (the rows not being refilled
+        # are padding: no K/V written for them, outputs discarded), so the GEMM
+        # shapes repeat from refill to refill (a new cuBLAS shape costs ~1 ms of
+        # host heuristics per call) and no row subset of the cache is gathered.
+        B = self.B
+        kv = np.full(B, -1, dtype=np.int64)
+        L = max(n)
+        host = np.zeros((B, L), dtype=np.int64)  # all prompt tokens, one upload
+        for r_, p, k in zip(rows, prompts, n):
+            kv[r_] = r_
+            host[r_, :k] = np.asarray(p[:k], dtype=np.int64)
+        toks_all = torch.from_numpy(host).to(self.device)
+        kv_rows = torch.from_numpy(kv).to(self.device)
         done = 0
-        while done < max(n):
-            S = min(chunk, max(n) - done)
-            toks = torch.zeros(R, S, dtype=torch.int64)
-            for i, p in enumerate(prompts):
-                seg = p[done: min(n[i], done + S)]
-                if seg:
-                    toks[i, : len(seg)] = torch.tensor([int(t) for t in seg])
-            W = (S + 63) // 64
-            bits = torch.tril(torch.ones(S, S, dtype=torch.bool))
-            mask = torch.zeros(S, W, dtype=torch.int64)
-            for w in range(W):
-                blk = bits[:, 64 * w: 64 * (w + 1)].to(torch.int64)
-                mask[:, w] = (blk << torch.arange(blk.shape[1], dtype=torch.int64)).sum(-1)
-            ctx = torch.full((R,), done, dtype=torch.int32, device=self.device)
+        while done < L:
+            S = min(chunk, L - done)
+            mask = _chain_mask(S, self.device)
+            ctx = torch.full((B,), done, dtype=torch.int32, device=self.device)
             pos = ctx.long()[:, None] + torch.arange(S, device=self.device)[None, :]
-            self.forward(toks.to(self.device), pos, mask[None].expand(R, S, W).contiguous().to(self.device), ctx,
-                         rows=r)
+            self.forward(toks_all[:, done: done + S].contiguous(), pos, mask[None].expand(B, S, -1).contiguous(), ctx,
+                         logits=False, kv_rows=kv_rows)
             done += S
 
     def compact(self, ctx_len: torch.Tensor, path: torch.Tensor, n_acc: torch.Tensor) -> None:

@@ -205,9 +205,12 @@ class ServeLoop:
         from .datastore import as_u32
 
         dev = self.seq.device
-        for s, p, m in zip(slots, prompts, max_new):
-            t = torch.from_numpy(as_u32(p, "prompt token").view(np.int32)).to(dev)
-            self.seq[s * self.cap: s * self.cap + len(p)] = t
+        # every prompt into its slot buffer with one upload + one scatter
+        lens = [len(p) for p in prompts]
+        flat = np.concatenate([as_u32(p, "prompt token") for p in prompts]) if prompts else np.zeros(0, "<u4")
+        dst = np.concatenate([np.arange(n, dtype=np.int64) + s * self.cap for s, n in zip(slots, lens)]) \
+            if prompts else np.zeros(0, np.int64)
+        self.seq[torch.from_numpy(dst).to(dev)] = torch.from_numpy(flat.view(np.int32)).to(dev)
         meta = torch.tensor([[len(p) for p in prompts], [len(p) + int(m) for p, m in zip(prompts, max_new)]],
                             dtype=torch.int32, device=dev)
         idx = torch.tensor(list(slots), dtype=torch.int64, device=dev)
