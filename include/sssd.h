@@ -417,6 +417,10 @@ int sssd_rope_kv_bf16(const void* qkv, const int64_t* pos, const int32_t* ctx_le
                       int32_t d, int32_t max_pos, float theta, void* stream);
 /* a[r][j] = silu(gu[r][j]) * gu[r][m + j] (fused gate|up projection) */
 int sssd_swiglu_bf16(const void* gu, void* a, int64_t rows, int32_t m, void* stream);
+/* Row argmax of fp32 logits [rows][cols] -> int32 [rows]: torch.argmax semantics
+ * (first index of the maximum; a NaN is the maximum).  The greedy predictions
+ * of a verify step (the oracle of draft.py:205-210). */
+int sssd_argmax_f32(const float* x, int64_t rows, int32_t cols, int32_t* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -87,6 +87,7 @@ _SIGS = {
     "sssd_rope_kv_bf16": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                     C.c_int32, C.c_int32, C.c_float, vp]),
     "sssd_swiglu_bf16": (C.c_int, [vp, vp, C.c_int64, C.c_int32, vp]),
+    "sssd_argmax_f32": (C.c_int, [vp, C.c_int64, C.c_int32, vp, vp]),
     "sssd_propose_workspace": (C.c_size_t, [C.POINTER(Cfg), C.c_int32, C.c_int32]),
     "sssd_propose_phase": (C.c_int, [C.POINTER(Ds), C.POINTER(Seqs), C.POINTER(Cfg), C.POINTER(DraftOut),
                                      C.POINTER(LookupOut), vp, C.c_size_t, C.c_int32, C.c_int32, C.c_int32,

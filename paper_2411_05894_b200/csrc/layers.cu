@@ -10,6 +10,7 @@
 // per PyTorch op boundary where that op materialised bf16).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 
 #include "common.cuh"
@@ -103,6 +104,62 @@ __global__ void __launch_bounds__(128) rope_kv_kernel(const __nv_bfloat16* qkv, 
   }
 }
 
+// Row argmax of fp32 logits (the greedy prediction of every draft node), same
+// result as torch.argmax: the first index of the maximum, a NaN counting as
+// the maximum (its first index).  One CTA per row, 16-byte loads.
+__device__ __forceinline__ bool am_better(float v, int i, float bv, int bi) {
+  const bool vn = v != v, bn = bv != bv;
+  if (vn || bn) return vn && (!bn || i < bi);
+  return v > bv || (v == bv && i < bi);
+}
+
+__global__ void __launch_bounds__(256) argmax_kernel(const float* x, int cols, int32_t* out, bool vec) {
+  const float* row = x + (int64_t)blockIdx.x * cols;
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  if (vec) {  // 4 independent 16-byte loads in flight per thread per round
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    const int n4 = cols / 4;
+    for (int j0 = threadIdx.x; j0 < n4; j0 += 4 * blockDim.x) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0 + u * blockDim.x;
+        v[u] = j < n4 ? __ldg(r4 + j) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = 4 * (j0 + u * blockDim.x);
+        if (am_better(v[u].x, i, bv, bi)) bv = v[u].x, bi = i;
+        if (am_better(v[u].y, i + 1, bv, bi)) bv = v[u].y, bi = i + 1;
+        if (am_better(v[u].z, i + 2, bv, bi)) bv = v[u].z, bi = i + 2;
+        if (am_better(v[u].w, i + 3, bv, bi)) bv = v[u].w, bi = i + 3;
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < cols; i += blockDim.x) {
+      const float v = row[i];
+      if (am_better(v, i, bv, bi)) bv = v, bi = i;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float v = __shfl_down_sync(0xffffffffu, bv, o);
+    const int i = __shfl_down_sync(0xffffffffu, bi, o);
+    if (am_better(v, i, bv, bi)) bv = v, bi = i;
+  }
+  __shared__ float s_v[8];
+  __shared__ int s_i[8];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) s_v[w] = bv, s_i[w] = bi;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+      if (am_better(s_v[k], s_i[k], bv, bi)) bv = s_v[k], bi = s_i[k];
+    out[blockIdx.x] = bi == 0x7fffffff ? 0 : bi;
+  }
+}
+
 __device__ __forceinline__ float silu_bf16(float g) {
   // torch: silu in fp32 on the bf16 gate, rounded to bf16 (F.silu output dtype)
   return __bfloat162float(__float2bfloat16_rn(g / (1.0f + expf(-g))));
@@ -158,6 +215,14 @@ int sssd_rope_kv_bf16(const void* qkv, const int64_t* pos, const int32_t* ctx_le
       static_cast<const __nv_bfloat16*>(qkv), pos, ctx_len, rows, static_cast<__nv_bfloat16*>(q_out),
       static_cast<__nv_bfloat16*>(k_cache), static_cast<__nv_bfloat16*>(v_cache), S, hq, hkv, d, max_pos, theta);
   return cuda_check(cudaGetLastError(), "rope_kv launch");
+}
+
+int sssd_argmax_f32(const float* x, int64_t rows, int32_t cols, int32_t* out, void* stream) {
+  if (!x || !out || rows < 0 || cols <= 0) return fail(SSSD_E_ARG, "argmax: bad arguments");
+  if (rows == 0) return SSSD_OK;
+  const bool vec = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && cols % 4 == 0;
+  argmax_kernel<<<(unsigned)rows, 256, 0, static_cast<cudaStream_t>(stream)>>>(x, cols, out, vec);
+  return cuda_check(cudaGetLastError(), "argmax launch");
 }
 
 int sssd_swiglu_bf16(const void* gu, void* a, int64_t rows, int32_t m, void* stream) {

@@ -22,6 +22,15 @@ from .engine import DraftEngine, InputIndex
 from .model import Decoder
 
 
+def argmax_rows(x: torch.Tensor) -> torch.Tensor:
+    """int32 argmax of every row of fp32 [rows, cols] (sssd_argmax_f32: torch.argmax
+    semantics, one launch, no int64 intermediate)."""
+    assert x.dtype == torch.float32 and x.is_contiguous()
+    out = torch.empty(x.shape[0], dtype=torch.int32, device=x.device)
+    check(lib().sssd_argmax_f32(ptr(x), x.shape[0], x.shape[1], ptr(out), stream_ptr(x.device)))
+    return out
+
+
 def spec_step(st, tokens, parents, depths, mask, size) -> None:
     """One verification step over every slot of ``st`` (a SpecDecoder or
     ServeLoop: model, seq / off / seq_len / seq_cap, path / n_acc / bonus /
@@ -30,8 +39,8 @@ def spec_step(st, tokens, parents, depths, mask, size) -> None:
     ctx = st.seq_len - 1
     pos = ctx.long()[:, None] + depths.clamp(min=0).long()
     logits = st.model.forward(tokens, pos, mask, ctx)
-    pred = logits.argmax(-1).to(torch.int32).contiguous()
     B, S = tokens.shape
+    pred = argmax_rows(logits.view(B * S, -1)).view(B, S)
     check(lib().sssd_accept(ptr(tokens), ptr(parents), ptr(size), S, ptr(pred), B, ptr(st.seq), ptr(st.off),
                             ptr(st.seq_len), ptr(st.seq_cap), ptr(st.path), ptr(st.n_acc), ptr(st.bonus),
                             ptr(st.emitted), stream_ptr(st.seq.device)))

@@ -187,3 +187,19 @@ def test_layer_kernels_match_torch():
         assert (got_k.float() - k_ref[bi].float()).abs().max() <= 2 ** -6 * k_ref.float().abs().max()
         assert torch.equal(vc[r, :, c0:c0 + S].transpose(0, 1), v3[bi, :, hq + hkv:])
     assert int(kc[1].abs().sum()) == 0 and int(vc[1].abs().sum()) == 0  # untouched row
+
+
+def test_argmax_kernel_matches_torch():
+    """sssd_argmax_f32 (the verify step's greedy predictions) = torch.argmax:
+    first index of the maximum, ties, a NaN counting as the maximum, odd
+    widths (scalar path) and the vocabulary widths of both models."""
+    from paper_2411_05894_b200.serving import argmax_rows
+
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for rows, cols in ((320, 32000), (64, 128256), (7, 33), (1, 1), (5, 4)):
+        x = torch.randn(rows, cols, device="cuda", generator=g)
+        if cols >= 8:
+            x[0, 3] = x[0, cols - 2] = x[0].max() + 1  # tie: the first wins
+            x[min(1, rows - 1), 5] = float("nan")      # a NaN is the maximum
+            x[min(2, rows - 1), :] = -float("inf")     # all -inf: index 0
+        assert torch.equal(argmax_rows(x), x.argmax(-1).to(torch.int32)), (rows, cols)
