@@ -131,9 +131,9 @@ class Decoder:
         tokens already in the cache.  Writes K/V of the S tokens to cache
         positions ctx..ctx+S-1 and returns logits [b, S, V] (fp32); with
         logits=False (prefill) only the K/V writes happen: the last layer stops
-        after its K/V and no lm_head is computed.  kv_rows [B] (with b = B, all
-        rows in order): the K/V of request b go to cache row kv_rows[b], -1 =
-        not written (a padding request of a fixed-shape prefill)."""
+        after its K/V and no lm_head is computed.  kv_rows [b]: the K/V of
+        request b go to cache row kv_rows[b], -1 = not written (a padding
+        request of a bucketed prefill); attention still reads row rows[b] (or b)."""
         sp = self.spec
         b, S = tokens.shape
         d, h = sp.head_dim, sp.hidden
@@ -143,8 +143,8 @@ class Decoder:
         pos = positions.reshape(-1).long().contiguous()
         ctx = ctx_len.to(torch.int32).contiguous()
         rows_l = rows.long().contiguous() if rows is not None else None
-        if kv_rows is not None:
-            assert rows is None and b == self.B
+        if kv_rows is not None:  # K/V destinations (-1: padding request, not written)
+            assert rows is not None or b == self.B
             rows_l = kv_rows.long().contiguous()
         hN = torch.empty_like(x)
         q = torch.empty(b, S, sp.n_q, d, dtype=self.dtype, device=self.device)
@@ -225,27 +225,42 @@ class Decoder:
         n = [len(p) - 1 for p in prompts]
         if not rows or max(n) <= 0:
             return
-        # Fixed shape: every prefill runs all B rows (the rows not being refilled
-        # are padding: no K/V written for them, outputs discarded), so the GEMM
-        # shapes repeat from refill to refill (a new cuBLAS shape costs ~1 ms of
-        # host heuristics per call) and no row subset of the cache is gathered.
+        # Bucketed shape: the batch is padded to the next power of two of
+        # refilled rows (all B rows at that size: the plain in-order path, no
+        # gathered copy of the cache); padding requests write no K/V and their
+        # outputs are discarded.  The GEMM shapes then repeat from refill to
+        # refill (a new cuBLAS shape costs ~1 ms of host heuristics per call)
+        # while a big model never prefills more than 2x the refilled rows.
         B = self.B
-        kv = np.full(B, -1, dtype=np.int64)
+        R = len(rows)
+        Rp = 1
+        while Rp < R:
+            Rp <<= 1
         L = max(n)
-        host = np.zeros((B, L), dtype=np.int64)  # all prompt tokens, one upload
-        for r_, p, k in zip(rows, prompts, n):
-            kv[r_] = r_
-            host[r_, :k] = np.asarray(p[:k], dtype=np.int64)
+        if Rp >= B:
+            Rp = B
+            att = None
+            kv = np.full(B, -1, dtype=np.int64)
+            host = np.zeros((B, L), dtype=np.int64)  # all prompt tokens, one upload
+            for r_, p, k in zip(rows, prompts, n):
+                kv[r_] = r_
+                host[r_, :k] = np.asarray(p[:k], dtype=np.int64)
+        else:
+            att = torch.tensor(list(rows) + [rows[0]] * (Rp - R), dtype=torch.int64, device=self.device)
+            kv = np.array(list(rows) + [-1] * (Rp - R), dtype=np.int64)
+            host = np.zeros((Rp, L), dtype=np.int64)
+            for i, (p, k) in enumerate(zip(prompts, n)):
+                host[i, :k] = np.asarray(p[:k], dtype=np.int64)
         toks_all = torch.from_numpy(host).to(self.device)
         kv_rows = torch.from_numpy(kv).to(self.device)
         done = 0
         while done < L:
             S = min(chunk, L - done)
             mask = _chain_mask(S, self.device)
-            ctx = torch.full((B,), done, dtype=torch.int32, device=self.device)
+            ctx = torch.full((Rp,), done, dtype=torch.int32, device=self.device)
             pos = ctx.long()[:, None] + torch.arange(S, device=self.device)[None, :]
-            self.forward(toks_all[:, done: done + S].contiguous(), pos, mask[None].expand(B, S, -1).contiguous(), ctx,
-                         logits=False, kv_rows=kv_rows)
+            self.forward(toks_all[:, done: done + S].contiguous(), pos, mask[None].expand(Rp, S, -1).contiguous(), ctx,
+                         rows=att, logits=False, kv_rows=kv_rows)
             done += S
 
     def compact(self, ctx_len: torch.Tensor, path: torch.Tensor, n_acc: torch.Tensor) -> None:

@@ -254,6 +254,14 @@ class ServeLoop:
         steps_of = np.zeros(n_req, dtype=np.int64)
         if use_graph and self._graph is None:
             self._step()  # eager warm-up step creates the lazily allocated buffers (results discarded below)
+            # one prefill per refill bucket (1, 2, 4, .. rows: Decoder.prefill_rows pads
+            # to these) so no refill meets a GEMM shape for the first time inside the
+            # loop; the caches it writes are reloaded below
+            plen = max(len(p) for p in prompts)
+            r = 1
+            while r < B:
+                self.model.prefill_rows(list(range(r)), [[0] * plen] * r)
+                r <<= 1
             torch.cuda.synchronize()
             try:
                 g = torch.cuda.CUDAGraph()
