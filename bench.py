@@ -850,10 +850,10 @@ def issue_roofline(fusion_ms: float, B: int, clk) -> dict | None:
     per lookup (ncu count of the committed capture, profiles/r2_propose_ncu.json:
     warp_inst / grid, one warp per request) over this run's kernel time, against
     148 SMs x 4 schedulers x the SM clock sampled during the timed region."""
-    path = os.path.join(ROOT, "profiles", "r1_propose_ncu.json")
+    path = os.path.join(ROOT, "profiles", "r2_propose_ncu.json")
     if not os.path.exists(path):
         return None
-    rows = [k for k in json.load(open(path))["kernels"] if k["kernel"] == "draft_ls_kernel"]
+    rows = [k for k in json.load(open(path))["kernels"] if k["kernel"].split("::")[-1] == "draft_ls_kernel"]
     if not rows:
         return None
     per_lookup = rows[0]["warp_inst"] / rows[0]["grid"]
