@@ -60,6 +60,12 @@ def _rmsnorm(x: torch.Tensor, w: torch.Tensor, eps: float) -> torch.Tensor:
     return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps) * w.float()).to(x.dtype)
 
 
+def _h2d(a: np.ndarray, device) -> torch.Tensor:
+    """Non-blocking upload through pinned memory (stream-ordered; the host does
+    not wait for the work queued before it)."""
+    return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().to(device, non_blocking=True)
+
+
 _CHAIN_MASKS: dict = {}
 
 
@@ -246,13 +252,13 @@ class Decoder:
                 kv[r_] = r_
                 host[r_, :k] = np.asarray(p[:k], dtype=np.int64)
         else:
-            att = torch.tensor(list(rows) + [rows[0]] * (Rp - R), dtype=torch.int64, device=self.device)
+            att = _h2d(np.array(list(rows) + [rows[0]] * (Rp - R), dtype=np.int64), self.device)
             kv = np.array(list(rows) + [-1] * (Rp - R), dtype=np.int64)
             host = np.zeros((Rp, L), dtype=np.int64)
             for i, (p, k) in enumerate(zip(prompts, n)):
                 host[i, :k] = np.asarray(p[:k], dtype=np.int64)
-        toks_all = torch.from_numpy(host).to(self.device)
-        kv_rows = torch.from_numpy(kv).to(self.device)
+        toks_all = _h2d(host, self.device)
+        kv_rows = _h2d(kv, self.device)
         done = 0
         while done < L:
             S = min(chunk, L - done)

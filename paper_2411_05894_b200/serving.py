@@ -22,6 +22,13 @@ from .engine import DraftEngine, InputIndex
 from .model import Decoder
 
 
+def h2d(a: np.ndarray, dev) -> torch.Tensor:
+    """Host array -> device tensor through pinned memory, non-blocking: the
+    copy is stream-ordered but the host does not wait for the work queued
+    before it (the pipelined decode loop refills slots while a step group runs)."""
+    return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().to(dev, non_blocking=True)
+
+
 def argmax_rows(x: torch.Tensor) -> torch.Tensor:
     """int32 argmax of every row of fp32 [rows, cols] (sssd_argmax_f32: torch.argmax
     semantics, one launch, no int64 intermediate)."""
@@ -199,6 +206,7 @@ class ServeLoop:
         self.emitted = torch.empty(B, dtype=torch.int32, device=dev)
         self.hist = torch.empty((self.group, B), dtype=torch.int32, device=dev)
         self._graph = None
+        self.ahead_below_ms = 4.0  # queue the next step group before reading this one below this group time
         # N2 per-slot input index (rebuilt on refill): each step scans only the appended tokens
         if use_index is None:  # (see DecodeLoop: the index pays past one 8k-position scan pass)
             use_index = self.cap > 8192
@@ -219,10 +227,10 @@ class ServeLoop:
         flat = np.concatenate([as_u32(p, "prompt token") for p in prompts]) if prompts else np.zeros(0, "<u4")
         dst = np.concatenate([np.arange(n, dtype=np.int64) + s * self.cap for s, n in zip(slots, lens)]) \
             if prompts else np.zeros(0, np.int64)
-        self.seq[torch.from_numpy(dst).to(dev)] = torch.from_numpy(flat.view(np.int32)).to(dev)
-        meta = torch.tensor([[len(p) for p in prompts], [len(p) + int(m) for p, m in zip(prompts, max_new)]],
-                            dtype=torch.int32, device=dev)
-        idx = torch.tensor(list(slots), dtype=torch.int64, device=dev)
+        self.seq[h2d(dst, dev)] = h2d(flat.view(np.int32), dev)
+        meta = h2d(np.array([[len(p) for p in prompts], [len(p) + int(m) for p, m in zip(prompts, max_new)]],
+                            dtype=np.int32), dev)
+        idx = h2d(np.array(list(slots), dtype=np.int64), dev)
         self.seq_len.index_copy_(0, idx, meta[0])
         self.seq_cap.index_copy_(0, idx, meta[1])
         self.model.prefill_rows(list(slots), [list(p) for p in prompts])
@@ -279,22 +287,56 @@ class ServeLoop:
                 self.load(free, [[int(prompts[0][-1])]] * len(free), [0] * len(free))
         lens = self.seq_len.cpu().numpy().astype(np.int64)
         caps = self.seq_cap.cpu().numpy().astype(np.int64)
+        dev = self.seq.device
+        # finished sequences are copied on the device (stream-ordered, before the
+        # refill overwrites the slot) and read back once at the end
+        out_dev = torch.zeros((n_req, self.cap), dtype=torch.int32, device=dev)
+        out_len = np.zeros(n_req, dtype=np.int64)
         torch.cuda.synchronize()
         t0 = perf_counter()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         dev_ms, groups, tokens = 0.0, 0, 0
         accepted = []
-        while (slot_req >= 0).any():
-            ev0.record()
+        # Pipelined host loop: group k+1 is queued before group k's history is
+        # read, so the GPU never waits for the host's bookkeeping; a slot refilled
+        # while group k+1 is queued starts with group k+2 (group k+1 saw it capped,
+        # its history there is the old request's and is skipped).
+        pin = [torch.empty((self.group, B), dtype=torch.int32).pin_memory() for _ in range(2)]
+        inflight: list = []  # (group index, ready event, timing events)
+        fresh_from = np.zeros(B, dtype=np.int64)  # first group whose history belongs to the slot's request
+
+        def launch(k: int) -> None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
             if self._graph is not None:
                 self._graph.replay()
             else:
                 self._group()
-            ev1.record()
-            H = self.hist.cpu().numpy().astype(np.int64)  # the group's one synchronisation
-            dev_ms += ev0.elapsed_time(ev1)
+            e1.record()
+            pin[k % 2].copy_(self.hist, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record()
+            inflight.append((k, ready, e0, e1))
+
+        # Queueing ahead pays when the host's bookkeeping is a sizeable part of a
+        # group (small models); for long groups it would only keep finished
+        # slots idle one group longer: decided from the first group's device time.
+        ahead = None
+        k_next = 0
+        launch(k_next)
+        k_next += 1
+        while inflight:
+            if ahead and (slot_req >= 0).any():  # keep one group queued ahead while any request is live
+                launch(k_next)
+                k_next += 1
+            k, ready, e0, e1 = inflight.pop(0)
+            ready.synchronize()
+            H = pin[k % 2].numpy().astype(np.int64)
+            gms = e0.elapsed_time(e1)
+            dev_ms += gms
+            if ahead is None:
+                ahead = gms < self.ahead_below_ms
             groups += 1
-            live = np.nonzero(slot_req >= 0)[0]
+            live = np.nonzero((slot_req >= 0) & (fresh_from <= k))[0]
             for g in range(self.group):
                 act = live[lens[live] < caps[live]]
                 if not len(act):
@@ -306,9 +348,10 @@ class ServeLoop:
                 lens[act] = H[g][act]
             done = live[lens[live] >= caps[live]]
             if len(done):
-                s = self.seq.view(B, self.cap)[torch.from_numpy(done).to(self.seq.device)].cpu().numpy()
-                for k, sl in enumerate(done):
-                    out[slot_req[sl]] = s[k, : lens[sl]].view(np.uint32).tolist()
+                rows = self.seq.view(B, self.cap)
+                for sl in done:
+                    out_dev[slot_req[sl]].copy_(rows[sl])
+                    out_len[slot_req[sl]] = lens[sl]
                 n_fill = min(len(done), n_req - nxt)
                 fill = done[:n_fill].tolist()
                 if fill:
@@ -316,8 +359,15 @@ class ServeLoop:
                     slot_req[done[:n_fill]] = np.arange(nxt, nxt + n_fill)
                     lens[done[:n_fill]] = [len(p) for p in prompts[nxt:nxt + n_fill]]
                     caps[done[:n_fill]] = lens[done[:n_fill]] + max_new
+                    fresh_from[done[:n_fill]] = k_next  # the first group queued after the refill
                     nxt += n_fill
                 slot_req[done[n_fill:]] = -1
+            if not inflight and (slot_req >= 0).any():  # (not queued ahead: the next group now)
+                launch(k_next)
+                k_next += 1
+        o = out_dev.cpu().numpy()
+        for r in range(n_req):
+            out[r] = o[r, : out_len[r]].view(np.uint32).tolist()
         torch.cuda.synchronize()
         wall = perf_counter() - t0
         return {"sequences": out, "tokens": tokens, "requests": n_req, "slots": B, "seconds": wall,

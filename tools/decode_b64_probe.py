@@ -26,7 +26,8 @@ def timed_load(*a, **k):
     t_load[0] += time.perf_counter() - t
 
 
-loop.load = timed_load
+if not os.environ.get("NO_WRAP"):
+    loop.load = timed_load
 t_pre = [0.0]
 orig_pre = dec.prefill_rows
 
@@ -43,7 +44,8 @@ def timed_pre(*a, **k):
 calls = []
 
 
-dec.prefill_rows = timed_pre
+if not os.environ.get("NO_WRAP"):
+    dec.prefill_rows = timed_pre
 r = loop.run(prompts, max_new)
 print({"tokens_per_s": round(r["tokens_per_s"]), "device_tokens_per_s": round(r["device_tokens_per_s"]),
        "wall_s": round(r["seconds"], 4), "device_s": round(r["device_ms"] / 1e3, 4), "load_s": round(t_load[0], 4), "prefill_s": round(t_pre[0], 4),
