@@ -107,10 +107,12 @@ class SpecDecoder:
         the first eager step and the graph capture).
 
         The first step runs eagerly (it creates every lazily allocated buffer);
-        later steps run in groups of ``graph_steps`` replayed from one CUDA
-        graph with the sequence lengths after each step recorded on the device
-        and read back once per group (a finished slot's appends are capped, so
-        steps past the end change nothing).  graph_steps <= 1: eager steps."""
+        later steps run in groups of ``graph_steps`` replayed from CUDA graphs
+        (two captures, alternating history buffers, so the next group is queued
+        while the host reads the previous one) with the sequence lengths after
+        each step recorded on the device and read back once per group (a
+        finished slot's appends are capped, so steps past the end change
+        nothing).  graph_steps <= 1: eager steps."""
         torch.cuda.synchronize()
         t0 = perf_counter()
         start = self.seq_len.clone()
@@ -122,41 +124,72 @@ class SpecDecoder:
             now = self.seq_len.cpu()
             per_step.append(now - lens)
             lens = now
-        graph = None
+        graphs = None
         if graph_steps > 1 and bool((lens < cap).any()):
-            hist = torch.empty((graph_steps, self.model.B), dtype=torch.int32, device=self.seq.device)
+            B = self.model.B
+            hist = [torch.empty((graph_steps, B), dtype=torch.int32, device=self.seq.device) for _ in range(2)]
+            pin = [torch.empty((graph_steps, B), dtype=torch.int32, pin_memory=True) for _ in range(2)]
+            evs = [torch.cuda.Event() for _ in range(2)]
 
-            def group() -> None:
+            def group(h: torch.Tensor) -> None:
                 for g in range(graph_steps):
                     self._step()
-                    hist[g].copy_(self.seq_len)
+                    h[g].copy_(self.seq_len)
 
             try:
                 torch.cuda.synchronize()
-                graph = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(graph, capture_error_mode="thread_local"):
-                    group()
+                graphs = []
+                for i in range(2):  # two copies, one per history buffer: group k+1 is queued before k is read
+                    gr = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(gr, capture_error_mode="thread_local"):
+                        group(hist[i])
+                    graphs.append(gr)
             except Exception as exc:  # capture not possible here: eager steps (same results)
                 torch.cuda.synchronize()
-                graph = None
+                graphs = None
                 self.graph_error = repr(exc)
         torch.cuda.synchronize()
         t1, lens1 = perf_counter(), lens.clone()  # steady state: after the eager first step and the capture
-        while bool((lens < cap).any()):
-            if graph is None:
+        if graphs is None:
+            while bool((lens < cap).any()):
                 self.step()
                 now = self.seq_len.cpu()
                 per_step.append(now - lens)
                 lens = now
-                continue
-            graph.replay()
-            H = hist.cpu()
-            for g in range(graph_steps):
-                if not bool((lens < cap).any()):
-                    break  # trailing steps after every slot finished are not counted
-                per_step.append(H[g] - lens)
-                lens = H[g]
-                self.steps += 1
+        else:
+            # pipelined groups: while group k runs, group k+1 is already queued
+            # when the progress so far says some slot will still be unfinished
+            # after k (a wrong guess costs one capped group or one lost overlap,
+            # never a different result)
+            launched = read = 0
+            gain = int(per_step[-1].max()) * graph_steps if per_step else 0
+
+            def launch() -> None:
+                nonlocal launched
+                i = launched & 1
+                graphs[i].replay()
+                pin[i].copy_(hist[i], non_blocking=True)
+                evs[i].record()
+                launched += 1
+
+            launch()
+            while read < launched:
+                if launched - read < 2 and int((cap - lens).max()) > gain:
+                    launch()
+                i = read & 1
+                evs[i].synchronize()
+                H = pin[i].clone()
+                read += 1
+                before = lens
+                for g in range(graph_steps):
+                    if not bool((lens < cap).any()):
+                        break  # trailing steps after every slot finished are not counted
+                    per_step.append(H[g] - lens)
+                    lens = H[g]
+                    self.steps += 1
+                gain = max(int((lens - before).max()), 1)
+                if read == launched and bool((lens < cap).any()):
+                    launch()
         torch.cuda.synchronize()
         t2 = perf_counter()
         dt = t2 - t0
@@ -165,7 +198,7 @@ class SpecDecoder:
         return {"tokens": gen, "steps": self.steps, "seconds": dt, "tokens_per_s": gen / dt,
                 "steady_tokens_per_s": steady / (t2 - t1) if t2 > t1 and steady else 0.0,
                 "accepted_per_step": float(torch.stack(per_step).float().mean()) if per_step else 0.0,
-                "cuda_graph": graph is not None}
+                "cuda_graph": graphs is not None}
 
     def sequences(self) -> list[list[int]]:
         s = self.seq.view(self.model.B, self.cap).cpu().numpy().view(np.uint32)
