@@ -12,17 +12,22 @@
 //              g+2, ... with its own online-softmax state (m, l) and its own O
 //              accumulator O[g] in TMEM — an intra-CTA split of the keys that
 //              doubles softmax issue width without a per-block cross-warpgroup
-//              sync; one thread per query row reads S with tcgen05.ld, writes P
-//              (bf16, 128B-swizzled K-major) over K_j, rescales O[g] lazily
-//              (only when the running max grows by > 2^8); the epilogue merges
-//              (m0, l0, O[0]) and (m1, l1, O[1])
-//   warp 8     TMA producer: K and V blocks of 128 keys (3 stages, 128B
-//              swizzle, 64 KB per stage) into smem, mbarrier complete_tx
+//              sync; one thread per query row reads S with tcgen05.ld and
+//              writes P (bf16 pairs) back over the S columns it has read with
+//              tcgen05.st, rescales O[g] lazily (only when the running max
+//              grows by > 2^8); the epilogue merges (m0, l0, O[0]) and
+//              (m1, l1, O[1])
+//   warp 8     TMA producer: K and V blocks of 128 keys into separate rings
+//              (2 K slots, 4 V slots of 32 KB, 128B swizzle), mbarrier
+//              complete_tx; a K slot is released when Q K^T completed, a V
+//              slot when P V completed
 //   warp 9     MMA issuer: S[j%2] = Q K_j^T (M128 N128 K16 x 8) as soon as the
-//              stage lands, so Q K^T of block j+1 overlaps the softmax of j;
-//              O[j%2] += P_j V_j (V as an MN-major operand) once P_j is ready
-// TMEM: S0 | S1 | O0 | O1 (4 x 128 fp32 columns).  Split-KV partials
-// (unnormalised O, row max, row sum) are merged by the log-sum-exp combine kernel.
+//              K slot lands, so Q K^T of block j+1 overlaps the softmax of j;
+//              O[j%2] += P_j V_j with P read from TMEM (the A-from-TMEM form)
+//              and V as an MN-major shared-memory operand once P_j is ready
+// TMEM: S0 | S1 | O0 | O1 (4 x 128 fp32 columns; P_j aliases the first 64
+// columns of its S).  Split-KV partials (unnormalised O, row max, row sum)
+// are merged by the log-sum-exp combine kernel.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -43,7 +48,14 @@ constexpr int kM = 128;             // rows per tile (UMMA M)
 constexpr int kN = 128;             // keys per block (UMMA N of QK^T, K of PV)
 constexpr int kTile = kM * kD * 2;  // 32 KB per bf16 128x128 tile
 constexpr int kHalf = kTile / 2;    // 16 KB: 128 rows x 64 columns (one 128B-swizzled TMA box)
-constexpr int kStages = 3;
+// K and V rings (separate barriers): a K slot is free once Q K_j^T has
+// completed, a V slot once P_j V_j has; 6 x 32 KB slots + the Q tile = 224 KB
+#ifndef SSSD_ATTN_KSTAGES
+#define SSSD_ATTN_KSTAGES 2
+#endif
+constexpr int kKStages = SSSD_ATTN_KSTAGES;
+constexpr int kVStages = 6 - kKStages;
+static_assert(kKStages >= 1 && kVStages >= 2, "ring split");
 constexpr int kWgWarps = 4;                  // one softmax warpgroup = 128 rows
 constexpr int kWgThreads = 32 * kWgWarps;
 constexpr int kTmaWarp = 2 * kWgWarps;       // warp 8
@@ -78,6 +90,15 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// A operand from TMEM (K-major: lane = row, one 32-bit column = 2 bf16 along K)
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -173,6 +194,16 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
       : "memory");
 }
 
+// 16 consecutive 32-bit columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
 struct Params {
   const uint16_t* q;     // [B][S][Hq][D]
   const uint64_t* mask;  // [B][S][W]
@@ -186,9 +217,10 @@ struct Params {
 
 struct Smem {  // 1024-aligned dynamic shared memory layout (224 KB)
   uint8_t q[kTile];           // Q tile; reused for the warpgroup merge once all MMAs completed
-  uint8_t k[kStages][kTile];  // K_j, then P_j once Q K_j^T has completed
-  uint8_t v[kStages][kTile];
-  uint64_t full[kStages], empty[kStages], s_full[2], s_free[2], p_ready[2], pv_done[2];
+  uint8_t k[kKStages][kTile];
+  uint8_t v[kVStages][kTile];
+  uint64_t kfull[kKStages], kempty[kKStages], vfull[kVStages], vempty[kVStages];
+  uint64_t s_full[2], s_free[2], p_ready[2], pv_done[2];
   uint32_t tmem;
 };
 
@@ -198,22 +230,24 @@ __device__ __forceinline__ void wg_bar() {  // both softmax warpgroups (256 thre
 
 // One key block of one softmax warpgroup (one thread per query row): the
 // visibility words of the block's 4 x 32 keys (prefix keys visible, tree key t
-// iff ancestor bit t), then P = 2^(S*scale - m) in bf16, written 128B-swizzled
-// over the dead K tile (pbuf), and the running (m, l) with a lazy rescale of O.
+// iff ancestor bit t), then P = 2^(S*scale - m) in bf16, written back into
+// TMEM over the S columns already read (P V then takes A from TMEM, so no
+// shared-memory P and the K slot is free as soon as Q K^T completed), and the
+// running (m, l) with a lazy rescale of O.
 //   * one pass over S (TMEM's read port is the scarce resource): P relative
-//     to the running max, valid whenever the block max does not exceed it by
-//     more than 2^8 — the lazy-rescale rule then keeps m and P unchanged; the
-//     first block of a row and the rare block that raises the max further
-//     take the two-pass form (warp-uniform: tcgen05.ld is warp-collective);
+//     to the running max, kept in registers until the block max is known to
+//     stay within 2^8 of it — the lazy-rescale rule then keeps m and P
+//     unchanged; the first block of a row and the rare block that raises the
+//     max further take the two-pass form (warp-uniform: tcgen05.ld/st are
+//     warp-collective) over the still intact S;
 //   * a warp whose rows are all padding (G*S < 128) skips the block (its P
-//     rows keep whatever the dead K tile held; P V rows are independent);
+//     rows keep stale S bits; P V rows are independent);
 //   * fully visible 32-key chunks (every prefix chunk) skip the per-key masks;
 //   * max / sum use 4 independent chains.
 __device__ __forceinline__ void softmax_block(uint64_t* s_full, uint64_t* s_free, uint64_t* pv_done,
-                                              uint64_t* p_ready, uint8_t* pbuf, int rt, bool row_ok,
-                                              const uint64_t* mrow, int S, int ctx, int k0, int kv1, uint32_t tS,
-                                              uint32_t tO, int it, bool has_prev, float sl2, float& m_run,
-                                              float& l_run) {
+                                              uint64_t* p_ready, bool row_ok, const uint64_t* mrow, int S,
+                                              int ctx, int k0, int kv1, uint32_t tS, uint32_t tO, int it,
+                                              bool has_prev, float sl2, float& m_run, float& l_run) {
   uint32_t visw[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
@@ -250,12 +284,12 @@ __device__ __forceinline__ void softmax_block(uint64_t* s_full, uint64_t* s_free
     bool two_pass = __any_sync(SSSD_FULL, row_ok && m_run == -INFINITY);
     if (!two_pass) {
       float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, ps[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
+      uint32_t pk[64];
+#pragma unroll
       for (int c = 0; c < 4; ++c) {
         float sv[32];
         tmem_ld32(tS + c * 32, sv);
         const uint32_t w = visw[c];
-        uint32_t pk[16];
         if (w == 0xffffffffu) {
 #pragma unroll
           for (int jj = 0; jj < 32; jj += 2) {
@@ -265,7 +299,7 @@ __device__ __forceinline__ void softmax_block(uint64_t* s_full, uint64_t* s_free
             const float e1 = fast_exp2(fmaf(sv[jj + 1], sl2, -m_run));
             ps[a] += e0 + e1;
             const __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
-            pk[jj >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
+            pk[c * 16 + (jj >> 1)] = *reinterpret_cast<const uint32_t*>(&h2);
           }
         } else {
 #pragma unroll
@@ -277,18 +311,18 @@ __device__ __forceinline__ void softmax_block(uint64_t* s_full, uint64_t* s_free
             const float e1 = v1 ? fast_exp2(fmaf(sv[jj + 1], sl2, -m_run)) : 0.f;
             ps[a] += e0 + e1;
             const __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
-            pk[jj >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
+            pk[c * 16 + (jj >> 1)] = *reinterpret_cast<const uint32_t*>(&h2);
           }
         }
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4)
-          *reinterpret_cast<uint4*>(pbuf + sw_off(rt, c * 4 + q4)) =
-              make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
       }
       psum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
       const float m4 = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
       const float bmax = (m4 == -INFINITY) ? m4 : m4 * sl2;
       two_pass = __any_sync(SSSD_FULL, bmax > m_run + 8.f);
+      if (!two_pass) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_st16(tS + c * 16, pk + c * 16);
+      }
     }
     if (two_pass) {
       float sv[32];
@@ -314,6 +348,7 @@ __device__ __forceinline__ void softmax_block(uint64_t* s_full, uint64_t* s_free
         m_use = bmax;
       }
       float ps[4] = {0.f, 0.f, 0.f, 0.f};
+      // chunk c's P goes to columns [16c, 16c + 16): S columns this pass has read
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         tmem_ld32(tS + c * 32, sv);
@@ -329,16 +364,11 @@ __device__ __forceinline__ void softmax_block(uint64_t* s_full, uint64_t* s_free
           const __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
           pk[jj >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
         }
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4)
-          *reinterpret_cast<uint4*>(pbuf + sw_off(rt, c * 4 + q4)) =
-              make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+        tmem_st16(tS + c * 16, pk);
       }
       psum = (ps[0] + ps[1]) + (ps[2] + ps[3]);
     }
   }
-  fence_before();
-  mbar_arrive(s_free);  // S[g] fully read
   l_run = l_run * corr + psum;
   // O[g] is stable once this warpgroup's previous P V completed
   if (has_prev && live) {
@@ -353,12 +383,12 @@ __device__ __forceinline__ void softmax_block(uint64_t* s_full, uint64_t* s_free
         for (int jj = 0; jj < 32; ++jj) ov[jj] *= corr;
         tmem_st32(tO + c * 32, ov);
       }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
   }
   m_run = m_use;
-  fence_async_smem();
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   fence_before();
+  mbar_arrive(s_free);
   mbar_arrive(p_ready);
 }
 
@@ -383,9 +413,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], 1);
+    for (int s = 0; s < kKStages; ++s) {
+      mbar_init(&sm.kfull[s], 1);
+      mbar_init(&sm.kempty[s], 1);
+    }
+    for (int s = 0; s < kVStages; ++s) {
+      mbar_init(&sm.vfull[s], 1);
+      mbar_init(&sm.vempty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.s_full[s], 1);
@@ -419,14 +453,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       for (int j = 0; j < nblk; ++j) {
-        const int st = j % kStages;
-        if (j >= kStages) mbar_wait(&sm.empty[st], ((j / kStages) - 1) & 1);
-        mbar_expect_tx(&sm.full[st], 2 * kTile);
         const int y = (int)(row0 + kv0 + j * kN);
-        tma_load_2d(sm.k[st], &kmap, 0, y, &sm.full[st]);
-        tma_load_2d(sm.k[st] + kHalf, &kmap, 64, y, &sm.full[st]);
-        tma_load_2d(sm.v[st], &vmap, 0, y, &sm.full[st]);
-        tma_load_2d(sm.v[st] + kHalf, &vmap, 64, y, &sm.full[st]);
+        const int sk = j % kKStages, sv = j % kVStages;
+        if (j >= kKStages) mbar_wait(&sm.kempty[sk], ((j / kKStages) - 1) & 1);
+        mbar_expect_tx(&sm.kfull[sk], kTile);
+        tma_load_2d(sm.k[sk], &kmap, 0, y, &sm.kfull[sk]);
+        tma_load_2d(sm.k[sk] + kHalf, &kmap, 64, y, &sm.kfull[sk]);
+        if (j >= kVStages) mbar_wait(&sm.vempty[sv], ((j / kVStages) - 1) & 1);
+        mbar_expect_tx(&sm.vfull[sv], kTile);
+        tma_load_2d(sm.v[sv], &vmap, 0, y, &sm.vfull[sv]);
+        tma_load_2d(sm.v[sv] + kHalf, &vmap, 64, y, &sm.vfull[sv]);
       }
     }
   } else if (warp == kMmaWarp) {
@@ -438,8 +474,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = -1; j < nblk; ++j) {
         const int jn = j + 1;  // Q K^T of the next block goes first so it overlaps softmax(j)
         if (jn < nblk) {
-          const int st = jn % kStages, g = jn & 1;
-          mbar_wait(&sm.full[st], (jn / kStages) & 1);
+          const int st = jn % kKStages, g = jn & 1;
+          mbar_wait(&sm.kfull[st], (jn / kKStages) & 1);
           if (jn >= 2) mbar_wait(&sm.s_free[g], ((jn >> 1) - 1) & 1);
           fence_after();
           const uint32_t aK = smem_u32(sm.k[st]);
@@ -450,22 +486,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_bf16(tS, sw128_desc(aQ + off, 16, 1024), sw128_desc(aK + off, 16, 1024), id_qk, ks > 0);
           }
           mma_commit(&sm.s_full[g]);
+          mma_commit(&sm.kempty[st]);
         }
         if (j < 0) continue;
         const int g = j & 1;
+        const int sv = j % kVStages;
+        mbar_wait(&sm.vfull[sv], (j / kVStages) & 1);
         mbar_wait(&sm.p_ready[g], (j >> 1) & 1);
         fence_after();
-        const uint32_t aV = smem_u32(sm.v[j % kStages]), aP = smem_u32(sm.k[j % kStages]);
-        const uint32_t tO = tbase + 2 * kN + g * kD;
+        const uint32_t aV = smem_u32(sm.v[sv]);
+        const uint32_t tO = tbase + 2 * kN + g * kD, tP = tbase + g * kN;
 #pragma unroll
         for (int ks = 0; ks < kN / 16; ++ks) {
-          // P: K-major over keys (two 64-key halves); V: MN-major, 8-key groups of 1024 B
-          const uint32_t poff = (ks >> 2) * kHalf + (ks & 3) * 32;
-          mma_bf16(tO, sw128_desc(aP + poff, 16, 1024), sw128_desc(aV + ks * 2048, kHalf, 1024), id_pv,
-                   (j >= 2 || ks > 0) ? 1u : 0u);
+          // P from TMEM (16 keys = 8 packed columns per step); V: MN-major, 8-key groups of 1024 B.
+          // Q K^T of block j+2 (into the same S/P columns) is issued after this
+          // in program order; tcgen05.mma from one thread executes in order
+          mma_bf16_ts(tO, tP + ks * 8, sw128_desc(aV + ks * 2048, kHalf, 1024), id_pv, (j >= 2 || ks > 0) ? 1u : 0u);
         }
         mma_commit(&sm.pv_done[g]);
-        mma_commit(&sm.empty[j % kStages]);
+        mma_commit(&sm.vempty[sv]);
       }
     }
   } else {
@@ -484,9 +523,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     float m_run = -INFINITY, l_run = 0.f;
     int it = 0;
     for (int j = g; j < nblk; j += 2, ++it) {
-      // P_j overwrites K_j (stage j%3), dead since Q K_j^T completed (s_full)
-      softmax_block(&sm.s_full[g], &sm.s_free[g], &sm.pv_done[g], &sm.p_ready[g], sm.k[j % kStages], rt, row_ok,
-                    mrow, p.S, ctx, kv0 + j * kN, kv1, tS, tO, it, it > 0, sl2, m_run, l_run);
+      softmax_block(&sm.s_full[g], &sm.s_free[g], &sm.pv_done[g], &sm.p_ready[g], row_ok, mrow, p.S, ctx,
+                    kv0 + j * kN, kv1, tS, tO, it, it > 0, sl2, m_run, l_run);
     }
     if (it > 0) mbar_wait(&sm.pv_done[g], (it - 1) & 1);
     // ---------------- epilogue: merge the two warpgroups ----------------
