@@ -49,12 +49,12 @@ constexpr int kN = 128;             // keys per block (UMMA N of QK^T, K of PV)
 constexpr int kTile = kM * kD * 2;  // 32 KB per bf16 128x128 tile
 constexpr int kHalf = kTile / 2;    // 16 KB: 128 rows x 64 columns (one 128B-swizzled TMA box)
 // K and V rings (separate barriers): a K slot is free once Q K_j^T has
-// completed, a V slot once P_j V_j has; 5 x 32 KB slots + two Q tiles = 224 KB
+// completed, a V slot once P_j V_j has; 6 x 32 KB slots + the Q tile = 224 KB
 #ifndef SSSD_ATTN_KSTAGES
 #define SSSD_ATTN_KSTAGES 2
 #endif
 constexpr int kKStages = SSSD_ATTN_KSTAGES;
-constexpr int kVStages = 5 - kKStages;
+constexpr int kVStages = 6 - kKStages;
 static_assert(kKStages >= 1 && kVStages >= 2, "ring split");
 constexpr int kWgWarps = 4;                  // one softmax warpgroup = 128 rows
 constexpr int kWgThreads = 32 * kWgWarps;
@@ -149,16 +149,6 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// Q box (64 dims x G heads x sbox queries x 1 batch) of the [B][S][Hq][D] tensor
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
-      "[%6];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
-      : "memory");
-}
-
 __device__ __forceinline__ float fast_exp2(float x) {
 #ifdef SSSD_ATTN_FAKE_EXP  // timing experiment only: softmax without the MUFU (wrong results)
   return fmaf(x, 1e-3f, 1.0f);
@@ -222,30 +212,15 @@ struct Params {
   float* part_o;         // [splits][B][Hq][S][D]   (splits > 1)
   float* part_ml;        // [splits][B][Hq][S][2]
   int B, S, Hq, Hkv, G, max_pos, W, splits, split_len;
-  int tiles, items, sbox;  // row tiles per (b, kv head); work items; queries per row tile
   float scale_log2;
-  unsigned long long* trace;  // diagnostic builds (SSSD_ATTN_TRACE): per-CTA clock stamps, else null
 };
 
-// SSSD_ATTN_TRACE builds: thread 0 stamps clock64 at the kernel start, per item
-// (loop start, first block done, epilogue done; up to 9 items) and at the end
-#ifdef SSSD_ATTN_TRACE
-#define ATTN_STAMP(p, slot)                                                        \
-  do {                                                                           \
-    if (threadIdx.x == 0 && (slot) < 32) (p).trace[blockIdx.x * 32 + (slot)] = clock64(); \
-  } while (0)
-#else
-#define ATTN_STAMP(p, slot) \
-  do {                      \
-  } while (0)
-#endif
-
 struct Smem {  // 1024-aligned dynamic shared memory layout (224 KB)
-  uint8_t q[2][kTile];  // Q tiles of two consecutive items; reused for the warpgroup merge once an item's MMAs completed
+  uint8_t q[kTile];           // Q tile; reused for the warpgroup merge once all MMAs completed
   uint8_t k[kKStages][kTile];
   uint8_t v[kVStages][kTile];
   uint64_t kfull[kKStages], kempty[kKStages], vfull[kVStages], vempty[kVStages];
-  uint64_t qfull[2], qempty[2], s_full[2], s_free[2], p_ready[2], pv_done[2], o_free;
+  uint64_t s_full[2], s_free[2], p_ready[2], pv_done[2];
   uint32_t tmem;
 };
 
@@ -417,40 +392,20 @@ __device__ __forceinline__ void softmax_block(uint64_t* s_full, uint64_t* s_free
   mbar_arrive(p_ready);
 }
 
-// One work item = (row tile, b * kv head, KV split); item w = tile + tiles *
-// (bh + B*Hkv * split).  The kernel is persistent (one CTA per SM, items
-// w = blockIdx.x, +gridDim.x, ...): the producer streams the next item's Q tile
-// (double-buffered) and K/V blocks through the same rings while this item's
-// last blocks and epilogue run, so an item boundary costs little more than a
-// key block.  Items with no keys (split past a short context) are skipped by
-// the producer and the MMA issuer and write an empty result.
-struct Item {
-  int tile, b, kvh, split, ctx, kv0, kv1, nblk;
-};
-
-__device__ __forceinline__ Item item_of(const Params& p, int w) {
-  Item it;
-  it.tile = w % p.tiles;
-  const int rest = w / p.tiles;
-  const int bh = rest % (p.B * p.Hkv);
-  it.split = rest / (p.B * p.Hkv);
-  it.b = bh / p.Hkv;
-  it.kvh = bh % p.Hkv;
-  it.ctx = p.ctx[it.b];
-  it.kv0 = it.split * p.split_len;
-  it.kv1 = min(it.ctx + p.S, it.kv0 + p.split_len);
-  it.nblk = it.kv1 > it.kv0 ? (it.kv1 - it.kv0 + kN - 1) / kN : 0;
-  return it;
-}
-
 __global__ void __launch_bounds__(kThreads, 1)
-    tree_attn_kernel(Params p, const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
-                     const __grid_constant__ CUtensorMap qmap) {
+    tree_attn_kernel(Params p, const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int qrows = p.G * p.sbox;  // Q tile rows the TMA box fills: r = (i - i0) * G + head_in_group
+  const int tile = blockIdx.x, bh = blockIdx.y, split = blockIdx.z;
+  const int b = bh / p.Hkv, kvh = bh % p.Hkv;
+  const int rows = p.G * p.S;
+  const int ctx = p.ctx[b];
+  const int total = ctx + p.S;
+  const int kv0 = split * p.split_len;
+  const int kv1 = min(total, kv0 + p.split_len);
+  const int nblk = kv1 > kv0 ? (kv1 - kv0 + kN - 1) / kN : 0;
 
   if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem)),
@@ -467,21 +422,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.vempty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&sm.qfull[s], 1);
-      mbar_init(&sm.qempty[s], 2 * kWgThreads);
       mbar_init(&sm.s_full[s], 1);
       mbar_init(&sm.s_free[s], kWgThreads);
       mbar_init(&sm.p_ready[s], kWgThreads);
       mbar_init(&sm.pv_done[s], 1);
     }
-    mbar_init(&sm.o_free, 2 * kWgThreads);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // rows the Q box never fills (G does not divide 128) stay zero
-  if (warp < 2 * kWgWarps && qrows < kM) {
-    for (int idx = tid; idx < 2 * (kM - qrows) * 16; idx += 2 * kWgThreads) {
-      const int qb = idx / ((kM - qrows) * 16), rem = idx % ((kM - qrows) * 16);
-      *reinterpret_cast<uint4*>(sm.q[qb] + sw_off(qrows + rem / 16, rem % 16)) = make_uint4(0, 0, 0, 0);
+  // Q tile (swizzled K-major): row r = (head_in_group, query i) -> q[b][i][kvh*G + hl][:]
+  if (warp < 2 * kWgWarps) {
+    for (int idx = tid; idx < kM * 16; idx += 2 * kWgThreads) {
+      const int rr = idx >> 4, c8 = idx & 15;
+      const int gr = tile * kM + rr;
+      uint4 val = make_uint4(0, 0, 0, 0);
+      if (gr < rows) {
+        const int h2 = kvh * p.G + gr / p.S, i2 = gr % p.S;
+        val = __ldg(reinterpret_cast<const uint4*>(p.q + (((int64_t)b * p.S + i2) * p.Hq + h2) * kD) + c8);
+      }
+      *reinterpret_cast<uint4*>(sm.q + sw_off(rr, c8)) = val;
     }
     fence_async_smem();
   }
@@ -489,198 +447,133 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   fence_after();
   const uint32_t tbase = sm.tmem;
-  ATTN_STAMP(p, 0);
+  const int64_t row0 = (int64_t)(b * p.Hkv + kvh) * p.max_pos;  // first K/V row of this (b, kv head)
 
   if (warp == kTmaWarp) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      const uint32_t qbytes = 2u * 128u * (uint32_t)qrows;
-      int n = 0, J = 0;  // non-empty items and key blocks issued so far
-      for (int w = blockIdx.x; w < p.items; w += gridDim.x) {
-        const Item it = item_of(p, w);
-        if (it.nblk == 0) continue;
-        const int qb = n & 1;
-        if (n >= 2) mbar_wait(&sm.qempty[qb], ((n >> 1) - 1) & 1);
-        mbar_expect_tx(&sm.qfull[qb], qbytes);
-        const int hq0 = it.kvh * p.G, i0 = it.tile * p.sbox;
-        tma_load_4d(sm.q[qb], &qmap, 0, hq0, i0, it.b, &sm.qfull[qb]);
-        tma_load_4d(sm.q[qb] + kHalf, &qmap, 64, hq0, i0, it.b, &sm.qfull[qb]);
-        const int64_t row0 = (int64_t)(it.b * p.Hkv + it.kvh) * p.max_pos + it.kv0;
-        for (int j = 0; j < it.nblk; ++j, ++J) {
-          const int y = (int)(row0 + j * kN);
-          const int sk = J % kKStages, sv = J % kVStages;
-          if (J >= kKStages) mbar_wait(&sm.kempty[sk], ((J / kKStages) - 1) & 1);
-          mbar_expect_tx(&sm.kfull[sk], kTile);
-          tma_load_2d(sm.k[sk], &kmap, 0, y, &sm.kfull[sk]);
-          tma_load_2d(sm.k[sk] + kHalf, &kmap, 64, y, &sm.kfull[sk]);
-          if (J >= kVStages) mbar_wait(&sm.vempty[sv], ((J / kVStages) - 1) & 1);
-          mbar_expect_tx(&sm.vfull[sv], kTile);
-          tma_load_2d(sm.v[sv], &vmap, 0, y, &sm.vfull[sv]);
-          tma_load_2d(sm.v[sv] + kHalf, &vmap, 64, y, &sm.vfull[sv]);
-        }
-        ++n;
+      for (int j = 0; j < nblk; ++j) {
+        const int y = (int)(row0 + kv0 + j * kN);
+        const int sk = j % kKStages, sv = j % kVStages;
+        if (j >= kKStages) mbar_wait(&sm.kempty[sk], ((j / kKStages) - 1) & 1);
+        mbar_expect_tx(&sm.kfull[sk], kTile);
+        tma_load_2d(sm.k[sk], &kmap, 0, y, &sm.kfull[sk]);
+        tma_load_2d(sm.k[sk] + kHalf, &kmap, 64, y, &sm.kfull[sk]);
+        if (j >= kVStages) mbar_wait(&sm.vempty[sv], ((j / kVStages) - 1) & 1);
+        mbar_expect_tx(&sm.vfull[sv], kTile);
+        tma_load_2d(sm.v[sv], &vmap, 0, y, &sm.vfull[sv]);
+        tma_load_2d(sm.v[sv] + kHalf, &vmap, 64, y, &sm.vfull[sv]);
       }
     }
   } else if (warp == kMmaWarp) {
     // ---------------- MMA issuer ----------------
-    // block j of an item: S[j&1] = Q K_j^T, O[j&1] += P_j V_j (warpgroup j&1
-    // owns S/O[j&1]); uses of S[g] / P[g] are counted across items for the
-    // barrier phases
+    // block j: S[j&1] = Q K_j^T, O[j&1] += P_j V_j (warpgroup j&1 owns S/O[j&1])
     if (lane == 0) {
       const uint32_t id_qk = idesc_bf16(false), id_pv = idesc_bf16(true);
-      int n = 0, J = 0, us[2] = {0, 0}, up[2] = {0, 0};
-      for (int w = blockIdx.x; w < p.items; w += gridDim.x) {
-        const Item it = item_of(p, w);
-        if (it.nblk == 0) continue;
-        const int qb = n & 1;
-        mbar_wait(&sm.qfull[qb], (n >> 1) & 1);
-        const uint32_t aQ = smem_u32(sm.q[qb]);
-        for (int j = -1; j < it.nblk; ++j) {
-          const int jn = j + 1;  // Q K^T of the next block goes first so it overlaps softmax(j)
-          if (jn < it.nblk) {
-            const int st = (J + jn) % kKStages, g = jn & 1;
-            mbar_wait(&sm.kfull[st], ((J + jn) / kKStages) & 1);
-            if (us[g] > 0) mbar_wait(&sm.s_free[g], (us[g] - 1) & 1);
-            fence_after();
-            const uint32_t aK = smem_u32(sm.k[st]);
-            const uint32_t tS = tbase + g * kN;
-#pragma unroll
-            for (int ks = 0; ks < kD / 16; ++ks) {
-              const uint32_t off = (ks >> 2) * kHalf + (ks & 3) * 32;  // K step of 16 columns
-              mma_bf16(tS, sw128_desc(aQ + off, 16, 1024), sw128_desc(aK + off, 16, 1024), id_qk, ks > 0);
-            }
-            mma_commit(&sm.s_full[g]);
-            mma_commit(&sm.kempty[st]);
-            ++us[g];
-          }
-          if (j < 0) continue;
-          const int g = j & 1, sv = (J + j) % kVStages;
-          mbar_wait(&sm.vfull[sv], ((J + j) / kVStages) & 1);
-          mbar_wait(&sm.p_ready[g], up[g] & 1);
-          // the first P V of an item overwrites O[g]: the previous item's epilogue must have read it
-          if (j < 2 && n > 0) mbar_wait(&sm.o_free, (n - 1) & 1);
+      const uint32_t aQ = smem_u32(sm.q);
+      for (int j = -1; j < nblk; ++j) {
+        const int jn = j + 1;  // Q K^T of the next block goes first so it overlaps softmax(j)
+        if (jn < nblk) {
+          const int st = jn % kKStages, g = jn & 1;
+          mbar_wait(&sm.kfull[st], (jn / kKStages) & 1);
+          if (jn >= 2) mbar_wait(&sm.s_free[g], ((jn >> 1) - 1) & 1);
           fence_after();
-          const uint32_t aV = smem_u32(sm.v[sv]);
-          const uint32_t tO = tbase + 2 * kN + g * kD, tP = tbase + g * kN;
+          const uint32_t aK = smem_u32(sm.k[st]);
+          const uint32_t tS = tbase + g * kN;
 #pragma unroll
-          for (int ks = 0; ks < kN / 16; ++ks) {
-            // P from TMEM (16 keys = 8 packed columns per step); V: MN-major, 8-key groups of 1024 B.
-            // Q K^T of block j+2 (into the same S/P columns) is issued after this
-            // in program order; tcgen05.mma from one thread executes in order
-            mma_bf16_ts(tO, tP + ks * 8, sw128_desc(aV + ks * 2048, kHalf, 1024), id_pv,
-                        (j >= 2 || ks > 0) ? 1u : 0u);
+          for (int ks = 0; ks < kD / 16; ++ks) {
+            const uint32_t off = (ks >> 2) * kHalf + (ks & 3) * 32;  // K step of 16 columns
+            mma_bf16(tS, sw128_desc(aQ + off, 16, 1024), sw128_desc(aK + off, 16, 1024), id_qk, ks > 0);
           }
-          mma_commit(&sm.pv_done[g]);
-          mma_commit(&sm.vempty[sv]);
-          ++up[g];
+          mma_commit(&sm.s_full[g]);
+          mma_commit(&sm.kempty[st]);
         }
-        J += it.nblk;
-        ++n;
+        if (j < 0) continue;
+        const int g = j & 1;
+        const int sv = j % kVStages;
+        mbar_wait(&sm.vfull[sv], (j / kVStages) & 1);
+        mbar_wait(&sm.p_ready[g], (j >> 1) & 1);
+        fence_after();
+        const uint32_t aV = smem_u32(sm.v[sv]);
+        const uint32_t tO = tbase + 2 * kN + g * kD, tP = tbase + g * kN;
+#pragma unroll
+        for (int ks = 0; ks < kN / 16; ++ks) {
+          // P from TMEM (16 keys = 8 packed columns per step); V: MN-major, 8-key groups of 1024 B.
+          // Q K^T of block j+2 (into the same S/P columns) is issued after this
+          // in program order; tcgen05.mma from one thread executes in order
+          mma_bf16_ts(tO, tP + ks * 8, sw128_desc(aV + ks * 2048, kHalf, 1024), id_pv, (j >= 2 || ks > 0) ? 1u : 0u);
+        }
+        mma_commit(&sm.pv_done[g]);
+        mma_commit(&sm.vempty[sv]);
       }
     }
   } else {
-    // ---------------- softmax: warpgroup g takes blocks j = g, g+2, ... of each item ----------------
+    // ---------------- softmax: warpgroup g takes blocks j = g, g+2, ... ----------------
     // one thread per query row; each warpgroup keeps its own (m, l, O[g]) — an
     // intra-CTA split of the keys merged in the epilogue
     const int g = warp / kWgWarps, rt = tid - g * kWgThreads;
+    const int r = tile * kM + rt;
+    const bool row_ok = r < rows;
+    const int hl = row_ok ? r / p.S : 0, qi = row_ok ? r % p.S : 0;
+    const int head = kvh * p.G + hl;
+    const uint64_t* mrow = p.mask + ((int64_t)b * p.S + qi) * p.W;
     const uint32_t lane_off = (uint32_t)((warp % kWgWarps) * 32) << 16;
     const uint32_t tS = tbase + g * kN + lane_off, tO = tbase + 2 * kN + g * kD + lane_off;
-    const uint32_t tO0 = tbase + 2 * kN + lane_off, tO1 = tO0 + kD;
     const float sl2 = p.scale_log2;
-    const int hl = rt % p.G;
-    int n = 0, itg = 0;  // non-empty items done; blocks this warpgroup processed (barrier phases)
-    for (int w = blockIdx.x; w < p.items; w += gridDim.x) {
-      const Item it = item_of(p, w);
-      const int qi = it.tile * p.sbox + rt / p.G;
-      const bool row_ok = rt < qrows && qi < p.S;
-      const int qs = row_ok ? qi : 0;
-      const int head = it.kvh * p.G + hl;
-      const uint64_t* mrow = p.mask + ((int64_t)it.b * p.S + qs) * p.W;
-      const int64_t prow = (((int64_t)it.split * p.B + it.b) * p.Hq + head) * p.S + qi;
-      if (it.nblk == 0) {  // no keys in this split: empty partial
-        if (row_ok) {
-          if (p.splits == 1) {
-            for (int d = 0; d < kD; d += 8)
-              *reinterpret_cast<uint4*>(p.o + (((int64_t)it.b * p.S + qi) * p.Hq + head) * kD + d) =
-                  make_uint4(0, 0, 0, 0);
-          } else if (g == 0) {
-            for (int d = 0; d < kD; ++d) p.part_o[prow * kD + d] = 0.f;
-            p.part_ml[prow * 2] = -INFINITY;
-            p.part_ml[prow * 2 + 1] = 0.f;
-          }
+    float m_run = -INFINITY, l_run = 0.f;
+    int it = 0;
+    for (int j = g; j < nblk; j += 2, ++it) {
+      softmax_block(&sm.s_full[g], &sm.s_free[g], &sm.pv_done[g], &sm.p_ready[g], row_ok, mrow, p.S, ctx,
+                    kv0 + j * kN, kv1, tS, tO, it, it > 0, sl2, m_run, l_run);
+    }
+    if (it > 0) mbar_wait(&sm.pv_done[g], (it - 1) & 1);
+    // ---------------- epilogue: merge the two warpgroups ----------------
+    // every MMA has completed once both warpgroups passed their last pv_done
+    // (commit tracks all earlier tcgen05 ops), so the Q tile is free for (m, l)
+    float* xm = reinterpret_cast<float*>(sm.q);  // [2][kM] m, then [2][kM] l
+    wg_bar();
+    xm[g * kM + rt] = m_run;
+    xm[2 * kM + g * kM + rt] = l_run;
+    wg_bar();
+    fence_after();
+    const float m0 = xm[rt], m1 = xm[kM + rt];
+    const float mm = fmaxf(m0, m1);
+    const float w0 = (m0 == -INFINITY) ? 0.f : fast_exp2(m0 - mm);
+    const float w1 = (m1 == -INFINITY) ? 0.f : fast_exp2(m1 - mm);
+    const float l = w0 * xm[2 * kM + rt] + w1 * xm[3 * kM + rt];
+    const bool has0 = nblk > 0, has1 = nblk > 1;  // warpgroup 1 owns no block when nblk == 1
+    const uint32_t tO0 = tbase + 2 * kN + lane_off, tO1 = tO0 + kD;
+    // warpgroup g writes output columns [64 g, 64 g + 64)
+    const int64_t prow = (((int64_t)split * p.B + b) * p.Hq + head) * p.S + qi;
+    const float inv = (l > 0.f) ? 1.f / l : 0.f;
+    for (int c = 2 * g; c < 2 * g + 2; ++c) {
+      float o0[32], o1[32];
+      if (has0) tmem_ld32(tO0 + c * 32, o0);
+      if (has1) tmem_ld32(tO1 + c * 32, o1);
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) o0[jj] = (has0 ? w0 * o0[jj] : 0.f) + (has1 ? w1 * o1[jj] : 0.f);
+      if (!row_ok) continue;
+      if (p.splits == 1) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int jj = 0; jj < 32; jj += 2) {
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(o0[jj] * inv, o0[jj + 1] * inv);
+          pk[jj >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
         }
-        continue;
-      }
-      float m_run = -INFINITY, l_run = 0.f;
-      const int first = itg;
-      const int tk = 1 + 3 * ((w - (int)blockIdx.x) / (int)gridDim.x);
-      ATTN_STAMP(p, tk);
-      for (int j = g; j < it.nblk; j += 2, ++itg) {
-        softmax_block(&sm.s_full[g], &sm.s_free[g], &sm.pv_done[g], &sm.p_ready[g], row_ok, mrow, p.S, it.ctx,
-                      it.kv0 + j * kN, it.kv1, tS, tO, itg, itg > first, sl2, m_run, l_run);
-        if (j == 0) ATTN_STAMP(p, tk + 1);
-      }
-      if (itg > first) mbar_wait(&sm.pv_done[g], (itg - 1) & 1);
-      // ---------------- epilogue: merge the two warpgroups ----------------
-      // every MMA of this item has completed once both warpgroups passed their
-      // last pv_done (commit tracks all earlier tcgen05 ops), so this item's Q
-      // tile is free for (m, l); it is handed back to the producer (qempty)
-      const int qb = n & 1;
-      float* xm = reinterpret_cast<float*>(sm.q[qb]);  // [2][kM] m, then [2][kM] l
-      wg_bar();
-      xm[g * kM + rt] = m_run;
-      xm[2 * kM + g * kM + rt] = l_run;
-      wg_bar();
-      fence_after();
-      const float m0 = xm[rt], m1 = xm[kM + rt];
-      const float mm = fmaxf(m0, m1);
-      const float w0 = (m0 == -INFINITY) ? 0.f : fast_exp2(m0 - mm);
-      const float w1 = (m1 == -INFINITY) ? 0.f : fast_exp2(m1 - mm);
-      const float l = w0 * xm[2 * kM + rt] + w1 * xm[3 * kM + rt];
-      const bool has1 = it.nblk > 1;  // warpgroup 1 owns no block when nblk == 1
-      const float inv = (l > 0.f) ? 1.f / l : 0.f;
-      // warpgroup g writes output columns [64 g, 64 g + 64)
-      for (int c = 2 * g; c < 2 * g + 2; ++c) {
-        float o0[32], o1[32];
-        tmem_ld32(tO0 + c * 32, o0);
-        if (has1) tmem_ld32(tO1 + c * 32, o1);
-        if (c == 2 * g + 1) {  // O fully read: the next item's first P V may overwrite it
-          fence_before();
-          mbar_arrive(&sm.o_free);
-        }
+        uint4* dst = reinterpret_cast<uint4*>(p.o + (((int64_t)b * p.S + qi) * p.Hq + head) * kD + c * 32);
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) o0[jj] = w0 * o0[jj] + (has1 ? w1 * o1[jj] : 0.f);
-        if (!row_ok) continue;
-        if (p.splits == 1) {
-          uint32_t pk[16];
+        for (int q4 = 0; q4 < 4; ++q4) dst[q4] = make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+      } else {
+        float4* dst = reinterpret_cast<float4*>(p.part_o + prow * kD + c * 32);
 #pragma unroll
-          for (int jj = 0; jj < 32; jj += 2) {
-            const __nv_bfloat162 h2 = __floats2bfloat162_rn(o0[jj] * inv, o0[jj + 1] * inv);
-            pk[jj >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
-          }
-          uint4* dst = reinterpret_cast<uint4*>(p.o + (((int64_t)it.b * p.S + qi) * p.Hq + head) * kD + c * 32);
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4)
-            dst[q4] = make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
-        } else {
-          float4* dst = reinterpret_cast<float4*>(p.part_o + prow * kD + c * 32);
-#pragma unroll
-          for (int q4 = 0; q4 < 8; ++q4)
-            dst[q4] = make_float4(o0[q4 * 4], o0[q4 * 4 + 1], o0[q4 * 4 + 2], o0[q4 * 4 + 3]);
-        }
+        for (int q4 = 0; q4 < 8; ++q4) dst[q4] = make_float4(o0[q4 * 4], o0[q4 * 4 + 1], o0[q4 * 4 + 2], o0[q4 * 4 + 3]);
       }
-      if (p.splits > 1 && row_ok && g == 0) {
-        p.part_ml[prow * 2] = mm;
-        p.part_ml[prow * 2 + 1] = l;
-      }
-      // xm was written through the generic proxy; the next TMA write of this buffer is async-proxy
-      fence_async_smem();
-      mbar_arrive(&sm.qempty[qb]);
-      ATTN_STAMP(p, tk + 2);
-      ++n;
+    }
+    if (p.splits > 1 && row_ok && g == 0) {
+      p.part_ml[prow * 2] = mm;
+      p.part_ml[prow * 2 + 1] = l;
     }
   }
-  ATTN_STAMP(p, 31);
   fence_before();
   __syncthreads();
   if (warp == kMmaWarp) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
@@ -711,22 +604,17 @@ __global__ void tree_attn_combine_kernel(Params p) {
 
 constexpr int kSmem = (int)sizeof(Smem) + 1024;
 
-static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+// TMA descriptor over a [rows][128] bf16 cache viewed as 2D, box 64 x 128, 128B swizzle
+static int make_kv_map(CUtensorMap* map, const void* base, uint64_t rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess && fn)
-      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(SSSD_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  return encode;
-}
-
-// TMA descriptor over a [rows][128] bf16 cache viewed as 2D, box 64 x 128, 128B swizzle
-static int make_kv_map(CUtensorMap* map, const void* base, uint64_t rows) {
-  const auto encode = tmap_encoder();
-  if (!encode) return fail(SSSD_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[2] = {(cuuint64_t)kD, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)kD * 2};
   const cuuint32_t box[2] = {64, (cuuint32_t)kN};
@@ -738,23 +626,6 @@ static int make_kv_map(CUtensorMap* map, const void* base, uint64_t rows) {
   return SSSD_OK;
 }
 
-// TMA descriptor over the queries [B][S][Hq][128] bf16, box 64 dims x G heads x
-// sbox queries x 1 batch, 128B swizzle: the box lands as Q tile rows
-// (i - i0) * G + head_in_group; queries past S are zero-filled
-static int make_q_map(CUtensorMap* map, const void* base, int B, int S, int Hq, int G, int sbox) {
-  const auto encode = tmap_encoder();
-  if (!encode) return fail(SSSD_E_CUDA, "cuTensorMapEncodeTiled unavailable");
-  const cuuint64_t dims[4] = {(cuuint64_t)kD, (cuuint64_t)Hq, (cuuint64_t)S, (cuuint64_t)B};
-  const cuuint64_t strides[3] = {(cuuint64_t)kD * 2, (cuuint64_t)Hq * kD * 2, (cuuint64_t)S * Hq * kD * 2};
-  const cuuint32_t box[4] = {64, (cuuint32_t)G, (cuuint32_t)sbox, 1};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
-                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(SSSD_E_CUDA, "cuTensorMapEncodeTiled (Q) failed (%d)", (int)r);
-  return SSSD_OK;
-}
-
 }  // namespace attn
 }  // namespace sssd
 
@@ -762,58 +633,33 @@ using namespace sssd;
 
 extern "C" {
 
-#ifdef SSSD_ATTN_TRACE
-static unsigned long long* g_attn_trace = nullptr;
-static int g_attn_trace_ctas = 0;
-// diagnostic builds only: copy the last launch's per-CTA stamps ([ctas][32] u64) to host
-int sssd_attn_trace_read(unsigned long long* host, int max_ctas) {
-  if (!g_attn_trace) return 0;
-  const int n = g_attn_trace_ctas < max_ctas ? g_attn_trace_ctas : max_ctas;
-  cudaDeviceSynchronize();
-  cudaMemcpy(host, g_attn_trace, (size_t)n * 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-  return n;
-}
-#endif
-
 static int attn_max_splits(int32_t max_pos) {  // every split keeps >= 1024 keys (bounds the workspace)
   int cap = 1;
   while (cap < 64 && (max_pos / (cap * 2)) >= 1024) cap *= 2;
   return cap;
 }
 
-static int attn_n_sm() {
+// Split count minimising waves x (key blocks per CTA + fixed per-CTA cost).
+// The fixed cost (TMEM alloc, Q tile, pipeline fill, epilogue, partial
+// write-back) was measured at ~4.5 key blocks on B200 (cfg3: 1 split beats 2;
+// cfg4: 2 beat 4 and 8).
+static int attn_splits(int32_t B, int32_t Hq, int32_t Hkv, int32_t S, int32_t max_pos) {
   static int n_sm = 0;
   if (!n_sm) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n_sm <= 0) n_sm = 148;
   }
-  return n_sm;
-}
-
-// queries per row tile: the Q box holds G heads x sbox queries (<= 128 rows)
-static int attn_sbox(int G, int S) { return S < attn::kM / G ? S : attn::kM / G; }
-
-// Split count minimising (items per CTA) x (key blocks per item + per-item
-// cost) for the persistent kernel (one CTA per SM, items round-robin).  The
-// per-item cost of an item boundary (epilogue and the next item's first
-// Q K^T, overlapped with the producer's prefetch) is ~1 key block.
-#ifndef SSSD_ATTN_ITEM_COST
-#define SSSD_ATTN_ITEM_COST 1.0
-#endif
-static int attn_splits(int32_t B, int32_t Hq, int32_t Hkv, int32_t S, int32_t max_pos) {
-  const int n_sm = attn_n_sm();
   const int G = Hq / Hkv;
-  const int sbox = attn_sbox(G, S);
-  const int tiles = (S + sbox - 1) / sbox;
-  const int64_t units = (int64_t)tiles * B * Hkv;
+  const int tiles = (G * S + attn::kM - 1) / attn::kM;
+  const int64_t ctas = (int64_t)tiles * B * Hkv;
   const int nb = (max_pos + attn::kN - 1) / attn::kN;
   const int cap = attn_max_splits(max_pos);
   int best = 1;
   double best_cost = 1e300;
   for (int s = 1; s <= cap; ++s) {
-    const double per_cta = (double)((units * s + n_sm - 1) / n_sm);
-    const double cost = per_cta * ((nb + s - 1) / s + SSSD_ATTN_ITEM_COST);
+    const double waves = (double)((ctas * s + n_sm - 1) / n_sm);
+    const double cost = waves * ((nb + s - 1) / s + 4.5);
     if (cost < best_cost * 0.999) best_cost = cost, best = s;
   }
   return best;
@@ -830,7 +676,6 @@ int sssd_tree_attention(const uint16_t* q, const uint16_t* k, const uint16_t* v,
                         size_t workspace_bytes, void* stream) {
   if (head_dim != attn::kD) return fail(SSSD_E_LIMIT, "tree attention supports head_dim 128, got %d", head_dim);
   if (B <= 0 || S <= 0 || Hq <= 0 || Hkv <= 0 || Hq % Hkv) return fail(SSSD_E_ARG, "bad attention shape");
-  if (Hq / Hkv > attn::kM) return fail(SSSD_E_LIMIT, "tree attention supports <= %d query heads per kv head", attn::kM);
   if (S > SSSD_MAX_DRAFT) return fail(SSSD_E_LIMIT, "S=%d exceeds %d", S, SSSD_MAX_DRAFT);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   attn::Params p;
@@ -858,31 +703,17 @@ int sssd_tree_attention(const uint16_t* q, const uint16_t* k, const uint16_t* v,
     p.part_o = nullptr;
     p.part_ml = nullptr;
   }
-  p.sbox = attn_sbox(p.G, S);
-  p.tiles = (S + p.sbox - 1) / p.sbox;
-  p.items = p.tiles * B * Hkv * p.splits;
-  CUtensorMap kmap, vmap, qmap;
+  CUtensorMap kmap, vmap;
   const uint64_t rows = (uint64_t)B * Hkv * max_pos;
   int rc = attn::make_kv_map(&kmap, k, rows);
   if (!rc) rc = attn::make_kv_map(&vmap, v, rows);
-  if (!rc) rc = attn::make_q_map(&qmap, q, B, S, Hq, p.G, p.sbox);
   if (rc) return rc;
-  const int grid = p.items < attn_n_sm() ? p.items : attn_n_sm();
+  const int tiles = (p.G * S + attn::kM - 1) / attn::kM;
   rc = cuda_check(cudaFuncSetAttribute(attn::tree_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        attn::kSmem),
                   "tree_attn smem attribute");
   if (rc) return rc;
-  p.trace = nullptr;
-#ifdef SSSD_ATTN_TRACE
-  static unsigned long long* trace_buf = nullptr;
-  if (!trace_buf && cudaMalloc(&trace_buf, 1024 * 32 * sizeof(unsigned long long)) != cudaSuccess)
-    return fail(SSSD_E_CUDA, "trace buffer");
-  cudaMemsetAsync(trace_buf, 0, 1024 * 32 * sizeof(unsigned long long), st);
-  p.trace = trace_buf;
-  g_attn_trace = trace_buf;
-  g_attn_trace_ctas = grid;
-#endif
-  attn::tree_attn_kernel<<<grid, attn::kThreads, attn::kSmem, st>>>(p, kmap, vmap, qmap);
+  attn::tree_attn_kernel<<<dim3(tiles, B * Hkv, p.splits), attn::kThreads, attn::kSmem, st>>>(p, kmap, vmap);
   if ((rc = cuda_check(cudaGetLastError(), "tree_attn_kernel launch"))) return rc;
   if (p.splits > 1) {
     attn::tree_attn_combine_kernel<<<B * Hq * S, attn::kD, 0, st>>>(p);
