@@ -17,11 +17,16 @@ for name, (B, S, Hq, Hkv, ctx) in {"cfg3": (32, 32, 32, 8, 4096), "cfg4": (8, 16
     mask = torch.full((B, S, 1), -1, dtype=torch.int64, device="cuda")
     c = torch.full((B,), ctx, dtype=torch.int32, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    # ATTN_FLUSH=rw: after the write, read a second 256 MB buffer so L2 holds
+    # clean lines (no dirty write-backs from the flush inside the timed region)
+    clean = torch.ones(64 << 20, dtype=torch.float32, device="cuda") if os.environ.get("ATTN_FLUSH") == "rw" else None
     for _ in range(3):
         tree_attention(q, k, v, mask, c)
     ts = []
     for _ in range(20):
         flush.zero_()
+        if clean is not None:
+            clean.sum()
         a, b = torch.cuda.Event(True), torch.cuda.Event(True)
         a.record(); tree_attention(q, k, v, mask, c); b.record()
         torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
