@@ -115,7 +115,7 @@ __device__ __forceinline__ void cta_generate(const LsPar par, int jb, int je, ui
     uint32_t pid = 0;
     if (live) {
       const uint32_t tr = par.tbr()[j], rk = tr >> kTbBits, pc = par.cnt()[j];
-      const double ratio = cnt == pc ? 1.0 : __ddiv_rn((double)cnt, (double)pc);  // ref fusion.py:259
+      const double ratio = ratio_rn(cnt, pc);  // ref fusion.py:259
       pp = __dmul_rn(par.pp()[j], ratio);
       const double pr = __dmul_rn(pp, drow[rk * disc_stride]);  // ref fusion.py:246
       k0 = ~(uint64_t)__double_as_longlong(pr);

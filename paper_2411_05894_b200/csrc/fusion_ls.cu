@@ -112,7 +112,7 @@ __device__ SSSD_LS_CALL uint2 ls_generate(const LsPar par, int np, uint32_t E, L
     uint32_t pid = 0;
     if (live) {
       const uint32_t tr = par.tbr()[j], rk = tr >> kTbBits, pc = par.cnt()[j];
-      const double ratio = cnt == pc ? 1.0 : __ddiv_rn((double)cnt, (double)pc);  // c/c == 1.0 exactly
+      const double ratio = ratio_rn(cnt, pc);  // == __ddiv_rn (common.cuh)
       pp = __dmul_rn(par.pp()[j], ratio);                                           // ref fusion.py:259
       const double pr = __dmul_rn(pp, drow[rk * disc_stride]);                    // ref fusion.py:246
       k0 = ~(uint64_t)__double_as_longlong(pr);
