@@ -212,9 +212,8 @@ __device__ SSSD_LS_CALL uint2 ls_generate(const LsPar par, int np, uint32_t E, L
     const uint32_t wt = w ? el_wt(lm) : 0u;
     const uint32_t hasm = __ballot_sync(SSSD_FULL, has);
     if (hasm) {  // (a carried run always continues at lane 0, so none is open otherwise)
-      const unsigned long long key = has ? ((unsigned long long)j << 32 | tk) : (1ull << 63 | (unsigned)lane);
-      const uint32_t gm = __match_any_sync(SSSD_FULL, key);
-      const int lo_l = __ffs(gm) - 1, hi_l = 31 - __clz(gm);
+      int lo_l, hi_l;
+      run_bounds(has, (uint32_t)j, tk, lo_l, hi_l);
       // run minimum of orig and run sum of weights (segmented down-scans;
       // runs are lane intervals)
       uint32_t fm = orig, cnt = wt;
@@ -235,7 +234,7 @@ __device__ SSSD_LS_CALL uint2 ls_generate(const LsPar par, int np, uint32_t E, L
         fm = min(fm, c_first);
         start = c_start;
       }
-      const bool to_next = !last && has && (gm >> 31) != 0;  // my run reaches the look-ahead
+      const bool to_next = !last && has && hi_l == 31;  // my run reaches the look-ahead
       emit(owned && has && lane == hi_l && !to_next, j, tk, cnt, fm, start, i + 1);
       c_open = __ballot_sync(SSSD_FULL, lane == 30 && to_next) != 0;
       if (c_open) {

@@ -93,6 +93,21 @@ __device__ __forceinline__ bool k_less(uint64_t a0, uint64_t a1, uint64_t b0, ui
 constexpr uint32_t kTbBits = 22;
 constexpr uint32_t kTbMask = (1u << kTbBits) - 1;
 
+// Lane bounds [lo, hi] of this lane's run of equal (parent j, token) keys in a
+// generation chunk.  Runs are lane intervals (a parent's elements are sorted
+// by their depth-d token; lanes without an element are runs of one), so a run
+// starts where the key differs from the previous lane's: one ballot of the run
+// heads (measured 2 % faster at cfg2 than __match_any_sync on the 64-bit key).
+__device__ __forceinline__ void run_bounds(bool has, uint32_t j, uint32_t tk, int& lo_l, int& hi_l) {
+  const int lane = lane_id();
+  const uint32_t kj = has ? j : 0xffffffffu, kt = has ? tk : (uint32_t)lane;
+  const uint32_t pj = __shfl_up_sync(SSSD_FULL, kj, 1), pt = __shfl_up_sync(SSSD_FULL, kt, 1);
+  const uint32_t heads = __ballot_sync(SSSD_FULL, lane == 0 || !has || pj != kj || pt != kt);
+  const uint32_t le = lanemask_lt() | (1u << lane), above = heads & ~le;
+  lo_l = 31 - __clz(heads & le);
+  hi_l = above ? __ffs(above) - 2 : 31;
+}
+
 __host__ __device__ inline int top_bytes(int S) { return (S * 24 + 15) / 16 * 16; }
 
 
