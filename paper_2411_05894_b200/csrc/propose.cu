@@ -1040,6 +1040,13 @@ __global__ void __launch_bounds__(1024)
                       uint32_t* idx_ws, int64_t cap, int64_t cap2, Cols cols) {
   const int b = c.b0 + blockIdx.x;
   const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5, nw = blockDim.x >> 5;
+#ifdef SSSD_LK_PROBE  // measurement builds: scan phases in slots 4-7 of the lookup probe
+  const long long sc_t0 = clock64();
+#define SC_STAMP(i) \
+  if (g_lk_cyc && tid == 0) g_lk_cyc[(size_t)b * 8 + (i)] = clock64() - sc_t0;
+#else
+#define SC_STAMP(i)
+#endif
   __shared__ uint32_t s_tail[SSSD_MAX_P];
   __shared__ int s_wsum[32];
   extern __shared__ __align__(16) uint32_t s_idx[];  // >= kSortSmem words
@@ -1184,6 +1191,7 @@ __global__ void __launch_bounds__(1024)
     __syncthreads();  // s_wsum reuse
   }
   if (tid == 0) in_n[b] = total;
+  SC_STAMP(4)
   sssd_elem* out = sorted + (size_t)b * cap;
   if (total == 0) return;
   __syncthreads();
@@ -1202,6 +1210,7 @@ __global__ void __launch_bounds__(1024)
     for (int e = tid; e < total; e += blockDim.x) {
       const sssd_elem el = r[e];
       const uint32_t len = el_len(el.len_m);
+      srt[e] = el.off << 4 | el_m(el.len_m);  // (position, m) for the merge path's output (L < 2^28)
       uint64_t h = 0, l = 0;
       for (uint32_t d = 0; d < len; ++d) {
         const uint32_t tk = seq[el.off + d];
@@ -1214,6 +1223,94 @@ __global__ void __launch_bounds__(1024)
       kl[e] = l;
     }
     const bool narrow_keys = !__syncthreads_or(wide);
+    SC_STAMP(5)
+    const int scan_words = input_scan_smem_bytes(blockDim.x, c.IBL) / 4;
+    if (narrow_keys && total > 256 && total * 10 + 2 <= scan_words && L < (1 << 28)) {
+      // merge sort (hundreds to a few thousand occurrences): 32-element runs
+      // rank-sorted, then log2(total / 32) merge levels in which every key finds
+      // its output slot with one binary search in the partner run (ties: the
+      // left run's keys first = position order).  Each thread's chain is
+      // ~6 + log2(total) steps per level instead of the run-rank path's
+      // (total / 32) binary searches or the bitonic network's shared-memory
+      // traffic (cfg4, 32k prompt-heavy contexts: 520 occurrences 17 -> 5 us,
+      // 1,047 occurrences 32 -> 6 us).  Keys, then ping-pong (h, l, index)
+      // arrays: B aliases kh / kl, A follows (10 words per occurrence).  The
+      // payload is (position << 4 | m), so the output needs no global reads:
+      // an element's tokens are its key's 16-bit fields.
+      uint64_t* Bh = kh;
+      uint64_t* Bl = kl;
+      uint32_t* Bi = reinterpret_cast<uint32_t*>(kl + total);
+      uint64_t* Ah = reinterpret_cast<uint64_t*>(s_idx + ((5 * total + 1) & ~1));
+      uint64_t* Al = Ah + total;
+      uint32_t* Ai = reinterpret_cast<uint32_t*>(Al + total);
+      for (int e = tid; e < total; e += blockDim.x) {
+        const int r0 = e & ~31, rn = min(32, total - r0);
+        const uint64_t h = kh[e], l = kl[e];
+        int lr = 0;
+        for (int j = r0; j < r0 + rn; ++j) {
+          const uint64_t hj = kh[j], lj = kl[j];
+          lr += (hj < h || (hj == h && (lj < l || (lj == l && j < e)))) ? 1 : 0;
+        }
+        Ah[r0 + lr] = h;
+        Al[r0 + lr] = l;
+        Ai[r0 + lr] = Bi[e];  // (position, m) stashed by the key build
+      }
+      __syncthreads();
+      uint64_t *sh = Ah, *sl = Al, *dh = Bh, *dl = Bl;
+      uint32_t *si = Ai, *di = Bi;
+      for (int lw = 5; (1 << lw) < total; ++lw) {
+        const int w = 1 << lw;
+        for (int i = tid; i < total; i += blockDim.x) {
+          const int rid = i >> lw, k = i - (rid << lw), ps = (rid ^ 1) << lw;
+          const int pl = max(0, min(w, total - ps));
+          const uint64_t h = sh[i], l = sl[i];
+          const bool left = (rid & 1) == 0;
+          int lo = 0, hi = pl;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            const uint64_t hx = sh[ps + mid], lx = sl[ps + mid];
+            if (hx < h || (hx == h && (left ? lx < l : lx <= l))) lo = mid + 1;
+            else hi = mid;
+          }
+          const int o = ((rid & ~1) << lw) + k + lo;
+          dh[o] = h;
+          dl[o] = l;
+          di[o] = si[i];
+        }
+        __syncthreads();
+        uint64_t* th = sh;
+        sh = dh;
+        dh = th;
+        uint64_t* tl = sl;
+        sl = dl;
+        dl = tl;
+        uint32_t* ti = si;
+        si = di;
+        di = ti;
+      }
+      SC_STAMP(6)
+      const Cols cb{cols.meta ? cols.meta + (size_t)b * cols.stride : nullptr,
+                    cols.orig + (size_t)b * cols.stride, cols.tok + (size_t)b * cols.stride * c.IBL, cols.stride};
+      for (int i = tid; i < total; i += blockDim.x) {
+        const uint32_t pm = si[i], pos = pm >> 4;
+        sssd_elem el;
+        el.off = pos;
+        el.orig = pos;
+        el.len_m = (uint32_t)min(c.IBL, L - (int)pos) | (pm & 15u) << 8;
+        el.pad = 0;
+        out[i] = el;
+        if (cb.meta) {
+          cb.meta[i] = el.len_m & 0xffffu;
+          cb.orig[i] = pos;
+          const uint64_t h = sh[i], l = sl[i];
+          const uint32_t len = el_len(el.len_m);
+          for (uint32_t d = 0; d < len; ++d)
+            cb.tok[d * cb.stride + i] = (uint32_t)(((d < 4 ? h >> (16 * (3 - d)) : l >> (16 * (7 - d))) & 0xffffu) - 1);
+        }
+      }
+      SC_STAMP(7)
+      return;
+    }
     if (narrow_keys && total > 1024) {
       // many occurrences (prompt-heavy long contexts): a bitonic sort of the
       // (key, position) triples in shared memory, O(n log^2 n) instead of
@@ -1247,6 +1344,7 @@ __global__ void __launch_bounds__(1024)
           __syncthreads();
         }
       }
+      SC_STAMP(6)
       const Cols cb{cols.meta ? cols.meta + (size_t)b * cols.stride : nullptr,
                     cols.orig + (size_t)b * cols.stride, cols.tok + (size_t)b * cols.stride * c.IBL, cols.stride};
       for (int i = tid; i < total; i += blockDim.x) {
@@ -1254,6 +1352,7 @@ __global__ void __launch_bounds__(1024)
         out[i] = el;
         if (cb.meta) write_cols(cb, i, el, seq);
       }
+      SC_STAMP(7)
       return;
     }
     if (narrow_keys) {
@@ -1269,6 +1368,7 @@ __global__ void __launch_bounds__(1024)
         lrk[e] = (uint32_t)lr;
       }
       __syncthreads();
+      SC_STAMP(6)
       const Cols cb{cols.meta ? cols.meta + (size_t)b * cols.stride : nullptr,
                     cols.orig + (size_t)b * cols.stride, cols.tok + (size_t)b * cols.stride * c.IBL, cols.stride};
       for (int e = tid; e < total; e += blockDim.x) {
@@ -1291,6 +1391,7 @@ __global__ void __launch_bounds__(1024)
         out[rank] = el;
         if (cb.meta) write_cols(cb, rank, el, seq);
       }
+      SC_STAMP(7)
       return;
     }
     __syncthreads();  // the key area is reused below

@@ -69,8 +69,11 @@ class InputCache:
         return input_trees_batch([self.sequence], self.max_prefix_len, self.input_branch_len)[0]
 
 
-def input_trees_batch(seqs: list[list[int]], P: int, ibl: int, device=None) -> list[list[ContinuationTree]]:
-    """Device input scan for B sequences, materialised as reference trees."""
+def input_elements_batch(seqs: list[list[int]], P: int, ibl: int, device=None) -> list[np.ndarray]:
+    """Device input scan for B sequences: per sequence the [n, 4] u32 element
+    rows (continuation start, first position, len | m << 8, 0) in the kernel's
+    output order -- sorted by continuation string (a proper prefix first),
+    ties by position, as the fusion consumes them."""
     from .fusion import _cfg_struct
 
     dev = torch.device(device) if device is not None else _lib.require_cuda()
@@ -96,9 +99,15 @@ def input_trees_batch(seqs: list[list[int]], P: int, ibl: int, device=None) -> l
     check(lib().sssd_input_scan(seqs_c, c, ptr(el), ptr(n_el), ptr(ws), ws.numel(), stream_ptr(dev)))
     el_h = el.cpu().numpy().view(np.uint32).reshape(B, cap, 4)
     n_h = n_el.cpu().tolist()
+    return [el_h[b, : n_h[b]].copy() for b in range(B)]
+
+
+def input_trees_batch(seqs: list[list[int]], P: int, ibl: int, device=None) -> list[list[ContinuationTree]]:
+    """Device input scan for B sequences, materialised as reference trees."""
+    rows_all = input_elements_batch(seqs, P, ibl, device)
     out = []
     for b, s in enumerate(seqs):
-        rows = el_h[b, : n_h[b]]
+        rows = rows_all[b]
         rows = rows[np.argsort(rows[:, 1], kind="stable")]  # insertion order = e ascending
         trees = []
         for p in range(1, P + 1):

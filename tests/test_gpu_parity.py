@@ -217,6 +217,34 @@ def test_long_context_bitonic_input_sort(alphabet, dec_len):
         assert (f.tokens, f.parents, f.depths) == (d.tokens, d.parents, d.depths)
 
 
+@pytest.mark.parametrize("L,alphabet", [(3000, 9), (4000, 12), (9000, 8), (20000, 10), (30000, 14), (2000, 3)])
+def test_input_scan_element_order(L, alphabet):
+    """The input scan's element rows, in output order, are sorted by
+    continuation string (a proper prefix first) with ties by position, and hold
+    exactly the occurrences of the last token with their backward-match
+    lengths: checked row by row against numpy for occurrence counts across the
+    run-rank (<= 256), merge (256-2,457 at 1,024 threads, 256-409 at 256) and
+    bitonic (> 2,457) sort paths of both launch widths."""
+    from paper_2411_05894_b200.input_cache import input_elements_batch
+
+    rng = np.random.default_rng(L + alphabet)
+    P, ibl = 4, 8
+    seqs = [rng.integers(0, alphabet, L).tolist() for _ in range(3)]
+    seqs.append(workload.prompt_heavy_contexts(1, max(L, 4097), 32000)[0].tolist())
+    got = input_elements_batch(seqs, P, ibl)
+    for seq, rows in zip(seqs, got):
+        s = np.asarray(seq)
+        n = len(s)
+        last = s[-1]
+        occ = [e for e in range(1, n) if s[e - 1] == last]
+        m = O.match_lengths(seq, P)
+        want = sorted(occ, key=lambda e: (tuple(s[e:e + min(ibl, n - e)].tolist()), e))
+        assert rows.shape[0] == len(want)
+        assert rows[:, 0].tolist() == want and rows[:, 1].tolist() == want
+        assert [int(x) & 0xFF for x in rows[:, 2]] == [min(ibl, n - e) for e in want]
+        assert [(int(x) >> 8) & 0xFF for x in rows[:, 2]] == [int(m[e]) for e in want]
+
+
 def test_verify_matches_oracle():
     rng = np.random.default_rng(9)
     corpus = workload.corpus(50_000, 50)
