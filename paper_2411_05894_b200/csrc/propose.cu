@@ -1032,6 +1032,9 @@ __global__ void __launch_bounds__(1024) input_index_build_kernel(sssd_seqs seqs,
 // --------------------------------------------------------------------------
 
 constexpr int kSortSmem = 4096;
+#ifndef SSSD_SCAN_MERGE_MIN
+#define SSSD_SCAN_MERGE_MIN 32  // occurrence counts above this take the merge sort (when it fits)
+#endif
 
 // Launched with 256 threads, or 1024 for long contexts (input_scan_threads);
 // dynamic shared memory input_scan_smem_bytes(threads, IBL).
@@ -1225,8 +1228,8 @@ __global__ void __launch_bounds__(1024)
     const bool narrow_keys = !__syncthreads_or(wide);
     SC_STAMP(5)
     const int scan_words = input_scan_smem_bytes(blockDim.x, c.IBL) / 4;
-    if (narrow_keys && total > 256 && total * 10 + 2 <= scan_words && L < (1 << 28)) {
-      // merge sort (hundreds to a few thousand occurrences): 32-element runs
+    if (narrow_keys && total > SSSD_SCAN_MERGE_MIN && total * 10 + 2 <= scan_words && L < (1 << 28)) {
+      // merge sort (33 to a few thousand occurrences): 32-element runs
       // rank-sorted, then log2(total / 32) merge levels in which every key finds
       // its output slot with one binary search in the partner run (ties: the
       // left run's keys first = position order).  Each thread's chain is

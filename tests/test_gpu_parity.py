@@ -217,14 +217,15 @@ def test_long_context_bitonic_input_sort(alphabet, dec_len):
         assert (f.tokens, f.parents, f.depths) == (d.tokens, d.parents, d.depths)
 
 
-@pytest.mark.parametrize("L,alphabet", [(3000, 9), (4000, 12), (9000, 8), (20000, 10), (30000, 14), (2000, 3)])
+@pytest.mark.parametrize("L,alphabet", [(3000, 9), (4000, 12), (9000, 8), (20000, 10), (30000, 14), (2000, 3),
+                                        (600, 40), (200, 50)])
 def test_input_scan_element_order(L, alphabet):
     """The input scan's element rows, in output order, are sorted by
     continuation string (a proper prefix first) with ties by position, and hold
     exactly the occurrences of the last token with their backward-match
     lengths: checked row by row against numpy for occurrence counts across the
-    run-rank (<= 256), merge (256-2,457 at 1,024 threads, 256-409 at 256) and
-    bitonic (> 2,457) sort paths of both launch widths."""
+    run-rank (<= 32), merge (33-2,457 at 1,024 threads, 33-409 at 256) and
+    bitonic / run-rank fallbacks (larger counts) of both launch widths."""
     from paper_2411_05894_b200.input_cache import input_elements_batch
 
     rng = np.random.default_rng(L + alphabet)
