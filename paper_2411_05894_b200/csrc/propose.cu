@@ -1035,6 +1035,9 @@ constexpr int kSortSmem = 4096;
 #ifndef SSSD_SCAN_MERGE_MIN
 #define SSSD_SCAN_MERGE_MIN 32  // occurrence counts above this take the merge sort (when it fits)
 #endif
+#ifndef SSSD_SCAN_HFIRST
+#define SSSD_SCAN_HFIRST 1
+#endif
 
 // Launched with 256 threads, or 1024 for long contexts (input_scan_threads);
 // dynamic shared memory input_scan_smem_bytes(threads, IBL).
@@ -1271,9 +1274,20 @@ __global__ void __launch_bounds__(1024)
           int lo = 0, hi = pl;
           while (lo < hi) {
             const int mid = (lo + hi) >> 1;
+#if SSSD_SCAN_HFIRST  // the low word only on a tie of the high words (half the shared-memory bytes)
+            const uint64_t hx = sh[ps + mid];
+            bool before = hx < h;
+            if (hx == h) {
+              const uint64_t lx = sl[ps + mid];
+              before = left ? lx < l : lx <= l;
+            }
+            if (before) lo = mid + 1;
+            else hi = mid;
+#else
             const uint64_t hx = sh[ps + mid], lx = sl[ps + mid];
             if (hx < h || (hx == h && (left ? lx < l : lx <= l))) lo = mid + 1;
             else hi = mid;
+#endif
           }
           const int o = ((rid & ~1) << lw) + k + lo;
           dh[o] = h;
