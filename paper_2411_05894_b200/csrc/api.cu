@@ -79,6 +79,8 @@ static KCfg kcfg(const sssd_cfg* c) {
   k.P = c->P;
   k.S = c->dec_len;
   k.BL = c->branch_len;
+  k.TS = (c->branch_len + 3) & ~3;
+  k.tab16 = 1;
   k.IBL = c->input_branch_len;
   k.M = c->M;
   k.T = c->T;
@@ -169,7 +171,7 @@ static PropWs carve_propose(uint8_t* base, const sssd_cfg* c, int B, int max_len
   unsigned long long* status = carve_status(cv);
   PropWs w;
   const size_t PM = (size_t)c->P * c->M;
-  w.ds_tab = cv.take<uint32_t>((size_t)B * PM * c->branch_len);
+  w.ds_tab = cv.take<uint32_t>((size_t)B * PM * ((c->branch_len + 3) & ~3));  // 16-byte rows (KCfg::TS)
   w.ds_len = cv.take<uint8_t>((size_t)B * PM);
   w.ds_el = cv.take<sssd_elem>((size_t)B * PM);
   w.ds_n = cv.take<int32_t>((size_t)B);
@@ -705,6 +707,8 @@ int sssd_ds_lookup(const sssd_ds* ds, const sssd_seqs* seqs, const sssd_cfg* cfg
   KCfg kk = kcfg(cfg);
   kk.b0 = 0;
   kk.b1 = seqs->B;
+  kk.TS = cfg->branch_len;  // the caller's table layout: [B][P][M][branch_len]
+  kk.tab16 = (cfg->branch_len % 4 == 0 && (reinterpret_cast<uintptr_t>(tab) & 15) == 0) ? 1 : 0;
   if (!cfg->has_separator)
     ds_lookup_warp_kernel<<<(seqs->B + 3) / 4, 128, 0, static_cast<cudaStream_t>(stream)>>>(
         *ds, *seqs, kk, tab, lens, el, n_el, lk, Cols{});

@@ -37,6 +37,21 @@ __device__ __forceinline__ int cmp_str(const uint32_t* a, uint32_t la, const uin
   return la < lb ? -1 : (la > lb ? 1 : 0);
 }
 
+// cmp_str for 16-byte aligned rows whose allocation extends to a multiple of 4
+// tokens (the gathered continuation table, KCfg::TS): 4 tokens per load, so a
+// long common prefix costs ceil(l / 4) dependent loads instead of l.
+__device__ __forceinline__ int cmp_row16(const uint32_t* a, uint32_t la, const uint32_t* b, uint32_t lb) {
+  const uint32_t l = la < lb ? la : lb;
+  for (uint32_t j = 0; j < l; j += 4) {
+    const uint4 x = *reinterpret_cast<const uint4*>(a + j), y = *reinterpret_cast<const uint4*>(b + j);
+    const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+    for (uint32_t k = 0; k < 4; ++k)
+      if (j + k < l && xs[k] != ys[k]) return xs[k] < ys[k] ? -1 : 1;
+  }
+  return la < lb ? -1 : (la > lb ? 1 : 0);
+}
+
 // Depth-major columns of one sorted source array (the fusion kernel's input):
 // element i's metadata, insertion position and token at depth d live at
 // meta[i], orig[i], tok[d * stride + i], so the lanes of a warp expanding a

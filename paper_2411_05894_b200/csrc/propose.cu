@@ -20,6 +20,11 @@
 
 namespace sssd {
 
+// continuation-table compare: vector loads when the rows allow them
+__device__ __forceinline__ int cmp_tab(const KCfg& c, const uint32_t* a, uint32_t la, const uint32_t* b, uint32_t lb) {
+  return c.tab16 ? cmp_row16(a, la, b, lb) : cmp_str(a, la, b, lb);
+}
+
 // --------------------------------------------------------------------------
 // suffix-row comparisons (ref datastore.py:129-141)
 // --------------------------------------------------------------------------
@@ -236,7 +241,7 @@ __device__ int gather_p(const sssd_ds& ds, const KCfg& c, int p, uint64_t lo, ui
   const int lane = lane_id();
   const uint64_t w = hi - lo;
   const int s = (int)min(w, (uint64_t)c.M);
-  uint32_t* ptab = tab + (size_t)(p - 1) * c.M * c.BL;
+  uint32_t* ptab = tab + (size_t)(p - 1) * c.M * c.TS;
   uint8_t* plen = lens + (size_t)(p - 1) * c.M;
   int cnt = 0;
   for (int k00 = 0; k00 < s; k00 += 32 * rpl) {
@@ -279,7 +284,7 @@ __device__ int gather_p(const sssd_ds& ds, const KCfg& c, int p, uint64_t lo, ui
       const int idx = cnt + __popc(bal & lanemask_lt());
       if (ne) {
         const uint64_t start = (uint64_t)pos + p;
-        uint32_t* dst = ptab + (size_t)idx * c.BL;
+        uint32_t* dst = ptab + (size_t)idx * c.TS;
         for (uint32_t j = 0; j < len; ++j)
           dst[j] = (p + j < SSSD_ROW_TOKENS) ? srow[1 + p + j] : __ldg(ds.tokens + start + j);
         plen[idx] = (uint8_t)len;
@@ -346,7 +351,7 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P, SSSD_LOOKUP_MINB)
   }
   __syncthreads();
 
-  uint32_t* tab = ds_tab + (size_t)b * c.P * c.M * c.BL;
+  uint32_t* tab = ds_tab + (size_t)b * c.P * c.M * c.TS;
   uint8_t* lens = ds_len + (size_t)b * c.P * c.M;
   int64_t* smp = lk.samples ? lk.samples + (size_t)b * c.P * c.M : nullptr;
 
@@ -405,7 +410,7 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P, SSSD_LOOKUP_MINB)
     if (p >= pcut && p <= pmax) {
       for (int i = lane; i < s_cnt[warp]; i += 32) {
         sssd_elem e;
-        e.off = (uint32_t)(((size_t)(p - 1) * c.M + i) * c.BL);
+        e.off = (uint32_t)(((size_t)(p - 1) * c.M + i) * c.TS);
         e.orig = (uint32_t)(before + i);
         e.len_m = (uint32_t)lens[(size_t)(p - 1) * c.M + i] | (255u << 8);
         e.pad = 0;
@@ -430,7 +435,7 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P, SSSD_LOOKUP_MINB)
   } else if (p >= pcut && p <= pmax) {
     const int cnt = s_cnt[warp];
     for (int i = lane; i < cnt; i += 32) {
-      const uint32_t* si = tab + ((size_t)(p - 1) * c.M + i) * c.BL;
+      const uint32_t* si = tab + ((size_t)(p - 1) * c.M + i) * c.TS;
       const uint32_t li = lens[(size_t)(p - 1) * c.M + i];
       int rank = i;
       for (int q = pcut; q <= pmax; ++q) {
@@ -439,7 +444,7 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P, SSSD_LOOKUP_MINB)
         int a = 0, z = cq;  // first element of run q that comes after string i
         while (a < z) {
           const int mid = (a + z) >> 1;
-          const int r = cmp_str(tab + ((size_t)(q - 1) * c.M + mid) * c.BL,
+          const int r = cmp_tab(c, tab + ((size_t)(q - 1) * c.M + mid) * c.TS,
                                 lens[(size_t)(q - 1) * c.M + mid], si, li);
           const bool before_i = q > p ? r <= 0 : r < 0;
           if (before_i) a = mid + 1; else z = mid;
@@ -447,7 +452,7 @@ __global__ void __launch_bounds__(32 * SSSD_MAX_P, SSSD_LOOKUP_MINB)
         rank += a;
       }
       sssd_elem e;
-      e.off = (uint32_t)(((size_t)(p - 1) * c.M + i) * c.BL);
+      e.off = (uint32_t)(((size_t)(p - 1) * c.M + i) * c.TS);
       e.orig = (uint32_t)(before + i);
       e.len_m = li | (255u << 8);
       e.pad = 0;
@@ -488,12 +493,12 @@ __device__ __forceinline__ void dedupe_request(const KCfg& c, int b, int n_all, 
   const int lane = lane_id(), warp = threadIdx.x >> 5;
   if (n_all <= 0) return;
   const sssd_elem* sorted = ds_el + (size_t)b * c.P * c.M;
-  const uint32_t* tab = ds_tab + (size_t)b * c.P * c.M * c.BL;
+  const uint32_t* tab = ds_tab + (size_t)b * c.P * c.M * c.TS;
   for (int r = threadIdx.x; r < n_all; r += blockDim.x) {
     int st = 1;
     if (r > 0) {
       const sssd_elem x = sorted[r - 1], y = sorted[r];
-      st = cmp_str(tab + x.off, el_len(x.len_m), tab + y.off, el_len(y.len_m)) != 0;
+      st = cmp_tab(c, tab + x.off, el_len(x.len_m), tab + y.off, el_len(y.len_m)) != 0;
     }
     gstart[r] = st;
   }
@@ -716,7 +721,7 @@ __global__ void __launch_bounds__(32 * kLkWarps, SSSD_LKW_MINB)
     lk.ranges[((size_t)b * c.P + lane) * 2 + 1] = ok ? (int64_t)(s_rhi[warp][lane] + ds.rank_base) : -1;
   }
 
-  uint32_t* tab = ds_tab + (size_t)b * c.P * c.M * c.BL;
+  uint32_t* tab = ds_tab + (size_t)b * c.P * c.M * c.TS;
   uint8_t* lens = ds_len + (size_t)b * c.P * c.M;
   int64_t* smp = lk.samples ? lk.samples + (size_t)b * c.P * c.M : nullptr;
   uint32_t* stage = s_stage[warp];
@@ -736,7 +741,7 @@ __global__ void __launch_bounds__(32 * kLkWarps, SSSD_LKW_MINB)
     for (int p = next; p >= blo; --p) {
       const uint64_t lo = s_rlo[warp][p - 1], w = s_rhi[warp][p - 1] - lo;
       const int sc = (int)min(w, (uint64_t)c.M);
-      uint32_t* ptab = tab + (size_t)(p - 1) * c.M * c.BL;
+      uint32_t* ptab = tab + (size_t)(p - 1) * c.M * c.TS;
       uint8_t* plen = lens + (size_t)(p - 1) * c.M;
       int cnt = 0;
       for (int k00 = 0; k00 < sc; k00 += kLkStage) {
@@ -770,7 +775,7 @@ __global__ void __launch_bounds__(32 * kLkWarps, SSSD_LKW_MINB)
           if (ne) {
             const int idx = cnt + __popc(bal & lanemask_lt());
             const uint64_t start = (uint64_t)pos + p;
-            uint32_t* dst = ptab + (size_t)idx * c.BL;
+            uint32_t* dst = ptab + (size_t)idx * c.TS;
             for (uint32_t j = 0; j < len; ++j)
               dst[j] = (p + j < SSSD_ROW_TOKENS) ? srow[1 + p + j] : __ldg(ds.tokens + start + j);
             plen[idx] = (uint8_t)len;
@@ -809,7 +814,7 @@ __global__ void __launch_bounds__(32 * kLkWarps, SSSD_LKW_MINB)
   for (int p = pmax; p >= pcut; --p) {
     const int cnt = s_cnt[warp][p - 1];
     for (int i = lane; i < cnt; i += 32) {
-      const uint32_t* si = tab + ((size_t)(p - 1) * c.M + i) * c.BL;
+      const uint32_t* si = tab + ((size_t)(p - 1) * c.M + i) * c.TS;
       const uint32_t li = lens[(size_t)(p - 1) * c.M + i];
       int rank = i;
       for (int q = pcut; q <= pmax; ++q) {
@@ -817,7 +822,7 @@ __global__ void __launch_bounds__(32 * kLkWarps, SSSD_LKW_MINB)
         int a = 0, z = s_cnt[warp][q - 1];
         while (a < z) {
           const int mid = (a + z) >> 1;
-          const int r = cmp_str(tab + ((size_t)(q - 1) * c.M + mid) * c.BL, lens[(size_t)(q - 1) * c.M + mid], si, li);
+          const int r = cmp_tab(c, tab + ((size_t)(q - 1) * c.M + mid) * c.TS, lens[(size_t)(q - 1) * c.M + mid], si, li);
           const bool before_i = q > p ? r <= 0 : r < 0;
           if (before_i) a = mid + 1;
           else z = mid;
@@ -825,7 +830,7 @@ __global__ void __launch_bounds__(32 * kLkWarps, SSSD_LKW_MINB)
         rank += a;
       }
       sssd_elem e;
-      e.off = (uint32_t)(((size_t)(p - 1) * c.M + i) * c.BL);
+      e.off = (uint32_t)(((size_t)(p - 1) * c.M + i) * c.TS);
       e.orig = (uint32_t)(before + i);
       e.len_m = li | (255u << 8);
       e.pad = 0;
@@ -849,7 +854,7 @@ __global__ void __launch_bounds__(32 * kLkWarps, SSSD_LKW_MINB)
           st = true;
         } else {
           const sssd_elem x = sorted[r - 1], y = sorted[r];
-          st = cmp_str(tab + x.off, el_len(x.len_m), tab + y.off, el_len(y.len_m)) != 0;
+          st = cmp_tab(c, tab + x.off, el_len(x.len_m), tab + y.off, el_len(y.len_m)) != 0;
         }
       }
       const uint32_t sm = __ballot_sync(SSSD_FULL, st);

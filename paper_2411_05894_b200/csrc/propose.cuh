@@ -9,6 +9,8 @@ namespace sssd {
 struct KCfg {
   int b0, b1;  // request range [b0, b1) handled by this launch (blockIdx.x is relative to b0)
   int P, S, BL, IBL, M, T, use_ds, use_in, n_trees, has_sep;
+  int TS;     // row stride of the gathered continuation table (propose: BL rounded up to 4)
+  int tab16;  // table rows 16-byte aligned with TS % 4 == 0 (vector compares)
   uint32_t sep;
   int disc_stride;
   const double* disc;
