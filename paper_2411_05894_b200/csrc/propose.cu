@@ -776,8 +776,20 @@ __global__ void __launch_bounds__(32 * kLkWarps, SSSD_LKW_MINB)
             const int idx = cnt + __popc(bal & lanemask_lt());
             const uint64_t start = (uint64_t)pos + p;
             uint32_t* dst = ptab + (size_t)idx * c.TS;
-            for (uint32_t j = 0; j < len; ++j)
-              dst[j] = (p + j < SSSD_ROW_TOKENS) ? srow[1 + p + j] : __ldg(ds.tokens + start + j);
+            if (c.tab16) {  // 16-byte stores (the row's tail past len is padding)
+              for (uint32_t j = 0; j < len; j += 4) {
+                uint32_t v[4];
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k) {
+                  const uint32_t jj = j + k;
+                  v[k] = jj >= len ? 0u : (p + jj < SSSD_ROW_TOKENS ? srow[1 + p + jj] : __ldg(ds.tokens + start + jj));
+                }
+                *reinterpret_cast<uint4*>(dst + j) = make_uint4(v[0], v[1], v[2], v[3]);
+              }
+            } else {
+              for (uint32_t j = 0; j < len; ++j)
+                dst[j] = (p + j < SSSD_ROW_TOKENS) ? srow[1 + p + j] : __ldg(ds.tokens + start + j);
+            }
             plen[idx] = (uint8_t)len;
           }
           cnt += __popc(bal);
