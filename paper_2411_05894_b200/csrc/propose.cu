@@ -548,7 +548,7 @@ constexpr int kLkWarps = 4;     // requests per CTA
 constexpr int kLkStage = SSSD_LK_STAGE;  // staged suffix rows per warp and round (2 per lane)
 
 #ifndef SSSD_LKW_MINB
-#define SSSD_LKW_MINB 1
+#define SSSD_LKW_MINB 8  // <= 64 registers (56, no spills): 64 warps per SM by registers
 #endif
 #ifdef SSSD_LK_PROBE  // per-phase cycle stamps of the lookup warp (measurement builds only)
 __device__ long long* g_lk_cyc;
