@@ -26,6 +26,10 @@
 #include "fusion_ls.cuh"
 #include "propose.cuh"
 
+#ifndef SSSD_CTA_RANK_MAX  // levels of (kCtaSortWarp, this] nodes: rank sort (<= 2 * kCtaThreads)
+#define SSSD_CTA_RANK_MAX (2 * kCtaThreads)
+#endif
+
 namespace sssd {
 
 #ifndef SSSD_CTA_WARPS
@@ -93,6 +97,41 @@ __device__ __forceinline__ void cta_sort(LsLevel L, uint32_t n) {
       __syncthreads();
     }
   }
+}
+
+// Levels of up to 2 * kCtaThreads nodes: every thread ranks (up to) two nodes
+// against all n keys (broadcast shared-memory reads; (k0, k1) keys are unique),
+// then writes them to their ranks -- two barriers instead of the bitonic
+// network's one per stage.
+static_assert(SSSD_CTA_RANK_MAX <= 2 * kCtaThreads, "two nodes per thread");
+__device__ __forceinline__ void cta_rank_sort(LsLevel L, uint32_t n) {
+  uint64_t m0[2] = {~0ull, ~0ull}, m1[2] = {~0ull, ~0ull};
+  uint32_t r[2] = {0, 0}, o[2] = {0, 0};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t i = threadIdx.x + h * kCtaThreads;
+    if (i < n) {
+      m0[h] = L.k0()[i];
+      m1[h] = L.k1()[i];
+      o[h] = L.ord()[i];
+    }
+  }
+  for (uint32_t q = 0; q < n; ++q) {
+    const uint64_t q0 = L.k0()[q], q1 = L.k1()[q];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) r[h] += k_less(q0, q1, m0[h], m1[h]) ? 1u : 0u;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t i = threadIdx.x + h * kCtaThreads;
+    if (i < n) {
+      L.k0()[r[h]] = m0[h];
+      L.k1()[r[h]] = m1[h];
+      L.ord()[r[h]] = o[h];
+    }
+  }
+  __syncthreads();
 }
 
 // One warp's share of a level's generation: parents [jb, je), whose elements
@@ -422,8 +461,10 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     ph_gen += (uint32_t)clock() - tp;
     tp = (uint32_t)clock();
     // 3. sort the level by (k0, k1) = (~priority, rank, parent tb, first)
-    if (n > (uint32_t)kCtaSortWarp) {
+    if (n > (uint32_t)SSSD_CTA_RANK_MAX) {
       cta_sort(L, n);
+    } else if (n > (uint32_t)kCtaSortWarp) {
+      cta_rank_sort(L, n);
     } else {
       if (warp == 0) ls_sort(L, n);
       __syncthreads();
