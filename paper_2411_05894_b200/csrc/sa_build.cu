@@ -163,152 +163,6 @@ __global__ void __launch_bounds__(kT) rs_scatter(const uint64_t* kin, const uint
 }
 
 
-// ---- onesweep passes (decoupled look-back) -----------------------------------
-// One histogram pass per sort gives every pass's global digit counts; each
-// scatter pass then finds its tile's digit offsets by looking back over the
-// tiles before it (dynamic tile ids, so every earlier tile is already running)
-// instead of a per-pass upsweep over the keys and a scan over tiles.
-// status[tile][digit]: 0 = not yet published, kAgg | tile count, kPre |
-// inclusive prefix over tiles 0..tile (counts < 2^30).
-constexpr uint32_t kAgg = 1u << 30, kPre = 2u << 30, kCnt = (1u << 30) - 1;
-
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// ghist[p][d] += count of digit d of pass p (shift 8p) over keys[0..n)
-__global__ void __launch_bounds__(kT) rs_hist_all(const uint64_t* keys, uint64_t n, int passes, uint32_t* ghist) {
-  __shared__ uint32_t h[8][kDigits];
-  for (int i = threadIdx.x; i < 8 * kDigits; i += kT) (&h[0][0])[i] = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const uint64_t stride = (uint64_t)gridDim.x * kT;
-  for (uint64_t i0 = (uint64_t)blockIdx.x * kT; i0 < n; i0 += stride) {
-    const uint64_t i = i0 + threadIdx.x;
-    const bool ok = i < n;
-    const uint64_t k = ok ? keys[i] : 0;
-    const uint32_t vm = __ballot_sync(SSSD_FULL, ok);
-    for (int p = 0; p < passes; ++p) {
-      const uint32_t d = (uint32_t)(k >> (8 * p)) & 255u;
-      // a warp whose valid lanes share the digit (clustered high digits) adds once
-      const uint32_t d0 = __shfl_sync(SSSD_FULL, d, __ffs(vm) - 1);
-      if (__all_sync(SSSD_FULL, !ok || d == d0)) {
-        if (lane == __ffs(vm) - 1) atomicAdd(&h[p][d0], (uint32_t)__popc(vm));
-      } else if (ok) {
-        atomicAdd(&h[p][d], 1u);
-      }
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < passes * kDigits; i += kT) {
-    const uint32_t v = (&h[0][0])[i];
-    if (v) atomicAdd(ghist + i, v);
-  }
-}
-
-// dbase[p][d] = exclusive prefix of ghist[p][0..d)
-__global__ void __launch_bounds__(kDigits) rs_digit_base(const uint32_t* ghist, uint32_t* dbase) {
-  __shared__ uint32_t part[kDigits / 32];
-  const int p = blockIdx.x, d = threadIdx.x, lane = d & 31, w = d >> 5;
-  const uint32_t v = ghist[p * kDigits + d];
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(SSSD_FULL, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) part[w] = x;
-  __syncthreads();
-  uint32_t base = 0;
-  for (int k = 0; k < w; ++k) base += part[k];
-  dbase[p * kDigits + d] = base + x - v;
-}
-
-// rs_scatter with the tile's digit offsets from the look-back
-__global__ void __launch_bounds__(kT) rs_scatter_ob(const uint64_t* kin, const uint32_t* vin, uint64_t n, int shift,
-                                                   const uint32_t* dbase, uint32_t* status, uint32_t* tile_ctr,
-                                                   uint64_t* kout, uint32_t* vout) {
-  __shared__ uint32_t base[kDigits];
-  __shared__ uint32_t wcnt[kT / 32][kDigits];
-  __shared__ uint32_t woff[kT / 32][kDigits];
-  __shared__ uint32_t hcnt[kDigits];
-  __shared__ uint32_t s_tile;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  hcnt[threadIdx.x] = 0;
-  for (int k = 0; k < kT / 32; ++k) wcnt[k][threadIdx.x] = 0xffffff00u;
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const uint64_t t0 = (uint64_t)tile * kTile;
-  uint64_t key[kItems];
-  uint32_t val[kItems];
-#pragma unroll
-  for (int r = 0; r < kItems; ++r) {
-    const uint64_t i = t0 + (uint64_t)r * kT + threadIdx.x;
-    key[r] = i < n ? kin[i] : 0;
-    val[r] = i < n ? vin[i] : 0;
-  }
-  // the tile's digit counts from the registers
-#pragma unroll
-  for (int r = 0; r < kItems; ++r) {
-    const bool ok = t0 + (uint64_t)r * kT + threadIdx.x < n;
-    const uint32_t d = ok ? (uint32_t)(key[r] >> shift) & 255u : 256u + lane;
-    const uint32_t peers = __match_any_sync(SSSD_FULL, d);
-    if (ok && lane == __ffs(peers) - 1) atomicAdd(&hcnt[d], (uint32_t)__popc(peers));
-  }
-  __syncthreads();
-  {  // thread t owns digit t: publish, look back, publish the inclusive prefix
-    const uint32_t dg = threadIdx.x, cnt = hcnt[dg];
-    uint32_t* mine = status + (size_t)tile * kDigits + dg;
-    uint32_t excl = 0;
-    if (tile > 0) {
-      st_release(mine, kAgg | cnt);
-      for (int64_t t = (int64_t)tile - 1; t >= 0; --t) {
-        uint32_t v;
-        do {
-          v = ld_acquire(status + (size_t)t * kDigits + dg);
-        } while (v == 0);
-        excl += v & kCnt;
-        if (v & kPre) break;
-      }
-    }
-    st_release(mine, kPre | (excl + cnt));
-    base[dg] = dbase[dg] + excl;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < kItems; ++r) {
-    const bool ok = t0 + (uint64_t)r * kT + threadIdx.x < n;
-    const uint32_t d = ok ? (uint32_t)(key[r] >> shift) & 255u : 256u + lane;
-    const uint32_t peers = __match_any_sync(SSSD_FULL, d);
-    const uint32_t lr = __popc(peers & lanemask_lt());
-    if (ok && lane == __ffs(peers) - 1) wcnt[w][d] = ((uint32_t)r << 8) | (uint32_t)__popc(peers);
-    __syncthreads();
-    {
-      const uint32_t dg = threadIdx.x;
-      uint32_t run = base[dg];
-#pragma unroll
-      for (int k = 0; k < kT / 32; ++k) {
-        const uint32_t e = wcnt[k][dg];
-        woff[k][dg] = run;
-        run += (e >> 8) == (uint32_t)r ? (e & 255u) : 0u;
-      }
-      base[dg] = run;
-    }
-    __syncthreads();
-    if (ok) {
-      const uint32_t pos = woff[w][d] + lr;
-      kout[pos] = key[r];
-      vout[pos] = val[r];
-    }
-  }
-}
-
 // ---- scans --------------------------------------------------------------------
 
 // per-tile reduce (op: 0 = sum of u32 flags, 1 = max of u32)
@@ -532,7 +386,7 @@ SaWs2 carve2(uint8_t* base, uint64_t n) {
   w.tmp = reinterpret_cast<uint32_t*>(take(4 * n));
   w.tmp2 = reinterpret_cast<uint32_t*>(take(4 * n));
   w.hist = reinterpret_cast<uint32_t*>(take(4 * nb * kDigits));
-  w.offs = reinterpret_cast<uint32_t*>(take(4 * (nb > 17 ? nb : 17) * kDigits + 64));  // (onesweep: 8 + 8 rows + counters)
+  w.offs = reinterpret_cast<uint32_t*>(take(4 * nb * kDigits));
   w.tiles = reinterpret_cast<uint32_t*>(take(4 * nb));
   w.grand = reinterpret_cast<uint32_t*>(take(16));
   w.totals = reinterpret_cast<uint32_t*>(take(4 * kDigits));
@@ -542,45 +396,10 @@ SaWs2 carve2(uint8_t* base, uint64_t n) {
 }
 
 // stable LSD sort of (key, val)[0..A) on the low `bits` bits; result in (k0, v0)
-#ifndef SSSD_SA_ONESWEEP
-#define SSSD_SA_ONESWEEP 1
-#endif
 void radix_sort(SaWs2& w, uint64_t A, int bits, cudaStream_t st) {
   const unsigned nb = tiles_of(A);
   uint64_t *ka = w.k0, *kb = w.k1;
   uint32_t *va = w.v0, *vb = w.v1;
-  const int passes = (bits + 7) / 8;
-  if (SSSD_SA_ONESWEEP && A > 0 && A < (1ull << 30) && passes <= 8) {
-    // status words reuse the hist array ([nb][256]); the offs array holds the
-    // digit histograms, the digit bases and the tile counter
-    uint32_t* ghist = w.offs;
-    uint32_t* dbase = w.offs + 8 * kDigits;
-    uint32_t* ctr = w.offs + 16 * kDigits;
-    cudaMemsetAsync(ghist, 0, 4 * 8 * kDigits, st);
-    int grid = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&grid, cudaDevAttrMultiProcessorCount, dev);
-    grid = grid * 8;
-    if ((uint64_t)grid * kT > A) grid = (int)((A + kT - 1) / kT);
-    rs_hist_all<<<grid, kT, 0, st>>>(ka, A, passes, ghist);
-    rs_digit_base<<<passes, kDigits, 0, st>>>(ghist, dbase);
-    for (int p = 0; p < passes; ++p) {
-      cudaMemsetAsync(w.hist, 0, (size_t)4 * nb * kDigits, st);
-      cudaMemsetAsync(ctr + p, 0, 4, st);
-      rs_scatter_ob<<<nb, kT, 0, st>>>(ka, va, A, 8 * p, dbase + p * kDigits, w.hist, ctr + p, kb, vb);
-      uint64_t* tk = ka;
-      ka = kb;
-      kb = tk;
-      uint32_t* tv = va;
-      va = vb;
-      vb = tv;
-    }
-    if (ka != w.k0) {
-      cudaMemcpyAsync(w.k0, ka, 8 * A, cudaMemcpyDeviceToDevice, st);
-      cudaMemcpyAsync(w.v0, va, 4 * A, cudaMemcpyDeviceToDevice, st);
-    }
-    return;
-  }
   for (int sh = 0; sh < bits; sh += 8) {
     cudaMemsetAsync(w.totals, 0, 4 * kDigits, st);
     rs_upsweep<<<nb, kT, 0, st>>>(ka, A, sh, w.hist, nb, w.totals);
